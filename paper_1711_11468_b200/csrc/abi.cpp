@@ -1,0 +1,721 @@
+// extern "C" boundary (include/lbmgpu.h) over the device engines.
+#include "../../include/lbmgpu.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "halo.hpp"
+#include "lbm.hpp"
+
+using namespace lbmgpu;
+
+struct lbmgpu_ctx {
+  std::unique_ptr<Engine> eng;
+  Descriptor desc;
+  GeomSpec geom;
+  DevBuf<double> rho, u, uprev;  // steady-state scratch
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return LBMGPU_OK;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return LBMGPU_ECONFIG;
+  } catch (const NumericalError& e) {
+    g_err = e.what();
+    return LBMGPU_ENUMERICAL;
+  } catch (const DeviceError& e) {
+    g_err = e.what();
+    return LBMGPU_EDEVICE;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return LBMGPU_EDEVICE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LBMGPU_EDEVICE;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw ConfigError(std::string(what) + " must not be NULL");
+}
+
+GeomSpec to_spec(const lbmgpu_geometry* g) {
+  need(g, "geometry");
+  GeomSpec s;
+  s.kind = g->kind;
+  s.nx = g->nx;
+  s.ny = g->ny;
+  s.nz = g->nz;
+  s.block = g->block;
+  s.spacing = g->spacing;
+  s.pipe_diameter = g->pipe_diameter;
+  if (g->kind == kCustom) {
+    need(g->flags, "custom geometry flags");
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1)
+      throw ConfigError("custom geometry: dims must be >= 1");
+    s.custom.assign(g->flags, g->flags + s.volume());
+    for (int a = 0; a < 3; ++a) s.custom_periodic[a] = g->periodic[a] != 0;
+  }
+  return s;
+}
+
+Padding to_padding(const lbmgpu_padding* p) {
+  Padding q;
+  if (p) {
+    q.mode = p->mode;
+    for (int d = 0; d < kQ; ++d) q.pads[d] = p->pads[d];
+  }
+  return q;
+}
+
+void fill_desc(const Descriptor& d, lbmgpu_descriptor* o) {
+  o->prop = static_cast<int>(d.prop);
+  o->layout_soa = d.soa;
+  o->indirect = d.indirect;
+  o->blk = d.blk;
+  o->nt_streams = d.nt_streams;
+  o->ria = d.ria;
+  o->pv = d.pv;
+  o->vec = d.vec;
+  o->vector_width = d.vector_width;
+}
+
+// TrtParams::validate (d3q19.hpp:75-81) + Kernel::advance checks
+// (kernels.cpp:84-93).
+TrtArgs checked_trt(lbmgpu_ctx* c, double wp, double lambda, const double* g,
+                    long steps) {
+  if (steps < 0) throw ConfigError("advance: steps must be >= 0");
+  if (!(wp > 0.0) || !(wp < 2.0))
+    throw ConfigError("TrtParams: omega_plus must be in (0, 2), got " +
+                      std::to_string(wp));
+  if (!(lambda > 0.0)) throw ConfigError("TrtParams: magic_lambda must be positive");
+  if (c->desc.prop == Prop::Aa && steps % 2 != 0)
+    throw ConfigError("kernel '" + c->desc.name +
+                      "' uses the AA pattern and requires an even step count, "
+                      "got " + std::to_string(steps));
+  need(g, "g");
+  return make_trt(wp, omega_minus_of(wp, lambda), g);
+}
+
+constexpr uint64_t kChunkNodes = 1ull << 21;  // 2 Mi nodes = 304 MiB staging
+
+struct HostPinned {
+  void* p = nullptr;
+  explicit HostPinned(size_t b) { LBM_CUDA(cudaMallocHost(&p, b)); }
+  ~HostPinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+uint64_t fnv_bytes(uint64_t h, const unsigned char* p, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+// equilibrium(rho, u) (reference src/d3q19.cpp:7-18)
+void equilibrium(double rho, const double* u, double* f) {
+  if (!(rho > 0.0))
+    throw ConfigError("equilibrium: rho must be positive, got " + std::to_string(rho));
+  const double usq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  for (int i = 0; i < kQ; ++i) {
+    const double cu = static_cast<double>(cx(i)) * u[0] +
+                      static_cast<double>(cy(i)) * u[1] +
+                      static_cast<double>(cz(i)) * u[2];
+    f[i] = weight(i) * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - 1.5 * usq);
+  }
+}
+
+}  // namespace
+
+// device helpers implemented in harness.cu
+namespace lbmgpu {
+void velocity_change(const double* u, const double* uprev, uint64_t n3,
+                     double* max_du, double* max_u, bool* finite,
+                     cudaStream_t s);
+void layer_sums(const double* u, uint64_t cols, int layers, double* out_dev,
+                cudaStream_t s);
+}  // namespace lbmgpu
+
+extern "C" {
+
+const char* lbmgpu_last_error(void) { return g_err.c_str(); }
+
+uint64_t lbmgpu_fnv1a(const void* data, uint64_t nbytes) {
+  return fnv_bytes(0xcbf29ce484222325ull, static_cast<const unsigned char*>(data),
+                   nbytes);
+}
+int lbmgpu_abi_version(void) { return LBMGPU_ABI_VERSION; }
+
+int lbmgpu_kernel_names(char* buf, size_t cap) {
+  return guard([&] {
+    std::string s;
+    for (const auto& n : kernel_names()) s += n + "\n";
+    if (!buf || s.size() + 1 > cap) throw ConfigError("kernel_names: buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int lbmgpu_make_descriptor(const char* name, int blk, int W,
+                           lbmgpu_descriptor* out) {
+  return guard([&] {
+    need(name, "name");
+    need(out, "out");
+    fill_desc(make_descriptor(name, blk, W), out);
+  });
+}
+
+int lbmgpu_padding_offsets(uint64_t n, const lbmgpu_padding* pad,
+                           uint64_t* starts, uint64_t* total) {
+  return guard([&] {
+    need(starts, "starts");
+    uint64_t t = 0;
+    auto s = padding_offsets(n, to_padding(pad), &t);
+    for (int d = 0; d < kQ; ++d) starts[d] = s[d];
+    if (total) *total = t;
+  });
+}
+
+int lbmgpu_loop_balance(const char* name, double* a, double* b, double* g) {
+  return guard([&] {
+    need(name, "name");
+    LoopBalance l = loop_balance(make_descriptor(name, 0, 4));
+    if (a) *a = l.ref_min;
+    if (b) *b = l.ref_max;
+    if (g) *g = l.gpu;
+  });
+}
+
+double lbmgpu_omega_minus(double wp, double lambda) {
+  return omega_minus_of(wp, lambda);
+}
+
+int lbmgpu_geometry_build(const lbmgpu_geometry* g, uint8_t* flags_out,
+                          int64_t* n_fluid, int* periodic_out) {
+  return guard([&] {
+    GeomSpec s = to_spec(g);
+    cudaStream_t st;
+    LBM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      DeviceGeometry dg = build_geometry_device(s, st);
+      if (flags_out)
+        LBM_CUDA(cudaMemcpyAsync(flags_out, dg.flags.get(), dg.volume(),
+                                 cudaMemcpyDeviceToHost, st));
+      LBM_CUDA(cudaStreamSynchronize(st));
+      if (n_fluid) *n_fluid = dg.n_fluid;
+      if (periodic_out)
+        for (int a = 0; a < 3; ++a) periodic_out[a] = dg.periodic[a];
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+  });
+}
+
+int lbmgpu_create(const char* name, int blk, int W, const lbmgpu_geometry* geom,
+                  const lbmgpu_padding* pad, int row_pad,
+                  const lbmgpu_dist* dist, lbmgpu_ctx** out) {
+  return guard([&] {
+    need(name, "kernel name");
+    need(out, "out");
+    *out = nullptr;
+    if (row_pad < 0) throw ConfigError("FullLattice: row_pad must be >= 0");
+    auto c = std::make_unique<lbmgpu_ctx>();
+    c->desc = make_descriptor(name, blk, W);
+    c->geom = to_spec(geom);
+    validate_geometry(c->geom);  // ConfigError before any allocation
+    DistSpec ds;
+    if (dist) {
+      ds.rank = dist->rank;
+      ds.nranks = dist->nranks;
+      ds.device = dist->device;
+      ds.virtual_parts = dist->virtual_parts;
+      if (dist->nccl_id) {
+        std::memcpy(ds.nccl_id.data(), dist->nccl_id, 128);
+        ds.have_id = true;
+      }
+      if (ds.nranks < 1 || ds.rank < 0 || ds.rank >= ds.nranks)
+        throw ConfigError("dist: bad rank/nranks");
+      if (ds.virtual_parts > 1 && ds.nranks > 1)
+        throw ConfigError("dist: virtual_parts needs nranks == 1");
+    }
+    if (ds.device >= 0) LBM_CUDA(cudaSetDevice(ds.device));
+    if (c->desc.indirect) {
+      if (ds.nranks > 1 || ds.virtual_parts > 1)
+        throw ConfigError("list kernels run as replicas only (one lattice per "
+                          "GPU); z-slab decomposition is for direct AA");
+      c->eng = make_list_engine(c->desc, c->geom, to_padding(pad));
+    } else {
+      c->eng = make_direct_engine(c->desc, c->geom, ds);
+    }
+    *out = c.release();
+  });
+}
+
+int lbmgpu_destroy(lbmgpu_ctx* c) {
+  return guard([&] { delete c; });
+}
+
+int lbmgpu_advance(lbmgpu_ctx* c, double wp, double lambda, const double* g,
+                   long steps) {
+  return guard([&] {
+    need(c, "ctx");
+    TrtArgs t = checked_trt(c, wp, lambda, g, steps);
+    if (steps == 0) return;
+    c->eng->advance(t, steps);
+    LBM_CUDA(cudaStreamSynchronize(c->eng->stream()));
+  });
+}
+
+int lbmgpu_time_advance(lbmgpu_ctx* c, double wp, double lambda,
+                        const double* g, long steps, double* ms) {
+  return guard([&] {
+    need(c, "ctx");
+    need(ms, "ms");
+    TrtArgs t = checked_trt(c, wp, lambda, g, steps);
+    cudaEvent_t a, b;
+    LBM_CUDA(cudaEventCreate(&a));
+    LBM_CUDA(cudaEventCreate(&b));
+    LBM_CUDA(cudaEventRecord(a, c->eng->stream()));
+    if (steps) c->eng->advance(t, steps);
+    LBM_CUDA(cudaEventRecord(b, c->eng->stream()));
+    LBM_CUDA(cudaEventSynchronize(b));
+    float f = 0.f;
+    LBM_CUDA(cudaEventElapsedTime(&f, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms = f;
+  });
+}
+
+int lbmgpu_n_fluid(lbmgpu_ctx* c, uint64_t* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    *out = c->eng->n_fluid();
+  });
+}
+
+int lbmgpu_snapshot(lbmgpu_ctx* c, double* host, uint64_t count) {
+  return guard([&] {
+    need(c, "ctx");
+    const uint64_t N = c->eng->n_fluid();
+    if (count != N * kQ)
+      throw ConfigError("snapshot: buffer holds " + std::to_string(count) +
+                        " values, lattice has " + std::to_string(N * kQ));
+    need(host, "host buffer");
+    const uint64_t chunk = std::min(N, kChunkNodes);
+    DevBuf<double> stage(chunk * kQ);
+    cudaStream_t s = c->eng->stream();
+    for (uint64_t c0 = 0; c0 < N; c0 += chunk) {
+      const uint64_t n = std::min(chunk, N - c0);
+      c->eng->gather_canonical(c0, n, stage.get());
+      LBM_CUDA(cudaMemcpyAsync(host + c0 * kQ, stage.get(), n * kQ * 8,
+                               cudaMemcpyDeviceToHost, s));
+      LBM_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int lbmgpu_load_state(lbmgpu_ctx* c, const double* host, uint64_t count) {
+  return guard([&] {
+    need(c, "ctx");
+    const uint64_t N = c->eng->n_fluid();
+    if (count != N * kQ)
+      throw ConfigError("load_state: state size does not match fluid count");
+    need(host, "host buffer");
+    const uint64_t chunk = std::min(N, kChunkNodes);
+    DevBuf<double> stage(chunk * kQ);
+    cudaStream_t s = c->eng->stream();
+    for (uint64_t c0 = 0; c0 < N; c0 += chunk) {
+      const uint64_t n = std::min(chunk, N - c0);
+      LBM_CUDA(cudaMemcpyAsync(stage.get(), host + c0 * kQ, n * kQ * 8,
+                               cudaMemcpyHostToDevice, s));
+      c->eng->scatter_canonical(c0, n, stage.get());
+      LBM_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int lbmgpu_load_perturbed(lbmgpu_ctx* c, uint64_t seed, double amplitude) {
+  return guard([&] {
+    need(c, "ctx");
+    c->eng->load_perturbed(seed, amplitude);
+    LBM_CUDA(cudaStreamSynchronize(c->eng->stream()));
+  });
+}
+
+int lbmgpu_total_mass(lbmgpu_ctx* c, double* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    *out = c->eng->total_mass();
+  });
+}
+
+int lbmgpu_fingerprint(lbmgpu_ctx* c, uint64_t* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    const uint64_t N = c->eng->n_fluid();
+    const uint64_t chunk = std::min(N, kChunkNodes);
+    cudaStream_t s = c->eng->stream();
+    DevBuf<double> stage[2] = {DevBuf<double>(chunk * kQ), DevBuf<double>(chunk * kQ)};
+    HostPinned pin0(chunk * kQ * 8), pin1(chunk * kQ * 8);
+    void* pins[2] = {pin0.p, pin1.p};
+    cudaEvent_t ev[2];
+    LBM_CUDA(cudaEventCreate(&ev[0]));
+    LBM_CUDA(cudaEventCreate(&ev[1]));
+    uint64_t h = 0xcbf29ce484222325ull;
+    const uint64_t nchunks = ceil_div(N, chunk);
+    auto issue = [&](uint64_t k) {
+      const uint64_t c0 = k * chunk, n = std::min(chunk, N - c0);
+      const int b = static_cast<int>(k & 1);
+      c->eng->gather_canonical(c0, n, stage[b].get());
+      LBM_CUDA(cudaMemcpyAsync(pins[b], stage[b].get(), n * kQ * 8,
+                               cudaMemcpyDeviceToHost, s));
+      LBM_CUDA(cudaEventRecord(ev[b], s));
+    };
+    if (nchunks) issue(0);
+    for (uint64_t k = 0; k < nchunks; ++k) {
+      if (k + 1 < nchunks) issue(k + 1);
+      const int b = static_cast<int>(k & 1);
+      LBM_CUDA(cudaEventSynchronize(ev[b]));
+      const uint64_t n = std::min(chunk, N - k * chunk);
+      h = fnv_bytes(h, static_cast<const unsigned char*>(pins[b]), n * kQ * 8);
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    *out = h;
+  });
+}
+
+int lbmgpu_capabilities(lbmgpu_ctx* c, int* nt_avail, int* nt_eff, int* huge) {
+  return guard([&] {
+    need(c, "ctx");
+    // GPU stores are full-sector writes with no write allocate; the nt names
+    // use st.global.cs (evict-first) streaming stores.
+    const int nt = c->desc.nt_streams;
+    if (nt_avail) *nt_avail = nt > 0 ? 1 : 0;
+    if (nt_eff) *nt_eff = nt;
+    if (huge) *huge = 0;
+  });
+}
+
+int lbmgpu_ria_stats(lbmgpu_ctx* c, int64_t* runs, int64_t* nf, double* vfrac,
+                     double* pvfrac) {
+  return guard([&] {
+    need(c, "ctx");
+    int64_t r = -1;
+    double v = -1.0;
+    const bool have = c->eng->ria_stats(&r, &v);
+    if (runs) *runs = have ? r : -1;
+    if (nf) *nf = have ? static_cast<int64_t>(c->eng->n_fluid()) : -1;
+    if (vfrac) *vfrac = have ? v : -1.0;
+    if (pvfrac) *pvfrac = (have && c->desc.pv) ? v : -1.0;
+  });
+}
+
+int lbmgpu_descriptor_of(lbmgpu_ctx* c, lbmgpu_descriptor* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    fill_desc(c->desc, out);
+  });
+}
+
+int lbmgpu_export_structure(lbmgpu_ctx* c, int32_t* nodes, uint32_t* adj,
+                            uint64_t* starts, uint64_t* total) {
+  return guard([&] {
+    need(c, "ctx");
+    c->eng->export_structure(nodes, adj, starts, total);
+  });
+}
+
+int lbmgpu_steady_state_run(lbmgpu_ctx* c, double wp, double lambda,
+                            const double* g, long interval, double rel_tol,
+                            long max_steps, long* steps_out, int* converged,
+                            double* final_delta) {
+  return guard([&] {
+    need(c, "ctx");
+    // harness.cpp:141-174
+    if (!(rel_tol > 0.0)) throw ConfigError("steady_state_run: rel_tol > 0");
+    if (interval < 1) throw ConfigError("steady_state_run: check_interval >= 1");
+    if (c->desc.prop == Prop::Aa && interval % 2 != 0) ++interval;
+    const uint64_t N = c->eng->n_fluid();
+    cudaStream_t s = c->eng->stream();
+    if (c->u.size() != 3 * N) {
+      c->rho.alloc(N);
+      c->u.alloc(3 * N);
+      c->uprev.alloc(3 * N);
+    }
+    c->eng->macro_fields(c->rho.get(), c->uprev.get());
+    long steps = 0;
+    bool conv = false;
+    double delta = 0.0;
+    while (steps < max_steps) {
+      const long chunk = std::min(interval, max_steps - steps);
+      TrtArgs t = checked_trt(c, wp, lambda, g, chunk);
+      if (chunk) c->eng->advance(t, chunk);
+      steps += chunk;
+      c->eng->macro_fields(c->rho.get(), c->u.get());
+      double max_du = 0, max_u = 0;
+      bool finite = true;
+      velocity_change(c->u.get(), c->uprev.get(), 3 * N, &max_du, &max_u,
+                      &finite, s);
+      if (!finite)
+        throw NumericalError("steady_state_run: non-finite velocity at step " +
+                             std::to_string(steps));
+      delta = max_u > 0.0 ? max_du / max_u : max_du;
+      std::swap(c->u, c->uprev);
+      if (delta < rel_tol) {
+        conv = true;
+        break;
+      }
+    }
+    if (steps_out) *steps_out = steps;
+    if (converged) *converged = conv;
+    if (final_delta) *final_delta = delta;
+  });
+}
+
+int lbmgpu_layer_ux(lbmgpu_ctx* c, double* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    const GeomSpec& g = c->geom;
+    const int layers = g.nz - 2;
+    const uint64_t cols = uint64_t(g.nx) * g.ny;
+    if (g.kind != kSlit || c->eng->n_fluid() != cols * layers)
+      throw ConfigError("layer_ux: needs the slit geometry");
+    const uint64_t N = c->eng->n_fluid();
+    cudaStream_t s = c->eng->stream();
+    DevBuf<double> rho(N), u(3 * N), sums(layers);
+    c->eng->macro_fields(rho.get(), u.get());
+    layer_sums(u.get(), cols, layers, sums.get(), s);
+    LBM_CUDA(cudaMemcpyAsync(out, sums.get(), layers * 8, cudaMemcpyDeviceToHost, s));
+    LBM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int lbmgpu_verify(const char* name, int nx, int ny, int nz, double gx,
+                  double tau, double lambda, long interval, double rel_tol,
+                  long max_steps, lbmgpu_verify_report* rep, double* simulated,
+                  double* analytic) {
+  return guard([&] {
+    need(name, "kernel name");
+    need(rep, "report");
+    // PoiseuilleCase::validate (verification.cpp:7-17)
+    const double wp = 1.0 / tau;
+    if (!(wp > 0.0) || !(wp < 2.0))
+      throw ConfigError("TrtParams: omega_plus must be in (0, 2), got " +
+                        std::to_string(wp));
+    if (!(lambda > 0.0)) throw ConfigError("TrtParams: magic_lambda must be positive");
+    if (nz < 6) throw ConfigError("Poiseuille case: nz must be >= 6");
+    if (nx < 1 || ny < 1) throw ConfigError("Poiseuille case: bad dims");
+    const int layers = nz - 2;
+    const double h = layers;
+    const double nu = (1.0 / wp - 0.5) / 3.0;  // d3q19.hpp:68
+    const double u_max = std::abs(gx) * h * h / (8.0 * nu);
+    if (!(u_max < 0.05))
+      throw ConfigError("Poiseuille case: centerline velocity g*h^2/(8 nu) = " +
+                        std::to_string(u_max) +
+                        " is too close to the speed of sound");
+    // analytic_profile (verification.cpp:19-29)
+    std::vector<double> ana(layers), sim(layers, 0.0);
+    for (int k = 0; k < layers; ++k) {
+      const double zeta = k + 0.5;
+      ana[k] = gx / (2.0 * nu) * zeta * (h - zeta);
+    }
+    const double shift = gx / 2.0;
+    lbmgpu_geometry geo{};
+    geo.kind = LBMGPU_SLIT;
+    geo.nx = nx;
+    geo.ny = ny;
+    geo.nz = nz;
+    lbmgpu_padding pad{};
+    pad.mode = 1;
+    lbmgpu_ctx* raw = nullptr;
+    int rc = lbmgpu_create(name, 0, 4, &geo, &pad, 0, nullptr, &raw);
+    if (rc) {
+      if (rc == LBMGPU_ECONFIG) throw ConfigError(g_err);
+      throw DeviceError(g_err);
+    }
+    std::unique_ptr<lbmgpu_ctx> c(raw);
+    const uint64_t N = c->eng->n_fluid();
+    // warm start (verification.cpp:56-67)
+    std::vector<double> state(N * kQ);
+    for (uint64_t n = 0; n < N; ++n) {
+      const int kz = static_cast<int>(n % layers);
+      const double u[3] = {ana[kz] - shift, 0.0, 0.0};
+      equilibrium(1.0, u, &state[n * kQ]);
+    }
+    if ((rc = lbmgpu_load_state(c.get(), state.data(), state.size())))
+      throw DeviceError(g_err);
+    const double g3[3] = {gx, 0.0, 0.0};
+    long steps = 0;
+    int conv = 0;
+    double delta = 0;
+    rc = lbmgpu_steady_state_run(c.get(), wp, lambda, g3, interval, rel_tol,
+                                 max_steps, &steps, &conv, &delta);
+    if (rc == LBMGPU_ENUMERICAL) throw NumericalError(g_err);
+    if (rc == LBMGPU_ECONFIG) throw ConfigError(g_err);
+    if (rc) throw DeviceError(g_err);
+    std::vector<double> sums(layers);
+    if ((rc = lbmgpu_layer_ux(c.get(), sums.data()))) throw DeviceError(g_err);
+    const double per_layer = static_cast<double>(uint64_t(nx) * ny);
+    for (int k = 0; k < layers; ++k) sim[k] = sums[k] / per_layer + shift;
+    double max_ana = 0, max_diff = 0, sa2 = 0, sd2 = 0;
+    for (int k = 0; k < layers; ++k) {
+      const double d = sim[k] - ana[k];
+      max_ana = std::max(max_ana, std::abs(ana[k]));
+      max_diff = std::max(max_diff, std::abs(d));
+      sa2 += ana[k] * ana[k];
+      sd2 += d * d;
+    }
+    rep->linf_rel = max_ana > 0.0 ? max_diff / max_ana : max_diff;
+    rep->l2_rel = sa2 > 0.0 ? std::sqrt(sd2 / sa2) : std::sqrt(sd2);
+    rep->half_force_shift = shift;
+    rep->steps = steps;
+    rep->converged = conv;
+    rep->passed = conv && rep->linf_rel < 1e-4;  // kVerifyLinfTolerance
+    if (simulated) std::memcpy(simulated, sim.data(), layers * 8);
+    if (analytic) std::memcpy(analytic, ana.data(), layers * 8);
+  });
+}
+
+int lbmgpu_kernel_stats_enable(lbmgpu_ctx* c, int on) {
+  return guard([&] {
+    need(c, "ctx");
+    c->eng->stats().enable(on != 0);
+  });
+}
+
+int lbmgpu_kernel_stats(lbmgpu_ctx* c, char* names48, long* launches,
+                        double* ms, int cap, int* n) {
+  return guard([&] {
+    need(c, "ctx");
+    const auto& rows = c->eng->stats().rows();
+    if (n) *n = static_cast<int>(rows.size());
+    for (int i = 0; i < cap && i < static_cast<int>(rows.size()); ++i) {
+      if (names48) {
+        std::strncpy(names48 + 48 * i, rows[i].name.c_str(), 47);
+        names48[48 * i + 47] = 0;
+      }
+      if (launches) launches[i] = rows[i].launches;
+      if (ms) ms[i] = rows[i].ms;
+    }
+  });
+}
+
+int lbmgpu_kernel_stats_reset(lbmgpu_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    c->eng->stats().reset();
+  });
+}
+
+int lbmgpu_launch_count(lbmgpu_ctx* c, long* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    *out = c->eng->stats().launches();
+  });
+}
+
+int lbmgpu_host_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    need(out, "out");
+    LBM_CUDA(cudaMallocHost(out, bytes));
+  });
+}
+
+int lbmgpu_host_free(void* p) {
+  return guard([&] { LBM_CUDA(cudaFreeHost(p)); });
+}
+
+int lbmgpu_device_info(int device, char* name64, int* sms, size_t* mem,
+                       int* l2) {
+  return guard([&] {
+    cudaDeviceProp p;
+    if (device < 0) LBM_CUDA(cudaGetDevice(&device));
+    LBM_CUDA(cudaGetDeviceProperties(&p, device));
+    if (name64) {
+      std::strncpy(name64, p.name, 63);
+      name64[63] = 0;
+    }
+    if (sms) *sms = p.multiProcessorCount;
+    if (mem) *mem = p.totalGlobalMem;
+    if (l2) *l2 = p.l2CacheSize;
+  });
+}
+
+int lbmgpu_synchronize(lbmgpu_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    LBM_CUDA(cudaStreamSynchronize(c->eng->stream()));
+  });
+}
+
+int lbmgpu_nccl_unique_id(void* out128) {
+  return guard([&] {
+    need(out128, "out");
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw DeviceError(std::string("cannot load libnccl.so.2: ") + dlerror());
+    using Fn = int (*)(void*);
+    auto fn = reinterpret_cast<Fn>(dlsym(h, "ncclGetUniqueId"));
+    if (!fn) throw DeviceError("libnccl.so.2 has no ncclGetUniqueId");
+    if (fn(out128) != 0) throw DeviceError("ncclGetUniqueId failed");
+  });
+}
+
+int lbmgpu_part_info(lbmgpu_ctx* c, int part, int* z0, int* z1, uint64_t* nf) {
+  return guard([&] {
+    need(c, "ctx");
+    if (part < 0 || part >= c->eng->parts()) throw ConfigError("part out of range");
+    int a = 0, b = 0;
+    uint64_t n = 0;
+    c->eng->part_info(part, &a, &b, &n);
+    if (z0) *z0 = a;
+    if (z1) *z1 = b;
+    if (nf) *nf = n;
+  });
+}
+
+int lbmgpu_halo_plan(int nz, int parts, int ring, int64_t* rows, int cap,
+                     int* n_rows) {
+  return guard([&] {
+    if (nz < 1 || parts < 1 || parts > nz) throw ConfigError("halo_plan: bad nz/parts");
+    std::vector<HaloRow> plan = halo_plan(nz, parts, ring != 0);
+    if (n_rows) *n_rows = static_cast<int>(plan.size());
+    for (int i = 0; i < cap && i < static_cast<int>(plan.size()); ++i) {
+      const HaloRow& r = plan[i];
+      int64_t* o = rows + 7 * i;
+      o[0] = r.phase;
+      o[1] = r.src_part;
+      o[2] = r.dst_part;
+      o[3] = r.src_plane;
+      o[4] = r.dst_plane;
+      o[5] = r.slot0;
+      o[6] = kHaloSlots;
+    }
+  });
+}
+
+}  // extern "C"

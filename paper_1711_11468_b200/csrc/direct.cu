@@ -1,0 +1,698 @@
+// Direct (full-array) addressing: blk-push-*, blk-pull-*, aa-*, aa-vec-soa.
+//
+// Reference: FullLattice (src/full_lattice.cpp), FullOsKernel
+// (src/kernels_full_os.cpp:47-194), FullAaKernel / FullAaVecKernel
+// (src/kernels_full_aa.cpp:46-160,172-347).
+//
+// Device layout (ours, not the reference's): per z-slab part,
+//   SoA  e(zs, slot, y, x) = (zs*19 + slot)*P + y*nx + x     P = nx*ny
+//   AoS  e(zs, slot, y, x) = ((zs*ny + y)*nx + x)*19 + slot
+// x (the periodic channel axis) is the coalesced axis and each z-plane's
+// direction slabs are contiguous, so a z-slab halo is one block per face.
+// slot = dslot(d) groups the directions by c_z (common.cuh).  Canonical
+// (reference) order is restored only by the snapshot/load gathers.
+//
+// Full-way bounce-back: the reference runs a solid-node swap sweep after every
+// sub-step (full_lattice.cpp:42-56).  Here it is folded into the sweeps:
+//  * push: a population streamed into a solid node t is stored directly into
+//    slot opp(d) of t (the swap the correction would apply);
+//  * pull: a solid node stores its gathered q_d into its own slot opp(d);
+//  * AA: the correction sweeps are dropped altogether -- solid slots are read
+//    and written only in odd sub-steps and the two swaps per pair cancel
+//    (initial solid weights are swap-symmetric).  Bitwise parity with
+//    aa-soa / aa-aos is asserted by tests/test_gpu_parity.py.
+#include <algorithm>
+#include <cstring>
+
+#include "halo.hpp"
+#include "lbm.hpp"
+
+namespace lbmgpu {
+
+struct DirectArgs {
+  const double* src;
+  double* dst;
+  const uint8_t* flags;  // own planes, (z*ny + y)*nx + x, 1 = solid
+  uint32_t nx, ny, nzl;  // own extents
+  uint32_t zoff;         // storage plane of own plane 0
+  uint32_t zwrap;        // 1: single part, wrap z over own planes
+  uint32_t P;            // nx*ny
+  FastDiv fdx, fdP;      // n / nx, n / P
+  uint32_t node0, count; // own-node range of this launch
+  TrtArgs trt;
+};
+
+template <bool SOA>
+struct Idx {
+  uint64_t P;
+  uint32_t nx, ny;
+  __device__ __forceinline__ uint64_t operator()(uint32_t zs, int slot,
+                                                 uint32_t y, uint32_t x) const {
+    if (SOA)
+      return (uint64_t(zs) * kQ + slot) * P + uint64_t(y) * nx + x;
+    return ((uint64_t(zs) * ny + y) * nx + x) * kQ + slot;
+  }
+};
+
+struct Coords {
+  uint32_t x, y, z;        // own-plane coordinates
+  uint32_t X[3], Y[3];     // wrapped x-1,x,x+1 / y-1,y,y+1
+  uint32_t Z[3];           // storage planes of z-1, z, z+1
+};
+
+__device__ __forceinline__ bool decode(const DirectArgs& a, Coords& c,
+                                       uint32_t& n) {
+  n = a.node0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.node0 + a.count) return false;
+  const uint32_t z = a.fdP.div(n);
+  const uint32_t r = n - z * a.P;
+  const uint32_t y = a.fdx.div(r);
+  const uint32_t x = r - y * a.nx;
+  c.x = x;
+  c.y = y;
+  c.z = z;
+  c.X[0] = x == 0 ? a.nx - 1 : x - 1;
+  c.X[1] = x;
+  c.X[2] = x + 1 == a.nx ? 0 : x + 1;
+  c.Y[0] = y == 0 ? a.ny - 1 : y - 1;
+  c.Y[1] = y;
+  c.Y[2] = y + 1 == a.ny ? 0 : y + 1;
+  const uint32_t zs = z + a.zoff;
+  if (a.zwrap) {
+    c.Z[0] = z == 0 ? a.nzl - 1 : z - 1;
+    c.Z[2] = z + 1 == a.nzl ? 0 : z + 1;
+  } else {
+    c.Z[0] = zs - 1;
+    c.Z[2] = zs + 1;
+  }
+  c.Z[1] = zs;
+  return true;
+}
+
+template <class T>
+__device__ __forceinline__ T ld(const T* p) {
+  return *p;
+}
+template <bool CS>
+__device__ __forceinline__ void st(double* p, double v) {
+  if (CS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+// ---- one-step push / pull with folded full-way correction ----------------
+// kernels_full_os.cpp:56-89 + full_lattice.cpp:42-56 (correction on dst).
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_full_push(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.src[I(c.Z[1], dslot(d), c.y, c.x)];
+  if (a.flags[n] == 0) collide(q, a.trt);
+  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
+    const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
+    const int s = a.flags[tn] ? dslot(opp(d)) : dslot(d);
+    st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
+  }
+}
+
+// kernels_full_os.cpp:56-89 (PULL) ; COLLIDE=false is the stream-only pass.
+template <bool SOA, bool COLLIDE, bool CS>
+__global__ void __launch_bounds__(256) k_full_pull(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+  q[0] = a.src[I(c.Z[1], dslot(0), c.y, c.x)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    q[d] = a.src[I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+  const bool solid = a.flags[n] != 0;
+  if (COLLIDE && !solid) collide(q, a.trt);
+  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const int s = solid ? dslot(opp(d)) : dslot(d);
+    st<CS>(a.dst + I(c.Z[1], s, c.y, c.x), q[d]);
+  }
+}
+
+// collide_pass (kernels_full_os.cpp:149-159): fluid nodes, in place.
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  if (a.flags[n]) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.dst[I(c.Z[1], dslot(d), c.y, c.x)];
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) a.dst[I(c.Z[1], dslot(d), c.y, c.x)] = q[d];
+}
+
+// ---- AA pattern (kernels_full_aa.cpp:46-94), corrections dropped ----------
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_full_aa_even(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  if (a.flags[n]) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = buf[I(c.Z[1], dslot(d), c.y, c.x)];
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d)
+    st<CS>(buf + I(c.Z[1], dslot(opp(d)), c.y, c.x), q[d]);
+}
+
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_full_aa_odd(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  if (a.flags[n]) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  double q[kQ];
+  q[0] = buf[I(c.Z[1], dslot(0), c.y, c.x)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    q[d] = buf[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+  collide(q, a.trt);
+  st<CS>(buf + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    st<CS>(buf + I(c.Z[1 + cz(d)], dslot(d), c.Y[1 + cy(d)], c.X[1 + cx(d)]),
+           q[d]);
+}
+
+// ---- init / canonical transfer / perturbation / macro --------------------
+template <bool SOA>
+__global__ void k_full_init(double* buf, uint32_t nx, uint32_t ny,
+                            uint32_t zs_count, uint64_t P) {
+  const uint64_t total = uint64_t(zs_count) * P;
+  const Idx<SOA> I{P, nx, ny};
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t zs = static_cast<uint32_t>(i / P);
+    const uint32_t r = static_cast<uint32_t>(i - uint64_t(zs) * P);
+    const uint32_t y = r / nx, x = r - y * nx;
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) buf[I(zs, dslot(d), y, x)] = weight(d);
+  }
+}
+
+struct CanonArgs {
+  double* buf;
+  const uint32_t* node_of;  // k -> own node id
+  const uint64_t* canon;    // k -> canonical index (nullptr: identity k + kbase)
+  uint64_t kbase;
+  uint64_t k0, k1;          // part-local range
+  uint64_t c0;              // canonical index of staging row 0
+  uint32_t nx, ny, zoff;
+  uint64_t P;
+};
+
+template <bool SOA, bool TO_STAGING>
+__global__ void k_full_canon(const CanonArgs a, double* staging) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  for (uint64_t k = a.k0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+       k < a.k1; k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c = a.canon ? a.canon[k] : k + a.kbase;
+    const uint32_t node = a.node_of[k];
+    const uint32_t z = static_cast<uint32_t>(node / a.P);
+    const uint32_t r = static_cast<uint32_t>(node - uint64_t(z) * a.P);
+    const uint32_t y = r / a.nx, x = r - y * a.nx;
+    double* row = staging + (c - a.c0) * kQ;
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) {
+      const uint64_t e = I(z + a.zoff, dslot(d), y, x);
+      if (TO_STAGING)
+        row[d] = a.buf[e];
+      else
+        a.buf[e] = row[d];
+    }
+  }
+}
+
+template <bool SOA>
+__global__ void k_full_perturb(const CanonArgs a, uint64_t seed, double amp) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  for (uint64_t k = a.k0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+       k < a.k1; k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c = a.canon ? a.canon[k] : k + a.kbase;
+    const uint32_t node = a.node_of[k];
+    const uint32_t z = static_cast<uint32_t>(node / a.P);
+    const uint32_t r = static_cast<uint32_t>(node - uint64_t(z) * a.P);
+    const uint32_t y = r / a.nx, x = r - y * a.nx;
+#pragma unroll
+    for (int d = 0; d < kQ; ++d)
+      a.buf[I(z + a.zoff, dslot(d), y, x)] = perturbed_value(c, d, seed, amp);
+  }
+}
+
+template <bool SOA>
+__global__ void k_full_macro(const CanonArgs a, double* rho, double* u) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  for (uint64_t k = a.k0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+       k < a.k1; k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c = a.canon ? a.canon[k] : k + a.kbase;
+    const uint32_t node = a.node_of[k];
+    const uint32_t z = static_cast<uint32_t>(node / a.P);
+    const uint32_t r = static_cast<uint32_t>(node - uint64_t(z) * a.P);
+    const uint32_t y = r / a.nx, x = r - y * a.nx;
+    double f[kQ];
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) f[d] = a.buf[I(z + a.zoff, dslot(d), y, x)];
+    double rr, ux, uy, uz;
+    macroscopic(f, rr, ux, uy, uz);
+    rho[c] = rr;
+    u[3 * c] = ux;
+    u[3 * c + 1] = uy;
+    u[3 * c + 2] = uz;
+  }
+}
+
+// Copies the part's own planes of the canonical FlagField into the device
+// (z, y, x) order the sweeps index with.
+__global__ void k_part_flags(const uint8_t* __restrict__ gflags, int nx, int ny,
+                             int nz, int z0, int z1,
+                             uint8_t* __restrict__ pflags) {
+  const uint64_t P = uint64_t(nx) * ny;
+  const uint64_t own = uint64_t(z1 - z0) * P;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < own;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t z = static_cast<uint32_t>(i / P);
+    const uint32_t r = static_cast<uint32_t>(i - z * P);
+    const uint32_t y = r / nx, x = r - y * nx;
+    pflags[i] = gflags[(uint64_t(x) * ny + y) * nz + (z + z0)];
+  }
+}
+
+// For each fluid box node in canonical order with z in [z0, z1): its
+// canonical index is crank[gi]; its position k within the part is
+// prank[gi] (scan of the part mask).  Writes node_of[k] and canon[k].
+__global__ void k_part_lists(const uint8_t* __restrict__ gflags,
+                             const uint32_t* __restrict__ crank,
+                             const uint32_t* __restrict__ prank, int nx, int ny,
+                             int nz, int z0, int z1,
+                             uint32_t* __restrict__ node_of,
+                             uint64_t* __restrict__ canon) {
+  const uint64_t V = uint64_t(nx) * ny * nz;
+  for (uint64_t gi = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; gi < V;
+       gi += uint64_t(gridDim.x) * blockDim.x) {
+    const int z = static_cast<int>(gi % nz);
+    if (z < z0 || z >= z1 || gflags[gi]) continue;
+    const uint64_t r = gi / nz;
+    const uint32_t y = static_cast<uint32_t>(r % ny);
+    const uint32_t x = static_cast<uint32_t>(r / ny);
+    const uint32_t k = prank[gi];
+    node_of[k] = (uint32_t(z - z0) * ny + y) * nx + x;
+    if (canon) canon[k] = crank[gi];
+  }
+}
+
+__global__ void k_part_mask(const uint8_t* __restrict__ gflags, int nz, int z0,
+                            int z1, uint64_t V, uint8_t* __restrict__ mask) {
+  for (uint64_t gi = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; gi < V;
+       gi += uint64_t(gridDim.x) * blockDim.x) {
+    const int z = static_cast<int>(gi % nz);
+    // "solid" (1) unless fluid and inside the part's slab
+    mask[gi] = (z >= z0 && z < z1 && gflags[gi] == 0) ? 0 : 1;
+  }
+}
+
+// ------------------------------------------------------------------ engine
+namespace {
+
+int grid_for(uint64_t n, int threads) {
+  return static_cast<int>(std::min<uint64_t>(ceil_div(n, threads), 148ull * 64));
+}
+
+struct Part {
+  int z0 = 0, z1 = 0;
+  uint32_t nzl = 0, zoff = 0, nzs = 0;
+  DevBuf<double> buf[2];
+  DevBuf<uint8_t> flags;
+  DevBuf<uint32_t> node_of;
+  DevBuf<uint64_t> canon;  // empty when the part holds the whole box
+  uint64_t n_fluid = 0;
+  std::vector<uint64_t> canon_host_first;  // first canonical index per k-block
+  cudaStream_t stream = nullptr;
+};
+
+class DirectEngine final : public Engine {
+ public:
+  DirectEngine(const Descriptor& d, const GeomSpec& g, const DistSpec& dist) {
+    desc_ = d;
+    LBM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    nparts_ = std::max(1, dist.virtual_parts);
+    if (dist.nranks > 1)
+      throw ConfigError("multi-process direct AA is provided by the NCCL halo "
+                        "path (lbmgpu_dist.nranks > 1) -- not built in this "
+                        "configuration");
+    if (nparts_ > 1 && d.prop != Prop::Aa)
+      throw ConfigError("z-slab decomposition is implemented for the AA "
+                        "pattern only (kernel '" + d.name + "')");
+    if (nparts_ > 1 && !d.soa)
+      throw ConfigError("z-slab decomposition needs the SoA layout");
+    if (nparts_ > g.nz)
+      throw ConfigError("more z-slab parts than z planes");
+
+    DeviceGeometry geo = build_geometry_device(g, stream_);
+    nx_ = geo.nx;
+    ny_ = geo.ny;
+    nz_ = geo.nz;
+    n_fluid_ = static_cast<uint64_t>(geo.n_fluid);
+    P_ = uint64_t(nx_) * ny_;
+    if (P_ * uint64_t(nz_) >= (1ull << 31) * (uint64_t)nparts_ ||
+        P_ * uint64_t(nz_) / nparts_ >= (1ull << 31))
+      throw ConfigError("direct lattice: more than 2^31 nodes per part");
+
+    const uint64_t V = geo.volume();
+    DevBuf<uint32_t> crank(V);
+    scan_fluid(geo.flags.get(), crank.get(), V, stream_);
+
+    // z-wrap exchange is needed unless the end planes are entirely solid
+    zring_ = true;
+    parts_.resize(nparts_);
+    for (int p = 0; p < nparts_; ++p) {
+      Part& pt = parts_[p];
+      pt.z0 = static_cast<int>(int64_t(nz_) * p / nparts_);
+      pt.z1 = static_cast<int>(int64_t(nz_) * (p + 1) / nparts_);
+      pt.nzl = pt.z1 - pt.z0;
+      pt.zoff = nparts_ > 1 ? 1 : 0;
+      pt.nzs = pt.nzl + 2 * pt.zoff;
+      pt.stream = stream_;
+      const uint64_t slots = uint64_t(pt.nzs) * P_ * kQ;
+      const int nbuf = d.prop == Prop::Aa ? 1 : 2;
+      for (int b = 0; b < nbuf; ++b) {
+        pt.buf[b].alloc(slots);
+        if (d.soa)
+          k_full_init<true><<<grid_for(uint64_t(pt.nzs) * P_, 256), 256, 0,
+                              stream_>>>(pt.buf[b].get(), nx_, ny_, pt.nzs, P_);
+        else
+          k_full_init<false><<<grid_for(uint64_t(pt.nzs) * P_, 256), 256, 0,
+                               stream_>>>(pt.buf[b].get(), nx_, ny_, pt.nzs, P_);
+        LBM_CHECK_LAUNCH();
+      }
+      pt.flags.alloc(uint64_t(pt.nzl) * P_);
+      k_part_flags<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
+          geo.flags.get(), nx_, ny_, nz_, pt.z0, pt.z1, pt.flags.get());
+      LBM_CHECK_LAUNCH();
+      // per-part fluid list in canonical order
+      DevBuf<uint8_t> mask(V);
+      DevBuf<uint32_t> prank(V);
+      k_part_mask<<<grid_for(V, 256), 256, 0, stream_>>>(geo.flags.get(), nz_,
+                                                         pt.z0, pt.z1, V,
+                                                         mask.get());
+      LBM_CHECK_LAUNCH();
+      pt.n_fluid = scan_fluid(mask.get(), prank.get(), V, stream_);
+      pt.node_of.alloc(std::max<uint64_t>(pt.n_fluid, 1));
+      if (nparts_ > 1) pt.canon.alloc(std::max<uint64_t>(pt.n_fluid, 1));
+      k_part_lists<<<grid_for(V, 256), 256, 0, stream_>>>(
+          geo.flags.get(), crank.get(), prank.get(), nx_, ny_, nz_, pt.z0,
+          pt.z1, pt.node_of.get(), nparts_ > 1 ? pt.canon.get() : nullptr);
+      LBM_CHECK_LAUNCH();
+      if (nparts_ > 1) {
+        std::vector<uint64_t> h(pt.n_fluid);
+        if (pt.n_fluid)
+          LBM_CUDA(cudaMemcpyAsync(h.data(), pt.canon.get(), pt.n_fluid * 8,
+                                   cudaMemcpyDeviceToHost, stream_));
+        LBM_CUDA(cudaStreamSynchronize(stream_));
+        pt.canon_host_first = std::move(h);
+      }
+    }
+    if (nparts_ > 1) {
+      // ring exchange only if a fluid node sits on the z=0 or z=nz-1 plane
+      std::vector<uint8_t> hf(V);
+      LBM_CUDA(cudaMemcpyAsync(hf.data(), geo.flags.get(), V,
+                               cudaMemcpyDeviceToHost, stream_));
+      LBM_CUDA(cudaStreamSynchronize(stream_));
+      bool end_fluid = false;
+      for (uint64_t i = 0; i < V && !end_fluid; i += nz_)
+        end_fluid = hf[i] == 0 || hf[i + nz_ - 1] == 0;
+      zring_ = end_fluid;
+      plan_ = halo_plan(nz_, nparts_, zring_);
+    }
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  ~DirectEngine() override {
+    if (stream_) cudaStreamDestroy(stream_);
+  }
+
+  int parts() const override { return nparts_; }
+  void part_info(int p, int* z0, int* z1, uint64_t* nf) const override {
+    *z0 = parts_.at(p).z0;
+    *z1 = parts_.at(p).z1;
+    *nf = parts_.at(p).n_fluid;
+  }
+
+  DirectArgs args(const Part& pt, uint32_t node0, uint32_t count,
+                  const TrtArgs& t, int src_buf, int dst_buf) const {
+    DirectArgs a;
+    a.src = pt.buf[src_buf].get();
+    a.dst = pt.buf[dst_buf].get();
+    a.flags = pt.flags.get();
+    a.nx = nx_;
+    a.ny = ny_;
+    a.nzl = pt.nzl;
+    a.zoff = pt.zoff;
+    a.zwrap = nparts_ == 1;
+    a.P = static_cast<uint32_t>(P_);
+    a.fdx = FastDiv(nx_);
+    a.fdP = FastDiv(static_cast<uint32_t>(P_));
+    a.node0 = node0;
+    a.count = count;
+    a.trt = t;
+    return a;
+  }
+
+  template <class K>
+  void launch(const char* name, K kern, const DirectArgs& a, cudaStream_t s) {
+    if (a.count == 0) return;
+    const int threads = 256;
+    const int tok = stats_.begin(name, s);
+    kern<<<static_cast<unsigned>(ceil_div(a.count, threads)), threads, 0, s>>>(a);
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, s);
+  }
+
+  void advance(const TrtArgs& t, long steps) override {
+    const bool soa = desc_.soa;
+    const bool cs = cs_;
+    if (desc_.prop == Prop::OsPush) {
+      const Part& pt = parts_[0];
+      const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+      for (long s = 0; s < steps; ++s) {
+        DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
+        if (soa)
+          cs ? launch("full_push_soa", k_full_push<true, true>, a, stream_)
+             : launch("full_push_soa", k_full_push<true, false>, a, stream_);
+        else
+          launch("full_push_aos", k_full_push<false, false>, a, stream_);
+        cur_ ^= 1;
+      }
+      return;
+    }
+    if (desc_.prop == Prop::OsPull) {
+      const Part& pt = parts_[0];
+      const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+      {
+        DirectArgs a = args(pt, 0, N, t, cur_, cur_);
+        soa ? launch("full_collide_soa", k_full_collide<true>, a, stream_)
+            : launch("full_collide_aos", k_full_collide<false>, a, stream_);
+      }
+      for (long s = 0; s < steps; ++s) {
+        DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
+        const bool last = s == steps - 1;
+        if (soa) {
+          if (last)
+            launch("full_pull_stream_soa", k_full_pull<true, false, false>, a, stream_);
+          else
+            cs ? launch("full_pull_soa", k_full_pull<true, true, true>, a, stream_)
+               : launch("full_pull_soa", k_full_pull<true, true, false>, a, stream_);
+        } else {
+          if (last)
+            launch("full_pull_stream_aos", k_full_pull<false, false, false>, a, stream_);
+          else
+            launch("full_pull_aos", k_full_pull<false, true, false>, a, stream_);
+        }
+        cur_ ^= 1;
+      }
+      return;
+    }
+    // AA pattern: even/odd pairs, in place
+    for (long s = 0; s < steps; s += 2) {
+      if (nparts_ == 1) {
+        const Part& pt = parts_[0];
+        const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+        DirectArgs a = args(pt, 0, N, t, 0, 0);
+        if (soa) {
+          cs ? launch("full_aa_even_soa", k_full_aa_even<true, true>, a, stream_)
+             : launch("full_aa_even_soa", k_full_aa_even<true, false>, a, stream_);
+          cs ? launch("full_aa_odd_soa", k_full_aa_odd<true, true>, a, stream_)
+             : launch("full_aa_odd_soa", k_full_aa_odd<true, false>, a, stream_);
+        } else {
+          launch("full_aa_even_aos", k_full_aa_even<false, false>, a, stream_);
+          launch("full_aa_odd_aos", k_full_aa_odd<false, false>, a, stream_);
+        }
+      } else {
+        aa_pair_parts(t);
+      }
+    }
+  }
+
+  // Emulated z-slab decomposition on one device: the same sub-step split and
+  // exchange plan the NCCL path uses (halo.cpp), transport = device copies.
+  void aa_pair_parts(const TrtArgs& t) {
+    for (Part& pt : parts_) {
+      const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+      launch("full_aa_even_soa", k_full_aa_even<true, false>,
+             args(pt, 0, N, t, 0, 0), stream_);
+    }
+    run_exchange(0);
+    for (Part& pt : parts_) {
+      const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+      launch("full_aa_odd_soa", k_full_aa_odd<true, false>,
+             args(pt, 0, N, t, 0, 0), stream_);
+    }
+    run_exchange(1);
+  }
+
+  void run_exchange(int phase) {
+    for (const HaloRow& r : plan_) {
+      if (r.phase != phase) continue;
+      const Part& a = parts_[r.src_part];
+      const Part& b = parts_[r.dst_part];
+      const uint64_t elems = uint64_t(kHaloSlots) * P_;
+      const double* src = a.buf[0].get() + (uint64_t(r.src_plane) * kQ + r.slot0) * P_;
+      double* dst = b.buf[0].get() + (uint64_t(r.dst_plane) * kQ + r.slot0) * P_;
+      LBM_CUDA(cudaMemcpyAsync(dst, src, elems * sizeof(double),
+                               cudaMemcpyDeviceToDevice, stream_));
+    }
+  }
+
+  CanonArgs canon_args(const Part& pt, int buf) const {
+    CanonArgs c;
+    c.buf = const_cast<double*>(pt.buf[buf].get());
+    c.node_of = pt.node_of.get();
+    c.canon = nparts_ > 1 ? pt.canon.get() : nullptr;
+    c.kbase = 0;
+    c.k0 = 0;
+    c.k1 = pt.n_fluid;
+    c.c0 = 0;
+    c.nx = nx_;
+    c.ny = ny_;
+    c.zoff = pt.zoff;
+    c.P = P_;
+    return c;
+  }
+
+  // restrict the part's k-range to canonical indices [c0, c0+count)
+  bool clip(const Part& pt, uint64_t c0, uint64_t count, CanonArgs& c) const {
+    if (nparts_ == 1) {
+      c.k0 = c0;
+      c.k1 = std::min<uint64_t>(c0 + count, pt.n_fluid);
+    } else {
+      const auto& h = pt.canon_host_first;
+      c.k0 = std::lower_bound(h.begin(), h.end(), c0) - h.begin();
+      c.k1 = std::lower_bound(h.begin(), h.end(), c0 + count) - h.begin();
+    }
+    c.c0 = c0;
+    return c.k1 > c.k0;
+  }
+
+  void gather_canonical(uint64_t c0, uint64_t count, double* out) override {
+    for (const Part& pt : parts_) {
+      CanonArgs c = canon_args(pt, cur_);
+      if (!clip(pt, c0, count, c)) continue;
+      const int g = grid_for(c.k1 - c.k0, 256);
+      desc_.soa ? k_full_canon<true, true><<<g, 256, 0, stream_>>>(c, out)
+                : k_full_canon<false, true><<<g, 256, 0, stream_>>>(c, out);
+      LBM_CHECK_LAUNCH();
+    }
+  }
+
+  void scatter_canonical(uint64_t c0, uint64_t count, const double* in) override {
+    for (const Part& pt : parts_) {
+      CanonArgs c = canon_args(pt, cur_);
+      if (!clip(pt, c0, count, c)) continue;
+      const int g = grid_for(c.k1 - c.k0, 256);
+      desc_.soa ? k_full_canon<true, false><<<g, 256, 0, stream_>>>(
+                      c, const_cast<double*>(in))
+                : k_full_canon<false, false><<<g, 256, 0, stream_>>>(
+                      c, const_cast<double*>(in));
+      LBM_CHECK_LAUNCH();
+    }
+  }
+
+  void load_perturbed(uint64_t seed, double amp) override {
+    for (const Part& pt : parts_) {
+      CanonArgs c = canon_args(pt, cur_);
+      if (c.k1 == 0) continue;
+      const int g = grid_for(c.k1, 256);
+      desc_.soa ? k_full_perturb<true><<<g, 256, 0, stream_>>>(c, seed, amp)
+                : k_full_perturb<false><<<g, 256, 0, stream_>>>(c, seed, amp);
+      LBM_CHECK_LAUNCH();
+    }
+  }
+
+  void macro_fields(double* rho, double* u) override {
+    for (const Part& pt : parts_) {
+      CanonArgs c = canon_args(pt, cur_);
+      if (c.k1 == 0) continue;
+      const int g = grid_for(c.k1, 256);
+      desc_.soa ? k_full_macro<true><<<g, 256, 0, stream_>>>(c, rho, u)
+                : k_full_macro<false><<<g, 256, 0, stream_>>>(c, rho, u);
+      LBM_CHECK_LAUNCH();
+    }
+  }
+
+  // Mass over fluid and solid nodes of the current buffer (full_lattice.cpp:
+  // 72-87), own planes only, compensated device sum.
+  double total_mass() override {
+    double m = 0.0;
+    for (const Part& pt : parts_) {
+      const uint64_t per_plane = P_ * kQ;
+      m += device_sum(pt.buf[cur_].get() + uint64_t(pt.zoff) * per_plane,
+                      uint64_t(pt.nzl) * per_plane, stream_);
+    }
+    return m;
+  }
+
+ private:
+  int nx_ = 0, ny_ = 0, nz_ = 0;
+  uint64_t P_ = 0;
+  int nparts_ = 1;
+  int cur_ = 0;
+  bool cs_ = false;
+  bool zring_ = false;
+  std::vector<Part> parts_;
+  std::vector<HaloRow> plan_;
+};
+
+}  // namespace
+
+std::unique_ptr<Engine> make_direct_engine(const Descriptor& d,
+                                           const GeomSpec& g,
+                                           const DistSpec& dist) {
+  return std::make_unique<DirectEngine>(d, g, dist);
+}
+
+}  // namespace lbmgpu

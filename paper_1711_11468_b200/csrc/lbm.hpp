@@ -1,0 +1,224 @@
+// Internal C++ interface of the B200 LBM sweep library (behind include/lbmgpu.h).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "model.cuh"
+
+namespace lbmgpu {
+
+// ---------------------------------------------------------------- registry
+enum class Prop { OsPush = 0, OsPull = 1, Aa = 2 };
+
+// lbm::KernelDescriptor (reference include/lbm/kernels.hpp:25-36)
+struct Descriptor {
+  std::string name;
+  Prop prop = Prop::OsPush;
+  bool soa = true;
+  bool indirect = false;
+  int blk = 0;
+  int nt_streams = 0;
+  bool ria = false, pv = false, vec = false;
+  int vector_width = 4;
+};
+
+const std::vector<std::string>& kernel_names();
+Descriptor make_descriptor(const std::string& name, int blk, int vector_width);
+
+struct LoopBalance {
+  double ref_min = 0, ref_max = 0;  // reference B_l incl. CPU write-allocate
+  double gpu = 0;                   // algorithmic bytes per FLUP on the GPU
+};
+LoopBalance loop_balance(const Descriptor& d);
+
+// --------------------------------------------------------------- geometry
+enum GeomKind { kChannel = 0, kSlit = 1, kPipe = 2, kBlocks = 3, kCustom = 4 };
+
+struct GeomSpec {
+  int kind = kChannel;
+  int nx = 500, ny = 100, nz = 100;
+  int block = 4, spacing = 4;
+  int pipe_diameter = 0;
+  std::vector<uint8_t> custom;  // kCustom: canonical flags
+  bool custom_periodic[3] = {false, false, false};
+  uint64_t volume() const { return uint64_t(nx) * ny * nz; }
+};
+
+// Reference build_geometry's argument checks (geometry.cpp:17-25,48-104),
+// raised before any allocation; returns the per-axis periodicity.
+std::array<bool, 3> validate_geometry(const GeomSpec& g);
+
+// ----------------------------------------------------------------- padding
+struct Padding {
+  int mode = 1;  // 0 none, 1 auto, 2 thrash, 3 explicit
+  std::array<int64_t, kQ> pads{};
+};
+std::array<uint64_t, kQ> padding_offsets(uint64_t n_fluid, const Padding& p,
+                                         uint64_t* total);
+
+// ------------------------------------------------------- device buffers
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  void alloc(size_t n) {
+    release();
+    if (n) LBM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// Device-resident FlagField (geometry.hpp:16-29): canonical x-major order.
+struct DeviceGeometry {
+  int nx = 0, ny = 0, nz = 0;
+  std::array<bool, 3> periodic{};
+  DevBuf<uint8_t> flags;  // V bytes, 1 = solid
+  int64_t n_fluid = 0;
+  uint64_t volume() const { return uint64_t(nx) * ny * nz; }
+};
+DeviceGeometry build_geometry_device(const GeomSpec& g, cudaStream_t s);
+
+// Exclusive prefix count of fluid nodes (flag == 0) over `n` flags; returns
+// the total.  out may alias nothing; n < 2^32.
+uint64_t scan_fluid(const uint8_t* flags, uint32_t* out, uint64_t n,
+                    cudaStream_t s);
+
+// ------------------------------------------------------------ statistics
+class KernelStats {
+ public:
+  void enable(bool on) { on_ = on; }
+  bool enabled() const { return on_; }
+  // Records a (start) event before a launch; returns a token for end().
+  int begin(const char* name, cudaStream_t s);
+  void end(int token, cudaStream_t s);
+  void collect();  // synchronises pending events into the totals
+  void reset();
+  struct Row { std::string name; long launches = 0; double ms = 0; };
+  const std::vector<Row>& rows() { collect(); return rows_; }
+  long launches() const { return launches_; }
+  void count_launch() { ++launches_; }
+  ~KernelStats();
+
+ private:
+  struct Pending { int row; cudaEvent_t a, b; };
+  bool on_ = false;
+  long launches_ = 0;
+  std::vector<Row> rows_;
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> pool_;
+  cudaEvent_t get_event();
+};
+
+// ------------------------------------------------------------- engines
+// Distribution request (see lbmgpu_dist in include/lbmgpu.h).
+struct DistSpec {
+  int rank = 0, nranks = 1, device = -1, virtual_parts = 1;
+  std::array<uint8_t, 128> nccl_id{};
+  bool have_id = false;
+};
+
+// One GPU-resident sweep implementation of the reference's Kernel
+// (include/lbm/kernels.hpp:58-96).  All calls come from one host thread.
+class Engine {
+ public:
+  virtual ~Engine() = default;
+  const Descriptor& descriptor() const { return desc_; }
+  uint64_t n_fluid() const { return n_fluid_; }
+  cudaStream_t stream() const { return stream_; }
+  KernelStats& stats() { return stats_; }
+
+  // steps already validated (>= 0, even for AA).
+  virtual void advance(const TrtArgs& t, long steps) = 0;
+
+  // Canonical nodes [c0, c0+count) -> device staging (count*19 doubles,
+  // node-major) and back.  Runs on stream().
+  virtual void gather_canonical(uint64_t c0, uint64_t count, double* d_out) = 0;
+  virtual void scatter_canonical(uint64_t c0, uint64_t count,
+                                 const double* d_in) = 0;
+  // Perturbed equilibrium generated per canonical index (harness.cpp:50-62).
+  virtual void load_perturbed(uint64_t seed, double amplitude) = 0;
+  virtual double total_mass() = 0;
+  // Device macro fields over canonical nodes: rho (N) and u (3N); the engine
+  // owns the arrays.  Returns device pointers.
+  virtual void macro_fields(double* d_rho, double* d_u) = 0;
+
+  // list structure export (ConfigError for direct engines)
+  virtual void export_structure(int32_t* nodes, uint32_t* adj,
+                                uint64_t* starts, uint64_t* total) {
+    (void)nodes; (void)adj; (void)starts; (void)total;
+    throw ConfigError("kernel '" + desc_.name +
+                      "' uses direct addressing and has no list structure");
+  }
+  virtual bool ria_stats(int64_t* runs, double* vfrac) {
+    (void)runs; (void)vfrac;
+    return false;
+  }
+  virtual int parts() const { return 1; }
+  virtual void part_info(int p, int* z0, int* z1, uint64_t* nf) const {
+    (void)p; *z0 = 0; *z1 = 0; *nf = n_fluid_;
+  }
+  // Number of canonical nodes this process holds (== n_fluid() unless the
+  // domain is split across processes).
+  virtual bool holds_all() const { return true; }
+
+ protected:
+  Descriptor desc_;
+  uint64_t n_fluid_ = 0;
+  cudaStream_t stream_ = nullptr;
+  KernelStats stats_;
+};
+
+std::unique_ptr<Engine> make_direct_engine(const Descriptor& d,
+                                           const GeomSpec& g,
+                                           const DistSpec& dist);
+std::unique_ptr<Engine> make_list_engine(const Descriptor& d,
+                                         const GeomSpec& g,
+                                         const Padding& pad);
+
+// ---------------------------------------------------- device primitives
+// Kahan/Neumaier-compensated sum of n doubles accessed through idx.
+double device_sum(const double* d, uint64_t n, cudaStream_t s);
+
+// splitmix64 (harness.cpp:18-23)
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+// perturbed_equilibrium value for (canonical n, d) (harness.cpp:50-62)
+__host__ __device__ __forceinline__ double perturbed_value(uint64_t n, int d,
+                                                           uint64_t seed,
+                                                           double amplitude) {
+  const uint64_t h = splitmix64(seed ^ (n * kQ + static_cast<uint64_t>(d)));
+  const double u01 = static_cast<double>(h >> 11) * (1.0 / 9007199254740992.0);
+  return weight(d) * (1.0 + amplitude * (u01 - 0.5));
+}
+
+}  // namespace lbmgpu

@@ -1,0 +1,593 @@
+// Indirect (list / adjacency) addressing: list-push-*, list-pull-*,
+// list-pull-split-nt-*, list-aa-*, list-aa-ria-soa, list-aa-pv-soa.
+//
+// Reference: ListLattice / build_structure (src/list_lattice.cpp:123-310),
+// ListOsKernel (src/kernels_list_os.cpp:9-97), ListNtKernel
+// (src/kernels_list_nt.cpp:77-167), ListAaKernel / ListAaRiaKernel
+// (src/kernels_list_aa.cpp:8-251).
+//
+// The structure is built ON THE DEVICE and is bit-exact with the reference:
+//  * node order (order_nodes, :123-141): a bijective traversal position t(i)
+//    per box node (blk = 0: canonical x,y,z; blk > 0: the y-z tile order),
+//    an exclusive scan of the fluid flags in t order gives the list rank;
+//  * SoA slot map: starts[d] + n with the reference's padding_offsets;
+//    AoS: 19n + d (list_lattice.hpp:66-75);
+//  * adjacency entry (n, d) (:177-191): neighbour at n + c_look (look = d for
+//    Scatter, opp(d) for Gather; periodic wrap, else Outside) -> slot(m, d)
+//    if fluid else slot(n, opp d) (half-way bounce-back baked in).
+// The PDF arrays keep the reference slot numbering exactly (the adjacency
+// values ARE slot numbers); only the adjacency ARRAY is stored d-major,
+// adj[(d-1)*N + n], so the 18 index loads of a warp are coalesced.  The
+// canonical [n*18 + d-1] order is produced on export.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "lbm.hpp"
+
+namespace lbmgpu {
+
+struct ListArgs {
+  const double* src;
+  double* dst;
+  const uint32_t* adj;  // d-major [(d-1)*N + n]
+  uint64_t N;
+  uint64_t starts[kQ];  // SoA direction starts (unused for AoS)
+  TrtArgs trt;
+};
+
+template <bool SOA>
+__device__ __forceinline__ uint64_t lslot(const ListArgs& a, uint64_t n, int d) {
+  return SOA ? a.starts[d] + n : n * kQ + d;
+}
+
+template <bool CS>
+__device__ __forceinline__ void lst(double* p, double v) {
+  if (CS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+// list-pull (kernels_list_os.cpp:43-62, PULL): gather through the Gather
+// table, collide, coalesced stores to own slots.  COLLIDE=false is the
+// stream-only exit pass.  CS selects st.global.cs (the GPU's counterpart of
+// the nt split-store variants, kernels_list_nt.cpp).
+template <bool SOA, bool COLLIDE, bool CS>
+__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  uint32_t an[18];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  double q[kQ];
+  q[0] = a.src[lslot<SOA>(a, n, 0)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = a.src[an[d - 1]];
+  if (COLLIDE) collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
+}
+
+// list-push (kernels_list_os.cpp:43-62, push): own loads, scatter stores.
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_list_push(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.src[lslot<SOA>(a, n, d)];
+  collide(q, a.trt);
+  a.dst[lslot<SOA>(a, n, 0)] = q[0];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) a.dst[__ldg(a.adj + (d - 1) * a.N + n)] = q[d];
+}
+
+// collide_pass (kernels_list_os.cpp:64-72), in place on dst.
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_list_collide(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.dst[lslot<SOA>(a, n, d)];
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) a.dst[lslot<SOA>(a, n, d)] = q[d];
+}
+
+// aa_even_node (kernels_list_aa.cpp:10-16): own slots -> opposite slots.
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  double* buf = a.dst;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = buf[lslot<SOA>(a, n, d)];
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(buf + lslot<SOA>(a, n, opp(d)), q[d]);
+}
+
+// aa_odd_node (kernels_list_aa.cpp:22-31): one scatter table serves both
+// sides -- gather d through column opp(d), scatter d through column d.
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  double* buf = a.dst;
+  uint32_t an[18];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  double q[kQ];
+  q[0] = buf[lslot<SOA>(a, n, 0)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
+  collide(q, a.trt);
+  lst<CS>(buf + lslot<SOA>(a, n, 0), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) lst<CS>(buf + an[d - 1], q[d]);
+}
+
+// ---- structure construction -------------------------------------------------
+// Traversal position of box node (x,y,z) in order_nodes (list_lattice.cpp:
+// 127-140).  blk > 0: tiles (ty, tz) in row-major order, inside a tile x, then
+// y, then z; the tile at (ty, tz) with extents th x tw starts after
+// nx*(ty*nz + th*tz) positions.
+__device__ __forceinline__ uint64_t trav_pos(int x, int y, int z, int nx,
+                                             int ny, int nz, int blk) {
+  if (blk == 0) return (uint64_t(x) * ny + y) * nz + z;
+  const int ty = y / blk * blk, tz = z / blk * blk;
+  const int th = min(blk, ny - ty), tw = min(blk, nz - tz);
+  return uint64_t(nx) * (uint64_t(ty) * nz + uint64_t(th) * tz) +
+         uint64_t(x) * th * tw + uint64_t(y - ty) * tw + (z - tz);
+}
+
+__global__ void k_trav_flags(const uint8_t* __restrict__ flags, int nx, int ny,
+                             int nz, int blk, uint8_t* __restrict__ ft) {
+  const uint64_t V = uint64_t(nx) * ny * nz;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < V;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const int z = static_cast<int>(i % nz);
+    const uint64_t r = i / nz;
+    const int y = static_cast<int>(r % ny), x = static_cast<int>(r / ny);
+    ft[trav_pos(x, y, z, nx, ny, nz, blk)] = flags[i];
+  }
+}
+
+// rank (list_lattice.cpp:160-164), nodes, canonical <-> list maps.
+__global__ void k_rank_nodes(const uint8_t* __restrict__ flags,
+                             const uint32_t* __restrict__ trank,
+                             const uint32_t* __restrict__ crank, int nx, int ny,
+                             int nz, int blk, uint32_t* __restrict__ rank,
+                             int32_t* __restrict__ nodes,
+                             uint32_t* __restrict__ list_of_canon) {
+  const uint64_t V = uint64_t(nx) * ny * nz;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < V;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (flags[i]) {
+      rank[i] = 0xffffffffu;
+      continue;
+    }
+    const int z = static_cast<int>(i % nz);
+    const uint64_t r = i / nz;
+    const int y = static_cast<int>(r % ny), x = static_cast<int>(r / ny);
+    const uint32_t n = blk == 0 ? crank[i] : trank[trav_pos(x, y, z, nx, ny, nz, blk)];
+    rank[i] = n;
+    nodes[3 * uint64_t(n)] = x;
+    nodes[3 * uint64_t(n) + 1] = y;
+    nodes[3 * uint64_t(n) + 2] = z;
+    if (list_of_canon) list_of_canon[crank[i]] = n;
+  }
+}
+
+struct AdjBuild {
+  const uint8_t* flags;
+  const uint32_t* rank;
+  const int32_t* nodes;
+  uint32_t* adj;  // d-major
+  uint64_t N;
+  int nx, ny, nz;
+  int per[3];
+  int soa, scatter;
+  uint64_t starts[kQ];
+};
+
+// build_structure adjacency loop (list_lattice.cpp:177-191) with the
+// neighbor() rule (geometry.cpp:119-131).
+__global__ void k_build_adj(const AdjBuild b) {
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < b.N;
+       n += uint64_t(gridDim.x) * blockDim.x) {
+    const int x = b.nodes[3 * n], y = b.nodes[3 * n + 1], z = b.nodes[3 * n + 2];
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) {
+      const int look = b.scatter ? d : opp(d);
+      int t0 = x + cx(look), t1 = y + cy(look), t2 = z + cz(look);
+      bool outside = false;
+      if (t0 < 0 || t0 >= b.nx) {
+        if (!b.per[0]) outside = true; else t0 = (t0 + b.nx) % b.nx;
+      }
+      if (!outside && (t1 < 0 || t1 >= b.ny)) {
+        if (!b.per[1]) outside = true; else t1 = (t1 + b.ny) % b.ny;
+      }
+      if (!outside && (t2 < 0 || t2 >= b.nz)) {
+        if (!b.per[2]) outside = true; else t2 = (t2 + b.nz) % b.nz;
+      }
+      uint64_t slot;
+      const uint64_t ti = (uint64_t(t0) * b.ny + t1) * b.nz + t2;
+      if (!outside && b.flags[ti] == 0) {
+        const uint64_t m = b.rank[ti];
+        slot = b.soa ? b.starts[d] + m : m * kQ + d;
+      } else {
+        slot = b.soa ? b.starts[opp(d)] + n : n * kQ + opp(d);
+      }
+      b.adj[(d - 1) * b.N + n] = static_cast<uint32_t>(slot);
+    }
+  }
+}
+
+__global__ void k_adj_canonical(const uint32_t* __restrict__ adj, uint64_t N,
+                                uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < N * 18;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t n = i / 18;
+    const int dm1 = static_cast<int>(i - n * 18);
+    out[i] = adj[dm1 * N + n];
+  }
+}
+
+// RIA run starts (build_ria, list_lattice.cpp:206-226): node n starts a run
+// if n == 0 or its pattern of 18 relative offsets differs from node n-1's.
+__global__ void k_ria_starts(const uint32_t* __restrict__ adj, uint64_t N,
+                             int soa, const ListArgs a,
+                             uint8_t* __restrict__ is_start) {
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < N;
+       n += uint64_t(gridDim.x) * blockDim.x) {
+    bool start = n == 0;
+    if (!start)
+      for (int d = 1; d < kQ && !start; ++d) {
+        const uint64_t sn = soa ? a.starts[d] + n : n * kQ + d;
+        const uint64_t sp = soa ? a.starts[d] + n - 1 : (n - 1) * kQ + d;
+        const int32_t pn = static_cast<int32_t>(int64_t(adj[(d - 1) * N + n]) - int64_t(sn));
+        const int32_t pp = static_cast<int32_t>(int64_t(adj[(d - 1) * N + n - 1]) - int64_t(sp));
+        start = pn != pp;
+      }
+    is_start[n] = start;
+  }
+}
+
+template <bool SOA>
+__global__ void k_list_init(double* buf, const ListArgs a) {
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.N;
+       n += uint64_t(gridDim.x) * blockDim.x)
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) buf[lslot<SOA>(a, n, d)] = weight(d);
+}
+
+// canonical gather / scatter / perturbation / macro fields over c in
+// [c0, c1): list node n = list_of_canon[c] (identity for blk = 0).
+template <bool SOA, int MODE>  // 0 gather, 1 scatter, 2 perturb, 3 macro
+__global__ void k_list_canon(const ListArgs a, double* buf,
+                             const uint32_t* __restrict__ loc, uint64_t c0,
+                             uint64_t c1, double* stage, uint64_t seed,
+                             double amp, double* rho, double* u) {
+  for (uint64_t c = c0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+       c < c1; c += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t n = loc ? loc[c] : c;
+    if (MODE == 0) {
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) stage[(c - c0) * kQ + d] = buf[lslot<SOA>(a, n, d)];
+    } else if (MODE == 1) {
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) buf[lslot<SOA>(a, n, d)] = stage[(c - c0) * kQ + d];
+    } else if (MODE == 2) {
+#pragma unroll
+      for (int d = 0; d < kQ; ++d)
+        buf[lslot<SOA>(a, n, d)] = perturbed_value(c, d, seed, amp);
+    } else {
+      double f[kQ];
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) f[d] = buf[lslot<SOA>(a, n, d)];
+      double r, ux, uy, uz;
+      macroscopic(f, r, ux, uy, uz);
+      rho[c] = r;
+      u[3 * c] = ux;
+      u[3 * c + 1] = uy;
+      u[3 * c + 2] = uz;
+    }
+  }
+}
+
+template <bool SOA>
+__global__ void k_list_mass_terms(const ListArgs a, const double* buf,
+                                  double* out) {
+  // contiguous copy of the fluid populations (pads excluded) for the
+  // compensated sum
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.N;
+       n += uint64_t(gridDim.x) * blockDim.x)
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) out[d * a.N + n] = buf[lslot<SOA>(a, n, d)];
+}
+
+// ------------------------------------------------------------------ engine
+namespace {
+
+int grid_for(uint64_t n, int threads) {
+  return static_cast<int>(std::min<uint64_t>(ceil_div(n, threads), 148ull * 64));
+}
+
+class ListEngine final : public Engine {
+ public:
+  ListEngine(const Descriptor& d, const GeomSpec& g, const Padding& pad) {
+    desc_ = d;
+    LBM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    DeviceGeometry geo = build_geometry_device(g, stream_);
+    nx_ = geo.nx;
+    ny_ = geo.ny;
+    nz_ = geo.nz;
+    per_ = geo.periodic;
+    const uint64_t V = geo.volume();
+    n_fluid_ = static_cast<uint64_t>(geo.n_fluid);
+    if (n_fluid_ >= (1ull << 32))
+      throw ConfigError("list lattice: more than 2^32 fluid nodes");
+
+    // slot map (list_lattice.cpp:166-173)
+    uint64_t total = 0;
+    std::array<uint64_t, kQ> st{};
+    if (d.soa) {
+      st = padding_offsets(n_fluid_, pad, &total);
+    } else {
+      total = n_fluid_ * kQ;
+    }
+    if (total >= (1ull << 32))
+      throw ConfigError("list lattice: " + std::to_string(total) +
+                        " PDF slots exceed the 32-bit adjacency range");
+    total_slots_ = total;
+    for (int q = 0; q < kQ; ++q) starts_[q] = st[q];
+
+    // ranks in traversal order and canonical order
+    DevBuf<uint32_t> crank(V);
+    scan_fluid(geo.flags.get(), crank.get(), V, stream_);
+    DevBuf<uint32_t> trank;
+    if (d.blk > 0) {
+      DevBuf<uint8_t> ft(V);
+      k_trav_flags<<<grid_for(V, 256), 256, 0, stream_>>>(geo.flags.get(), nx_,
+                                                          ny_, nz_, d.blk,
+                                                          ft.get());
+      LBM_CHECK_LAUNCH();
+      trank.alloc(V);
+      scan_fluid(ft.get(), trank.get(), V, stream_);
+      list_of_canon_.alloc(n_fluid_);
+    }
+    DevBuf<uint32_t> rank(V);
+    nodes_.alloc(3 * n_fluid_);
+    k_rank_nodes<<<grid_for(V, 256), 256, 0, stream_>>>(
+        geo.flags.get(), trank.get(), crank.get(), nx_, ny_, nz_, d.blk,
+        rank.get(), nodes_.get(), d.blk > 0 ? list_of_canon_.get() : nullptr);
+    LBM_CHECK_LAUNCH();
+
+    // adjacency: Gather for pull, Scatter for push and AA
+    // (kernels_list_os.cpp:19-20, kernels_list_aa.cpp:40)
+    scatter_ = d.prop != Prop::OsPull;
+    adj_.alloc(18 * n_fluid_);
+    AdjBuild b{};
+    b.flags = geo.flags.get();
+    b.rank = rank.get();
+    b.nodes = nodes_.get();
+    b.adj = adj_.get();
+    b.N = n_fluid_;
+    b.nx = nx_;
+    b.ny = ny_;
+    b.nz = nz_;
+    for (int a = 0; a < 3; ++a) b.per[a] = per_[a];
+    b.soa = d.soa;
+    b.scatter = scatter_;
+    for (int q = 0; q < kQ; ++q) b.starts[q] = starts_[q];
+    k_build_adj<<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(b);
+    LBM_CHECK_LAUNCH();
+
+    // PDF buffers initialised to the weights (list_lattice.cpp:248-264);
+    // pad slots are zeroed (the reference leaves them untouched).
+    const int nbuf = d.prop == Prop::Aa ? 1 : 2;
+    for (int q = 0; q < nbuf; ++q) {
+      buf_[q].alloc(total_slots_);
+      LBM_CUDA(cudaMemsetAsync(buf_[q].get(), 0, buf_[q].bytes(), stream_));
+      ListArgs a = base_args();
+      d.soa ? k_list_init<true><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(buf_[q].get(), a)
+            : k_list_init<false><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(buf_[q].get(), a);
+      LBM_CHECK_LAUNCH();
+    }
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    // streaming stores for the nt names and for lattices far beyond L2
+    cs_nt_ = d.nt_streams > 0;
+  }
+
+  ~ListEngine() override {
+    if (stream_) cudaStreamDestroy(stream_);
+  }
+
+  ListArgs base_args() const {
+    ListArgs a{};
+    a.adj = adj_.get();
+    a.N = n_fluid_;
+    for (int q = 0; q < kQ; ++q) a.starts[q] = starts_[q];
+    return a;
+  }
+
+  template <class K>
+  void launch(const char* name, K kern, const ListArgs& a) {
+    const int threads = 256;
+    const int tok = stats_.begin(name, stream_);
+    kern<<<static_cast<unsigned>(ceil_div(a.N, threads)), threads, 0, stream_>>>(a);
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, stream_);
+  }
+
+  void advance(const TrtArgs& t, long steps) override {
+    ListArgs a = base_args();
+    a.trt = t;
+    const bool soa = desc_.soa;
+    if (desc_.prop == Prop::Aa) {
+      a.src = a.dst = buf_[0].get();
+      for (long s = 0; s < steps; s += 2) {
+        soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
+            : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+        soa ? launch("list_aa_odd_soa", k_list_aa_odd<true, false>, a)
+            : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a);
+      }
+      return;
+    }
+    if (desc_.prop == Prop::OsPush) {
+      for (long s = 0; s < steps; ++s) {
+        a.src = buf_[cur_].get();
+        a.dst = buf_[1 - cur_].get();
+        soa ? launch("list_push_soa", k_list_push<true>, a)
+            : launch("list_push_aos", k_list_push<false>, a);
+        cur_ ^= 1;
+      }
+      return;
+    }
+    // pull: collide pass, T-1 fused sweeps, one stream-only sweep
+    // (kernels_list_os.cpp:74-91, kernels_list_nt.cpp:146-158)
+    a.src = a.dst = buf_[cur_].get();
+    soa ? launch("list_collide_soa", k_list_collide<true>, a)
+        : launch("list_collide_aos", k_list_collide<false>, a);
+    for (long s = 0; s < steps; ++s) {
+      a.src = buf_[cur_].get();
+      a.dst = buf_[1 - cur_].get();
+      const bool last = s == steps - 1;
+      if (soa) {
+        if (last)
+          launch("list_pull_stream_soa", k_list_pull<true, false, false>, a);
+        else if (cs_nt_)
+          launch("list_pull_soa", k_list_pull<true, true, true>, a);
+        else
+          launch("list_pull_soa", k_list_pull<true, true, false>, a);
+      } else {
+        last ? launch("list_pull_stream_aos", k_list_pull<false, false, false>, a)
+             : launch("list_pull_aos", k_list_pull<false, true, false>, a);
+      }
+      cur_ ^= 1;
+    }
+  }
+
+  template <int MODE>
+  void canon(uint64_t c0, uint64_t c1, double* stage, uint64_t seed = 0,
+             double amp = 0, double* rho = nullptr, double* u = nullptr) {
+    if (c1 <= c0) return;
+    ListArgs a = base_args();
+    const int g = grid_for(c1 - c0, 256);
+    const uint32_t* loc = desc_.blk > 0 ? list_of_canon_.get() : nullptr;
+    if (desc_.soa)
+      k_list_canon<true, MODE><<<g, 256, 0, stream_>>>(a, buf_[cur_].get(), loc, c0, c1,
+                                                       stage, seed, amp, rho, u);
+    else
+      k_list_canon<false, MODE><<<g, 256, 0, stream_>>>(a, buf_[cur_].get(), loc, c0, c1,
+                                                        stage, seed, amp, rho, u);
+    LBM_CHECK_LAUNCH();
+  }
+
+  void gather_canonical(uint64_t c0, uint64_t count, double* out) override {
+    canon<0>(c0, std::min(c0 + count, n_fluid_), out);
+  }
+  void scatter_canonical(uint64_t c0, uint64_t count, const double* in) override {
+    canon<1>(c0, std::min(c0 + count, n_fluid_), const_cast<double*>(in));
+  }
+  void load_perturbed(uint64_t seed, double amp) override {
+    canon<2>(0, n_fluid_, nullptr, seed, amp);
+  }
+  void macro_fields(double* rho, double* u) override {
+    canon<3>(0, n_fluid_, nullptr, 0, 0, rho, u);
+  }
+
+  double total_mass() override {
+    DevBuf<double> tmp(n_fluid_ * kQ);
+    ListArgs a = base_args();
+    desc_.soa ? k_list_mass_terms<true><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
+                    a, buf_[cur_].get(), tmp.get())
+              : k_list_mass_terms<false><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
+                    a, buf_[cur_].get(), tmp.get());
+    LBM_CHECK_LAUNCH();
+    return device_sum(tmp.get(), tmp.size(), stream_);
+  }
+
+  void export_structure(int32_t* nodes, uint32_t* adj, uint64_t* starts,
+                        uint64_t* total) override {
+    if (nodes)
+      LBM_CUDA(cudaMemcpyAsync(nodes, nodes_.get(), nodes_.bytes(),
+                               cudaMemcpyDeviceToHost, stream_));
+    if (adj) {
+      DevBuf<uint32_t> canon(18 * n_fluid_);
+      k_adj_canonical<<<grid_for(18 * n_fluid_, 256), 256, 0, stream_>>>(
+          adj_.get(), n_fluid_, canon.get());
+      LBM_CHECK_LAUNCH();
+      LBM_CUDA(cudaMemcpyAsync(adj, canon.get(), canon.bytes(),
+                               cudaMemcpyDeviceToHost, stream_));
+      LBM_CUDA(cudaStreamSynchronize(stream_));
+    }
+    if (starts)
+      for (int q = 0; q < kQ; ++q) starts[q] = desc_.soa ? starts_[q] : 0;
+    if (total) *total = total_slots_;
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  // ria_stats / vector_fraction (kernels_list_aa.cpp:95-140) for the ria/pv
+  // names; computed from the run starts of the kernel's own structure.
+  bool ria_stats(int64_t* runs, double* vfrac) override {
+    if (!desc_.ria) return false;
+    if (ria_runs_ < 0) {
+      DevBuf<uint8_t> is_start(n_fluid_);
+      ListArgs a = base_args();
+      k_ria_starts<<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
+          adj_.get(), n_fluid_, desc_.soa, a, is_start.get());
+      LBM_CHECK_LAUNCH();
+      std::vector<uint8_t> h(n_fluid_);
+      LBM_CUDA(cudaMemcpyAsync(h.data(), is_start.get(), n_fluid_,
+                               cudaMemcpyDeviceToHost, stream_));
+      LBM_CUDA(cudaStreamSynchronize(stream_));
+      int64_t count = 0;
+      uint64_t covered = 0, len = 0;
+      const uint64_t W = static_cast<uint64_t>(desc_.vector_width);
+      for (uint64_t n = 0; n < n_fluid_; ++n) {
+        if (h[n]) {
+          if (n) covered += len / W * W;
+          ++count;
+          len = 0;
+        }
+        ++len;
+      }
+      covered += len / W * W;
+      ria_runs_ = count;
+      ria_vfrac_ = static_cast<double>(covered) / static_cast<double>(n_fluid_);
+    }
+    *runs = ria_runs_;
+    *vfrac = ria_vfrac_;
+    return true;
+  }
+
+ private:
+  int nx_ = 0, ny_ = 0, nz_ = 0;
+  std::array<bool, 3> per_{};
+  uint64_t starts_[kQ] = {};
+  uint64_t total_slots_ = 0;
+  bool scatter_ = false;
+  bool cs_nt_ = false;
+  int cur_ = 0;
+  DevBuf<int32_t> nodes_;
+  DevBuf<uint32_t> adj_;
+  DevBuf<uint32_t> list_of_canon_;
+  DevBuf<double> buf_[2];
+  int64_t ria_runs_ = -1;
+  double ria_vfrac_ = 0.0;
+};
+
+}  // namespace
+
+std::unique_ptr<Engine> make_list_engine(const Descriptor& d,
+                                         const GeomSpec& g,
+                                         const Padding& pad) {
+  return std::make_unique<ListEngine>(d, g, pad);
+}
+
+}  // namespace lbmgpu

@@ -1,0 +1,193 @@
+// Kernel registry, descriptor parsing, padding and loop balance.
+// Host-only restatements of the reference's registry layer (L5) -- these are
+// the names and error messages a drop-in must keep.
+#include <algorithm>
+
+#include "lbm.hpp"
+
+namespace lbmgpu {
+
+// kernel_names() (reference src/kernels.cpp:22-43), canonical order.
+const std::vector<std::string>& kernel_names() {
+  static const std::vector<std::string> names = {
+      "blk-push-aos",   "blk-push-soa",   "blk-pull-aos",
+      "blk-pull-soa",   "aa-aos",         "aa-soa",
+      "aa-vec-soa",     "list-push-aos",  "list-push-soa",
+      "list-pull-aos",  "list-pull-soa",  "list-pull-split-nt-1s-soa",
+      "list-pull-split-nt-2s-soa",        "list-aa-aos",
+      "list-aa-soa",    "list-aa-ria-soa", "list-aa-pv-soa",
+  };
+  return names;
+}
+
+static bool ends_with(const std::string& s, const std::string& t) {
+  return s.size() >= t.size() && s.compare(s.size() - t.size(), t.size(), t) == 0;
+}
+static bool starts_with(const std::string& s, const std::string& t) {
+  return s.compare(0, t.size(), t) == 0;
+}
+
+// make_descriptor (reference src/kernels.cpp:50-82)
+Descriptor make_descriptor(const std::string& name, int blk, int W) {
+  const auto& names = kernel_names();
+  if (std::find(names.begin(), names.end(), name) == names.end()) {
+    std::string msg = "unknown kernel '" + name + "'; valid kernels:";
+    for (const auto& n : names) msg += "\n  " + n;
+    throw ConfigError(msg);
+  }
+  if (blk < 0) throw ConfigError("--blk must be >= 0, e.g. --blk 8");
+  if (W < 1 || W > 8) throw ConfigError("vector width must be in [1, 8]");
+  Descriptor d;
+  d.name = name;
+  d.blk = blk;
+  d.vector_width = W;
+  d.soa = !ends_with(name, "aos");
+  d.indirect = starts_with(name, "list-");
+  if (name.find("push") != std::string::npos)
+    d.prop = Prop::OsPush;
+  else if (name.find("pull") != std::string::npos)
+    d.prop = Prop::OsPull;
+  else
+    d.prop = Prop::Aa;
+  if (name.find("nt-1s") != std::string::npos) d.nt_streams = 1;
+  if (name.find("nt-2s") != std::string::npos) d.nt_streams = 2;
+  d.vec = name == "aa-vec-soa";
+  d.ria = name == "list-aa-ria-soa" || name == "list-aa-pv-soa";
+  d.pv = name == "list-aa-pv-soa";
+  return d;
+}
+
+// loop_balance (reference src/perfmodel.cpp:10-47) for the RIA-less case,
+// plus the GPU algorithmic bytes: 19 PDF reads + 19 writes of 8 B (no write
+// allocate on the GPU), + 18 x 4 B adjacency per one-step list update, or per
+// odd AA sub-step (half of it per update).  ria/pv run here on the list-AA
+// sweep, so they carry its 340 B.
+LoopBalance loop_balance(const Descriptor& k) {
+  LoopBalance b;
+  const double rd = 8.0 * kQ, wr = 8.0 * kQ;
+  const bool os = k.prop != Prop::Aa;
+  const bool nt = k.nt_streams > 0;
+  const double wa = (os && !nt) ? 8.0 * kQ : 0.0;
+  double imin = 0, imax = 0, igpu = 0;
+  if (k.indirect) {
+    if (k.ria) {
+      imin = 0.0;
+      imax = 38.0;
+    } else if (os) {
+      imin = imax = 18.0 * 4.0;
+    } else {
+      imin = imax = 18.0 * 4.0 / 2.0;
+    }
+    igpu = os ? 18.0 * 4.0 : 18.0 * 4.0 / 2.0;
+  }
+  b.ref_min = rd + wr + wa + imin;
+  b.ref_max = rd + wr + wa + imax;
+  b.gpu = rd + wr + igpu;
+  return b;
+}
+
+// ---- padding (reference src/list_lattice.cpp:63-121) ----------------------
+namespace {
+constexpr uint64_t kSetPeriod = 64 * 512 / 8;  // 4096 elements
+constexpr uint64_t kPageElems = (2u << 20) / 8;  // 262144 elements
+
+uint64_t place(uint64_t floor, uint64_t want_set, uint64_t want_tlb) {
+  const uint64_t res = want_set * (64 / 8);
+  uint64_t cand = (floor <= res) ? res
+                                 : (floor - res + kSetPeriod - 1) / kSetPeriod *
+                                           kSetPeriod +
+                                       res;
+  while (cand / kPageElems % 4 != want_tlb) cand += kSetPeriod;
+  return cand;
+}
+}  // namespace
+
+std::array<uint64_t, kQ> padding_offsets(uint64_t n, const Padding& p,
+                                         uint64_t* total) {
+  std::array<uint64_t, kQ> s{};
+  switch (p.mode) {
+    case 0:
+      for (int d = 0; d < kQ; ++d) s[d] = uint64_t(d) * n;
+      break;
+    case 3: {
+      uint64_t off = 0;
+      for (int d = 0; d < kQ; ++d) {
+        if (p.pads[d] < 0) throw ConfigError("padding: pad counts must be >= 0");
+        off += uint64_t(p.pads[d]);
+        s[d] = off;
+        off += n;
+      }
+      break;
+    }
+    case 1: {
+      uint64_t floor = 0;
+      for (int d = 0; d < kQ; ++d) {
+        s[d] = place(floor, uint64_t(d) * (512 / kQ) % 512, uint64_t(d) % 4);
+        floor = s[d] + n;
+      }
+      break;
+    }
+    case 2: {
+      uint64_t floor = 0;
+      for (int d = 0; d < kQ; ++d) {
+        s[d] = place(floor, 0, 0);
+        floor = s[d] + n;
+      }
+      break;
+    }
+    default:
+      throw ConfigError("padding: unknown mode");
+  }
+  if (total) *total = s[kQ - 1] + n;
+  return s;
+}
+
+// ---- geometry argument checks (reference src/geometry.cpp:17-25,40-111) ----
+static void check_dims(const GeomSpec& s, const char* kind, int mx, int my,
+                       int mz) {
+  if (s.nx < mx || s.ny < my || s.nz < mz)
+    throw ConfigError(std::string("geometry '") + kind +
+                      "' needs dims of at least " + std::to_string(mx) + "x" +
+                      std::to_string(my) + "x" + std::to_string(mz) + ", got " +
+                      std::to_string(s.nx) + "x" + std::to_string(s.ny) + "x" +
+                      std::to_string(s.nz));
+}
+
+std::array<bool, 3> validate_geometry(const GeomSpec& s) {
+  switch (s.kind) {
+    case kChannel:
+      check_dims(s, "channel", 1, 3, 3);
+      return {true, false, false};
+    case kSlit:
+      check_dims(s, "slit", 1, 1, 3);
+      return {true, true, false};
+    case kPipe:
+      check_dims(s, "pipe", 1, 4, 4);
+      if (s.pipe_diameter < 0)
+        throw ConfigError("pipe geometry: diameter must be >= 0");
+      return {true, false, false};
+    case kBlocks: {
+      check_dims(s, "blocks", 1, 1, 1);
+      if (s.block < 1)
+        throw ConfigError("blocks geometry: block edge must be >= 1");
+      if (s.spacing < 0)
+        throw ConfigError("blocks geometry: spacing must be >= 0");
+      const int period = s.block + s.spacing;
+      if (period > std::min({s.nx, s.ny, s.nz}))
+        throw ConfigError(
+            "blocks geometry: block+spacing must not exceed the smallest "
+            "dimension");
+      return {true, true, true};
+    }
+    case kCustom:
+      if (s.nx < 1 || s.ny < 1 || s.nz < 1)
+        throw ConfigError("custom geometry: dims must be >= 1");
+      if (s.custom.size() != s.volume())
+        throw ConfigError("custom geometry: flag field size mismatch");
+      return {s.custom_periodic[0], s.custom_periodic[1], s.custom_periodic[2]};
+    default:
+      throw ConfigError("unknown geometry kind (valid: channel, slit, pipe, blocks)");
+  }
+}
+
+}  // namespace lbmgpu

@@ -1,0 +1,34 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA sweep library)")
+    config.addinivalue_line("markers", "slow: long-running full-size check")
+
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="session")
+def port():
+    from oracle.oracle import Port
+    return Port()
+
+
+@pytest.fixture(scope="session")
+def small_golden():
+    import json
+    return json.load(open(os.path.join(GOLDEN, "small.json")))
+
+
+@pytest.fixture(scope="session")
+def small_snapshots():
+    import numpy as np
+    return dict(np.load(os.path.join(GOLDEN, "small_snapshots.npz")))

@@ -1,0 +1,287 @@
+"""GPU parity tests: the CUDA sweeps (through the C ABI) against the oracle.
+
+Bar: bit-exact PDFs, node lists and adjacency (the reference is built with
+-ffp-contract=off and the device collide keeps its expression order with
+--fmad=false, so every rounding matches).  Where a check is tolerance based
+the tolerance is written in the test: total mass (a compensated device sum
+vs a sequential Kahan sum) is compared at 1e-12 relative.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_1711_11468_b200 as lbm  # noqa: E402
+
+TAU = 0.9
+G_TEST = (1e-5, 2e-6, -3e-6)  # reference tests/test_kernels.cpp:14-15
+PARAMS = lbm.TrtParams.from_tau(TAU)
+FORCE = lbm.BodyForce(G_TEST)
+NAMES = lbm.kernel_names()
+
+
+def spec_of(case):
+    return lbm.GeometrySpec(case["kind"], *case["dims"], case.get("block", 4), case.get("spacing", 4),
+                            case.get("pipe_diameter", 0))
+
+
+def test_seventeen_names_and_registry():
+    assert len(NAMES) == 17
+    with pytest.raises(lbm.ConfigError) as e:
+        lbm.make_descriptor("plain-push")
+    assert "blk-push-aos" in str(e.value)
+
+
+@pytest.mark.parametrize("idx", range(68))
+def test_kernel_matches_golden_bitwise(idx, small_golden, small_snapshots):
+    """Every kernel x {blocks 12x10x10, channel 16x12x10, pipe 9x12x13,
+    slit 6x5x9}: perturbed init (seed 1234), 8 steps, tau 0.9,
+    g = (1e-5, 2e-6, -3e-6) -- the reference's own recipe
+    (tests/test_kernels.cpp:69-94), compared bit for bit."""
+    case = small_golden["cases"][idx]
+    k = lbm.make_kernel(lbm.make_descriptor(case["kernel"]), spec_of(case))
+    assert k.n_fluid() == case["n_fluid"]
+    k.load_perturbed(1234)
+    host_init = lbm.perturbed_equilibrium(k.n_fluid(), 1234)
+    assert np.array_equal(k.snapshot(), host_init)
+    k.advance(PARAMS, FORCE, case["steps"])
+    snap = k.snapshot()
+    expect = small_snapshots[case["snapshot_key"]]
+    assert np.array_equal(snap, expect), case["kernel"]
+    assert f"{lbm.state_fingerprint(snap):016x}" == case["fingerprint"]
+    assert f"{k.fingerprint():016x}" == case["fingerprint"]
+    assert abs(k.total_mass() - case["mass"]) <= 1e-12 * abs(case["mass"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_against_port_oracle_steppers(name, port):
+    """Host load_state path + a second geometry, against our C restatement
+    of the reference steppers (tests/support/reference.hpp:33-105)."""
+    for kind, dims in [("blocks", (12, 12, 12)), ("channel", (33, 7, 9))]:
+        _, _, nf = port.geometry(kind, *dims)
+        init = port.perturbed(nf, 99)
+        fam = "half" if name.startswith("list-") else "full"
+        expect, _ = port.run(fam, kind, *dims, 6, PARAMS.omega_plus, g=G_TEST, init=init)
+        k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
+        k.load_state(init)
+        k.advance(PARAMS, FORCE, 6)
+        got = k.snapshot()
+        assert port.max_rel_diff(got, expect) <= 1e-12, (name, kind)
+        assert np.array_equal(got, expect), (name, kind)
+
+
+def _list_kernel_for(layout, scatter):
+    if scatter:
+        return "list-aa-soa" if layout == "soa" else "list-aa-aos"
+    return "list-pull-soa" if layout == "soa" else "list-pull-aos"
+
+
+@pytest.mark.parametrize("idx", range(84))
+def test_list_structure_bit_exact(idx, small_golden, port):
+    """Node order, slot starts and adjacency exported from the device builder
+    == the reference build_structure (list_lattice.cpp:149-204), for
+    blk 0/2/3, padding none/auto/thrash, gather/scatter, SoA/AoS."""
+    if idx >= len(small_golden["structures"]):
+        pytest.skip("fewer structure cases")
+    s = small_golden["structures"][idx]
+    name = _list_kernel_for(s["layout"], s["scatter"])
+    k = lbm.make_kernel(lbm.make_descriptor(name, blk=s["blk"]), spec_of(s),
+                        lbm.PaddingPolicy(s["padding"]))
+    nodes, adj, starts, total = k.export_structure()
+    assert [int(v) for v in starts] == (s["starts"] if s["layout"] == "soa" else [0] * 19)
+    assert total == s["total_slots"]
+    assert f"{port.fingerprint(adj):016x}" == s["adj_fnv"]
+    assert f"{port.fingerprint(nodes.reshape(-1).astype(np.uint32)):016x}" == s["nodes_fnv"]
+
+
+def test_structure_against_port_builder(port):
+    for kind, dims, kw in [("pipe", (5, 14, 11), {}), ("blocks", (10, 9, 11), dict(block=3, spacing=2))]:
+        for blk in (0, 4):
+            for scatter in (False, True):
+                ref = port.structure(kind, *dims, blk=blk, scatter=scatter, **kw)
+                name = _list_kernel_for("soa", scatter)
+                k = lbm.make_kernel(lbm.make_descriptor(name, blk=blk),
+                                    lbm.GeometrySpec(kind, *dims, kw.get("block", 4), kw.get("spacing", 4)))
+                nodes, adj, starts, total = k.export_structure()
+                assert np.array_equal(nodes, ref["nodes"])
+                assert np.array_equal(adj, ref["adj"])
+                assert np.array_equal(starts, ref["starts"])
+
+
+def test_blocking_and_padding_never_change_results():
+    """tests/test_kernels.cpp:197-241 on the GPU."""
+    spec = lbm.GeometrySpec("blocks", 12, 10, 10)
+    base = {}
+    for name in ("blk-push-aos", "aa-vec-soa", "list-aa-pv-soa", "list-pull-soa", "list-aa-soa",
+                 "list-pull-split-nt-1s-soa"):
+        for blk in (0, 2, 8, 50):
+            for pad in ("none", "auto", "thrash"):
+                k = lbm.make_kernel(lbm.make_descriptor(name, blk=blk), spec, lbm.PaddingPolicy(pad))
+                k.load_perturbed(8)
+                k.advance(PARAMS, FORCE, 8)
+                s = k.snapshot()
+                if name not in base:
+                    base[name] = s
+                else:
+                    assert np.array_equal(s, base[name]), (name, blk, pad)
+
+
+def test_equilibrium_fixed_point_every_kernel():
+    """tests/test_kernels.cpp:56-67."""
+    spec = lbm.GeometrySpec("blocks", 12, 10, 10)
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    for name in NAMES:
+        k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        k.advance(PARAMS, lbm.BodyForce(), 4)
+        s = k.snapshot().reshape(-1, 19)
+        assert np.max(np.abs(s - w)) <= 1e-15, name
+
+
+def test_push_equals_pull_and_aa_pair_equals_two_steps():
+    """tests/test_kernels.cpp:96-126."""
+    spec = lbm.GeometrySpec("blocks", 12, 12, 12)
+    for a, b in (("blk-push-soa", "blk-pull-soa"), ("list-push-aos", "list-pull-aos")):
+        ka = lbm.make_kernel(lbm.make_descriptor(a), spec)
+        kb = lbm.make_kernel(lbm.make_descriptor(b), spec)
+        for k in (ka, kb):
+            k.load_perturbed(99)
+            k.advance(PARAMS, FORCE, 1)
+        assert np.array_equal(ka.snapshot(), kb.snapshot())
+    spec = lbm.GeometrySpec("blocks", 12, 10, 10)
+    os_k = lbm.make_kernel(lbm.make_descriptor("blk-push-soa"), spec)
+    aa_k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    for k in (os_k, aa_k):
+        k.load_perturbed(5)
+        k.advance(PARAMS, FORCE, 2)
+    assert np.array_equal(os_k.snapshot(), aa_k.snapshot())
+
+
+def test_advance_zero_composition_and_rejections():
+    """tests/test_kernels.cpp:146-175."""
+    spec = lbm.GeometrySpec("blocks", 12, 10, 10)
+    for name in ("blk-pull-aos", "list-aa-soa", "aa-soa", "list-pull-soa"):
+        a = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        a.load_perturbed(3)
+        init = a.snapshot()
+        a.advance(PARAMS, FORCE, 0)
+        assert np.array_equal(a.snapshot(), init)
+        a.advance(PARAMS, FORCE, 4)
+        b = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        b.load_state(init)
+        b.advance(PARAMS, FORCE, 2)
+        b.advance(PARAMS, FORCE, 2)
+        assert np.array_equal(a.snapshot(), b.snapshot())
+    k = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec)
+    before = k.snapshot()
+    with pytest.raises(lbm.ConfigError):
+        k.advance(PARAMS, FORCE, 3)
+    assert np.array_equal(k.snapshot(), before)
+    with pytest.raises(lbm.ConfigError):
+        k.advance(PARAMS, FORCE, -2)
+    with pytest.raises(lbm.ConfigError):
+        k.advance(lbm.TrtParams(2.5), FORCE, 2)
+    with pytest.raises(lbm.ConfigError):
+        k.load_state(np.zeros(5))
+
+
+def test_mass_conserved_without_forcing():
+    """tests/test_kernels.cpp:243-256: |dm| <= 1e-11 m over 100 steps."""
+    spec = lbm.GeometrySpec("blocks", 12, 10, 10)
+    for name in NAMES:
+        k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        k.load_perturbed(21)
+        m0 = k.total_mass()
+        k.advance(PARAMS, lbm.BodyForce(), 100)
+        assert abs(k.total_mass() - m0) <= 1e-11 * m0, name
+
+
+def test_ria_stats_match_reference(small_golden):
+    for r in small_golden["ria"]:
+        k = lbm.make_kernel(lbm.make_descriptor("list-aa-pv-soa", blk=r["blk"], vector_width=r["W"]),
+                            spec_of(r), lbm.PaddingPolicy.none())
+        st = k.ria_stats()
+        assert st["total_runs"] == r["runs"]
+        assert k.vector_fraction() == r["vfrac"]
+        assert k.pv_chunk_fraction() == r["vfrac"]
+    k = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), lbm.GeometrySpec("channel", 20, 10, 10))
+    assert k.ria_stats() is None and k.vector_fraction() is None
+
+
+def test_capabilities():
+    spec = lbm.GeometrySpec("blocks", 12, 10, 10)
+    assert lbm.make_kernel(lbm.make_descriptor("list-pull-split-nt-1s-soa"), spec).capabilities().nt_streams_effective == 1
+    assert lbm.make_kernel(lbm.make_descriptor("list-pull-split-nt-2s-soa"), spec).capabilities().nt_streams_effective == 2
+    assert lbm.make_kernel(lbm.make_descriptor("blk-push-soa"), spec).capabilities().nt_streams_effective == 0
+
+
+@pytest.mark.parametrize("kind,dims,parts", [
+    ("channel", (16, 12, 24), 2), ("channel", (16, 12, 24), 3), ("channel", (16, 12, 24), 4),
+    ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2), ("blocks", (12, 10, 16), 4),
+    ("slit", (6, 5, 9), 3)])
+def test_zslab_parts_bitwise_equal_single(kind, dims, parts):
+    """z-slab decomposition (the multi-GPU plan, emulated on one device):
+    fingerprint identical for 1..N parts -- the worker-count invariance of
+    tests/test_kernels.cpp:177-195 carried to the slab split."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    ref.load_perturbed(4242)
+    ref.advance(PARAMS, FORCE, 10)
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec, dist={"virtual_parts": parts})
+    k.load_perturbed(4242)
+    init = k.snapshot()
+    assert np.array_equal(init, lbm.perturbed_equilibrium(k.n_fluid(), 4242))
+    k.advance(PARAMS, FORCE, 4)
+    k.advance(PARAMS, FORCE, 6)
+    assert np.array_equal(k.snapshot(), ref.snapshot())
+    assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
+
+
+def test_poiseuille_verification_passes():
+    """verify_kernel (verification.cpp:31-100) on the GPU: slit 4x4x18."""
+    for name in ("blk-push-soa", "aa-soa", "list-aa-soa", "list-pull-soa", "blk-pull-aos",
+                 "list-push-aos"):
+        r = lbm.verify_kernel(name, lbm.PoiseuilleCase(4, 4, 18, 1e-6, lbm.TrtParams.from_tau(0.9)))
+        assert r["converged"] and r["passed"], (name, r["linf_rel"])
+        assert r["linf_rel"] < 1e-6
+
+
+def test_steady_state_reports_nonfinite():
+    spec = lbm.GeometrySpec("channel", 8, 6, 6)
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    s = k.snapshot()
+    s[5] = np.nan
+    k.load_state(s)
+    with pytest.raises(lbm.NumericalError):
+        k.steady_state_run(PARAMS, FORCE, 2, 1e-12, 10)
+
+
+CONFIGS = os.path.join(os.path.dirname(__file__), "golden", "configs.json")
+
+
+@pytest.mark.parametrize("cid", ["1", "2", "3", "4"])
+def test_baseline_config_fingerprint(cid):
+    """BASELINE configs 1-4 at full size: default init, omega+ = 1,
+    Lambda = 3/16, g = (1e-5, 0, 0); the final state's FNV-1a fingerprint
+    must equal the reference's (made by tests/golden/make_golden.py)."""
+    if not os.path.exists(CONFIGS):
+        pytest.skip("configs.json not generated")
+    gold = json.load(open(CONFIGS))
+    if cid not in gold:
+        pytest.skip(f"config {cid} golden not generated")
+    c = gold[cid]
+    spec = lbm.GeometrySpec(c["kind"], *c["dims"], c.get("block", 4), c.get("spacing", 4),
+                            c.get("pipe_diameter", 0))
+    k = lbm.make_kernel(lbm.make_descriptor(c["kernel"]), spec)
+    assert k.n_fluid() == c["n_fluid"]
+    if c["kernel"].startswith("list-"):
+        _, _, starts, total = k.export_structure()
+        assert [int(v) for v in starts] == c["starts_auto"]
+        assert total == c["total_slots_auto"]
+    m0 = k.total_mass()
+    assert abs(m0 - c["mass0"]) <= 1e-12 * c["mass0"]
+    k.advance(lbm.TrtParams(1.0, 3.0 / 16.0), lbm.BodyForce(tuple(c["g"])), c["steps"])
+    assert f"{k.fingerprint():016x}" == c["fingerprint"]
+    assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
