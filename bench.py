@@ -1,0 +1,379 @@
+#!/usr/bin/env python3
+"""Benchmark driver (contract in the task statement; numbers in DESIGN.md).
+
+Default workload = BASELINE config 5: channel 1024x512x512 fp64 D3Q19 TRT,
+direct addressing, AA pattern (aa-soa), omega+ = 1, Lambda = 3/16,
+g = (1e-5, 0, 0), initial state = weights; z-slab decomposed over the
+ranks (1 GPU = the whole box).  One bench "step" = one AA pair = two lattice
+updates of every fluid node (AA needs even counts, reference
+kernels.cpp:87-91).  MFLUP/s = N_fluid * lattice_steps / s / 1e6
+(reference harness.cpp:115-116).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 1..5]
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/liblbm_ref.so = lbmbench compiled from its sources) on the
+host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # id: (kernel, kind, dims, extra, baseline steps, cpu sample dims)
+    1: ("blk-push-soa", "channel", (64, 64, 64), {}, 100, (64, 64, 64)),
+    2: ("list-aa-soa", "channel", (256, 256, 256), {}, 1000, (32, 256, 256)),
+    3: ("list-pull-soa", "pipe", (512, 256, 256), {"pipe_diameter": 250}, 500, (32, 256, 256)),
+    4: ("list-aa-soa", "blocks", (400, 400, 400), {"block": 8, "spacing": 8}, 500, (64, 400, 400)),
+    5: ("aa-soa", "channel", (1024, 512, 512), {}, 200, (128, 512, 512)),
+}
+OMEGA_PLUS, LAMBDA, G = 1.0, 3.0 / 16.0, (1e-5, 0.0, 0.0)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic(kernel_name):
+    """dram bytes per launch for `kernel_name` from the committed ncu summary
+    (profiles/ncu_summary.json, written by tools/ncu_summary.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("kernels", {}).get(kernel_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- CPU legs
+def cpu_reference_run(cid, steps_per_sample, samples, warmup_samples):
+    """The reference lbmbench (oracle/_ref) on the host cores: every sample is
+    `steps_per_sample` lattice steps of the reference kernel on the bounded
+    sample box.  Returns (MFLUP/s, cores, description, kind)."""
+    kernel, kind, dims, extra, _, sdims = CONFIGS[cid]
+    threads = os.cpu_count() or 1
+    from oracle.oracle import Ref, Port  # test/baseline infrastructure only
+    try:
+        ref = Ref()
+    except FileNotFoundError:
+        ref = None
+    if ref is not None:
+        k = ref.kernel(kernel, kind, *sdims, threads=threads, block=extra.get("block", 4),
+                       spacing=extra.get("spacing", 4), pipe_diameter=extra.get("pipe_diameter", 0))
+        for _ in range(warmup_samples):
+            k.advance(OMEGA_PLUS, LAMBDA, G, steps_per_sample)
+        secs = [k.advance(OMEGA_PLUS, LAMBDA, G, steps_per_sample) for _ in range(samples)]
+        n = k.n_fluid
+        tot = sum(secs)
+        desc = (f"reference lbmbench {kernel} (oracle/_ref, -O3 -ffp-contract=off -march=x86-64-v4, "
+                f"WorkerPool({threads})) on {kind} {'x'.join(map(str, sdims))} "
+                f"({n} fluid nodes), {samples} x {steps_per_sample} steps timed")
+        return n * steps_per_sample * samples / tot / 1e6, threads, desc, "reference"
+    # fallback: our C restatement, textbook stepper, single thread
+    port = Port()
+    fam = "half" if kernel.startswith("list-") else "full"
+    t0 = time.perf_counter()
+    port.run(fam, kind, *sdims, steps_per_sample * samples, OMEGA_PLUS, g=G,
+             block=extra.get("block", 4), spacing=extra.get("spacing", 4),
+             pipe_diameter=extra.get("pipe_diameter", 0))
+    dt = time.perf_counter() - t0
+    _, _, nf = port.geometry(kind, *sdims, extra.get("block", 4), extra.get("spacing", 4),
+                             extra.get("pipe_diameter", 0))
+    return (nf * steps_per_sample * samples / dt / 1e6, 1,
+            f"port oracle textbook stepper on {kind} {'x'.join(map(str, sdims))}", "port")
+
+
+def base_line(cid, n_gpus, steps, warmup, lattice_per_step):
+    kernel, kind, dims, extra, bsteps, _ = CONFIGS[cid]
+    return {
+        "metric": "MFLUP/s (fp64 D3Q19 TRT)",
+        "unit": "MFLUP/s",
+        "n_gpus": n_gpus,
+        "steps": steps,
+        "warmup": warmup,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE config: initial state = D3Q19 weights, rho=1, u=0)",
+        "config": {
+            "workload": f"cfg{cid}: {kind} {'x'.join(map(str, dims))} {kernel}"
+                        + (f" {extra}" if extra else ""),
+            "kernel": kernel, "geometry": kind, "dims": list(dims), **extra,
+            "omega_plus": OMEGA_PLUS, "magic_lambda": LAMBDA, "g": list(G),
+            "lattice_updates_per_step": lattice_per_step,
+            "baseline_steps": bsteps,
+            "parallelism": f"z-slab x{n_gpus}" if n_gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2" if cid != 1 else
+                  "lattice (2 x 40 MB) fits the 126 MB L2; no flush (reported as is)",
+        },
+    }
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    cid = args.config
+    kernel = CONFIGS[cid][0]
+    per = 2 if "aa" in kernel.split("-") else 1
+    mflups, cores, desc, kind = cpu_reference_run(cid, per, args.steps, args.warmup)
+    line = base_line(cid, args.gpus, args.steps, args.warmup, per)
+    line.update({"impl": "reference", "value": mflups, "ms_per_step": None,
+                 "cpu_baseline": {"value": mflups, "unit": "MFLUP/s", "cores": cores,
+                                  "kind": kind, "sample": desc},
+                 "e2e": {"value": mflups, "unit": "MFLUP/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+
+    import paper_1711_11468_b200 as lbm
+
+    cid = args.config
+    kernel, kind, dims, extra, _, _ = CONFIGS[cid]
+    desc = lbm.make_descriptor(kernel)
+    aa = desc.prop == "aa"
+    per = 2 if aa else 1
+    spec = lbm.GeometrySpec(kind, *dims, extra.get("block", 4), extra.get("spacing", 4),
+                            extra.get("pipe_diameter", 0))
+    dspec = None
+    if world > 1:
+        if desc.addr != "direct" or not aa:
+            raise SystemExit("multi-GPU runs decompose the direct AA sweep (config 5)")
+        obj = [lbm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        dspec = {"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0]}
+    k = lbm.make_kernel(desc, spec, lbm.PaddingPolicy.automatic(), dist=dspec)
+    N = k.n_fluid()
+    params = lbm.TrtParams(OMEGA_PLUS, LAMBDA)
+    force = lbm.BodyForce(G)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k.synchronize()
+
+    # warm-up
+    if args.warmup:
+        k.advance(params, force, per * args.warmup)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    k.kernel_stats_reset()
+    k.kernel_stats_enable(True)
+    launches0 = k.launch_count()
+    barrier()
+    ms = k.time_advance(params, force, per * args.steps)
+    barrier()
+    launches = k.launch_count() - launches0
+    k.kernel_stats_enable(False)
+    stats = k.kernel_stats()
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    mflups = N * per * args.steps / (ms / 1e3) / 1e6
+
+    # roofline of the dominant kernel (largest share of the timed region)
+    hbm, peak_src = peaks()
+    _, _, gpu_b = lbm.loop_balance(kernel)
+    local_nf = k.part_info(0)[2] if (world > 1) else N
+    rows = sorted(stats.items(), key=lambda kv: -kv[1]["ms"])
+    roof = None
+    kernels_out = {}
+    for name, st in rows:
+        if st["launches"] == 0:
+            continue
+        avg_ms = st["ms"] / st["launches"]
+        # every sweep launch of the timed region touches each fluid node once:
+        # 19 reads + 19 writes of 8 B (+ 72 B of adjacency for list one-step,
+        # 72 B for the odd AA list sub-step only)
+        if "list_aa_odd" in name or ("list_pull" in name) or ("list_push" in name):
+            per_node = 304 + 72
+        else:
+            per_node = 304
+        alg = local_nf * per_node
+        ach = alg / (avg_ms / 1e3) / 1e9
+        kernels_out[name] = {"launches": st["launches"], "avg_ms": avg_ms,
+                             "share": st["ms"] / ms if ms else None,
+                             "alg_bytes_per_launch": alg, "achieved_GBps": ach}
+        if roof is None:
+            traffic = ncu_traffic(name)
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": traffic, "kernel": name,
+                    "alg_bytes_per_launch": alg, "peak_source": peak_src,
+                    "bytes_per_node": per_node}
+
+    line = base_line(cid, world, args.steps, args.warmup, per)
+    line.update({
+        "value": mflups,
+        "ms_per_step": ms / args.steps,
+        "n_fluid": N,
+        "roofline": roof,
+        "kernels": kernels_out,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "achieved_hbm_GBps_step": N * per * gpu_b / (ms / args.steps / 1e3) / 1e9 / max(world, 1),
+        "gpu_bytes_per_flup": gpu_b,
+    })
+
+    # ---- end to end through the public API with host buffers: the initial
+    # state is loaded from pinned host memory, K steps run, the final state is
+    # read back to pinned host memory -- all inside the timed region.
+    if not args.no_e2e:
+        e2e = run_e2e(lbm, k, params, force, per, args.steps, world, dist, torch)
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, sdesc, skind = cpu_reference_run(cid, per, 3 if cid != 1 else 20, 1)
+            line["cpu_baseline"] = {"value": v, "unit": "MFLUP/s", "cores": cores,
+                                    "kind": skind, "sample": sdesc}
+        except Exception as e:  # report, never fail the GPU line
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(lbm, k, params, force, per, steps, world, dist, torch):
+    n_local = k.local_state_size() if world > 1 else k.n_fluid() * 19
+    buf = lbm.PinnedBuffer(n_local)
+    # initial state = weights (the BASELINE init), prepared on the host
+    w = [1 / 3] + [1 / 18] * 6 + [1 / 36] * 12
+    import numpy as np
+    arr = buf.array
+    arr.reshape(-1, 19)[:] = np.asarray(w)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if world > 1:
+        k.load_state_local(arr)
+        k.advance(params, force, per * steps)
+        k.snapshot_local(arr)
+    else:
+        k.load_state(arr)
+        k.advance(params, force, per * steps)
+        k.snapshot(arr)
+    k.synchronize()
+    dt = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    N = k.n_fluid()
+    buf.free()
+    return {"value": N * per * steps / dt / 1e6, "unit": "MFLUP/s",
+            "h2d_bytes_per_step": N * 19 * 8 / steps, "d2h_bytes_per_step": N * 19 * 8 / steps,
+            "seconds": dt, "what": "load_state(pinned host) + advance + snapshot(pinned host) "
+                                   "through the C ABI, wall clock, max over ranks"}
+
+
+if __name__ == "__main__":
+    main()
