@@ -1,0 +1,145 @@
+"""CPU, world_size 2 (gloo): the multi-GPU z-slab protocol end to end.
+
+Each rank holds its slab in the device layout the CUDA path uses
+([storage plane][slot][y][x], one ghost plane per side, slots grouped by c_z),
+runs the AA even/odd sub-steps over its own fluid nodes with the oracle's
+collision, and exchanges exactly the rows of the library's halo plan
+(lbmgpu_halo_plan, the same plan the NCCL path executes) with
+torch.distributed send/recv.  The gathered result must equal the full-domain
+oracle bit for bit -- for a channel (no z wrap) and for z-periodic blocks
+(ring exchange)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+Q = 19
+CX = [0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0]
+CY = [0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1]
+CZ = [0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1]
+OPP = [0, 2, 1, 4, 3, 6, 5, 8, 7, 10, 9, 12, 11, 14, 13, 16, 15, 18, 17]
+SLOT = [5, 6, 7, 8, 9, 14, 0, 10, 11, 12, 13, 15, 1, 2, 16, 17, 3, 4, 18]  # common.cuh dslot
+TAU, G = 0.8, (1e-5, -2e-6, 3e-6)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port_no, kind, dims, steps, q):
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        from paper_1711_11468_b200 import lbmgpu as L
+        port = Port()
+        nx, ny, nz = dims
+        flags, per, nf = port.geometry(kind, nx, ny, nz)
+        solid = flags.reshape(nx, ny, nz)
+        z0, z1 = nz * rank // world, nz * (rank + 1) // world
+        nzl = z1 - z0
+        ring = bool(solid[:, :, 0].min() == 0 or solid[:, :, nz - 1].min() == 0)
+        plan = L.halo_plan(nz, world, ring)
+        wp = 1.0 / TAU
+        wm = port.omega_minus(wp)
+        buf = np.empty((nzl + 2, Q, ny, nx))
+        init = port.perturbed(nf, 77)
+        # canonical -> slab (weights on solids, perturbed state on fluid nodes)
+        w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+        for d in range(Q):
+            buf[:, SLOT[d]] = w[d]
+        k = 0
+        for x in range(nx):
+            for y in range(ny):
+                for z in range(nz):
+                    if solid[x, y, z]:
+                        continue
+                    if z0 <= z < z1:
+                        for d in range(Q):
+                            buf[z - z0 + 1, SLOT[d], y, x] = init[k * Q + d]
+                    k += 1
+        own = [(x, y, z) for z in range(nzl) for y in range(ny) for x in range(nx)
+               if not solid[x, y, z + z0]]
+
+        def exchange(phase):
+            reqs = []
+            for i, (ph, src, dst, sp, dp, s0, ns) in enumerate(plan):
+                if ph != phase:
+                    continue
+                if src == rank:
+                    t = torch.from_numpy(np.ascontiguousarray(buf[sp, s0:s0 + ns]))
+                    reqs.append(("s", dist.isend(t, dst, tag=i), None, None))
+                if dst == rank:
+                    t = torch.empty((ns, ny, nx), dtype=torch.float64)
+                    reqs.append(("r", dist.irecv(t, src, tag=i), t, (dp, s0, ns)))
+            for kind_, r, t, where in reqs:
+                r.wait()
+                if kind_ == "r":
+                    dp, s0, ns = where
+                    buf[dp, s0:s0 + ns] = t.numpy()
+
+        for _ in range(steps // 2):
+            for (x, y, z) in own:          # even: own slots -> opposite slots
+                zs = z + 1
+                f = np.array([buf[zs, SLOT[d], y, x] for d in range(Q)])
+                f = port.collide(f, wp, wm, G)
+                for d in range(Q):
+                    buf[zs, SLOT[OPP[d]], y, x] = f[d]
+            exchange(0)
+            for (x, y, z) in own:          # odd: gather (x-c, opp d), scatter (x+c, d)
+                zs = z + 1
+                f = np.empty(Q)
+                f[0] = buf[zs, SLOT[0], y, x]
+                for d in range(1, Q):
+                    f[d] = buf[zs - CZ[d], SLOT[OPP[d]], (y - CY[d]) % ny, (x - CX[d]) % nx]
+                f = port.collide(f, wp, wm, G)
+                buf[zs, SLOT[0], y, x] = f[0]
+                for d in range(1, Q):
+                    buf[zs + CZ[d], SLOT[d], (y + CY[d]) % ny, (x + CX[d]) % nx] = f[d]
+            exchange(1)
+        # gather own fluid rows in canonical order to rank 0
+        rows = {}
+        k = 0
+        for x in range(nx):
+            for y in range(ny):
+                for z in range(nz):
+                    if solid[x, y, z]:
+                        continue
+                    if z0 <= z < z1:
+                        rows[k] = [buf[z - z0 + 1, SLOT[d], y, x] for d in range(Q)]
+                    k += 1
+        out = [None] * world
+        dist.all_gather_object(out, rows)
+        if rank == 0:
+            full = np.zeros(nf * Q)
+            for part in out:
+                for kk, v in part.items():
+                    full[kk * Q:(kk + 1) * Q] = v
+            expect, _ = port.run("full", kind, nx, ny, nz, steps, wp, g=G, init=init)
+            q.put((bool(np.array_equal(full, expect)), float(port.max_rel_diff(full, expect))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,dims", [("channel", (6, 5, 8)), ("blocks", (8, 8, 8))])
+def test_two_rank_zslab_protocol_gloo(kind, dims):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port_no, kind, dims, 4, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    equal, rel = q.get(timeout=5)
+    assert equal, rel
