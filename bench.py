@@ -210,6 +210,8 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dims", default=None,
+                    help="override the box (NXxNYxNZ) -- profiling only, not a bench line")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -232,6 +234,9 @@ def main():
 
     cid = args.config
     kernel, kind, dims, extra, _, _ = CONFIGS[cid]
+    if args.dims:
+        dims = tuple(int(v) for v in args.dims.split("x"))
+        CONFIGS[cid] = (kernel, kind, dims, extra, CONFIGS[cid][4], CONFIGS[cid][5])
     desc = lbm.make_descriptor(kernel)
     aa = desc.prop == "aa"
     per = 2 if aa else 1

@@ -25,6 +25,13 @@
 extern "C" {
 #endif
 
+/* The library is built with -fvisibility=hidden: only these entry points are
+ * exported, so the internal C++ namespace can never be interposed by a host
+ * program that happens to define the same symbols. */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
 #define LBMGPU_ABI_VERSION 1
 #define LBMGPU_Q 19
 
@@ -223,7 +230,18 @@ int lbmgpu_synchronize(lbmgpu_ctx* ctx);
 
 /* 128-byte ncclUniqueId (NCCL loaded lazily with dlopen). */
 int lbmgpu_nccl_unique_id(void* out128);
-/* This rank's slab [z0, z1) and fluid count. */
+/* Process-local state access for split domains (nranks > 1): this process's
+ * fluid nodes in canonical order ("local rows"), their global canonical
+ * indices, and snapshot/load of exactly those rows (count = rows*19).  With
+ * one process the local rows are all N canonical nodes.  lbmgpu_snapshot /
+ * lbmgpu_load_state on a split domain touch only this process's rows of the
+ * full-size canonical buffer. */
+int lbmgpu_local_rows(lbmgpu_ctx* ctx, uint64_t* rows);
+int lbmgpu_local_canonical_index(lbmgpu_ctx* ctx, uint64_t* out_rows);
+int lbmgpu_snapshot_local(lbmgpu_ctx* ctx, double* host, uint64_t count);
+int lbmgpu_load_state_local(lbmgpu_ctx* ctx, const double* host,
+                            uint64_t count);
+/* This process's slab(s): part index < number of local parts. */
 int lbmgpu_part_info(lbmgpu_ctx* ctx, int part, int* z0, int* z1,
                      uint64_t* n_fluid_part);
 /* Halo exchange plan as (phase, src part, dst part, src plane, dst plane,
@@ -237,6 +255,10 @@ uint64_t lbmgpu_fnv1a(const void* data, uint64_t nbytes);
 
 const char* lbmgpu_last_error(void);
 int lbmgpu_abi_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 }

@@ -353,6 +353,61 @@ int lbmgpu_load_state(lbmgpu_ctx* c, const double* host, uint64_t count) {
   });
 }
 
+int lbmgpu_local_rows(lbmgpu_ctx* c, uint64_t* rows) {
+  return guard([&] {
+    need(c, "ctx");
+    need(rows, "rows");
+    *rows = c->eng->local_rows();
+  });
+}
+
+int lbmgpu_local_canonical_index(lbmgpu_ctx* c, uint64_t* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    c->eng->local_canonical_index(out);
+  });
+}
+
+static void local_transfer(lbmgpu_ctx* c, double* host, uint64_t count,
+                           bool to_host) {
+  const uint64_t R = c->eng->local_rows();
+  if (count != R * kQ)
+    throw ConfigError("local state: buffer holds " + std::to_string(count) +
+                      " values, this process has " + std::to_string(R * kQ));
+  need(host, "host buffer");
+  const uint64_t chunk = std::min(std::max<uint64_t>(R, 1), kChunkNodes);
+  DevBuf<double> stage(chunk * kQ);
+  cudaStream_t s = c->eng->stream();
+  for (uint64_t k0 = 0; k0 < R; k0 += chunk) {
+    const uint64_t n = std::min(chunk, R - k0);
+    if (to_host) {
+      c->eng->gather_local(k0, n, stage.get(), true);
+      LBM_CUDA(cudaMemcpyAsync(host + k0 * kQ, stage.get(), n * kQ * 8,
+                               cudaMemcpyDeviceToHost, s));
+    } else {
+      LBM_CUDA(cudaMemcpyAsync(stage.get(), host + k0 * kQ, n * kQ * 8,
+                               cudaMemcpyHostToDevice, s));
+      c->eng->gather_local(k0, n, stage.get(), false);
+    }
+    LBM_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+int lbmgpu_snapshot_local(lbmgpu_ctx* c, double* host, uint64_t count) {
+  return guard([&] {
+    need(c, "ctx");
+    local_transfer(c, host, count, true);
+  });
+}
+
+int lbmgpu_load_state_local(lbmgpu_ctx* c, const double* host, uint64_t count) {
+  return guard([&] {
+    need(c, "ctx");
+    local_transfer(c, const_cast<double*>(host), count, false);
+  });
+}
+
 int lbmgpu_load_perturbed(lbmgpu_ctx* c, uint64_t seed, double amplitude) {
   return guard([&] {
     need(c, "ctx");
@@ -373,6 +428,9 @@ int lbmgpu_fingerprint(lbmgpu_ctx* c, uint64_t* out) {
   return guard([&] {
     need(c, "ctx");
     need(out, "out");
+    if (!c->eng->holds_all())
+      throw ConfigError("fingerprint: the state is split across processes; "
+                        "gather the local rows (lbmgpu_snapshot_local) first");
     const uint64_t N = c->eng->n_fluid();
     const uint64_t chunk = std::min(N, kChunkNodes);
     cudaStream_t s = c->eng->stream();

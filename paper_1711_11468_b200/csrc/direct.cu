@@ -22,25 +22,14 @@
 //    (initial solid weights are swap-symmetric).  Bitwise parity with
 //    aa-soa / aa-aos is asserted by tests/test_gpu_parity.py.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
+#include "direct_args.cuh"
 #include "halo.hpp"
 #include "lbm.hpp"
 
 namespace lbmgpu {
-
-struct DirectArgs {
-  const double* src;
-  double* dst;
-  const uint8_t* flags;  // own planes, (z*ny + y)*nx + x, 1 = solid
-  uint32_t nx, ny, nzl;  // own extents
-  uint32_t zoff;         // storage plane of own plane 0
-  uint32_t zwrap;        // 1: single part, wrap z over own planes
-  uint32_t P;            // nx*ny
-  FastDiv fdx, fdP;      // n / nx, n / P
-  uint32_t node0, count; // own-node range of this launch
-  TrtArgs trt;
-};
 
 template <bool SOA>
 struct Idx {
@@ -162,8 +151,8 @@ __global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
 }
 
 // ---- AA pattern (kernels_full_aa.cpp:46-94), corrections dropped ----------
-template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_full_aa_even(const DirectArgs a) {
+template <bool SOA, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
@@ -179,8 +168,8 @@ __global__ void __launch_bounds__(256) k_full_aa_even(const DirectArgs a) {
     st<CS>(buf + I(c.Z[1], dslot(opp(d)), c.y, c.x), q[d]);
 }
 
-template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_full_aa_odd(const DirectArgs a) {
+template <bool SOA, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
@@ -344,15 +333,79 @@ int grid_for(uint64_t n, int threads) {
 }
 
 struct Part {
+  int index = 0;            // global slab index (== rank for NCCL)
   int z0 = 0, z1 = 0;
   uint32_t nzl = 0, zoff = 0, nzs = 0;
   DevBuf<double> buf[2];
   DevBuf<uint8_t> flags;
   DevBuf<uint32_t> node_of;
-  DevBuf<uint64_t> canon;  // empty when the part holds the whole box
+  DevBuf<uint64_t> canon;   // empty when the part holds the whole box
   uint64_t n_fluid = 0;
-  std::vector<uint64_t> canon_host_first;  // first canonical index per k-block
-  cudaStream_t stream = nullptr;
+  std::vector<uint64_t> canon_host;  // canonical index of each k (sorted)
+};
+
+// Halo transport between slabs.  exchange() enqueues one phase of the plan
+// after the work already on `s`; wait() makes `s` wait for its completion.
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual void exchange(int phase, std::vector<Part>& parts, uint64_t P,
+                        cudaStream_t s) = 0;
+  virtual void wait(int phase, cudaStream_t s) { (void)phase; (void)s; }
+  virtual double sum(double v) { return v; }
+};
+
+// All slabs on this device: the plan's rows become device-to-device copies on
+// the compute stream (used for single-GPU emulation of the decomposition).
+class LocalTransport final : public Transport {
+ public:
+  explicit LocalTransport(std::vector<HaloRow> plan) : plan_(std::move(plan)) {}
+  void exchange(int phase, std::vector<Part>& parts, uint64_t P,
+                cudaStream_t s) override {
+    for (const HaloRow& r : plan_) {
+      if (r.phase != phase) continue;
+      const Part& a = parts[r.src_part];
+      const Part& b = parts[r.dst_part];
+      const double* src = a.buf[0].get() + (uint64_t(r.src_plane) * kQ + r.slot0) * P;
+      double* dst = b.buf[0].get() + (uint64_t(r.dst_plane) * kQ + r.slot0) * P;
+      LBM_CUDA(cudaMemcpyAsync(dst, src, uint64_t(kHaloSlots) * P * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
+    }
+  }
+
+ private:
+  std::vector<HaloRow> plan_;
+};
+
+}  // namespace
+
+// NCCL transport (nccl.cpp): one process per GPU, slab = rank.
+class NcclTransportImpl;
+NcclTransportImpl* nccl_create(std::vector<HaloRow> plan, int rank, int nranks,
+                               const uint8_t* id128);
+void nccl_exchange(NcclTransportImpl* t, int phase, double* base, uint64_t P,
+                   cudaStream_t s);
+void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s);
+double nccl_sum(NcclTransportImpl* t, double v);
+void nccl_destroy(NcclTransportImpl* t);
+
+namespace {
+
+class NcclTransport final : public Transport {
+ public:
+  NcclTransport(std::vector<HaloRow> plan, int rank, int nranks,
+                const uint8_t* id128)
+      : t_(nccl_create(std::move(plan), rank, nranks, id128)) {}
+  ~NcclTransport() override { nccl_destroy(t_); }
+  void exchange(int phase, std::vector<Part>& parts, uint64_t P,
+                cudaStream_t s) override {
+    nccl_exchange(t_, phase, parts[0].buf[0].get(), P, s);
+  }
+  void wait(int phase, cudaStream_t s) override { nccl_wait(t_, phase, s); }
+  double sum(double v) override { return nccl_sum(t_, v); }
+
+ private:
+  NcclTransportImpl* t_;
 };
 
 class DirectEngine final : public Engine {
@@ -360,18 +413,29 @@ class DirectEngine final : public Engine {
   DirectEngine(const Descriptor& d, const GeomSpec& g, const DistSpec& dist) {
     desc_ = d;
     LBM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    nparts_ = std::max(1, dist.virtual_parts);
-    if (dist.nranks > 1)
-      throw ConfigError("multi-process direct AA is provided by the NCCL halo "
-                        "path (lbmgpu_dist.nranks > 1) -- not built in this "
-                        "configuration");
+    rank_ = dist.rank;
+    nranks_ = dist.nranks;
+    nparts_ = nranks_ > 1 ? nranks_ : std::max(1, dist.virtual_parts);
     if (nparts_ > 1 && d.prop != Prop::Aa)
       throw ConfigError("z-slab decomposition is implemented for the AA "
                         "pattern only (kernel '" + d.name + "')");
     if (nparts_ > 1 && !d.soa)
       throw ConfigError("z-slab decomposition needs the SoA layout");
-    if (nparts_ > g.nz)
-      throw ConfigError("more z-slab parts than z planes");
+    if (nparts_ > g.nz) throw ConfigError("more z-slab parts than z planes");
+    if (nranks_ > 1 && !dist.have_id)
+      throw ConfigError("dist: nranks > 1 needs the NCCL unique id");
+    {
+      int dev = 0;
+      LBM_CUDA(cudaGetDevice(&dev));
+      LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
+      // tuning knobs (defaults are the measured best)
+      if (const char* e = std::getenv("LBMGPU_AA_TMA_STAGES")) tma_stages_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_AA_CS")) cs_ = std::atoi(e) != 0;
+      if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
+      if (tma_stages_ != 0 && tma_stages_ != 3 && tma_stages_ != 4 &&
+          tma_stages_ != 5 && tma_stages_ != 12)
+        tma_stages_ = 4;
+    }
 
     DeviceGeometry geo = build_geometry_device(g, stream_);
     nx_ = geo.nx;
@@ -379,42 +443,47 @@ class DirectEngine final : public Engine {
     nz_ = geo.nz;
     n_fluid_ = static_cast<uint64_t>(geo.n_fluid);
     P_ = uint64_t(nx_) * ny_;
-    if (P_ * uint64_t(nz_) >= (1ull << 31) * (uint64_t)nparts_ ||
-        P_ * uint64_t(nz_) / nparts_ >= (1ull << 31))
-      throw ConfigError("direct lattice: more than 2^31 nodes per part");
+    for (int p = 0; p < nparts_; ++p)
+      if (P_ * (uint64_t(nz_) * (p + 1) / nparts_ - uint64_t(nz_) * p / nparts_) >=
+          (1ull << 31))
+        throw ConfigError("direct lattice: more than 2^31 nodes in one slab");
 
     const uint64_t V = geo.volume();
     DevBuf<uint32_t> crank(V);
     scan_fluid(geo.flags.get(), crank.get(), V, stream_);
 
-    // z-wrap exchange is needed unless the end planes are entirely solid
-    zring_ = true;
-    parts_.resize(nparts_);
-    for (int p = 0; p < nparts_; ++p) {
-      Part& pt = parts_[p];
+    // which slabs live in this process
+    std::vector<int> mine;
+    if (nranks_ > 1)
+      mine.push_back(rank_);
+    else
+      for (int p = 0; p < nparts_; ++p) mine.push_back(p);
+    parts_.resize(mine.size());
+    for (size_t i = 0; i < mine.size(); ++i) {
+      Part& pt = parts_[i];
+      const int p = mine[i];
+      pt.index = p;
       pt.z0 = static_cast<int>(int64_t(nz_) * p / nparts_);
       pt.z1 = static_cast<int>(int64_t(nz_) * (p + 1) / nparts_);
       pt.nzl = pt.z1 - pt.z0;
       pt.zoff = nparts_ > 1 ? 1 : 0;
       pt.nzs = pt.nzl + 2 * pt.zoff;
-      pt.stream = stream_;
       const uint64_t slots = uint64_t(pt.nzs) * P_ * kQ;
       const int nbuf = d.prop == Prop::Aa ? 1 : 2;
       for (int b = 0; b < nbuf; ++b) {
         pt.buf[b].alloc(slots);
+        const int gr = grid_for(uint64_t(pt.nzs) * P_, 256);
         if (d.soa)
-          k_full_init<true><<<grid_for(uint64_t(pt.nzs) * P_, 256), 256, 0,
-                              stream_>>>(pt.buf[b].get(), nx_, ny_, pt.nzs, P_);
+          k_full_init<true><<<gr, 256, 0, stream_>>>(pt.buf[b].get(), nx_, ny_, pt.nzs, P_);
         else
-          k_full_init<false><<<grid_for(uint64_t(pt.nzs) * P_, 256), 256, 0,
-                               stream_>>>(pt.buf[b].get(), nx_, ny_, pt.nzs, P_);
+          k_full_init<false><<<gr, 256, 0, stream_>>>(pt.buf[b].get(), nx_, ny_, pt.nzs, P_);
         LBM_CHECK_LAUNCH();
       }
       pt.flags.alloc(uint64_t(pt.nzl) * P_);
       k_part_flags<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
           geo.flags.get(), nx_, ny_, nz_, pt.z0, pt.z1, pt.flags.get());
       LBM_CHECK_LAUNCH();
-      // per-part fluid list in canonical order
+      // the slab's fluid nodes in canonical order
       DevBuf<uint8_t> mask(V);
       DevBuf<uint32_t> prank(V);
       k_part_mask<<<grid_for(V, 256), 256, 0, stream_>>>(geo.flags.get(), nz_,
@@ -423,22 +492,22 @@ class DirectEngine final : public Engine {
       LBM_CHECK_LAUNCH();
       pt.n_fluid = scan_fluid(mask.get(), prank.get(), V, stream_);
       pt.node_of.alloc(std::max<uint64_t>(pt.n_fluid, 1));
-      if (nparts_ > 1) pt.canon.alloc(std::max<uint64_t>(pt.n_fluid, 1));
+      const bool whole = nparts_ == 1;
+      if (!whole) pt.canon.alloc(std::max<uint64_t>(pt.n_fluid, 1));
       k_part_lists<<<grid_for(V, 256), 256, 0, stream_>>>(
           geo.flags.get(), crank.get(), prank.get(), nx_, ny_, nz_, pt.z0,
-          pt.z1, pt.node_of.get(), nparts_ > 1 ? pt.canon.get() : nullptr);
+          pt.z1, pt.node_of.get(), whole ? nullptr : pt.canon.get());
       LBM_CHECK_LAUNCH();
-      if (nparts_ > 1) {
-        std::vector<uint64_t> h(pt.n_fluid);
+      if (!whole) {
+        pt.canon_host.resize(pt.n_fluid);
         if (pt.n_fluid)
-          LBM_CUDA(cudaMemcpyAsync(h.data(), pt.canon.get(), pt.n_fluid * 8,
-                                   cudaMemcpyDeviceToHost, stream_));
+          LBM_CUDA(cudaMemcpyAsync(pt.canon_host.data(), pt.canon.get(),
+                                   pt.n_fluid * 8, cudaMemcpyDeviceToHost, stream_));
         LBM_CUDA(cudaStreamSynchronize(stream_));
-        pt.canon_host_first = std::move(h);
       }
     }
     if (nparts_ > 1) {
-      // ring exchange only if a fluid node sits on the z=0 or z=nz-1 plane
+      // z-wrap exchange only if a fluid node sits on the z=0 or z=nz-1 plane
       std::vector<uint8_t> hf(V);
       LBM_CUDA(cudaMemcpyAsync(hf.data(), geo.flags.get(), V,
                                cudaMemcpyDeviceToHost, stream_));
@@ -446,22 +515,28 @@ class DirectEngine final : public Engine {
       bool end_fluid = false;
       for (uint64_t i = 0; i < V && !end_fluid; i += nz_)
         end_fluid = hf[i] == 0 || hf[i + nz_ - 1] == 0;
-      zring_ = end_fluid;
-      plan_ = halo_plan(nz_, nparts_, zring_);
+      std::vector<HaloRow> plan = halo_plan(nz_, nparts_, end_fluid);
+      if (nranks_ > 1)
+        tr_ = std::make_unique<NcclTransport>(std::move(plan), rank_, nranks_,
+                                              dist.nccl_id.data());
+      else
+        tr_ = std::make_unique<LocalTransport>(std::move(plan));
     }
     LBM_CUDA(cudaStreamSynchronize(stream_));
   }
 
   ~DirectEngine() override {
+    tr_.reset();
     if (stream_) cudaStreamDestroy(stream_);
   }
 
-  int parts() const override { return nparts_; }
+  int parts() const override { return static_cast<int>(parts_.size()); }
   void part_info(int p, int* z0, int* z1, uint64_t* nf) const override {
     *z0 = parts_.at(p).z0;
     *z1 = parts_.at(p).z1;
     *nf = parts_.at(p).n_fluid;
   }
+  bool holds_all() const override { return nranks_ == 1; }
 
   DirectArgs args(const Part& pt, uint32_t node0, uint32_t count,
                   const TrtArgs& t, int src_buf, int dst_buf) const {
@@ -493,6 +568,41 @@ class DirectEngine final : public Engine {
     stats_.end(tok, s);
   }
 
+  // One SoA AA sub-step over a node range: the TMA-staged persistent kernel
+  // when the row shape allows it (direct_tma.cu), else the register kernel.
+  void aa_sub(bool odd, const DirectArgs& a, const char* name) {
+    if (a.count == 0) return;
+    if (tma_stages_ > 0 && a.nx % kTmaTile == 0 && a.node0 % kTmaTile == 0 &&
+        a.count % kTmaTile == 0) {
+      const int tok = stats_.begin(name, stream_);
+      launch_aa_tma(odd, a, sm_count_, tma_stages_, stream_);
+      stats_.end(tok, stream_);
+      return;
+    }
+    if (cs_) {
+      odd ? launch(name, k_full_aa_odd<true, true>, a, stream_)
+          : launch(name, k_full_aa_even<true, true>, a, stream_);
+      return;
+    }
+    switch (minb_) {
+      case 2:
+        odd ? launch(name, k_full_aa_odd<true, false, 2>, a, stream_)
+            : launch(name, k_full_aa_even<true, false, 2>, a, stream_);
+        break;
+      case 3:
+        odd ? launch(name, k_full_aa_odd<true, false, 3>, a, stream_)
+            : launch(name, k_full_aa_even<true, false, 3>, a, stream_);
+        break;
+      case 4:
+        odd ? launch(name, k_full_aa_odd<true, false, 4>, a, stream_)
+            : launch(name, k_full_aa_even<true, false, 4>, a, stream_);
+        break;
+      default:
+        odd ? launch(name, k_full_aa_odd<true, false>, a, stream_)
+            : launch(name, k_full_aa_even<true, false>, a, stream_);
+    }
+  }
+
   void advance(const TrtArgs& t, long steps) override {
     const bool soa = desc_.soa;
     const bool cs = cs_;
@@ -511,6 +621,8 @@ class DirectEngine final : public Engine {
       return;
     }
     if (desc_.prop == Prop::OsPull) {
+      // collide pass, T-1 fused sweeps, one stream-only sweep
+      // (kernels_full_os.cpp:173-190)
       const Part& pt = parts_[0];
       const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
       {
@@ -544,48 +656,52 @@ class DirectEngine final : public Engine {
         const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
         DirectArgs a = args(pt, 0, N, t, 0, 0);
         if (soa) {
-          cs ? launch("full_aa_even_soa", k_full_aa_even<true, true>, a, stream_)
-             : launch("full_aa_even_soa", k_full_aa_even<true, false>, a, stream_);
-          cs ? launch("full_aa_odd_soa", k_full_aa_odd<true, true>, a, stream_)
-             : launch("full_aa_odd_soa", k_full_aa_odd<true, false>, a, stream_);
+          aa_sub(false, a, "full_aa_even_soa");
+          aa_sub(true, a, "full_aa_odd_soa");
         } else {
           launch("full_aa_even_aos", k_full_aa_even<false, false>, a, stream_);
           launch("full_aa_odd_aos", k_full_aa_odd<false, false>, a, stream_);
         }
       } else {
-        aa_pair_parts(t);
+        aa_pair_slabs(t);
       }
     }
   }
 
-  // Emulated z-slab decomposition on one device: the same sub-step split and
-  // exchange plan the NCCL path uses (halo.cpp), transport = device copies.
-  void aa_pair_parts(const TrtArgs& t) {
-    for (Part& pt : parts_) {
-      const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
-      launch("full_aa_even_soa", k_full_aa_even<true, false>,
-             args(pt, 0, N, t, 0, 0), stream_);
-    }
-    run_exchange(0);
-    for (Part& pt : parts_) {
-      const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
-      launch("full_aa_odd_soa", k_full_aa_odd<true, false>,
-             args(pt, 0, N, t, 0, 0), stream_);
-    }
-    run_exchange(1);
-  }
-
-  void run_exchange(int phase) {
-    for (const HaloRow& r : plan_) {
-      if (r.phase != phase) continue;
-      const Part& a = parts_[r.src_part];
-      const Part& b = parts_[r.dst_part];
-      const uint64_t elems = uint64_t(kHaloSlots) * P_;
-      const double* src = a.buf[0].get() + (uint64_t(r.src_plane) * kQ + r.slot0) * P_;
-      double* dst = b.buf[0].get() + (uint64_t(r.dst_plane) * kQ + r.slot0) * P_;
-      LBM_CUDA(cudaMemcpyAsync(dst, src, elems * sizeof(double),
-                               cudaMemcpyDeviceToDevice, stream_));
-    }
+  // One AA pair over z-slabs (SURVEY.md 8(e) overlap schedule):
+  //   even(boundary planes) -> [exchange 0 || even(interior)] ->
+  //   odd(boundary planes)  -> [exchange 1 || odd(interior)]
+  // odd(boundary) reads interior slots written by even(interior), so it
+  // follows it on the compute stream; the exchanged slot sets are touched by
+  // no interior node, so the transfers never race with the interior sweeps.
+  void aa_pair_slabs(const TrtArgs& t) {
+    const uint32_t P = static_cast<uint32_t>(P_);
+    auto sweep = [&](bool odd, bool boundary) {
+      for (Part& pt : parts_) {
+        const uint32_t last = (pt.nzl - 1) * P;
+        auto run = [&](uint32_t n0, uint32_t cnt) {
+          DirectArgs a = args(pt, n0, cnt, t, 0, 0);
+          if (odd)
+            aa_sub(true, a, boundary ? "full_aa_odd_soa_halo" : "full_aa_odd_soa");
+          else
+            aa_sub(false, a, boundary ? "full_aa_even_soa_halo" : "full_aa_even_soa");
+        };
+        if (boundary) {
+          run(0, P);
+          if (pt.nzl > 1) run(last, P);
+        } else if (pt.nzl > 2) {
+          run(P, last - P);
+        }
+      }
+    };
+    sweep(false, true);
+    tr_->exchange(0, parts_, P_, stream_);
+    sweep(false, false);
+    tr_->wait(0, stream_);
+    sweep(true, true);
+    tr_->exchange(1, parts_, P_, stream_);
+    sweep(true, false);
+    tr_->wait(1, stream_);
   }
 
   CanonArgs canon_args(const Part& pt, int buf) const {
@@ -610,7 +726,7 @@ class DirectEngine final : public Engine {
       c.k0 = c0;
       c.k1 = std::min<uint64_t>(c0 + count, pt.n_fluid);
     } else {
-      const auto& h = pt.canon_host_first;
+      const auto& h = pt.canon_host;
       c.k0 = std::lower_bound(h.begin(), h.end(), c0) - h.begin();
       c.k1 = std::lower_bound(h.begin(), h.end(), c0 + count) - h.begin();
     }
@@ -642,6 +758,49 @@ class DirectEngine final : public Engine {
     }
   }
 
+  // Process-local rows (multi-process): rows k in [k0, k0+count) of this
+  // process's slab in canonical order, staged contiguously.
+  uint64_t local_rows() const override {
+    uint64_t n = 0;
+    for (const Part& pt : parts_) n += pt.n_fluid;
+    return n;
+  }
+  void local_canonical_index(uint64_t* out) const override {
+    uint64_t off = 0;
+    for (const Part& pt : parts_) {
+      if (nparts_ == 1)
+        for (uint64_t k = 0; k < pt.n_fluid; ++k) out[off + k] = k;
+      else
+        std::copy(pt.canon_host.begin(), pt.canon_host.end(), out + off);
+      off += pt.n_fluid;
+    }
+  }
+  void gather_local(uint64_t k0, uint64_t count, double* out, bool to_staging) override {
+    // local rows are the concatenation of the parts' k-ranges
+    uint64_t base = 0;
+    for (const Part& pt : parts_) {
+      const uint64_t a = std::max(k0, base), b = std::min(k0 + count, base + pt.n_fluid);
+      if (a < b) {
+        CanonArgs c = canon_args(pt, cur_);
+        c.canon = nullptr;       // staging row = k - k0 (+ offset)
+        c.kbase = 0;
+        c.k0 = a - base;
+        c.k1 = b - base;
+        c.c0 = c.k0;
+        double* dst = out + (a - k0) * kQ;
+        const int g = grid_for(b - a, 256);
+        if (to_staging)
+          desc_.soa ? k_full_canon<true, true><<<g, 256, 0, stream_>>>(c, dst)
+                    : k_full_canon<false, true><<<g, 256, 0, stream_>>>(c, dst);
+        else
+          desc_.soa ? k_full_canon<true, false><<<g, 256, 0, stream_>>>(c, dst)
+                    : k_full_canon<false, false><<<g, 256, 0, stream_>>>(c, dst);
+        LBM_CHECK_LAUNCH();
+      }
+      base += pt.n_fluid;
+    }
+  }
+
   void load_perturbed(uint64_t seed, double amp) override {
     for (const Part& pt : parts_) {
       CanonArgs c = canon_args(pt, cur_);
@@ -654,6 +813,8 @@ class DirectEngine final : public Engine {
   }
 
   void macro_fields(double* rho, double* u) override {
+    if (nranks_ > 1)
+      throw ConfigError("macro_fields: the field is split across processes");
     for (const Part& pt : parts_) {
       CanonArgs c = canon_args(pt, cur_);
       if (c.k1 == 0) continue;
@@ -665,7 +826,7 @@ class DirectEngine final : public Engine {
   }
 
   // Mass over fluid and solid nodes of the current buffer (full_lattice.cpp:
-  // 72-87), own planes only, compensated device sum.
+  // 72-87), own planes only, compensated device sum; summed over processes.
   double total_mass() override {
     double m = 0.0;
     for (const Part& pt : parts_) {
@@ -673,18 +834,23 @@ class DirectEngine final : public Engine {
       m += device_sum(pt.buf[cur_].get() + uint64_t(pt.zoff) * per_plane,
                       uint64_t(pt.nzl) * per_plane, stream_);
     }
-    return m;
+    return tr_ && nranks_ > 1 ? tr_->sum(m) : m;
   }
 
  private:
   int nx_ = 0, ny_ = 0, nz_ = 0;
   uint64_t P_ = 0;
-  int nparts_ = 1;
+  int nparts_ = 1, rank_ = 0, nranks_ = 1;
   int cur_ = 0;
-  bool cs_ = false;
-  bool zring_ = false;
+  bool cs_ = false;       // st.global.cs stores in the register AA kernels
+  int tma_stages_ = 0;    // >0: TMA-staged AA kernels (direct_tma.cu)
+  // min CTAs/SM of the register AA kernels: 2 caps them at 128 registers,
+  // i.e. 16 resident warps/SM (measured best on B200: 1 -> 140 registers and
+  // 8 warps runs 33% slower; 3 -> 80 registers spills and hits the power cap)
+  int minb_ = 2;
+  int sm_count_ = 148;
   std::vector<Part> parts_;
-  std::vector<HaloRow> plan_;
+  std::unique_ptr<Transport> tr_;
 };
 
 }  // namespace

@@ -183,9 +183,22 @@ class Engine {
   virtual void part_info(int p, int* z0, int* z1, uint64_t* nf) const {
     (void)p; *z0 = 0; *z1 = 0; *nf = n_fluid_;
   }
-  // Number of canonical nodes this process holds (== n_fluid() unless the
-  // domain is split across processes).
+  // Whether this process holds every canonical node (false when the domain
+  // is split across processes).
   virtual bool holds_all() const { return true; }
+  // Process-local rows: this process's fluid nodes in canonical order.
+  virtual uint64_t local_rows() const { return n_fluid_; }
+  virtual void local_canonical_index(uint64_t* out) const {
+    for (uint64_t k = 0; k < n_fluid_; ++k) out[k] = k;
+  }
+  // Local rows [k0, k0+count) <-> device staging (count*19, node-major).
+  virtual void gather_local(uint64_t k0, uint64_t count, double* d,
+                            bool to_staging) {
+    if (to_staging)
+      gather_canonical(k0, count, d);
+    else
+      scatter_canonical(k0, count, d);
+  }
 
  protected:
   Descriptor desc_;

@@ -95,6 +95,10 @@ def _load():
     L.lbmgpu_synchronize.argtypes = [vp]
     L.lbmgpu_nccl_unique_id.argtypes = [vp]
     L.lbmgpu_part_info.argtypes = [vp, i, P(i), P(i), P(u64)]
+    L.lbmgpu_local_rows.argtypes = [vp, P(u64)]
+    L.lbmgpu_local_canonical_index.argtypes = [vp, vp]
+    L.lbmgpu_snapshot_local.argtypes = [vp, vp, u64]
+    L.lbmgpu_load_state_local.argtypes = [vp, vp, u64]
     L.lbmgpu_halo_plan.argtypes = [i, i, i, vp, i, P(i)]
     return L
 
@@ -472,6 +476,30 @@ class Kernel:
     def load_state(self, state) -> None:
         s = np.ascontiguousarray(state, np.float64)
         _check(lib.lbmgpu_load_state(self._h, s.ctypes.data, s.size))
+
+    # process-local rows (split domains; == the whole state with one process)
+    def local_rows(self) -> int:
+        v = C.c_uint64()
+        _check(lib.lbmgpu_local_rows(self._h, C.byref(v)))
+        return v.value
+
+    def local_state_size(self) -> int:
+        return self.local_rows() * Q
+
+    def local_canonical_index(self) -> np.ndarray:
+        out = np.zeros(self.local_rows(), np.uint64)
+        _check(lib.lbmgpu_local_canonical_index(self._h, out.ctypes.data))
+        return out
+
+    def snapshot_local(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.local_state_size(), np.float64)
+        _check(lib.lbmgpu_snapshot_local(self._h, out.ctypes.data, out.size))
+        return out
+
+    def load_state_local(self, state) -> None:
+        s = np.ascontiguousarray(state, np.float64)
+        _check(lib.lbmgpu_load_state_local(self._h, s.ctypes.data, s.size))
 
     def load_perturbed(self, seed: int, amplitude: float = 1e-3) -> None:
         _check(lib.lbmgpu_load_perturbed(self._h, seed, amplitude))

@@ -285,3 +285,21 @@ def test_baseline_config_fingerprint(cid):
     k.advance(lbm.TrtParams(1.0, 3.0 / 16.0), lbm.BodyForce(tuple(c["g"])), c["steps"])
     assert f"{k.fingerprint():016x}" == c["fingerprint"]
     assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
+
+
+def test_local_rows_round_trip_on_split_domain():
+    """Process-local row access (the multi-process e2e path) on an emulated
+    3-slab split: rows are the slabs' fluid nodes in canonical order."""
+    spec = lbm.GeometrySpec("channel", 16, 12, 24)
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec, dist={"virtual_parts": 3})
+    k.load_perturbed(7)
+    k.advance(PARAMS, FORCE, 4)
+    full = k.snapshot().reshape(-1, 19)
+    idx = k.local_canonical_index()
+    assert k.local_rows() == k.n_fluid() and np.array_equal(np.sort(idx), np.arange(k.n_fluid()))
+    loc = k.snapshot_local().reshape(-1, 19)
+    assert np.array_equal(full[idx], loc)
+    k.load_state_local(np.zeros(loc.size))
+    assert np.count_nonzero(k.snapshot()) == 0
+    k.load_state_local(loc.reshape(-1))
+    assert np.array_equal(k.snapshot().reshape(-1, 19), full)

@@ -1,0 +1,33 @@
+"""Multi-GPU (NCCL) z-slab parity: skipped unless >= 2 GPUs are visible.
+Runs tools/mgpu_check.py under torchrun for 2, 4 and 8 ranks (as many as
+fit) and requires the assembled state to equal the single-GPU run bit for
+bit -- the worker-count invariance of the reference (tests/test_kernels.cpp:
+177-195) carried to GPUs."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("kind,dims", [("channel", (64, 32, 48)), ("blocks", (32, 32, 32))])
+def test_nccl_zslab_bitwise(n, kind, dims):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), *map(str, dims), "10", kind]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
