@@ -287,6 +287,65 @@ def test_baseline_config_fingerprint(cid):
     assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
 
 
+def test_custom_flagfield_path(port):
+    """make_kernel takes any FlagField (kernels.hpp:102-105): a host flag
+    field uploaded through LBMGPU_CUSTOM gives the same results as the device
+    generator, and an irregular hand-made geometry matches the oracle."""
+    spec = lbm.GeometrySpec("pipe", 9, 12, 13)
+    ff = lbm.build_geometry(spec)
+    fl, per, nf = port.geometry("pipe", 9, 12, 13)
+    assert np.array_equal(ff.flags, fl) and ff.periodic == tuple(bool(p) for p in per)
+    for name in ("aa-soa", "list-pull-soa", "blk-push-aos"):
+        a = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        b = lbm.make_kernel(lbm.make_descriptor(name), ff)
+        for k in (a, b):
+            k.load_perturbed(3)
+            k.advance(PARAMS, FORCE, 6)
+        assert np.array_equal(a.snapshot(), b.snapshot()), name
+    # random obstacles inside a fully periodic box: compare to the oracle's
+    # half-way stepper through the reference neighbor rule
+    rng = np.random.default_rng(5)
+    flags = (rng.random(10 * 9 * 8) < 0.2).astype(np.uint8)
+    custom = lbm.FlagField(10, 9, 8, (True, True, True), flags)
+    k = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), custom)
+    nfl = int(np.count_nonzero(flags == 0))
+    assert k.n_fluid() == nfl
+    k.load_perturbed(11)
+    k.advance(PARAMS, FORCE, 4)
+    got = k.snapshot()
+    # oracle on the same flags: reuse the C stepper through a blocks spec is
+    # impossible, so compare against a direct per-node restatement
+    init = lbm.perturbed_equilibrium(nfl, 11)
+    expect = _halfway_reference(port, flags, (10, 9, 8), init, 4)
+    assert np.array_equal(got, expect)
+
+
+def _halfway_reference(port, flags, dims, init, steps):
+    """Half-way bounce-back textbook stepper (tests/support/reference.hpp:72-105)
+    in numpy + the oracle collision, fully periodic."""
+    nx, ny, nz = dims
+    cxs = [0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0]
+    cys = [0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1]
+    czs = [0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1]
+    opp = [0, 2, 1, 4, 3, 6, 5, 8, 7, 10, 9, 12, 11, 14, 13, 16, 15, 18, 17]
+    solid = flags.reshape(nx, ny, nz)
+    fluid = [(x, y, z) for x in range(nx) for y in range(ny) for z in range(nz) if not solid[x, y, z]]
+    f = {c: init[i * 19:(i + 1) * 19].copy() for i, c in enumerate(fluid)}
+    wp, wm = PARAMS.omega_plus, port.omega_minus(PARAMS.omega_plus)
+    for _ in range(steps):
+        post = {c: port.collide(v, wp, wm, G_TEST) for c, v in f.items()}
+        nxt = {}
+        for (x, y, z) in fluid:
+            q = np.empty(19)
+            q[0] = post[(x, y, z)][0]
+            for d in range(1, 19):
+                s = ((x - cxs[d]) % nx, (y - cys[d]) % ny, (z - czs[d]) % nz)
+                q[d] = post[s][d] if not solid[s] else post[(x, y, z)][opp[d]]
+            nxt[(x, y, z)] = q
+        f = nxt
+    return np.concatenate([f[c] for c in fluid])
+
+
 def test_local_rows_round_trip_on_split_domain():
     """Process-local row access (the multi-process e2e path) on an emulated
     3-slab split: rows are the slabs' fluid nodes in canonical order."""
