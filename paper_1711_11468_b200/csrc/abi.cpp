@@ -19,6 +19,10 @@ struct lbmgpu_ctx {
   Descriptor desc;
   GeomSpec geom;
   DevBuf<double> rho, u, uprev;  // steady-state scratch
+  cudaStream_t copy = nullptr;   // host<->device staging copies
+  ~lbmgpu_ctx() {
+    if (copy) cudaStreamDestroy(copy);
+  }
 };
 
 namespace {
@@ -119,6 +123,63 @@ struct HostPinned {
     if (p) cudaFreeHost(p);
   }
 };
+
+// Host <-> device transfer of `rows` node rows (19 doubles each) through two
+// staging buffers: the layout conversion (dev: gather/scatter kernel) runs on
+// the engine stream, the PCIe copies on a copy stream, so chunk k's copy
+// overlaps chunk k+1's kernel.  dev(row0, n, staging, to_host).
+template <class Dev>
+void pipelined(lbmgpu_ctx* c, double* host, uint64_t rows, bool to_host, Dev dev) {
+  if (rows == 0) return;
+  if (!c->copy) LBM_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  const uint64_t chunk = std::min(rows, kChunkNodes);
+  DevBuf<double> st[2];
+  st[0].alloc(chunk * kQ);
+  if (rows > chunk) st[1].alloc(chunk * kQ);
+  cudaStream_t s = c->eng->stream(), cs = c->copy;
+  cudaEvent_t ready[2], freed[2];
+  for (int b = 0; b < 2; ++b) {
+    LBM_CUDA(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
+    LBM_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+  }
+  try {
+    uint64_t k = 0;
+    for (uint64_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
+      const int b = static_cast<int>(k & 1);
+      const uint64_t n = std::min(chunk, rows - r0);
+      double* sb = st[b].get();
+      if (to_host) {
+        if (k >= 2) LBM_CUDA(cudaStreamWaitEvent(s, freed[b], 0));
+        dev(r0, n, sb, true);
+        LBM_CUDA(cudaEventRecord(ready[b], s));
+        LBM_CUDA(cudaStreamWaitEvent(cs, ready[b], 0));
+        LBM_CUDA(cudaMemcpyAsync(host + r0 * kQ, sb, n * kQ * 8, cudaMemcpyDeviceToHost, cs));
+        LBM_CUDA(cudaEventRecord(freed[b], cs));
+      } else {
+        if (k >= 2) LBM_CUDA(cudaStreamWaitEvent(cs, freed[b], 0));
+        LBM_CUDA(cudaMemcpyAsync(sb, host + r0 * kQ, n * kQ * 8, cudaMemcpyHostToDevice, cs));
+        LBM_CUDA(cudaEventRecord(ready[b], cs));
+        LBM_CUDA(cudaStreamWaitEvent(s, ready[b], 0));
+        dev(r0, n, sb, false);
+        LBM_CUDA(cudaEventRecord(freed[b], s));
+      }
+    }
+    LBM_CUDA(cudaStreamSynchronize(cs));
+    LBM_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(s);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(ready[b]);
+      cudaEventDestroy(freed[b]);
+    }
+    throw;
+  }
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(ready[b]);
+    cudaEventDestroy(freed[b]);
+  }
+}
 
 uint64_t fnv_bytes(uint64_t h, const unsigned char* p, size_t n) {
   for (size_t i = 0; i < n; ++i) {
@@ -320,16 +381,9 @@ int lbmgpu_snapshot(lbmgpu_ctx* c, double* host, uint64_t count) {
       throw ConfigError("snapshot: buffer holds " + std::to_string(count) +
                         " values, lattice has " + std::to_string(N * kQ));
     need(host, "host buffer");
-    const uint64_t chunk = std::min(N, kChunkNodes);
-    DevBuf<double> stage(chunk * kQ);
-    cudaStream_t s = c->eng->stream();
-    for (uint64_t c0 = 0; c0 < N; c0 += chunk) {
-      const uint64_t n = std::min(chunk, N - c0);
-      c->eng->gather_canonical(c0, n, stage.get());
-      LBM_CUDA(cudaMemcpyAsync(host + c0 * kQ, stage.get(), n * kQ * 8,
-                               cudaMemcpyDeviceToHost, s));
-      LBM_CUDA(cudaStreamSynchronize(s));
-    }
+    pipelined(c, host, N, true, [&](uint64_t c0, uint64_t n, double* st, bool) {
+      c->eng->gather_canonical(c0, n, st);
+    });
   });
 }
 
@@ -340,16 +394,10 @@ int lbmgpu_load_state(lbmgpu_ctx* c, const double* host, uint64_t count) {
     if (count != N * kQ)
       throw ConfigError("load_state: state size does not match fluid count");
     need(host, "host buffer");
-    const uint64_t chunk = std::min(N, kChunkNodes);
-    DevBuf<double> stage(chunk * kQ);
-    cudaStream_t s = c->eng->stream();
-    for (uint64_t c0 = 0; c0 < N; c0 += chunk) {
-      const uint64_t n = std::min(chunk, N - c0);
-      LBM_CUDA(cudaMemcpyAsync(stage.get(), host + c0 * kQ, n * kQ * 8,
-                               cudaMemcpyHostToDevice, s));
-      c->eng->scatter_canonical(c0, n, stage.get());
-      LBM_CUDA(cudaStreamSynchronize(s));
-    }
+    pipelined(c, const_cast<double*>(host), N, false,
+              [&](uint64_t c0, uint64_t n, double* st, bool) {
+                c->eng->scatter_canonical(c0, n, st);
+              });
   });
 }
 
@@ -376,22 +424,9 @@ static void local_transfer(lbmgpu_ctx* c, double* host, uint64_t count,
     throw ConfigError("local state: buffer holds " + std::to_string(count) +
                       " values, this process has " + std::to_string(R * kQ));
   need(host, "host buffer");
-  const uint64_t chunk = std::min(std::max<uint64_t>(R, 1), kChunkNodes);
-  DevBuf<double> stage(chunk * kQ);
-  cudaStream_t s = c->eng->stream();
-  for (uint64_t k0 = 0; k0 < R; k0 += chunk) {
-    const uint64_t n = std::min(chunk, R - k0);
-    if (to_host) {
-      c->eng->gather_local(k0, n, stage.get(), true);
-      LBM_CUDA(cudaMemcpyAsync(host + k0 * kQ, stage.get(), n * kQ * 8,
-                               cudaMemcpyDeviceToHost, s));
-    } else {
-      LBM_CUDA(cudaMemcpyAsync(stage.get(), host + k0 * kQ, n * kQ * 8,
-                               cudaMemcpyHostToDevice, s));
-      c->eng->gather_local(k0, n, stage.get(), false);
-    }
-    LBM_CUDA(cudaStreamSynchronize(s));
-  }
+  pipelined(c, host, R, to_host, [&](uint64_t k0, uint64_t n, double* st, bool th) {
+    c->eng->gather_local(k0, n, st, th);
+  });
 }
 
 int lbmgpu_snapshot_local(lbmgpu_ctx* c, double* host, uint64_t count) {

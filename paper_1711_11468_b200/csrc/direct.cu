@@ -176,17 +176,20 @@ __global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
   if (a.flags[n]) return;
   const Idx<SOA> I{a.P, a.nx, a.ny};
   double* buf = a.dst;
+  // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
+  // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
+  // per direction serves both the load and the store.
+  double* p[kQ];
+  p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
   double q[kQ];
-  q[0] = buf[I(c.Z[1], dslot(0), c.y, c.x)];
 #pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    q[d] = buf[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+  for (int d = 0; d < kQ; ++d) q[d] = *p[d];
   collide(q, a.trt);
-  st<CS>(buf + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
 #pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    st<CS>(buf + I(c.Z[1 + cz(d)], dslot(d), c.Y[1 + cy(d)], c.X[1 + cx(d)]),
-           q[d]);
+  for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
 }
 
 // ---- init / canonical transfer / perturbation / macro --------------------
