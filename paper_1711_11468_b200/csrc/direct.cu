@@ -386,8 +386,8 @@ class LocalTransport final : public Transport {
 class NcclTransportImpl;
 NcclTransportImpl* nccl_create(std::vector<HaloRow> plan, int rank, int nranks,
                                const uint8_t* id128);
-void nccl_exchange(NcclTransportImpl* t, int phase, double* base, uint64_t P,
-                   cudaStream_t s);
+void nccl_exchange(NcclTransportImpl* t, int phase, const std::vector<double*>& bases,
+                   uint64_t P, cudaStream_t s);
 void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s);
 double nccl_sum(NcclTransportImpl* t, double v);
 void nccl_destroy(NcclTransportImpl* t);
@@ -396,19 +396,21 @@ namespace {
 
 class NcclTransport final : public Transport {
  public:
-  NcclTransport(std::vector<HaloRow> plan, int rank, int nranks,
+  NcclTransport(std::vector<HaloRow> plan, int rank, int nranks, int nparts,
                 const uint8_t* id128)
-      : t_(nccl_create(std::move(plan), rank, nranks, id128)) {}
+      : t_(nccl_create(std::move(plan), rank, nranks, id128)), bases_(nparts, nullptr) {}
   ~NcclTransport() override { nccl_destroy(t_); }
   void exchange(int phase, std::vector<Part>& parts, uint64_t P,
                 cudaStream_t s) override {
-    nccl_exchange(t_, phase, parts[0].buf[0].get(), P, s);
+    for (Part& pt : parts) bases_[pt.index] = pt.buf[0].get();
+    nccl_exchange(t_, phase, bases_, P, s);
   }
   void wait(int phase, cudaStream_t s) override { nccl_wait(t_, phase, s); }
   double sum(double v) override { return nccl_sum(t_, v); }
 
  private:
   NcclTransportImpl* t_;
+  std::vector<double*> bases_;
 };
 
 class DirectEngine final : public Engine {
@@ -519,9 +521,12 @@ class DirectEngine final : public Engine {
       for (uint64_t i = 0; i < V && !end_fluid; i += nz_)
         end_fluid = hf[i] == 0 || hf[i + nz_ - 1] == 0;
       std::vector<HaloRow> plan = halo_plan(nz_, nparts_, end_fluid);
-      if (nranks_ > 1)
+      // NCCL between processes; with one process the copies are local, and
+      // an NCCL id selects NCCL self send/recv instead (tests the NCCL path on
+      // one GPU).
+      if (nranks_ > 1 || dist.have_id)
         tr_ = std::make_unique<NcclTransport>(std::move(plan), rank_, nranks_,
-                                              dist.nccl_id.data());
+                                              nparts_, dist.nccl_id.data());
       else
         tr_ = std::make_unique<LocalTransport>(std::move(plan));
     }

@@ -76,7 +76,7 @@ class NcclTransportImpl {
  public:
   NcclTransportImpl(std::vector<HaloRow> plan, int rank, int nranks,
                     const uint8_t* id128)
-      : plan_(std::move(plan)), rank_(rank) {
+      : plan_(std::move(plan)), rank_(rank), nranks_(nranks) {
     const NcclApi& api = NcclApi::get();
     ncclUniqueId id;
     static_assert(sizeof(id) == 128, "ncclUniqueId size");
@@ -99,22 +99,27 @@ class NcclTransportImpl {
     if (dsum_) cudaFree(dsum_);
   }
 
-  // base: this rank's slab storage (planes x 19 slots x P doubles)
-  void exchange(int phase, double* base, uint64_t P, cudaStream_t s) {
+  // bases[p]: storage (planes x 19 slots x P doubles) of slab p if it lives
+  // in this process, else nullptr.  Slab p belongs to rank p, or to rank 0
+  // when the communicator has a single rank (self send/recv: the NCCL code
+  // path exercised on one GPU by the tests).
+  void exchange(int phase, const std::vector<double*>& bases, uint64_t P,
+                cudaStream_t s) {
     const NcclApi& api = NcclApi::get();
     LBM_CUDA(cudaEventRecord(ready_[phase], s));
     LBM_CUDA(cudaStreamWaitEvent(comm_stream_, ready_[phase], 0));
     const size_t count = size_t(kHaloSlots) * P;
+    auto peer = [&](int part) { return nranks_ == 1 ? 0 : part; };
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (const HaloRow& r : plan_) {
       if (r.phase != phase) continue;
-      if (r.src_part == rank_)
-        nccl_check(api.Send(base + (uint64_t(r.src_plane) * kQ + r.slot0) * P, count,
-                            ncclFloat64, r.dst_part, comm_, comm_stream_),
+      if (double* b = bases[r.src_part])
+        nccl_check(api.Send(b + (uint64_t(r.src_plane) * kQ + r.slot0) * P, count,
+                            ncclFloat64, peer(r.dst_part), comm_, comm_stream_),
                    "ncclSend");
-      if (r.dst_part == rank_)
-        nccl_check(api.Recv(base + (uint64_t(r.dst_plane) * kQ + r.slot0) * P, count,
-                            ncclFloat64, r.src_part, comm_, comm_stream_),
+      if (double* b = bases[r.dst_part])
+        nccl_check(api.Recv(b + (uint64_t(r.dst_plane) * kQ + r.slot0) * P, count,
+                            ncclFloat64, peer(r.src_part), comm_, comm_stream_),
                    "ncclRecv");
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
@@ -141,7 +146,7 @@ class NcclTransportImpl {
 
  private:
   std::vector<HaloRow> plan_;
-  int rank_;
+  int rank_, nranks_;
   ncclComm_t comm_ = nullptr;
   cudaStream_t comm_stream_ = nullptr;
   cudaEvent_t ready_[2] = {nullptr, nullptr}, done_[2] = {nullptr, nullptr};
@@ -152,9 +157,9 @@ NcclTransportImpl* nccl_create(std::vector<HaloRow> plan, int rank, int nranks,
                                const uint8_t* id128) {
   return new NcclTransportImpl(std::move(plan), rank, nranks, id128);
 }
-void nccl_exchange(NcclTransportImpl* t, int phase, double* base, uint64_t P,
-                   cudaStream_t s) {
-  t->exchange(phase, base, P, s);
+void nccl_exchange(NcclTransportImpl* t, int phase, const std::vector<double*>& bases,
+                   uint64_t P, cudaStream_t s) {
+  t->exchange(phase, bases, P, s);
 }
 void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s) { t->wait(phase, s); }
 double nccl_sum(NcclTransportImpl* t, double v) { return t->sum(v); }

@@ -239,6 +239,23 @@ def test_zslab_parts_bitwise_equal_single(kind, dims, parts):
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
+@pytest.mark.parametrize("kind,dims,parts", [("channel", (32, 12, 24), 3), ("blocks", (16, 16, 16), 2)])
+def test_zslab_nccl_transport_single_gpu(kind, dims, parts):
+    """The NCCL halo transport (grouped ncclSend/ncclRecv on a comm stream,
+    event-ordered against the compute stream) exercised on one GPU: one NCCL
+    rank owning all slabs, self send/recv per plan row.  Bitwise equal to the
+    single-slab run."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    ref.load_perturbed(31)
+    ref.advance(PARAMS, FORCE, 8)
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
+                        dist={"virtual_parts": parts, "nccl_id": lbm.lbmgpu.nccl_unique_id()})
+    k.load_perturbed(31)
+    k.advance(PARAMS, FORCE, 8)
+    assert np.array_equal(k.snapshot(), ref.snapshot())
+
+
 def test_poiseuille_verification_passes():
     """verify_kernel (verification.cpp:31-100) on the GPU: slit 4x4x18."""
     for name in ("blk-push-soa", "aa-soa", "list-aa-soa", "list-pull-soa", "blk-pull-aos",
