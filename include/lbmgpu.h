@@ -221,6 +221,13 @@ int lbmgpu_launch_count(lbmgpu_ctx* ctx, long* out);
 /* Page-locked host allocation helpers for end-to-end timing. */
 int lbmgpu_host_alloc(size_t bytes, void** out);
 int lbmgpu_host_free(void* p);
+/* Device bandwidth micro-benchmarks (reference run_microbench,
+ * microbench.cpp:57-175): kind = "copy" | "copy-19" | "copy-19-nt-sl" |
+ * "update-19"; median GB/s of `reps` passes over `working_set_bytes`
+ * (>= 4x L2), GPU accounting without write allocate (16 B per element and
+ * stream). */
+int lbmgpu_microbench(const char* kind, uint64_t working_set_bytes, int reps,
+                      double* gbps);
 /* Device properties for reports. */
 int lbmgpu_device_info(int device, char* name64, int* sm_count,
                        size_t* total_mem, int* l2_bytes);

@@ -211,6 +211,7 @@ void velocity_change(const double* u, const double* uprev, uint64_t n3,
                      cudaStream_t s);
 void layer_sums(const double* u, uint64_t cols, int layers, double* out_dev,
                 cudaStream_t s);
+double run_microbench(const std::string& kind, uint64_t working_set_bytes, int reps);
 }  // namespace lbmgpu
 
 extern "C" {
@@ -741,6 +742,14 @@ int lbmgpu_host_alloc(size_t bytes, void** out) {
 
 int lbmgpu_host_free(void* p) {
   return guard([&] { LBM_CUDA(cudaFreeHost(p)); });
+}
+
+int lbmgpu_microbench(const char* kind, uint64_t bytes, int reps, double* gbps) {
+  return guard([&] {
+    need(kind, "kind");
+    need(gbps, "gbps");
+    *gbps = run_microbench(kind, bytes, reps);
+  });
 }
 
 int lbmgpu_device_info(int device, char* name64, int* sms, size_t* mem,

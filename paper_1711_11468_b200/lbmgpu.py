@@ -95,6 +95,7 @@ def _load():
     L.lbmgpu_synchronize.argtypes = [vp]
     L.lbmgpu_nccl_unique_id.argtypes = [vp]
     L.lbmgpu_part_info.argtypes = [vp, i, P(i), P(i), P(u64)]
+    L.lbmgpu_microbench.argtypes = [C.c_char_p, u64, i, P(d)]
     L.lbmgpu_local_rows.argtypes = [vp, P(u64)]
     L.lbmgpu_local_canonical_index.argtypes = [vp, vp]
     L.lbmgpu_snapshot_local.argtypes = [vp, vp, u64]
@@ -657,6 +658,23 @@ def halo_plan(nz: int, parts: int, ring: bool):
     n = C.c_int()
     _check(lib.lbmgpu_halo_plan(nz, parts, int(ring), rows.ctypes.data, cap, C.byref(n)))
     return rows[:7 * n.value].reshape(-1, 7)
+
+
+def microbench(kind: str, working_set_bytes: int = 8 << 30, reps: int = 5) -> float:
+    """Device copy / copy-19 / copy-19-nt-sl / update-19 bandwidth in GB/s
+    (reference run_microbench, microbench.cpp:57-175; GPU accounting)."""
+    v = C.c_double()
+    _check(lib.lbmgpu_microbench(kind.encode(), working_set_bytes, reps, C.byref(v)))
+    return v.value
+
+
+def micro_for(desc: KernelDescriptor) -> str:
+    """Which micro-benchmark models which kernel (perfmodel.cpp:68-72)."""
+    if desc.nt_streams > 0:
+        return "copy-19-nt-sl"
+    if desc.prop == "aa":
+        return "update-19"
+    return "copy-19"
 
 
 def nccl_unique_id() -> bytes:
