@@ -101,11 +101,13 @@ __global__ void __launch_bounds__(256) k_full_push(const DirectArgs a) {
   double q[kQ];
 #pragma unroll
   for (int d = 0; d < kQ; ++d) q[d] = a.src[I(c.Z[1], dslot(d), c.y, c.x)];
-  if (a.flags[n] == 0) collide(q, a.trt);
+  if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
   st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
 #pragma unroll
   for (int d = 1; d < kQ; ++d) {
     const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
+    // neighbour flags come from L1 (the small push configs are L2
+    // resident; measured faster than the arithmetic test here)
     const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
     const int s = a.flags[tn] ? dslot(opp(d)) : dslot(d);
     st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(256) k_full_pull(const DirectArgs a) {
 #pragma unroll
   for (int d = 1; d < kQ; ++d)
     q[d] = a.src[I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
-  const bool solid = a.flags[n] != 0;
+  const bool solid = solid_node(a, c.x, c.y, c.z, n);
   if (COLLIDE && !solid) collide(q, a.trt);
   st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
 #pragma unroll
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
-  if (a.flags[n]) return;
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
   const Idx<SOA> I{a.P, a.nx, a.ny};
   double q[kQ];
 #pragma unroll
@@ -156,7 +158,9 @@ __global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) 
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
-  if (a.flags[n]) return;
+  // Built-in geometries test solidity arithmetically (no flag load ahead of
+  // the PDF loads; solid nodes issue no loads at all).
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
   const Idx<SOA> I{a.P, a.nx, a.ny};
   double* buf = a.dst;
   double q[kQ];
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
-  if (a.flags[n]) return;
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
   const Idx<SOA> I{a.P, a.nx, a.ny};
   double* buf = a.dst;
   // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
@@ -190,6 +194,132 @@ __global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
   collide(q, a.trt);
 #pragma unroll
   for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
+}
+
+// ---- AA sub-steps, software-pipelined through shared memory ---------------
+// Persistent variant of the two kernels above.  Each thread walks nodes
+// n, n + G, n + 2G, ... (G = grid size) and, while it collides node n, the
+// 19 populations of its next node are already in flight as per-thread
+// cp.async (LDGSTS) copies into its own shared-memory column: the load
+// latency of node n+G overlaps the collision of node n inside every warp
+// instead of depending on other resident warps.  Each thread only ever
+// reads the shared-memory slots it filled itself, so no block barrier is
+// needed -- cp.async.wait_group orders it.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coords& c) {
+  const uint32_t z = a.fdP.div(n);
+  const uint32_t r = n - z * a.P;
+  const uint32_t y = a.fdx.div(r);
+  const uint32_t x = r - y * a.nx;
+  c.x = x;
+  c.y = y;
+  c.z = z;
+  c.X[0] = x == 0 ? a.nx - 1 : x - 1;
+  c.X[1] = x;
+  c.X[2] = x + 1 == a.nx ? 0 : x + 1;
+  c.Y[0] = y == 0 ? a.ny - 1 : y - 1;
+  c.Y[1] = y;
+  c.Y[2] = y + 1 == a.ny ? 0 : y + 1;
+  const uint32_t zs = z + a.zoff;
+  if (a.zwrap) {
+    c.Z[0] = z == 0 ? a.nzl - 1 : z - 1;
+    c.Z[2] = z + 1 == a.nzl ? 0 : z + 1;
+  } else {
+    c.Z[0] = zs - 1;
+    c.Z[2] = zs + 1;
+  }
+  c.Z[1] = zs;
+}
+
+// Address of the slot a node gathers direction d from (odd: (x - c_d, opp d);
+// even: (x, d)); in the odd step it is also where direction opp(d) is stored.
+template <bool ODD>
+__device__ __forceinline__ uint64_t aa_src(const Idx<true>& I, const Coords& c, int d) {
+  if (ODD && d != 0)
+    return I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+  return I(c.Z[1], dslot(d), c.y, c.x);
+}
+
+constexpr int kPipeThreads = 256;
+
+template <bool ODD, int STAGES, int MINB>
+__global__ void __launch_bounds__(kPipeThreads, MINB) k_full_aa_pipe(const DirectArgs a) {
+  extern __shared__ double sm_pipe[];  // [STAGES][19][kPipeThreads]
+  const uint32_t tid = threadIdx.x;
+  const uint32_t G = gridDim.x * kPipeThreads;
+  const uint32_t end = a.node0 + a.count;
+  const Idx<true> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  uint8_t solid[STAGES];
+  auto prefetch = [&](uint32_t n, int s) {
+    if (n < end) {
+      Coords c;
+      decode_node(a, n, c);
+      solid[s] = a.flags[n];
+      double* col = sm_pipe + size_t(s) * kQ * kPipeThreads + tid;
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) cp_async8(col + d * kPipeThreads, buf + aa_src<ODD>(I, c, d));
+    }
+    cp_async_commit();
+  };
+  uint32_t n = a.node0 + blockIdx.x * kPipeThreads + tid;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) prefetch(n + s * G, s);
+  while (n < end) {
+    // unrolled by STAGES so the ring index (and solid[]) is a constant
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      if (n < end) {
+        prefetch(n + (STAGES - 1) * G, (s + STAGES - 1) % STAGES);
+        cp_async_wait<STAGES - 1>();
+        if (!solid[s]) {
+          const double* col = sm_pipe + size_t(s) * kQ * kPipeThreads + tid;
+          double q[kQ];
+#pragma unroll
+          for (int d = 0; d < kQ; ++d) q[d] = col[d * kPipeThreads];
+          collide(q, a.trt);
+          Coords c;
+          decode_node(a, n, c);
+          if (ODD) {
+#pragma unroll
+            for (int d = 0; d < kQ; ++d) buf[aa_src<true>(I, c, d)] = q[opp(d)];
+          } else {
+#pragma unroll
+            for (int d = 0; d < kQ; ++d) buf[I(c.Z[1], dslot(opp(d)), c.y, c.x)] = q[d];
+          }
+        }
+        n += G;
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <bool ODD, int STAGES, int MINB>
+void launch_aa_pipe(const DirectArgs& a, int sm_count, cudaStream_t s) {
+  const size_t smem = size_t(STAGES) * kQ * kPipeThreads * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    LBM_CUDA(cudaFuncSetAttribute(k_full_aa_pipe<ODD, STAGES, MINB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    configured = true;
+  }
+  const uint64_t blocks = ceil_div(a.count, kPipeThreads);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(blocks, uint64_t(sm_count) * MINB));
+  k_full_aa_pipe<ODD, STAGES, MINB><<<grid, kPipeThreads, smem, s>>>(a);
+  LBM_CHECK_LAUNCH();
 }
 
 // ---- init / canonical transfer / perturbation / macro --------------------
@@ -437,12 +567,15 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_TMA_STAGES")) tma_stages_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AA_CS")) cs_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
       if (tma_stages_ != 0 && tma_stages_ != 3 && tma_stages_ != 4 &&
           tma_stages_ != 5 && tma_stages_ != 12)
         tma_stages_ = 4;
     }
 
     DeviceGeometry geo = build_geometry_device(g, stream_);
+    geom_ = g;
+    geom_.custom.clear();  // the device flags are kept per part
     nx_ = geo.nx;
     ny_ = geo.ny;
     nz_ = geo.nz;
@@ -563,6 +696,15 @@ class DirectEngine final : public Engine {
     a.node0 = node0;
     a.count = count;
     a.trt = t;
+    a.geom = geom_.kind;
+    a.gny = ny_;
+    a.gnz = nz_;
+    a.z0 = pt.z0;
+    a.period = geom_.block + geom_.spacing;
+    a.spacing = geom_.spacing;
+    const long long D = geom_.pipe_diameter > 0 ? geom_.pipe_diameter
+                                                : (long long)std::min(ny_, nz_) - 2;
+    a.d2 = D * D;
     return a;
   }
 
@@ -584,6 +726,28 @@ class DirectEngine final : public Engine {
         a.count % kTmaTile == 0) {
       const int tok = stats_.begin(name, stream_);
       launch_aa_tma(odd, a, sm_count_, tma_stages_, stream_);
+      stats_.end(tok, stream_);
+      return;
+    }
+    if (pipe_ != 0) {
+      const int tok = stats_.begin(name, stream_);
+      switch (pipe_) {
+        case 21:
+          odd ? launch_aa_pipe<true, 2, 1>(a, sm_count_, stream_)
+              : launch_aa_pipe<false, 2, 1>(a, sm_count_, stream_);
+          break;
+        case 31:
+          odd ? launch_aa_pipe<true, 3, 1>(a, sm_count_, stream_)
+              : launch_aa_pipe<false, 3, 1>(a, sm_count_, stream_);
+          break;
+        case 41:
+          odd ? launch_aa_pipe<true, 4, 1>(a, sm_count_, stream_)
+              : launch_aa_pipe<false, 4, 1>(a, sm_count_, stream_);
+          break;
+        default:
+          odd ? launch_aa_pipe<true, 2, 2>(a, sm_count_, stream_)
+              : launch_aa_pipe<false, 2, 2>(a, sm_count_, stream_);
+      }
       stats_.end(tok, stream_);
       return;
     }
@@ -856,9 +1020,11 @@ class DirectEngine final : public Engine {
   // i.e. 16 resident warps/SM (measured best on B200: 1 -> 140 registers and
   // 8 warps runs 33% slower; 3 -> 80 registers spills and hits the power cap)
   int minb_ = 2;
+  int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;
+  GeomSpec geom_;  // kind/parameters for the analytic solid test (custom: flags)
 };
 
 }  // namespace
