@@ -193,7 +193,11 @@ def run_reference_arm(args, rank, world):
     per = 2 if "aa" in kernel.split("-") else 1
     mflups, cores, desc, kind = cpu_reference_run(cid, per, args.steps, args.warmup)
     line = base_line(cid, args.gpus, args.steps, args.warmup, per)
-    line.update({"impl": "reference", "value": mflups, "ms_per_step": None,
+    # ms per bench step of the FULL workload at the measured CPU rate (the
+    # timed samples run on the bounded sample box, see cpu_baseline.sample)
+    n_full = {1: 246016, 2: 16516096, 3: 25128960, 4: 56000000, 5: 266342400}[cid]
+    line.update({"impl": "reference", "value": mflups,
+                 "ms_per_step": n_full * per / (mflups * 1e6) * 1e3,
                  "cpu_baseline": {"value": mflups, "unit": "MFLUP/s", "cores": cores,
                                   "kind": kind, "sample": desc},
                  "e2e": {"value": mflups, "unit": "MFLUP/s", "h2d_bytes_per_step": 0,
@@ -212,6 +216,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
+    ap.add_argument("--kernel", default=None,
+                    help="run another kernel name on the config's geometry (extra lines)")
     ap.add_argument("--dims", default=None,
                     help="override the box (NXxNYxNZ) -- profiling only, not a bench line")
     args = ap.parse_args()
@@ -236,8 +242,11 @@ def main():
 
     cid = args.config
     kernel, kind, dims, extra, _, _ = CONFIGS[cid]
-    if args.dims:
-        dims = tuple(int(v) for v in args.dims.split("x"))
+    if args.dims or args.kernel:
+        if args.dims:
+            dims = tuple(int(v) for v in args.dims.split("x"))
+        if args.kernel:
+            kernel = args.kernel
         CONFIGS[cid] = (kernel, kind, dims, extra, CONFIGS[cid][4], CONFIGS[cid][5])
     desc = lbm.make_descriptor(kernel)
     aa = desc.prop == "aa"
@@ -299,7 +308,11 @@ def main():
         # every sweep launch of the timed region touches each fluid node once:
         # 19 reads + 19 writes of 8 B (+ 72 B of adjacency for list one-step,
         # 72 B for the odd AA list sub-step only)
-        if "list_aa_odd" in name or ("list_pull" in name) or ("list_push" in name):
+        if "ria" in name:
+            # run-coded odd step: 304 B of PDFs + 8 B of run table per 32
+            # nodes (the pattern rows are L1/L2 resident)
+            per_node = 304 + 0.25
+        elif "list_aa_odd" in name or ("list_pull" in name) or ("list_push" in name):
             per_node = 304 + 72
         else:
             per_node = 304

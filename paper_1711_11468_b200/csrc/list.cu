@@ -292,6 +292,76 @@ __global__ void k_ria_starts(const uint32_t* __restrict__ adj, uint64_t N,
   }
 }
 
+// ---- RIA: run-coded odd step (list-aa-ria-soa / list-aa-pv-soa) -------------
+struct IsStart {
+  __host__ __device__ __forceinline__ uint32_t operator()(uint8_t f) const { return f; }
+};
+
+// The reference (kernels_list_aa.cpp:185-224) walks runs of consecutive nodes
+// that share one pattern of 18 relative offsets (entry - own slot) and
+// resolves the slot bases once per run.  GPU form: the run of node n is found
+// from a per-32-node table (first run id + a bitmask of run starts, 8 B per
+// 32 nodes) and the run's 18 offsets are read from a small pattern table that
+// stays in L1/L2 (warps mostly share one run).  Index traffic drops from
+// 72 B per odd update to ~0.25 B + the amortised pattern rows; results are
+// bitwise those of list-aa-soa (same loads, same collide, same stores).
+__global__ void k_ria_tables(const uint8_t* __restrict__ is_start,
+                             const uint32_t* __restrict__ run_incl, uint64_t N,
+                             uint32_t* __restrict__ run_start,
+                             uint32_t* __restrict__ warp_run0,
+                             uint32_t* __restrict__ warp_mask) {
+  // launched with blockDim a multiple of 32 and N padded to whole warps
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const bool valid = n < N;
+  const bool st = valid && is_start[n];
+  const uint32_t r = valid ? run_incl[n] - 1 : 0;
+  if (st) run_start[r] = static_cast<uint32_t>(n);
+  const uint32_t mask = __ballot_sync(0xffffffffu, st);
+  if ((threadIdx.x & 31) == 0 && valid) {
+    warp_run0[n >> 5] = r;
+    warp_mask[n >> 5] = mask;
+  }
+}
+
+__global__ void k_ria_patterns(const uint32_t* __restrict__ adj,
+                               const uint32_t* __restrict__ run_start, uint64_t R,
+                               const ListArgs a, int32_t* __restrict__ pat) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < R * 18;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / 18;
+    const int d = static_cast<int>(i - r * 18) + 1;
+    const uint64_t s = run_start[r];
+    pat[i] = static_cast<int32_t>(int64_t(adj[(d - 1) * a.N + s]) -
+                                  int64_t(a.starts[d] + s));
+  }
+}
+
+template <bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_odd_ria(const ListArgs a,
+                                                         const int32_t* __restrict__ pat,
+                                                         const uint32_t* __restrict__ warp_run0,
+                                                         const uint32_t* __restrict__ warp_mask) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t below = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
+  const uint32_t r = __ldg(warp_run0 + (n >> 5)) + __popc(__ldg(warp_mask + (n >> 5)) & below);
+  const int32_t* p = pat + uint64_t(r) * 18;
+  double* buf = a.dst;
+  // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
+  int64_t off[18];
+#pragma unroll
+  for (int k = 0; k < 18; ++k) off[k] = __ldg(p + k);
+  double q[kQ];
+  q[0] = buf[a.starts[0] + n];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = buf[int64_t(a.starts[opp(d)] + n) + off[opp(d) - 1]];
+  collide(q, a.trt);
+  lst<CS>(buf + a.starts[0] + n, q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) lst<CS>(buf + int64_t(a.starts[d] + n) + off[d - 1], q[d]);
+}
+
 template <bool SOA>
 __global__ void k_list_init(double* buf, const ListArgs a) {
   for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.N;
@@ -436,6 +506,7 @@ class ListEngine final : public Engine {
     LBM_CUDA(cudaStreamSynchronize(stream_));
     // streaming stores for the nt names and for lattices far beyond L2
     cs_nt_ = d.nt_streams > 0;
+    if (d.ria) build_ria();
     {
       int dev = 0;
       LBM_CUDA(cudaGetDevice(&dev));
@@ -474,7 +545,13 @@ class ListEngine final : public Engine {
       for (long s = 0; s < steps; s += 2) {
         soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
             : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
-        if (odd_pipe_) {
+        if (desc_.ria && soa) {
+          const int tok = stats_.begin("list_aa_odd_ria_soa", stream_);
+          k_list_aa_odd_ria<false><<<static_cast<unsigned>(ceil_div(a.N, 256)), 256, 0, stream_>>>(
+              a, ria_pat_.get(), ria_run0_.get(), ria_mask_.get());
+          LBM_CHECK_LAUNCH();
+          stats_.end(tok, stream_);
+        } else if (odd_pipe_) {
           const int tok = stats_.begin(soa ? "list_aa_odd_soa" : "list_aa_odd_aos", stream_);
           const unsigned grid = static_cast<unsigned>(
               std::min<uint64_t>(ceil_div(a.N, 256), uint64_t(sm_count_) * 2));
@@ -587,33 +664,56 @@ class ListEngine final : public Engine {
 
   // ria_stats / vector_fraction (kernels_list_aa.cpp:95-140) for the ria/pv
   // names; computed from the run starts of the kernel's own structure.
+  // Run coding of the scatter table (build_ria, list_lattice.cpp:206-226) and
+  // the device tables of the run-coded odd step.
+  void build_ria() {
+    DevBuf<uint8_t> is_start(n_fluid_);
+    ListArgs a = base_args();
+    k_ria_starts<<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
+        adj_.get(), n_fluid_, desc_.soa, a, is_start.get());
+    LBM_CHECK_LAUNCH();
+    DevBuf<uint32_t> incl(n_fluid_);
+    {
+      cub::TransformInputIterator<uint32_t, IsStart, const uint8_t*> it(is_start.get(), IsStart{});
+      size_t tmp = 0;
+      LBM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, it, incl.get(),
+                                             static_cast<int64_t>(n_fluid_), stream_));
+      DevBuf<uint8_t> t(tmp);
+      LBM_CUDA(cub::DeviceScan::InclusiveSum(t.get(), tmp, it, incl.get(),
+                                             static_cast<int64_t>(n_fluid_), stream_));
+    }
+    uint32_t R = 0;
+    LBM_CUDA(cudaMemcpyAsync(&R, incl.get() + n_fluid_ - 1, 4, cudaMemcpyDeviceToHost, stream_));
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    ria_R_ = R;
+    DevBuf<uint32_t> run_start(R);
+    const uint64_t warps = ceil_div(n_fluid_, 32);
+    ria_run0_.alloc(warps);
+    ria_mask_.alloc(warps);
+    k_ria_tables<<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, stream_>>>(
+        is_start.get(), incl.get(), n_fluid_, run_start.get(), ria_run0_.get(), ria_mask_.get());
+    LBM_CHECK_LAUNCH();
+    ria_pat_.alloc(uint64_t(R) * 18);
+    k_ria_patterns<<<grid_for(uint64_t(R) * 18, 256), 256, 0, stream_>>>(
+        adj_.get(), run_start.get(), R, a, ria_pat_.get());
+    LBM_CHECK_LAUNCH();
+    // run lengths -> vectorizable fraction (list_lattice.cpp:228-236)
+    std::vector<uint32_t> h(R);
+    LBM_CUDA(cudaMemcpyAsync(h.data(), run_start.get(), uint64_t(R) * 4,
+                             cudaMemcpyDeviceToHost, stream_));
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    const uint64_t W = static_cast<uint64_t>(desc_.vector_width);
+    uint64_t covered = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+      const uint64_t end = r + 1 < R ? h[r + 1] : n_fluid_;
+      covered += (end - h[r]) / W * W;
+    }
+    ria_runs_ = R;
+    ria_vfrac_ = static_cast<double>(covered) / static_cast<double>(n_fluid_);
+  }
+
   bool ria_stats(int64_t* runs, double* vfrac) override {
     if (!desc_.ria) return false;
-    if (ria_runs_ < 0) {
-      DevBuf<uint8_t> is_start(n_fluid_);
-      ListArgs a = base_args();
-      k_ria_starts<<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
-          adj_.get(), n_fluid_, desc_.soa, a, is_start.get());
-      LBM_CHECK_LAUNCH();
-      std::vector<uint8_t> h(n_fluid_);
-      LBM_CUDA(cudaMemcpyAsync(h.data(), is_start.get(), n_fluid_,
-                               cudaMemcpyDeviceToHost, stream_));
-      LBM_CUDA(cudaStreamSynchronize(stream_));
-      int64_t count = 0;
-      uint64_t covered = 0, len = 0;
-      const uint64_t W = static_cast<uint64_t>(desc_.vector_width);
-      for (uint64_t n = 0; n < n_fluid_; ++n) {
-        if (h[n]) {
-          if (n) covered += len / W * W;
-          ++count;
-          len = 0;
-        }
-        ++len;
-      }
-      covered += len / W * W;
-      ria_runs_ = count;
-      ria_vfrac_ = static_cast<double>(covered) / static_cast<double>(n_fluid_);
-    }
     *runs = ria_runs_;
     *vfrac = ria_vfrac_;
     return true;
@@ -637,6 +737,10 @@ class ListEngine final : public Engine {
   DevBuf<double> buf_[2];
   int64_t ria_runs_ = -1;
   double ria_vfrac_ = 0.0;
+  uint64_t ria_R_ = 0;
+  DevBuf<int32_t> ria_pat_;     // [run][18] relative offsets
+  DevBuf<uint32_t> ria_run0_;   // run id of node 32w
+  DevBuf<uint32_t> ria_mask_;   // run starts within nodes 32w .. 32w+31
 };
 
 }  // namespace
