@@ -265,6 +265,22 @@ def test_poiseuille_verification_passes():
         assert r["linf_rel"] < 1e-6
 
 
+@pytest.mark.parametrize("name", NAMES)
+def test_poiseuille_every_kernel(name):
+    """Reference acceptance criterion 6 (tests/acceptance.cpp:170-208) with its
+    parameters: slit 8x8x34 (g=1e-6, interval 500, tol 3e-8) and 8x8x66
+    (g=1e-6/4, interval 2000), 17/17 pass, L_inf not increasing above the
+    1e-6 noise floor."""
+    r34 = lbm.verify_kernel(name, lbm.PoiseuilleCase(8, 8, 34, 1e-6, lbm.TrtParams.from_tau(0.9)),
+                            check_interval=500, rel_tol=3e-8, max_steps=100000)
+    r66 = lbm.verify_kernel(name, lbm.PoiseuilleCase(8, 8, 66, 1e-6 / 4.0,
+                                                     lbm.TrtParams.from_tau(0.9)),
+                            check_interval=2000, rel_tol=3e-8, max_steps=200000)
+    for r in (r34, r66):
+        assert r["converged"] and r["passed"] and r["linf_rel"] < 1e-4, (name, r["linf_rel"])
+    assert r66["linf_rel"] <= max(r34["linf_rel"], 1e-6)
+
+
 def test_steady_state_reports_nonfinite():
     spec = lbm.GeometrySpec("channel", 8, 6, 6)
     k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
