@@ -98,11 +98,14 @@ CONFIGS = [
     (2, "list-aa-soa", "channel", (256, 256, 256), {}, 1000),
     (3, "list-pull-soa", "pipe", (512, 256, 256), {"pipe_diameter": 250}, 500),
     (4, "list-aa-soa", "blocks", (400, 400, 400), {"block": 8, "spacing": 8}, 500),
+    # cfg 5 needs ~82 GB of host RAM (lattice + snapshot): generated on the
+    # GPU box's host (196 GB) with LBMGPU_GOLDEN_OUT=gpurun_out/configs5.json
+    (5, "aa-soa", "channel", (1024, 512, 512), {}, 200),
 ]
 
 
 def configs(ref: Ref, which):
-    path = os.path.join(HERE, "configs.json")
+    path = os.environ.get("LBMGPU_GOLDEN_OUT", os.path.join(HERE, "configs.json"))
     out = json.load(open(path)) if os.path.exists(path) else {}
     for cid, name, kind, dims, extra, steps in CONFIGS:
         if which and cid not in which:
