@@ -362,6 +362,57 @@ __global__ void __launch_bounds__(256) k_list_aa_odd_ria(const ListArgs a,
   for (int d = 1; d < kQ; ++d) lst<CS>(buf + int64_t(a.starts[d] + n) + off[d - 1], q[d]);
 }
 
+// Group-pattern form of the run coding: a 32-node group (one warp) that lies
+// inside a single run carries that run's 18 offsets inline (72 B per 32
+// nodes, loaded as warp broadcasts with no dependent lookup in front); a
+// group that straddles run boundaries is marked (first offset = INT32_MIN)
+// and its nodes read their own scatter-table entries.  Same loads, collide
+// and stores as list-aa-soa, so bitwise identical.
+constexpr int32_t kMixedGroup = INT32_MIN;
+
+__global__ void k_ria_group_patterns(const int32_t* __restrict__ pat,
+                                     const uint32_t* __restrict__ warp_run0,
+                                     const uint32_t* __restrict__ warp_mask, uint64_t N,
+                                     int32_t* __restrict__ gpat) {
+  const uint64_t groups = (N + 31) / 32;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < groups * 18;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t g = i / 18;
+    const int k = static_cast<int>(i - g * 18);
+    const bool full = (g + 1) * 32 <= N;
+    const bool uniform = full && (warp_mask[g] & ~1u) == 0;
+    gpat[i] = uniform ? pat[uint64_t(warp_run0[g]) * 18 + k] : (k == 0 ? kMixedGroup : 0);
+  }
+}
+
+template <bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_odd_gpat(const ListArgs a,
+                                                          const int32_t* __restrict__ gpat) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  const int32_t* row = gpat + (n >> 5) * 18;
+  double* buf = a.dst;
+  int64_t ent[18];  // scatter-table entries of node n
+  const int32_t first = __ldg(row);
+  if (first != kMixedGroup) {
+    // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
+    ent[0] = int64_t(a.starts[1] + n) + first;
+#pragma unroll
+    for (int k = 1; k < 18; ++k) ent[k] = int64_t(a.starts[k + 1] + n) + __ldg(row + k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 18; ++k) ent[k] = __ldg(a.adj + uint64_t(k) * a.N + n);
+  }
+  double q[kQ];
+  q[0] = buf[a.starts[0] + n];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = buf[ent[opp(d) - 1]];
+  collide(q, a.trt);
+  lst<CS>(buf + a.starts[0] + n, q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) lst<CS>(buf + ent[d - 1], q[d]);
+}
+
 template <bool SOA>
 __global__ void k_list_init(double* buf, const ListArgs a) {
   for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.N;
@@ -512,6 +563,7 @@ class ListEngine final : public Engine {
       LBM_CUDA(cudaGetDevice(&dev));
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
       if (const char* e = std::getenv("LBMGPU_LIST_ODD_PIPE")) odd_pipe_ = std::atoi(e) != 0;
+      if (const char* e = std::getenv("LBMGPU_RIA_MODE")) ria_mode_ = std::atoi(e);
     }
   }
 
@@ -547,8 +599,12 @@ class ListEngine final : public Engine {
             : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         if (desc_.ria && soa) {
           const int tok = stats_.begin("list_aa_odd_ria_soa", stream_);
-          k_list_aa_odd_ria<false><<<static_cast<unsigned>(ceil_div(a.N, 256)), 256, 0, stream_>>>(
-              a, ria_pat_.get(), ria_run0_.get(), ria_mask_.get());
+          const unsigned g = static_cast<unsigned>(ceil_div(a.N, 256));
+          if (ria_mode_ == 1)
+            k_list_aa_odd_gpat<false><<<g, 256, 0, stream_>>>(a, ria_gpat_.get());
+          else
+            k_list_aa_odd_ria<false><<<g, 256, 0, stream_>>>(a, ria_pat_.get(), ria_run0_.get(),
+                                                             ria_mask_.get());
           LBM_CHECK_LAUNCH();
           stats_.end(tok, stream_);
         } else if (odd_pipe_) {
@@ -697,6 +753,10 @@ class ListEngine final : public Engine {
     k_ria_patterns<<<grid_for(uint64_t(R) * 18, 256), 256, 0, stream_>>>(
         adj_.get(), run_start.get(), R, a, ria_pat_.get());
     LBM_CHECK_LAUNCH();
+    ria_gpat_.alloc(warps * 18);
+    k_ria_group_patterns<<<grid_for(warps * 18, 256), 256, 0, stream_>>>(
+        ria_pat_.get(), ria_run0_.get(), ria_mask_.get(), n_fluid_, ria_gpat_.get());
+    LBM_CHECK_LAUNCH();
     // run lengths -> vectorizable fraction (list_lattice.cpp:228-236)
     std::vector<uint32_t> h(R);
     LBM_CUDA(cudaMemcpyAsync(h.data(), run_start.get(), uint64_t(R) * 4,
@@ -741,6 +801,8 @@ class ListEngine final : public Engine {
   DevBuf<int32_t> ria_pat_;     // [run][18] relative offsets
   DevBuf<uint32_t> ria_run0_;   // run id of node 32w
   DevBuf<uint32_t> ria_mask_;   // run starts within nodes 32w .. 32w+31
+  DevBuf<int32_t> ria_gpat_;    // [group][18] inline pattern or kMixedGroup
+  int ria_mode_ = 1;            // 1: group patterns, 0: run table (LBMGPU_RIA_MODE)
 };
 
 }  // namespace
