@@ -55,9 +55,15 @@ __device__ __forceinline__ void lst(double* p, double v) {
 // stream-only exit pass.  CS selects st.global.cs (the GPU's counterpart of
 // the nt split-store variants, kernels_list_nt.cpp).
 template <bool SOA, bool COLLIDE, bool CS>
-__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a) {
+__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a, uint64_t pf) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
+  if (pf) {  // adjacency L2 prefetch for a later wave (see k_list_aa_odd)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t m = (n & ~uint64_t(31)) + pf;
+    if (lane < 18 && m < a.N)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
+  }
   uint32_t an[18];
 #pragma unroll
   for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
@@ -114,10 +120,20 @@ __global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
 // aa_odd_node (kernels_list_aa.cpp:22-31): one scatter table serves both
 // sides -- gather d through column opp(d), scatter d through column d.
 template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a) {
+__global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a, uint64_t pf) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
   double* buf = a.dst;
+  // L2 prefetch of the adjacency lines a block about `pf` nodes ahead will
+  // need (blocks are dispatched in index order): the index load of later
+  // blocks then hits L2 and the index -> gather chain shortens.  Lanes 0..17
+  // of each warp each touch one 128 B column line of that warp.
+  if (pf) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t m = (n & ~uint64_t(31)) + pf;
+    if (lane < 18 && m < a.N)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
+  }
   uint32_t an[18];
 #pragma unroll
   for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
@@ -340,10 +356,18 @@ template <bool CS>
 __global__ void __launch_bounds__(256) k_list_aa_odd_ria(const ListArgs a,
                                                          const int32_t* __restrict__ pat,
                                                          const uint32_t* __restrict__ warp_run0,
-                                                         const uint32_t* __restrict__ warp_mask) {
+                                                         const uint32_t* __restrict__ warp_mask,
+                                                         uint64_t pf) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
   const uint32_t lane = threadIdx.x & 31;
+  if (pf && lane == 0) {  // L2 prefetch of a later wave's run-table words
+    const uint64_t w = (n >> 5) + pf / 32;
+    if (w * 32 < a.N) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(warp_run0 + w));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(warp_mask + w));
+    }
+  }
   const uint32_t below = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
   const uint32_t r = __ldg(warp_run0 + (n >> 5)) + __popc(__ldg(warp_mask + (n >> 5)) & below);
   const int32_t* p = pat + uint64_t(r) * 18;
@@ -387,9 +411,16 @@ __global__ void k_ria_group_patterns(const int32_t* __restrict__ pat,
 
 template <bool CS>
 __global__ void __launch_bounds__(256) k_list_aa_odd_gpat(const ListArgs a,
-                                                          const int32_t* __restrict__ gpat) {
+                                                          const int32_t* __restrict__ gpat,
+                                                          uint64_t pf) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
+  if (pf) {  // L2 prefetch of the group row a later wave needs (see k_list_aa_odd)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t g = (n >> 5) + pf / 32;
+    if (lane < 2 && g * 32 < a.N)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(gpat + g * 18 + lane * 16));
+  }
   const int32_t* row = gpat + (n >> 5) * 18;
   double* buf = a.dst;
   int64_t ent[18];  // scatter-table entries of node n
@@ -564,6 +595,13 @@ class ListEngine final : public Engine {
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
       if (const char* e = std::getenv("LBMGPU_LIST_ODD_PIPE")) odd_pipe_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_RIA_MODE")) ria_mode_ = std::atoi(e);
+      // adjacency L2 prefetch distance, in resident-grid waves (0 = off)
+      int waves = 1;  // measured best on B200 (cfg 2 list-aa odd: 5946 -> 6530 GB/s)
+      if (const char* e = std::getenv("LBMGPU_LIST_PF_WAVES")) waves = std::atoi(e);
+      pf_ = uint64_t(waves) * uint64_t(sm_count_) * 2 * 256;
+      int pwaves = 0;
+      if (const char* e = std::getenv("LBMGPU_PULL_PF_WAVES")) pwaves = std::atoi(e);
+      pull_pf_ = uint64_t(pwaves) * uint64_t(sm_count_) * 2 * 256;
     }
   }
 
@@ -579,11 +617,11 @@ class ListEngine final : public Engine {
     return a;
   }
 
-  template <class K>
-  void launch(const char* name, K kern, const ListArgs& a) {
+  template <class K, class... Extra>
+  void launch(const char* name, K kern, const ListArgs& a, Extra... extra) {
     const int threads = 256;
     const int tok = stats_.begin(name, stream_);
-    kern<<<static_cast<unsigned>(ceil_div(a.N, threads)), threads, 0, stream_>>>(a);
+    kern<<<static_cast<unsigned>(ceil_div(a.N, threads)), threads, 0, stream_>>>(a, extra...);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);
   }
@@ -601,10 +639,10 @@ class ListEngine final : public Engine {
           const int tok = stats_.begin("list_aa_odd_ria_soa", stream_);
           const unsigned g = static_cast<unsigned>(ceil_div(a.N, 256));
           if (ria_mode_ == 1)
-            k_list_aa_odd_gpat<false><<<g, 256, 0, stream_>>>(a, ria_gpat_.get());
+            k_list_aa_odd_gpat<false><<<g, 256, 0, stream_>>>(a, ria_gpat_.get(), pf_);
           else
             k_list_aa_odd_ria<false><<<g, 256, 0, stream_>>>(a, ria_pat_.get(), ria_run0_.get(),
-                                                             ria_mask_.get());
+                                                             ria_mask_.get(), pf_);
           LBM_CHECK_LAUNCH();
           stats_.end(tok, stream_);
         } else if (odd_pipe_) {
@@ -618,8 +656,8 @@ class ListEngine final : public Engine {
           LBM_CHECK_LAUNCH();
           stats_.end(tok, stream_);
         } else {
-          soa ? launch("list_aa_odd_soa", k_list_aa_odd<true, false>, a)
-              : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a);
+          soa ? launch("list_aa_odd_soa", k_list_aa_odd<true, false>, a, pf_)
+              : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a, pf_);
         }
       }
       return;
@@ -645,14 +683,14 @@ class ListEngine final : public Engine {
       const bool last = s == steps - 1;
       if (soa) {
         if (last)
-          launch("list_pull_stream_soa", k_list_pull<true, false, false>, a);
+          launch("list_pull_stream_soa", k_list_pull<true, false, false>, a, pull_pf_);
         else if (cs_nt_)
-          launch("list_pull_soa", k_list_pull<true, true, true>, a);
+          launch("list_pull_soa", k_list_pull<true, true, true>, a, pull_pf_);
         else
-          launch("list_pull_soa", k_list_pull<true, true, false>, a);
+          launch("list_pull_soa", k_list_pull<true, true, false>, a, pull_pf_);
       } else {
-        last ? launch("list_pull_stream_aos", k_list_pull<false, false, false>, a)
-             : launch("list_pull_aos", k_list_pull<false, true, false>, a);
+        last ? launch("list_pull_stream_aos", k_list_pull<false, false, false>, a, pull_pf_)
+             : launch("list_pull_aos", k_list_pull<false, true, false>, a, pull_pf_);
       }
       cur_ ^= 1;
     }
@@ -802,7 +840,9 @@ class ListEngine final : public Engine {
   DevBuf<uint32_t> ria_run0_;   // run id of node 32w
   DevBuf<uint32_t> ria_mask_;   // run starts within nodes 32w .. 32w+31
   DevBuf<int32_t> ria_gpat_;    // [group][18] inline pattern or kMixedGroup
-  int ria_mode_ = 1;            // 1: group patterns, 0: run table (LBMGPU_RIA_MODE)
+  int ria_mode_ = 0;            // 0: run table, 1: group patterns (LBMGPU_RIA_MODE)
+  uint64_t pf_ = 0;             // adjacency L2 prefetch distance in nodes (AA odd)
+  uint64_t pull_pf_ = 0;        // same for the one-step pull sweeps
 };
 
 }  // namespace

@@ -294,7 +294,7 @@ def test_steady_state_reports_nonfinite():
 CONFIGS = os.path.join(os.path.dirname(__file__), "golden", "configs.json")
 
 
-@pytest.mark.parametrize("cid", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("cid", ["1", "2", "3", "4", "5"])
 def test_baseline_config_fingerprint(cid):
     """BASELINE configs 1-4 at full size: default init, omega+ = 1,
     Lambda = 3/16, g = (1e-5, 0, 0); the final state's FNV-1a fingerprint
