@@ -49,174 +49,7 @@ struct Coords {
   uint32_t Z[3];           // storage planes of z-1, z, z+1
 };
 
-__device__ __forceinline__ bool decode(const DirectArgs& a, Coords& c,
-                                       uint32_t& n) {
-  n = a.node0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= a.node0 + a.count) return false;
-  const uint32_t z = a.fdP.div(n);
-  const uint32_t r = n - z * a.P;
-  const uint32_t y = a.fdx.div(r);
-  const uint32_t x = r - y * a.nx;
-  c.x = x;
-  c.y = y;
-  c.z = z;
-  c.X[0] = x == 0 ? a.nx - 1 : x - 1;
-  c.X[1] = x;
-  c.X[2] = x + 1 == a.nx ? 0 : x + 1;
-  c.Y[0] = y == 0 ? a.ny - 1 : y - 1;
-  c.Y[1] = y;
-  c.Y[2] = y + 1 == a.ny ? 0 : y + 1;
-  const uint32_t zs = z + a.zoff;
-  if (a.zwrap) {
-    c.Z[0] = z == 0 ? a.nzl - 1 : z - 1;
-    c.Z[2] = z + 1 == a.nzl ? 0 : z + 1;
-  } else {
-    c.Z[0] = zs - 1;
-    c.Z[2] = zs + 1;
-  }
-  c.Z[1] = zs;
-  return true;
-}
-
-template <class T>
-__device__ __forceinline__ T ld(const T* p) {
-  return *p;
-}
-template <bool CS>
-__device__ __forceinline__ void st(double* p, double v) {
-  if (CS)
-    __stcs(p, v);
-  else
-    *p = v;
-}
-
-// ---- one-step push / pull with folded full-way correction ----------------
-// kernels_full_os.cpp:56-89 + full_lattice.cpp:42-56 (correction on dst).
-template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_full_push(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = a.src[I(c.Z[1], dslot(d), c.y, c.x)];
-  if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
-  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) {
-    const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
-    // neighbour flags come from L1 (the small push configs are L2
-    // resident; measured faster than the arithmetic test here)
-    const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
-    const int s = a.flags[tn] ? dslot(opp(d)) : dslot(d);
-    st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
-  }
-}
-
-// kernels_full_os.cpp:56-89 (PULL) ; COLLIDE=false is the stream-only pass.
-template <bool SOA, bool COLLIDE, bool CS>
-__global__ void __launch_bounds__(256) k_full_pull(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double q[kQ];
-  q[0] = a.src[I(c.Z[1], dslot(0), c.y, c.x)];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    q[d] = a.src[I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
-  const bool solid = solid_node(a, c.x, c.y, c.z, n);
-  if (COLLIDE && !solid) collide(q, a.trt);
-  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) {
-    const int s = solid ? dslot(opp(d)) : dslot(d);
-    st<CS>(a.dst + I(c.Z[1], s, c.y, c.x), q[d]);
-  }
-}
-
-// collide_pass (kernels_full_os.cpp:149-159): fluid nodes, in place.
-template <bool SOA>
-__global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = a.dst[I(c.Z[1], dslot(d), c.y, c.x)];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) a.dst[I(c.Z[1], dslot(d), c.y, c.x)] = q[d];
-}
-
-// ---- AA pattern (kernels_full_aa.cpp:46-94), corrections dropped ----------
-template <bool SOA, bool CS, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  // Built-in geometries test solidity arithmetically (no flag load ahead of
-  // the PDF loads; solid nodes issue no loads at all).
-  if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double* buf = a.dst;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = buf[I(c.Z[1], dslot(d), c.y, c.x)];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d)
-    st<CS>(buf + I(c.Z[1], dslot(opp(d)), c.y, c.x), q[d]);
-}
-
-template <bool SOA, bool CS, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double* buf = a.dst;
-  // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
-  // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
-  // per direction serves both the load and the store.
-  double* p[kQ];
-  p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = *p[d];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
-}
-
-// ---- AA sub-steps, software-pipelined through shared memory ---------------
-// Persistent variant of the two kernels above.  Each thread walks nodes
-// n, n + G, n + 2G, ... (G = grid size) and, while it collides node n, the
-// 19 populations of its next node are already in flight as per-thread
-// cp.async (LDGSTS) copies into its own shared-memory column: the load
-// latency of node n+G overlaps the collision of node n inside every warp
-// instead of depending on other resident warps.  Each thread only ever
-// reads the shared-memory slots it filled itself, so no block barrier is
-// needed -- cp.async.wait_group orders it.
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
+// own-node id n -> coordinates, wrapped x/y neighbours and storage planes
 __device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coords& c) {
   const uint32_t z = a.fdP.div(n);
   const uint32_t r = n - z * a.P;
@@ -241,6 +74,257 @@ __device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coo
   }
   c.Z[1] = zs;
 }
+
+__device__ __forceinline__ bool decode(const DirectArgs& a, Coords& c,
+                                       uint32_t& n) {
+  n = a.node0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.node0 + a.count) return false;
+  decode_node(a, n, c);
+  return true;
+}
+
+// Loads of lattice data: plain (L1-cached) in the one-sweep-per-launch
+// kernels; L2-only (ld.global.cg) in the fused multi-step kernel, whose later
+// sweeps read lines other SMs wrote after a grid barrier.
+template <bool CG>
+__device__ __forceinline__ double ldp(const double* p) {
+  if (CG) return __ldcg(p);
+  return *p;
+}
+template <bool CS>
+__device__ __forceinline__ void st(double* p, double v) {
+  if (CS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+// ---- per-node bodies (shared by the sweep kernels and the fused kernel) ----
+// kernels_full_os.cpp:56-89 + full_lattice.cpp:42-56 (push, correction on dst)
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.src + I(c.Z[1], dslot(d), c.y, c.x));
+  if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
+  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
+    // neighbour flags come from L1 (the small push configs are L2
+    // resident; measured faster than the arithmetic test here)
+    const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
+    const int s = a.flags[tn] ? dslot(opp(d)) : dslot(d);
+    st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
+  }
+}
+
+// kernels_full_os.cpp:56-89 (PULL); COLLIDE=false is the stream-only pass
+template <bool SOA, bool COLLIDE, bool CS, bool CG>
+__device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+  q[0] = ldp<CG>(a.src + I(c.Z[1], dslot(0), c.y, c.x));
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    q[d] = ldp<CG>(a.src + I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)]));
+  const bool solid = solid_node(a, c.x, c.y, c.z, n);
+  if (COLLIDE && !solid) collide(q, a.trt);
+  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const int s = solid ? dslot(opp(d)) : dslot(d);
+    st<CS>(a.dst + I(c.Z[1], s, c.y, c.x), q[d]);
+  }
+}
+
+// collide_pass (kernels_full_os.cpp:149-159): fluid nodes, in place on dst
+template <bool SOA, bool CG>
+__device__ __forceinline__ void collide_node_pass(const DirectArgs& a, const Coords& c, uint32_t n) {
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.dst + I(c.Z[1], dslot(d), c.y, c.x));
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) a.dst[I(c.Z[1], dslot(d), c.y, c.x)] = q[d];
+}
+
+// AA pattern (kernels_full_aa.cpp:46-94), corrections dropped.  Built-in
+// geometries test solidity arithmetically (no flag load ahead of the PDF
+// loads; solid nodes issue no loads at all).
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void aa_even_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(buf + I(c.Z[1], dslot(d), c.y, c.x));
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) st<CS>(buf + I(c.Z[1], dslot(opp(d)), c.y, c.x), q[d]);
+}
+
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void aa_odd_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
+  // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
+  // per direction serves both the load and the store.
+  double* p[kQ];
+  p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(p[d]);
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
+}
+
+// ---- one sweep per launch, one node per thread ------------------------------
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_full_push(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  push_node<SOA, CS, false>(a, c, n);
+}
+
+template <bool SOA, bool COLLIDE, bool CS>
+__global__ void __launch_bounds__(256) k_full_pull(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  pull_node<SOA, COLLIDE, CS, false>(a, c, n);
+}
+
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  collide_node_pass<SOA, false>(a, c, n);
+}
+
+template <bool SOA, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  aa_even_node<SOA, CS, false>(a, c, n);
+}
+
+template <bool SOA, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  aa_odd_node<SOA, CS, false>(a, c, n);
+}
+
+// ---- fused multi-step sweeps for small lattices ----------------------------
+// For lattices that live in L2 (cfg 1: 2 x 40 MB) a sweep takes ~15 us and
+// the per-launch fill/drain and launch gaps cost as much as the work.  One
+// cooperative launch runs all T sweeps with a grid barrier between them;
+// every block walks the nodes grid-stride.  Same per-node bodies, so the
+// results are bitwise those of the per-sweep kernels.
+struct GridBarrier {
+  unsigned* count;
+  unsigned* gen;
+};
+
+__device__ __forceinline__ void grid_sync(const GridBarrier& b) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = b.gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(b.count, 1u) == gridDim.x - 1) {
+      atomicExch(b.count, 0u);
+      __threadfence();
+      atomicAdd(b.gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+enum FusedKind { kFusedPush = 0, kFusedPull = 1, kFusedAA = 2 };
+
+template <bool SOA, int KIND>
+__global__ void __launch_bounds__(256) k_full_fused(DirectArgs a, double* other, long steps,
+                                                    GridBarrier bar) {
+  const uint32_t G = gridDim.x * blockDim.x;
+  auto sweep = [&](auto body) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.count; i += G) {
+      const uint32_t n = a.node0 + i;
+      Coords c;
+      decode_node(a, n, c);
+      body(c, n);
+    }
+  };
+  if (KIND == kFusedAA) {
+    for (long s = 0; s < steps; s += 2) {
+      sweep([&](const Coords& c, uint32_t n) { aa_even_node<SOA, false, true>(a, c, n); });
+      grid_sync(bar);
+      sweep([&](const Coords& c, uint32_t n) { aa_odd_node<SOA, false, true>(a, c, n); });
+      grid_sync(bar);
+    }
+    return;
+  }
+  // two grids: a.src -> a.dst, then swap (the host tracks the parity)
+  double* bufs[2] = {const_cast<double*>(a.src), other};
+  int cur = 0;
+  if (KIND == kFusedPull) {
+    a.dst = bufs[0];
+    sweep([&](const Coords& c, uint32_t n) { collide_node_pass<SOA, true>(a, c, n); });
+    grid_sync(bar);
+  }
+  for (long s = 0; s < steps; ++s) {
+    a.src = bufs[cur];
+    a.dst = bufs[1 - cur];
+    if (KIND == kFusedPush)
+      sweep([&](const Coords& c, uint32_t n) { push_node<SOA, false, true>(a, c, n); });
+    else if (s + 1 < steps)
+      sweep([&](const Coords& c, uint32_t n) { pull_node<SOA, true, false, true>(a, c, n); });
+    else
+      sweep([&](const Coords& c, uint32_t n) { pull_node<SOA, false, false, true>(a, c, n); });
+    grid_sync(bar);
+    cur ^= 1;
+  }
+}
+
+// ---- AA sub-steps, software-pipelined through shared memory ---------------
+// Persistent variant of the two kernels above.  Each thread walks nodes
+// n, n + G, n + 2G, ... (G = grid size) and, while it collides node n, the
+// 19 populations of its next node are already in flight as per-thread
+// cp.async (LDGSTS) copies into its own shared-memory column: the load
+// latency of node n+G overlaps the collision of node n inside every warp
+// instead of depending on other resident warps.  Each thread only ever
+// reads the shared-memory slots it filled itself, so no block barrier is
+// needed -- cp.async.wait_group orders it.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 
 // Address of the slot a node gathers direction d from (odd: (x - c_d, opp d);
 // even: (x, d)); in the odd step it is also where direction opp(d) is stored.
@@ -568,6 +652,10 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_CS")) cs_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
+        fused_bytes_ = uint64_t(std::atoll(e)) << 20;
+      barrier_.alloc(2);
+      LBM_CUDA(cudaMemsetAsync(barrier_.get(), 0, 2 * sizeof(unsigned), stream_));
       if (tma_stages_ != 0 && tma_stages_ != 3 && tma_stages_ != 4 &&
           tma_stages_ != 5 && tma_stages_ != 12)
         tma_stages_ = 4;
@@ -775,9 +863,61 @@ class DirectEngine final : public Engine {
     }
   }
 
+  // Whether advance() runs as one cooperative multi-sweep launch: single
+  // slab, lattice small enough to live in L2 (<= fused_bytes_, default
+  // 96 MiB of PDF buffers), at least two sweeps.
+  bool use_fused(long steps) const {
+    if (nparts_ != 1 || steps < 2 || fused_bytes_ == 0) return false;
+    const Part& pt = parts_[0];
+    const uint64_t bufs = desc_.prop == Prop::Aa ? 1 : 2;
+    return uint64_t(pt.nzs) * P_ * kQ * 8 * bufs <= fused_bytes_;
+  }
+
+  template <bool SOA, int KIND>
+  void launch_fused(const DirectArgs& a, double* other, long steps, const char* name,
+                    long sweeps) {
+    auto kern = k_full_fused<SOA, KIND>;
+    int per_sm = 0;
+    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const uint64_t want = ceil_div(a.count, 256);
+    const int grid = static_cast<int>(
+        std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(per_sm, 1)) * sm_count_)));
+    GridBarrier bar{barrier_.get(), barrier_.get() + 1};
+    DirectArgs aa = a;
+    void* params[] = {&aa, &other, &steps, &bar};
+    const int tok = stats_.begin(name, stream_, sweeps);
+    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, params, 0,
+                                         stream_));
+    stats_.end(tok, stream_);
+  }
+
+  bool advance_fused(const TrtArgs& t, long steps) {
+    if (!use_fused(steps)) return false;
+    const Part& pt = parts_[0];
+    const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+    const bool soa = desc_.soa;
+    if (desc_.prop == Prop::Aa) {
+      DirectArgs a = args(pt, 0, N, t, 0, 0);
+      soa ? launch_fused<true, kFusedAA>(a, nullptr, steps, "full_aa_soa_fused", steps)
+          : launch_fused<false, kFusedAA>(a, nullptr, steps, "full_aa_aos_fused", steps);
+      return true;
+    }
+    DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
+    double* other = parts_[0].buf[1 - cur_].get();
+    if (desc_.prop == Prop::OsPush)
+      soa ? launch_fused<true, kFusedPush>(a, other, steps, "full_push_soa_fused", steps)
+          : launch_fused<false, kFusedPush>(a, other, steps, "full_push_aos_fused", steps);
+    else
+      soa ? launch_fused<true, kFusedPull>(a, other, steps, "full_pull_soa_fused", steps + 1)
+          : launch_fused<false, kFusedPull>(a, other, steps, "full_pull_aos_fused", steps + 1);
+    if (steps & 1) cur_ ^= 1;
+    return true;
+  }
+
   void advance(const TrtArgs& t, long steps) override {
     const bool soa = desc_.soa;
     const bool cs = cs_;
+    if (advance_fused(t, steps)) return;
     if (desc_.prop == Prop::OsPush) {
       const Part& pt = parts_[0];
       const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
@@ -1021,6 +1161,8 @@ class DirectEngine final : public Engine {
   // 8 warps runs 33% slower; 3 -> 80 registers spills and hits the power cap)
   int minb_ = 2;
   int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
+  uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
+  DevBuf<unsigned> barrier_;            // grid barrier {count, generation}
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;

@@ -194,7 +194,7 @@ cudaEvent_t KernelStats::get_event() {
   return e;
 }
 
-int KernelStats::begin(const char* name, cudaStream_t s) {
+int KernelStats::begin(const char* name, cudaStream_t s, long sweeps) {
   ++launches_;
   if (!on_) return -1;
   int row = -1;
@@ -204,7 +204,7 @@ int KernelStats::begin(const char* name, cudaStream_t s) {
     rows_.push_back({name, 0, 0.0});
     row = static_cast<int>(rows_.size()) - 1;
   }
-  Pending p{row, get_event(), get_event()};
+  Pending p{row, get_event(), get_event(), sweeps};
   LBM_CUDA(cudaEventRecord(p.a, s));
   pending_.push_back(p);
   return static_cast<int>(pending_.size()) - 1;
@@ -220,7 +220,7 @@ void KernelStats::collect() {
     LBM_CUDA(cudaEventSynchronize(p.b));
     float ms = 0.f;
     LBM_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
-    rows_[p.row].launches += 1;
+    rows_[p.row].launches += p.sweeps;
     rows_[p.row].ms += ms;
     pool_.push_back(p.a);
     pool_.push_back(p.b);

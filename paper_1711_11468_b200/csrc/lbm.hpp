@@ -115,7 +115,9 @@ class KernelStats {
   void enable(bool on) { on_ = on; }
   bool enabled() const { return on_; }
   // Records a (start) event before a launch; returns a token for end().
-  int begin(const char* name, cudaStream_t s);
+  // `sweeps` = lattice sweeps the launch performs (a fused multi-step launch
+  // counts T); the per-row "launches" total is in sweeps.
+  int begin(const char* name, cudaStream_t s, long sweeps = 1);
   void end(int token, cudaStream_t s);
   void collect();  // synchronises pending events into the totals
   void reset();
@@ -126,7 +128,7 @@ class KernelStats {
   ~KernelStats();
 
  private:
-  struct Pending { int row; cudaEvent_t a, b; };
+  struct Pending { int row; cudaEvent_t a, b; long sweeps; };
   bool on_ = false;
   long launches_ = 0;
   std::vector<Row> rows_;

@@ -56,21 +56,33 @@ def test_kernel_matches_golden_bitwise(idx, small_golden, small_snapshots):
     assert abs(k.total_mass() - case["mass"]) <= 1e-12 * abs(case["mass"])
 
 
+@pytest.mark.parametrize("fused", ["default", "per-sweep"])
 @pytest.mark.parametrize("name", NAMES)
-def test_against_port_oracle_steppers(name, port):
+def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
     """Host load_state path + a second geometry, against our C restatement
-    of the reference steppers (tests/support/reference.hpp:33-105)."""
+    of the reference steppers (tests/support/reference.hpp:33-105).  Small
+    direct lattices normally run as one fused cooperative launch; the
+    per-sweep kernels (used for large lattices) are forced with
+    LBMGPU_FUSED_MB=0 so both code paths are checked bit for bit."""
+    if fused == "per-sweep":
+        monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
     for kind, dims in [("blocks", (12, 12, 12)), ("channel", (33, 7, 9))]:
         _, _, nf = port.geometry(kind, *dims)
         init = port.perturbed(nf, 99)
         fam = "half" if name.startswith("list-") else "full"
-        expect, _ = port.run(fam, kind, *dims, 6, PARAMS.omega_plus, g=G_TEST, init=init)
-        k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
-        k.load_state(init)
-        k.advance(PARAMS, FORCE, 6)
-        got = k.snapshot()
-        assert port.max_rel_diff(got, expect) <= 1e-12, (name, kind)
-        assert np.array_equal(got, expect), (name, kind)
+        for steps in (6, 7) if not name.startswith(("aa", "list-aa")) else (6,):
+            expect, _ = port.run(fam, kind, *dims, steps, PARAMS.omega_plus, g=G_TEST, init=init)
+            k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
+            k.load_state(init)
+            k.advance(PARAMS, FORCE, steps)
+            got = k.snapshot()
+            assert port.max_rel_diff(got, expect) <= 1e-12, (name, kind)
+            assert np.array_equal(got, expect), (name, kind, steps)
+            # a second advance continues from the swapped buffers correctly
+            k.advance(PARAMS, FORCE, 2)
+            expect2, _ = port.run(fam, kind, *dims, steps + 2, PARAMS.omega_plus, g=G_TEST,
+                                  init=init)
+            assert np.array_equal(k.snapshot(), expect2), (name, kind, steps + 2)
 
 
 def _list_kernel_for(layout, scatter):
