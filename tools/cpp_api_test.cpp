@@ -1,0 +1,137 @@
+// C++ host-API checks over include/lbmgpu.hpp, written like the reference's
+// doctest kernel tests (proj/tests/test_kernels.cpp) so an lbmbench user can
+// read them side by side.  Built by tools/Makefile, run by
+// tests/test_cpp_api.py (GPU) and prints "ALL PASSED".
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "../include/lbmgpu.hpp"
+
+using namespace lbmgpu;
+
+static int failures = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      std::printf("FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      ++failures;                                                          \
+    }                                                                      \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static const TrtParams kParams = TrtParams::from_tau(0.9);
+static const BodyForce kForce{{1e-5, 2e-6, -3e-6}};
+
+static GeometrySpec bench_blocks() {
+  GeometrySpec g;
+  g.kind = GeometryKind::Blocks;
+  g.nx = 12;
+  g.ny = 10;
+  g.nz = 10;
+  g.block = 4;
+  g.spacing = 4;
+  return g;
+}
+
+// "registry lists exactly the 17 kernel names" (test_kernels.cpp:29-54)
+static void registry() {
+  CHECK(kernel_names().size() == 17);
+  CHECK(throws<ConfigError>([] { make_descriptor("plain-push"); }));
+  const KernelDescriptor nt = make_descriptor("list-pull-split-nt-2s-soa");
+  CHECK(nt.prop == Propagation::OsPull && nt.addr == Addressing::Indirect && nt.nt_streams == 2);
+  const KernelDescriptor pv = make_descriptor("list-aa-pv-soa");
+  CHECK(pv.prop == Propagation::Aa && pv.ria && pv.pv);
+}
+
+// "uniform equilibrium is a fixed point of every kernel" (:56-67)
+static void fixed_point() {
+  const double w[19] = {1.0 / 3, 1.0 / 18, 1.0 / 18, 1.0 / 18, 1.0 / 18, 1.0 / 18, 1.0 / 18,
+                        1.0 / 36, 1.0 / 36, 1.0 / 36, 1.0 / 36, 1.0 / 36, 1.0 / 36,
+                        1.0 / 36, 1.0 / 36, 1.0 / 36, 1.0 / 36, 1.0 / 36, 1.0 / 36};
+  for (const std::string& name : kernel_names()) {
+    auto k = make_kernel(make_descriptor(name), bench_blocks());
+    k->advance(kParams, BodyForce{}, 4);
+    const std::vector<double> s = k->snapshot();
+    bool ok = true;
+    for (std::size_t n = 0; n < s.size() / 19; ++n)
+      for (int d = 0; d < 19; ++d) ok = ok && std::abs(s[n * 19 + d] - w[d]) <= 1e-15;
+    CHECK(ok);
+  }
+}
+
+// "results are bitwise identical across ..." + golden fingerprint of the
+// reference (tests/golden/small.json, blocks_12x10x10 full / half family)
+static void golden(const char* full_fp, const char* half_fp) {
+  for (const std::string& name : kernel_names()) {
+    auto k = make_kernel(make_descriptor(name), bench_blocks());
+    k->load_perturbed(1234);
+    k->advance(kParams, kForce, 8);
+    char buf[20];
+    std::snprintf(buf, sizeof(buf), "%016llx",
+                  static_cast<unsigned long long>(state_fingerprint(k->snapshot())));
+    const bool list = name.rfind("list-", 0) == 0;
+    if (std::string(buf) != (list ? half_fp : full_fp)) {
+      std::printf("fingerprint %s: %s\n", name.c_str(), buf);
+      ++failures;
+    }
+  }
+}
+
+// "AA kernels reject odd step counts before touching state" (:167-175)
+static void rejections() {
+  auto k = make_kernel(make_descriptor("list-aa-soa"), bench_blocks());
+  const std::vector<double> before = k->snapshot();
+  CHECK(throws<ConfigError>([&] { k->advance(kParams, kForce, 3); }));
+  CHECK(k->snapshot() == before);
+  CHECK(throws<ConfigError>([&] { k->advance(kParams, kForce, -2); }));
+  GeometrySpec bad = bench_blocks();
+  bad.block = 0;
+  CHECK(throws<ConfigError>([&] { make_kernel(make_descriptor("aa-soa"), bad); }));
+}
+
+// verify_kernel (verification.cpp) through the C++ API
+static void verification() {
+  PoiseuilleCase c;
+  c.nx = 4;
+  c.ny = 4;
+  c.nz = 18;
+  const VerificationReport r = verify_kernel(make_descriptor("aa-soa"), c);
+  CHECK(r.converged && r.passed && r.linf_rel < 1e-6);
+}
+
+int main(int argc, char** argv) {
+  if (argc < 3) {
+    std::printf("usage: cpp_api_test FULL_FP HALF_FP\n");
+    return 2;
+  }
+  try {
+    registry();
+    fixed_point();
+    golden(argv[1], argv[2]);
+    rejections();
+    verification();
+  } catch (const std::exception& e) {
+    std::printf("unexpected exception: %s\n", e.what());
+    return 1;
+  }
+  if (failures) {
+    std::printf("%d FAILED\n", failures);
+    return 1;
+  }
+  std::printf("ALL PASSED\n");
+  return 0;
+}
