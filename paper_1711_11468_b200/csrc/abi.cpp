@@ -319,10 +319,11 @@ int lbmgpu_create(const char* name, int blk, int W, const lbmgpu_geometry* geom,
     }
     if (ds.device >= 0) LBM_CUDA(cudaSetDevice(ds.device));
     if (c->desc.indirect) {
-      if (ds.nranks > 1 || ds.virtual_parts > 1)
-        throw ConfigError("list kernels run as replicas only (one lattice per "
-                          "GPU); z-slab decomposition is for direct AA");
-      c->eng = make_list_engine(c->desc, c->geom, to_padding(pad));
+      if ((ds.nranks > 1 || ds.virtual_parts > 1) &&
+          (c->desc.prop != Prop::Aa || c->desc.ria || c->desc.blk != 0))
+        throw ConfigError("list decomposition is implemented for list-aa-soa / list-aa-aos "
+                          "with blk = 0 (kernel '" + c->desc.name + "')");
+      c->eng = make_list_engine(c->desc, c->geom, to_padding(pad), ds);
     } else {
       c->eng = make_direct_engine(c->desc, c->geom, ds);
     }

@@ -596,15 +596,8 @@ class LocalTransport final : public Transport {
 
 }  // namespace
 
-// NCCL transport (nccl.cpp): one process per GPU, slab = rank.
-class NcclTransportImpl;
-NcclTransportImpl* nccl_create(std::vector<HaloRow> plan, int rank, int nranks,
-                               const uint8_t* id128);
-void nccl_exchange(NcclTransportImpl* t, int phase, const std::vector<double*>& bases,
-                   uint64_t P, cudaStream_t s);
-void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s);
-double nccl_sum(NcclTransportImpl* t, double v);
-void nccl_destroy(NcclTransportImpl* t);
+// NCCL transport (nccl.cpp, declared in halo.hpp): one process per GPU,
+// slab = rank.
 
 namespace {
 

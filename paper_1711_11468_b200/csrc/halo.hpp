@@ -16,6 +16,9 @@
 // exchange is race-free and the result is bitwise the single-part result.
 #pragma once
 
+#include <cuda_runtime.h>
+
+#include <cstddef>
 #include <cstdint>
 #include <vector>
 
@@ -31,5 +34,25 @@ struct HaloRow {
 // nz planes cut into `parts` slabs [nz*p/parts, nz*(p+1)/parts); ring adds
 // the boundary between the last and the first slab (z-periodic exchange).
 std::vector<HaloRow> halo_plan(int nz, int parts, bool ring);
+
+// ---- NCCL transport (nccl.cpp), shared by the direct and list engines ----
+class NcclTransportImpl;
+struct NcclP2P {
+  int peer;                // part index (== rank; 0 with one rank)
+  const double* send;      // nullptr: no send
+  double* recv;            // nullptr: no recv
+  size_t count;            // doubles
+};
+NcclTransportImpl* nccl_create(std::vector<HaloRow> plan, int rank, int nranks,
+                               const uint8_t* id128);
+void nccl_exchange(NcclTransportImpl* t, int phase, const std::vector<double*>& bases,
+                   uint64_t P, cudaStream_t s);
+void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s);
+void nccl_begin(NcclTransportImpl* t, int phase, cudaStream_t s);
+void nccl_p2p(NcclTransportImpl* t, const std::vector<NcclP2P>& ops);
+void nccl_end(NcclTransportImpl* t, int phase);
+cudaStream_t nccl_comm_stream(NcclTransportImpl* t);
+double nccl_sum(NcclTransportImpl* t, double v);
+void nccl_destroy(NcclTransportImpl* t);
 
 }  // namespace lbmgpu

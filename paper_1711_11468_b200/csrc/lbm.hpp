@@ -214,7 +214,8 @@ std::unique_ptr<Engine> make_direct_engine(const Descriptor& d,
                                            const DistSpec& dist);
 std::unique_ptr<Engine> make_list_engine(const Descriptor& d,
                                          const GeomSpec& g,
-                                         const Padding& pad);
+                                         const Padding& pad,
+                                         const DistSpec& dist);
 
 // ---------------------------------------------------- device primitives
 // Kahan/Neumaier-compensated sum of n doubles accessed through idx.

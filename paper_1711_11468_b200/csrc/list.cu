@@ -23,7 +23,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <tuple>
 
+#include "halo.hpp"
 #include "lbm.hpp"
 
 namespace lbmgpu {
@@ -35,6 +37,7 @@ struct ListArgs {
   uint64_t N;
   uint64_t starts[kQ];  // SoA direction starts (unused for AoS)
   TrtArgs trt;
+  uint64_t nb, ne;      // node range of this launch (AA sweeps); [0, N) by default
 };
 
 template <bool SOA>
@@ -106,8 +109,8 @@ __global__ void __launch_bounds__(256) k_list_collide(const ListArgs a) {
 // aa_even_node (kernels_list_aa.cpp:10-16): own slots -> opposite slots.
 template <bool SOA, bool CS>
 __global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
+  const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.ne) return;
   double* buf = a.dst;
   double q[kQ];
 #pragma unroll
@@ -121,8 +124,8 @@ __global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
 // sides -- gather d through column opp(d), scatter d through column d.
 template <bool SOA, bool CS>
 __global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a, uint64_t pf) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
+  const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.ne) return;
   double* buf = a.dst;
   // L2 prefetch of the adjacency lines a block about `pf` nodes ahead will
   // need (blocks are dispatched in index order): the index load of later
@@ -489,12 +492,83 @@ __global__ void k_list_canon(const ListArgs a, double* buf,
 template <bool SOA>
 __global__ void k_list_mass_terms(const ListArgs a, const double* buf,
                                   double* out) {
-  // contiguous copy of the fluid populations (pads excluded) for the
-  // compensated sum
-  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.N;
+  // contiguous copy of the fluid populations (pads excluded) of nodes
+  // [nb, ne) for the compensated sum
+  const uint64_t cnt = a.ne - a.nb;
+  for (uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.ne;
        n += uint64_t(gridDim.x) * blockDim.x)
 #pragma unroll
-    for (int d = 0; d < kQ; ++d) out[d * a.N + n] = buf[lslot<SOA>(a, n, d)];
+    for (int d = 0; d < kQ; ++d) out[d * cnt + (n - a.nb)] = buf[lslot<SOA>(a, n, d)];
+}
+
+// ---- node-range decomposition of list AA (multi-GPU) ----
+// Part p owns the contiguous list nodes [n0_p, n1_p) (blk = 0: x-major, so
+// parts are x-slabs) and keeps the full slot array; its odd step gathers from
+// and scatters to the slots of neighbour-owned nodes listed in its links.
+// Link (r <- s) = the slots of s's nodes that r's scatter entries point to;
+// every slot is referenced by exactly one node, so r's odd step is the only
+// reader/writer of those slots in that sub-step.  Exchange per AA pair:
+// phase 0 (after even) s -> r, phase 1 (after odd) r -> s, of exactly these
+// slots -- the list analogue of the direct z-slab plan (halo.hpp).
+
+// node owning the slot that entry (n, column d) points to (SlotMap::slot,
+// list_lattice.hpp:66-75: a fluid neighbour's slot d, else n's own opp slot)
+__device__ __forceinline__ uint64_t entry_owner(const ListArgs& a, int soa, uint64_t n, int d,
+                                                uint32_t e) {
+  if (soa) {
+    const uint64_t s = a.starts[d];
+    return (e >= s && e < s + a.N) ? e - s : n;
+  }
+  return e / kQ;
+}
+
+__global__ void k_link_flags(const ListArgs a, int soa, uint64_t nb, uint64_t ne, uint64_t olo,
+                             uint64_t ohi, uint8_t* __restrict__ flags,
+                             uint32_t* __restrict__ vals) {
+  const uint64_t cnt = ne - nb;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt * 18;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const int d = static_cast<int>(i / cnt) + 1;
+    const uint64_t n = nb + (i - uint64_t(d - 1) * cnt);
+    const uint32_t e = a.adj[uint64_t(d - 1) * a.N + n];
+    const uint64_t m = entry_owner(a, soa, n, d, e);
+    flags[i] = m >= olo && m < ohi;
+    vals[i] = e;
+  }
+}
+
+__global__ void k_boundary_mask(const ListArgs a, int soa, uint64_t nb, uint64_t ne,
+                                uint8_t* __restrict__ mask) {
+  for (uint64_t n = nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < ne;
+       n += uint64_t(gridDim.x) * blockDim.x) {
+    bool remote = false;
+    for (int d = 1; d < kQ && !remote; ++d) {
+      const uint64_t m = entry_owner(a, soa, n, d, a.adj[uint64_t(d - 1) * a.N + n]);
+      remote = m < nb || m >= ne;
+    }
+    mask[n - nb] = remote;
+  }
+}
+
+__global__ void k_slots_copy(const uint32_t* __restrict__ slots, uint64_t cnt,
+                             const double* __restrict__ src, double* __restrict__ dst) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dst[slots[i]] = src[slots[i]];
+}
+
+__global__ void k_slots_pack(const uint32_t* __restrict__ slots, uint64_t cnt,
+                             const double* __restrict__ buf, double* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = buf[slots[i]];
+}
+
+__global__ void k_slots_unpack(const uint32_t* __restrict__ slots, uint64_t cnt,
+                               const double* __restrict__ in, double* __restrict__ buf) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    buf[slots[i]] = in[i];
 }
 
 // ------------------------------------------------------------------ engine
@@ -506,7 +580,22 @@ int grid_for(uint64_t n, int threads) {
 
 class ListEngine final : public Engine {
  public:
-  ListEngine(const Descriptor& d, const GeomSpec& g, const Padding& pad) {
+  // node-range part of a decomposed list lattice
+  struct LPart {
+    int index = 0;
+    uint64_t n0 = 0, n1 = 0, head = 0, tail = 0;
+    DevBuf<double> own;  // full slot array (parts other than the first)
+    double* buf = nullptr;
+  };
+  struct LLink {
+    int r = 0, s = 0;      // slots of s's nodes referenced by r's nodes
+    uint64_t count = 0;
+    DevBuf<uint32_t> slots;
+    DevBuf<double> send, recv;  // NCCL staging
+  };
+
+  ListEngine(const Descriptor& d, const GeomSpec& g, const Padding& pad,
+             const DistSpec& dist) {
     desc_ = d;
     LBM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     DeviceGeometry geo = build_geometry_device(g, stream_);
@@ -603,10 +692,229 @@ class ListEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_PULL_PF_WAVES")) pwaves = std::atoi(e);
       pull_pf_ = uint64_t(pwaves) * uint64_t(sm_count_) * 2 * 256;
     }
+    const int parts = dist.nranks > 1 ? dist.nranks : std::max(1, dist.virtual_parts);
+    if (parts > 1) setup_parts(dist, parts);
   }
 
   ~ListEngine() override {
+    if (lnccl_) nccl_destroy(lnccl_);
     if (stream_) cudaStreamDestroy(stream_);
+  }
+
+  // ---- node-range decomposition -------------------------------------------
+  void setup_parts(const DistSpec& dist, int parts) {
+    if (desc_.prop != Prop::Aa || desc_.ria)
+      throw ConfigError("list decomposition is implemented for list-aa-soa / list-aa-aos "
+                        "(kernel '" + desc_.name + "')");
+    if (desc_.blk != 0)
+      throw ConfigError("list decomposition needs blk = 0 (node ranges = x-slabs)");
+    if (uint64_t(parts) > n_fluid_) throw ConfigError("more parts than fluid nodes");
+    if (dist.nranks > 1 && !dist.have_id)
+      throw ConfigError("dist: nranks > 1 needs the NCCL unique id");
+    lnparts_ = parts;
+    lrank_ = dist.rank;
+    lnranks_ = dist.nranks;
+    const bool multi_process = dist.nranks > 1;
+    auto range = [&](int p) {
+      return std::pair<uint64_t, uint64_t>(n_fluid_ * uint64_t(p) / parts,
+                                           n_fluid_ * uint64_t(p + 1) / parts);
+    };
+    ListArgs a = base_args();
+    // parts living in this process; part 0 (or this rank's part) reuses buf_[0]
+    for (int p = 0; p < parts; ++p) {
+      if (multi_process && p != lrank_) continue;
+      LPart lp;
+      lp.index = p;
+      std::tie(lp.n0, lp.n1) = range(p);
+      if (lparts_.empty()) {
+        lp.buf = buf_[0].get();
+      } else {
+        lp.own.alloc(total_slots_);
+        LBM_CUDA(cudaMemcpyAsync(lp.own.get(), buf_[0].get(), total_slots_ * 8,
+                                 cudaMemcpyDeviceToDevice, stream_));
+        lp.buf = lp.own.get();
+      }
+      // boundary nodes (any entry owned by another part) -> head / tail spans
+      const uint64_t cnt = lp.n1 - lp.n0;
+      DevBuf<uint8_t> mask(cnt);
+      k_boundary_mask<<<grid_for(cnt, 256), 256, 0, stream_>>>(a, desc_.soa, lp.n0, lp.n1,
+                                                                mask.get());
+      LBM_CHECK_LAUNCH();
+      std::vector<uint8_t> h(cnt);
+      LBM_CUDA(cudaMemcpyAsync(h.data(), mask.get(), cnt, cudaMemcpyDeviceToHost, stream_));
+      LBM_CUDA(cudaStreamSynchronize(stream_));
+      uint64_t head = 0, tail = 0;
+      for (uint64_t i = 0; i < cnt / 2; ++i)
+        if (h[i]) head = i + 1;
+      for (uint64_t i = cnt / 2; i < cnt; ++i)
+        if (h[i]) {
+          tail = cnt - i;
+          break;
+        }
+      lp.head = head;
+      lp.tail = std::min(tail, cnt - head);
+      lparts_.push_back(std::move(lp));
+    }
+    // links (r <- s) this process takes part in
+    for (int r = 0; r < parts; ++r)
+      for (int s = 0; s < parts; ++s) {
+        if (r == s) continue;
+        if (multi_process && r != lrank_ && s != lrank_) continue;
+        const auto [rn0, rn1] = range(r);
+        const auto [sn0, sn1] = range(s);
+        const uint64_t cnt = (rn1 - rn0) * 18;
+        DevBuf<uint8_t> flags(cnt);
+        DevBuf<uint32_t> vals(cnt);
+        k_link_flags<<<grid_for(cnt, 256), 256, 0, stream_>>>(a, desc_.soa, rn0, rn1, sn0, sn1,
+                                                              flags.get(), vals.get());
+        LBM_CHECK_LAUNCH();
+        DevBuf<uint32_t> out(cnt);
+        DevBuf<unsigned long long> nsel(1);
+        size_t tmp = 0;
+        LBM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, vals.get(), flags.get(), out.get(),
+                                            nsel.get(), static_cast<int64_t>(cnt), stream_));
+        DevBuf<uint8_t> t(tmp);
+        LBM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, vals.get(), flags.get(), out.get(),
+                                            nsel.get(), static_cast<int64_t>(cnt), stream_));
+        unsigned long long k = 0;
+        LBM_CUDA(cudaMemcpyAsync(&k, nsel.get(), 8, cudaMemcpyDeviceToHost, stream_));
+        LBM_CUDA(cudaStreamSynchronize(stream_));
+        if (k == 0) continue;
+        LLink l;
+        l.r = r;
+        l.s = s;
+        l.count = k;
+        l.slots.alloc(k);
+        LBM_CUDA(cudaMemcpyAsync(l.slots.get(), out.get(), k * 4, cudaMemcpyDeviceToDevice,
+                                 stream_));
+        if (multi_process || dist.have_id) {
+          l.send.alloc(k);
+          l.recv.alloc(k);
+        }
+        links_.push_back(std::move(l));
+      }
+    if (multi_process || dist.have_id)
+      lnccl_ = nccl_create({}, multi_process ? lrank_ : 0, multi_process ? lnranks_ : 1,
+                           dist.nccl_id.data());
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  LPart* part_of(int index) {
+    for (LPart& p : lparts_)
+      if (p.index == index) return &p;
+    return nullptr;
+  }
+
+  // phase 0 (after even): slots flow s -> r; phase 1 (after odd): r -> s.
+  void list_exchange(int phase) {
+    if (!lnccl_) {  // all parts in this process: direct slot copies
+      for (LLink& l : links_) {
+        LPart* from = part_of(phase == 0 ? l.s : l.r);
+        LPart* to = part_of(phase == 0 ? l.r : l.s);
+        k_slots_copy<<<grid_for(l.count, 256), 256, 0, stream_>>>(l.slots.get(), l.count,
+                                                                   from->buf, to->buf);
+        LBM_CHECK_LAUNCH();
+      }
+      return;
+    }
+    std::vector<NcclP2P> ops;
+    for (LLink& l : links_) {  // pack what this process sends
+      LPart* from = part_of(phase == 0 ? l.s : l.r);
+      if (!from) continue;
+      k_slots_pack<<<grid_for(l.count, 256), 256, 0, stream_>>>(l.slots.get(), l.count,
+                                                                 from->buf, l.send.get());
+      LBM_CHECK_LAUNCH();
+    }
+    nccl_begin(lnccl_, phase, stream_);
+    for (LLink& l : links_) {  // global link order on every rank -> matched pairs
+      const int src = phase == 0 ? l.s : l.r, dst = phase == 0 ? l.r : l.s;
+      if (part_of(src)) ops.push_back({dst, l.send.get(), nullptr, l.count});
+      if (part_of(dst)) ops.push_back({src, nullptr, l.recv.get(), l.count});
+    }
+    nccl_p2p(lnccl_, ops);
+    cudaStream_t cs = nccl_comm_stream(lnccl_);
+    for (LLink& l : links_) {
+      LPart* to = part_of(phase == 0 ? l.r : l.s);
+      if (!to) continue;
+      k_slots_unpack<<<grid_for(l.count, 256), 256, 0, cs>>>(l.slots.get(), l.count,
+                                                             l.recv.get(), to->buf);
+      LBM_CHECK_LAUNCH();
+    }
+    nccl_end(lnccl_, phase);
+  }
+
+  void list_wait(int phase) {
+    if (lnccl_) nccl_wait(lnccl_, phase, stream_);
+  }
+
+  // one AA pair over node-range parts: even(boundary) -> [exchange 0 ||
+  // even(interior)] -> odd(boundary) -> [exchange 1 || odd(interior)]
+  void aa_pair_parts(const TrtArgs& t) {
+    const bool soa = desc_.soa;
+    auto sweep = [&](bool odd, bool boundary) {
+      for (LPart& p : lparts_) {
+        ListArgs a = base_args();
+        a.trt = t;
+        a.src = a.dst = p.buf;
+        auto run = [&](uint64_t b0, uint64_t b1) {
+          a.nb = b0;
+          a.ne = b1;
+          if (odd)
+            soa ? launch("list_aa_odd_soa", k_list_aa_odd<true, false>, a, pf_)
+                : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a, pf_);
+          else
+            soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
+                : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+        };
+        if (boundary) {
+          run(p.n0, p.n0 + p.head);
+          run(p.n1 - p.tail, p.n1);
+        } else {
+          run(p.n0 + p.head, p.n1 - p.tail);
+        }
+      }
+    };
+    sweep(false, true);
+    list_exchange(0);
+    sweep(false, false);
+    list_wait(0);
+    sweep(true, true);
+    list_exchange(1);
+    sweep(true, false);
+    list_wait(1);
+  }
+
+  int parts() const override { return lparts_.empty() ? 1 : static_cast<int>(lparts_.size()); }
+  void part_info(int p, int* z0, int* z1, uint64_t* nf) const override {
+    if (lparts_.empty()) {
+      *z0 = 0;
+      *z1 = nz_;
+      *nf = n_fluid_;
+      return;
+    }
+    const LPart& lp = lparts_.at(p);
+    *z0 = static_cast<int>(lp.n0);  // node range for list parts
+    *z1 = static_cast<int>(lp.n1);
+    *nf = lp.n1 - lp.n0;
+  }
+  bool holds_all() const override { return lnranks_ == 1; }
+  uint64_t local_rows() const override {
+    if (lparts_.empty() || lnranks_ == 1) return n_fluid_;
+    return lparts_[0].n1 - lparts_[0].n0;
+  }
+  void local_canonical_index(uint64_t* out) const override {
+    if (lparts_.empty() || lnranks_ == 1) {
+      for (uint64_t k = 0; k < n_fluid_; ++k) out[k] = k;
+      return;
+    }
+    for (uint64_t k = lparts_[0].n0; k < lparts_[0].n1; ++k) out[k - lparts_[0].n0] = k;
+  }
+  void gather_local(uint64_t k0, uint64_t count, double* d, bool to_staging) override {
+    const uint64_t base = (lparts_.empty() || lnranks_ == 1) ? 0 : lparts_[0].n0;
+    if (to_staging)
+      gather_canonical(base + k0, count, d);
+    else
+      scatter_canonical(base + k0, count, d);
   }
 
   ListArgs base_args() const {
@@ -614,14 +922,18 @@ class ListEngine final : public Engine {
     a.adj = adj_.get();
     a.N = n_fluid_;
     for (int q = 0; q < kQ; ++q) a.starts[q] = starts_[q];
+    a.nb = 0;
+    a.ne = n_fluid_;
     return a;
   }
 
   template <class K, class... Extra>
   void launch(const char* name, K kern, const ListArgs& a, Extra... extra) {
     const int threads = 256;
+    if (a.ne <= a.nb) return;
     const int tok = stats_.begin(name, stream_);
-    kern<<<static_cast<unsigned>(ceil_div(a.N, threads)), threads, 0, stream_>>>(a, extra...);
+    kern<<<static_cast<unsigned>(ceil_div(a.ne - a.nb, threads)), threads, 0, stream_>>>(
+        a, extra...);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);
   }
@@ -630,6 +942,10 @@ class ListEngine final : public Engine {
     ListArgs a = base_args();
     a.trt = t;
     const bool soa = desc_.soa;
+    if (desc_.prop == Prop::Aa && !lparts_.empty()) {
+      for (long s = 0; s < steps; s += 2) aa_pair_parts(t);
+      return;
+    }
     if (desc_.prop == Prop::Aa) {
       a.src = a.dst = buf_[0].get();
       for (long s = 0; s < steps; s += 2) {
@@ -701,15 +1017,27 @@ class ListEngine final : public Engine {
              double amp = 0, double* rho = nullptr, double* u = nullptr) {
     if (c1 <= c0) return;
     ListArgs a = base_args();
-    const int g = grid_for(c1 - c0, 256);
     const uint32_t* loc = desc_.blk > 0 ? list_of_canon_.get() : nullptr;
-    if (desc_.soa)
-      k_list_canon<true, MODE><<<g, 256, 0, stream_>>>(a, buf_[cur_].get(), loc, c0, c1,
-                                                       stage, seed, amp, rho, u);
-    else
-      k_list_canon<false, MODE><<<g, 256, 0, stream_>>>(a, buf_[cur_].get(), loc, c0, c1,
-                                                        stage, seed, amp, rho, u);
-    LBM_CHECK_LAUNCH();
+    auto run = [&](double* buf, uint64_t b0, uint64_t b1) {
+      if (b1 <= b0) return;
+      const int g = grid_for(b1 - b0, 256);
+      // the kernels index stage relative to c0; pass an offset pointer
+      double* st = stage ? stage + (b0 - c0) * kQ : nullptr;
+      if (desc_.soa)
+        k_list_canon<true, MODE><<<g, 256, 0, stream_>>>(a, buf, loc, b0, b1, st, seed, amp,
+                                                         rho, u);
+      else
+        k_list_canon<false, MODE><<<g, 256, 0, stream_>>>(a, buf, loc, b0, b1, st, seed, amp,
+                                                          rho, u);
+      LBM_CHECK_LAUNCH();
+    };
+    if (lparts_.empty()) {
+      run(buf_[cur_].get(), c0, c1);
+      return;
+    }
+    // node-range parts (blk = 0: canonical index == list index): each node's
+    // PDFs live in its owner part's buffer
+    for (LPart& p : lparts_) run(p.buf, std::max(c0, p.n0), std::min(c1, p.n1));
   }
 
   void gather_canonical(uint64_t c0, uint64_t count, double* out) override {
@@ -726,14 +1054,23 @@ class ListEngine final : public Engine {
   }
 
   double total_mass() override {
-    DevBuf<double> tmp(n_fluid_ * kQ);
-    ListArgs a = base_args();
-    desc_.soa ? k_list_mass_terms<true><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
-                    a, buf_[cur_].get(), tmp.get())
-              : k_list_mass_terms<false><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
-                    a, buf_[cur_].get(), tmp.get());
-    LBM_CHECK_LAUNCH();
-    return device_sum(tmp.get(), tmp.size(), stream_);
+    auto part_mass = [&](double* buf, uint64_t b0, uint64_t b1) {
+      if (b1 <= b0) return 0.0;
+      DevBuf<double> tmp((b1 - b0) * kQ);
+      ListArgs a = base_args();
+      a.nb = b0;
+      a.ne = b1;
+      desc_.soa ? k_list_mass_terms<true><<<grid_for(b1 - b0, 256), 256, 0, stream_>>>(
+                      a, buf, tmp.get())
+                : k_list_mass_terms<false><<<grid_for(b1 - b0, 256), 256, 0, stream_>>>(
+                      a, buf, tmp.get());
+      LBM_CHECK_LAUNCH();
+      return device_sum(tmp.get(), tmp.size(), stream_);
+    };
+    if (lparts_.empty()) return part_mass(buf_[cur_].get(), 0, n_fluid_);
+    double m = 0.0;
+    for (LPart& p : lparts_) m += part_mass(p.buf, p.n0, p.n1);
+    return lnccl_ && lnranks_ > 1 ? nccl_sum(lnccl_, m) : m;
   }
 
   void export_structure(int32_t* nodes, uint32_t* adj, uint64_t* starts,
@@ -833,6 +1170,11 @@ class ListEngine final : public Engine {
   DevBuf<uint32_t> adj_;
   DevBuf<uint32_t> list_of_canon_;
   DevBuf<double> buf_[2];
+  // node-range decomposition (list AA over several GPUs / emulated parts)
+  std::vector<LPart> lparts_;
+  std::vector<LLink> links_;
+  int lnparts_ = 1, lrank_ = 0, lnranks_ = 1;
+  NcclTransportImpl* lnccl_ = nullptr;
   int64_t ria_runs_ = -1;
   double ria_vfrac_ = 0.0;
   uint64_t ria_R_ = 0;
@@ -849,8 +1191,9 @@ class ListEngine final : public Engine {
 
 std::unique_ptr<Engine> make_list_engine(const Descriptor& d,
                                          const GeomSpec& g,
-                                         const Padding& pad) {
-  return std::make_unique<ListEngine>(d, g, pad);
+                                         const Padding& pad,
+                                         const DistSpec& dist) {
+  return std::make_unique<ListEngine>(d, g, pad, dist);
 }
 
 }  // namespace lbmgpu

@@ -130,6 +130,29 @@ class NcclTransportImpl {
     LBM_CUDA(cudaStreamWaitEvent(s, done_[phase], 0));
   }
 
+  // Generic grouped point-to-point for index-list halos (list lattices):
+  // begin() hands the compute stream's work over to the comm stream, p2p()
+  // issues one NCCL group, end() marks the phase done on the comm stream
+  // (after any unpack kernels the caller queued there).
+  void begin(int phase, cudaStream_t s) {
+    LBM_CUDA(cudaEventRecord(ready_[phase], s));
+    LBM_CUDA(cudaStreamWaitEvent(comm_stream_, ready_[phase], 0));
+  }
+  void p2p(const std::vector<NcclP2P>& ops) {
+    const NcclApi& api = NcclApi::get();
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (const NcclP2P& o : ops) {
+      const int peer = nranks_ == 1 ? 0 : o.peer;
+      if (o.send)
+        nccl_check(api.Send(o.send, o.count, ncclFloat64, peer, comm_, comm_stream_), "ncclSend");
+      if (o.recv)
+        nccl_check(api.Recv(o.recv, o.count, ncclFloat64, peer, comm_, comm_stream_), "ncclRecv");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  }
+  void end(int phase) { LBM_CUDA(cudaEventRecord(done_[phase], comm_stream_)); }
+  cudaStream_t comm_stream() const { return comm_stream_; }
+
   double sum(double v) {
     const NcclApi& api = NcclApi::get();
     LBM_CUDA(cudaMemcpyAsync(dsum_, &v, sizeof(double), cudaMemcpyHostToDevice,
@@ -162,6 +185,10 @@ void nccl_exchange(NcclTransportImpl* t, int phase, const std::vector<double*>& 
   t->exchange(phase, bases, P, s);
 }
 void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s) { t->wait(phase, s); }
+void nccl_begin(NcclTransportImpl* t, int phase, cudaStream_t s) { t->begin(phase, s); }
+void nccl_p2p(NcclTransportImpl* t, const std::vector<NcclP2P>& ops) { t->p2p(ops); }
+void nccl_end(NcclTransportImpl* t, int phase) { t->end(phase); }
+cudaStream_t nccl_comm_stream(NcclTransportImpl* t) { return t->comm_stream(); }
 double nccl_sum(NcclTransportImpl* t, double v) { return t->sum(v); }
 void nccl_destroy(NcclTransportImpl* t) { delete t; }
 

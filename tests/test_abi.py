@@ -152,6 +152,7 @@ def test_config_errors_before_device_work():
             lbm.make_kernel(d, spec)
     with pytest.raises(lbm.ConfigError):
         lbm.make_kernel(d, lbm.GeometrySpec("channel", 8, 8, 8), row_pad=-1)
-    with pytest.raises(lbm.ConfigError):
-        lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), lbm.GeometrySpec("channel", 8, 8, 8),
-                        dist={"virtual_parts": 2})
+    for name, blk in (("list-pull-soa", 0), ("list-aa-ria-soa", 0), ("list-aa-soa", 2)):
+        with pytest.raises(lbm.ConfigError):
+            lbm.make_kernel(lbm.make_descriptor(name, blk=blk),
+                            lbm.GeometrySpec("channel", 8, 8, 8), dist={"virtual_parts": 2})

@@ -268,6 +268,41 @@ def test_zslab_nccl_transport_single_gpu(kind, dims, parts):
     assert np.array_equal(k.snapshot(), ref.snapshot())
 
 
+@pytest.mark.parametrize("name", ["list-aa-soa", "list-aa-aos"])
+@pytest.mark.parametrize("kind,dims,parts", [
+    ("channel", (20, 12, 10), 2), ("channel", (20, 12, 10), 3), ("blocks", (16, 16, 16), 2),
+    ("blocks", (16, 16, 16), 5), ("pipe", (12, 14, 13), 4)])
+def test_list_node_range_parts_bitwise(name, kind, dims, parts):
+    """List AA decomposed into contiguous node ranges (x-slabs for blk = 0)
+    with index-list halos, emulated on one GPU: bitwise
+    equal to the single-part run, including the periodic wrap between the
+    last and the first part (blocks)."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    ref.load_perturbed(17)
+    ref.advance(PARAMS, FORCE, 8)
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec, dist={"virtual_parts": parts})
+    k.load_perturbed(17)
+    k.advance(PARAMS, FORCE, 4)
+    k.advance(PARAMS, FORCE, 4)
+    assert np.array_equal(k.snapshot(), ref.snapshot())
+    assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
+
+
+def test_list_parts_nccl_transport_single_gpu():
+    """The list halo over NCCL (pack -> grouped send/recv -> unpack on the comm
+    stream), one NCCL rank owning every part (self send/recv)."""
+    spec = lbm.GeometrySpec("blocks", 16, 16, 16)
+    ref = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec)
+    ref.load_perturbed(23)
+    ref.advance(PARAMS, FORCE, 6)
+    k = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec,
+                        dist={"virtual_parts": 3, "nccl_id": lbm.lbmgpu.nccl_unique_id()})
+    k.load_perturbed(23)
+    k.advance(PARAMS, FORCE, 6)
+    assert np.array_equal(k.snapshot(), ref.snapshot())
+
+
 def test_poiseuille_verification_passes():
     """verify_kernel (verification.cpp:31-100) on the GPU: slit 4x4x18."""
     for name in ("blk-push-soa", "aa-soa", "list-aa-soa", "list-pull-soa", "blk-pull-aos",
