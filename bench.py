@@ -216,6 +216,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
+    ap.add_argument("--decompose", action="store_true",
+                    help="list-aa configs at N>1: node-range decomposition instead of replicas")
+    ap.add_argument("--virtual-parts", type=int, default=1,
+                    help="1 GPU: emulate the multi-GPU decomposition with this many parts "
+                         "(device-copy halos) -- an overhead probe, not a bench line")
     ap.add_argument("--kernel", default=None,
                     help="run another kernel name on the config's geometry (extra lines)")
     ap.add_argument("--dims", default=None,
@@ -257,7 +262,10 @@ def main():
     # direct AA (cfg 5) is z-slab decomposed over the ranks (strong scaling);
     # every other kernel runs as independent replicas, one lattice per GPU
     # (the list configs are replicas only) -> weak scaling
-    replicas = world > 1 and not (desc.addr == "direct" and aa)
+    decomposable = aa and (desc.addr == "direct" or (args.decompose and not desc.ria))
+    replicas = world > 1 and not decomposable
+    if world == 1 and args.virtual_parts > 1:
+        dspec = {"virtual_parts": args.virtual_parts}
     if world > 1 and not replicas:
         obj = [lbm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -351,6 +359,11 @@ def main():
     if replicas:
         line["scaling"] = "weak"
         line["config"]["parallelism"] = f"{world} independent replicas (list kernels do not shard)"
+    elif world > 1 and desc.addr == "indirect":
+        line["config"]["parallelism"] = f"node-range (x-slab) decomposition x{world}, NCCL index-list halos"
+    if world == 1 and args.virtual_parts > 1:
+        line["config"]["parallelism"] = (f"EMULATED {args.virtual_parts}-part decomposition on 1 GPU "
+                                         "(device-copy halos; overhead probe)")
     line.update({
         "value": mflups,
         "ms_per_step": ms / args.steps,

@@ -22,12 +22,13 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("name", ["aa-soa", "list-aa-soa"])
 @pytest.mark.parametrize("kind,dims", [("channel", (64, 32, 48)), ("blocks", (32, 32, 32))])
-def test_nccl_zslab_bitwise(n, kind, dims):
+def test_nccl_decomposition_bitwise(n, kind, dims, name):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
-           os.path.join(ROOT, "tools", "mgpu_check.py"), *map(str, dims), "10", kind]
+           os.path.join(ROOT, "tools", "mgpu_check.py"), *map(str, dims), "10", kind, name]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr

@@ -21,6 +21,7 @@ import paper_1711_11468_b200 as lbm  # noqa: E402
 def main():
     nx, ny, nz, steps = (int(v) for v in (sys.argv[1:5] if len(sys.argv) > 4 else (64, 32, 48, 10)))
     kind = sys.argv[5] if len(sys.argv) > 5 else "channel"
+    name = sys.argv[6] if len(sys.argv) > 6 else "aa-soa"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -29,7 +30,7 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     spec = lbm.GeometrySpec(kind, nx, ny, nz)
     params, force = lbm.TrtParams.from_tau(0.9), lbm.BodyForce((1e-5, 2e-6, -3e-6))
-    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec,
                         dist={"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0]})
     k.load_perturbed(4242)
     k.advance(params, force, steps)
@@ -39,7 +40,7 @@ def main():
     dist.gather_object(rows, out if rank == 0 else None, dst=0)
     ok = True
     if rank == 0:
-        ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+        ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
         ref.load_perturbed(4242)
         ref.advance(params, force, steps)
         expect = ref.snapshot().reshape(-1, 19)
