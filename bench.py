@@ -281,13 +281,14 @@ def main():
         torch.cuda.synchronize()
         k.synchronize()
 
-    # warm-up
-    if args.warmup:
-        k.advance(params, force, per * args.warmup)
-    barrier()
+    # clock sampler first, then the warm-up right before the timed region (an
+    # idle gap in between lets the GPU drop out of its boost state)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    if args.warmup:
+        k.advance(params, force, per * args.warmup)
+    barrier()
     k.kernel_stats_reset()
     k.kernel_stats_enable(True)
     launches0 = k.launch_count()
@@ -378,10 +379,15 @@ def main():
     })
 
     # ---- end to end through the public API with host buffers: the initial
-    # state is loaded from pinned host memory, K steps run, the final state is
-    # read back to pinned host memory -- all inside the timed region.
+    # state is loaded from pinned host memory, the job's steps run, the final
+    # state is read back to pinned host memory -- all inside the timed region.
+    # The e2e job is the BASELINE run itself (cfg 5: 200 lattice steps,
+    # harness.cpp:97-131) or K bench steps if that is longer: load the initial
+    # state from the host, advance, read the final state back.
     if not args.no_e2e:
-        e2e = run_e2e(lbm, k, params, force, per, args.steps, world, dist, torch, N)
+        job_steps = max(args.steps, CONFIGS[cid][4] // per)
+        e2e = run_e2e(lbm, k, params, force, per, job_steps, world, dist, torch, N)
+        e2e["job_lattice_steps"] = per * job_steps
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

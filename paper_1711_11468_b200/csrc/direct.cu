@@ -105,6 +105,7 @@ template <bool SOA, bool CS, bool CG>
 __device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, uint32_t n) {
   const Idx<SOA> I{a.P, a.nx, a.ny};
   double q[kQ];
+  const uint32_t tm = a.tmask ? a.tmask[n] : 0u;
 #pragma unroll
   for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.src + I(c.Z[1], dslot(d), c.y, c.x));
   if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
@@ -112,10 +113,12 @@ __device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, 
 #pragma unroll
   for (int d = 1; d < kQ; ++d) {
     const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
-    // neighbour flags come from L1 (the small push configs are L2
-    // resident; measured faster than the arithmetic test here)
+    // solid target: the precomputed mask, else the neighbour's flag from L1
+    // (measured faster than the arithmetic test here: cfg 1 fused 15.5k vs
+    // 13.9k MFLUP/s)
     const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
-    const int s = a.flags[tn] ? dslot(opp(d)) : dslot(d);
+    const bool ts = a.tmask ? ((tm >> d) & 1u) != 0 : a.flags[tn] != 0;
+    const int s = ts ? dslot(opp(d)) : dslot(d);
     st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
   }
 }
@@ -176,12 +179,26 @@ __device__ __forceinline__ void aa_odd_node(const DirectArgs& a, const Coords& c
   // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
   // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
   // per direction serves both the load and the store.
+  double q[kQ];
+  // Warp-uniform fast path: no active lane touches a wrapped neighbour, so
+  // every address is the own slot-0 element plus a per-direction constant
+  // (recomputed for the stores: only `own` stays live across the collision).
+  const bool inner = c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u &&
+                     (!a.zwrap || c.z - 1u < a.nzl - 2u);
+  if (__all_sync(__activemask(), inner)) {
+    double* own = buf + I(c.Z[1], 0, c.y, c.x);
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(own + a.odd_off[d]);
+    collide(q, a.trt);
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) st<CS>(own + a.odd_off[d], q[opp(d)]);
+    return;
+  }
   double* p[kQ];
   p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
 #pragma unroll
   for (int d = 1; d < kQ; ++d)
     p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
-  double q[kQ];
 #pragma unroll
   for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(p[d]);
   collide(q, a.trt);
@@ -261,9 +278,9 @@ __device__ __forceinline__ void grid_sync(const GridBarrier& b) {
 
 enum FusedKind { kFusedPush = 0, kFusedPull = 1, kFusedAA = 2 };
 
-template <bool SOA, int KIND>
-__global__ void __launch_bounds__(256) k_full_fused(DirectArgs a, double* other, long steps,
-                                                    GridBarrier bar) {
+template <bool SOA, int KIND, int TPB = 256, int MINB = 1>
+__global__ void __launch_bounds__(TPB, MINB) k_full_fused(DirectArgs a, double* other,
+                                                          long steps, GridBarrier bar) {
   const uint32_t G = gridDim.x * blockDim.x;
   auto sweep = [&](auto body) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.count; i += G) {
@@ -301,6 +318,121 @@ __global__ void __launch_bounds__(256) k_full_fused(DirectArgs a, double* other,
       sweep([&](const Coords& c, uint32_t n) { pull_node<SOA, false, false, true>(a, c, n); });
     grid_sync(bar);
     cur ^= 1;
+  }
+}
+
+// ---- the same multi-sweep run as a plane-level dataflow --------------------
+// No grid barrier: the T sweeps are cut into tasks (sweep s, plane z, chunk i)
+// of blockDim nodes.  A task of sweep s > 0 waits until sweep s-1 has
+// finished planes z-1, z, z+1 (z wrapped); that covers every read and write
+// hazard of push, pull and AA (each sweep touches only the planes next to its
+// own, and the chains close transitively -- DESIGN.md section 4).
+// plane_done[z] counts finished chunks of plane z over all sweeps, so "sweep
+// s-1 done on z" is plane_done[z] >= s * chunks_per_plane (release add by the
+// finishing block, acquire load by the waiting one; lattice loads are
+// ld.global.cg, so no stale L1 line is read).  All blocks are co-resident
+// (cooperative launch).  Blocks that finish their part of a sweep start the
+// next one instead of idling at a barrier.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <bool SOA, int KIND>
+__global__ void __launch_bounds__(256) k_full_flow(DirectArgs a, double* other, long sweeps,
+                                                   unsigned* plane_done, unsigned base) {
+  // Tasks are blockDim-node chunks run by whole blocks.  (32-node warp
+  // tasks without block barriers measured 2x slower: the release/acquire
+  // fences per task dominate.)
+  const uint32_t lane = threadIdx.x;
+  const uint64_t worker = blockIdx.x;
+  const uint64_t workers = gridDim.x;
+  const uint32_t cpp = (a.P + blockDim.x - 1) / blockDim.x;  // chunks per plane
+  const uint64_t per_sweep = uint64_t(a.nzl) * cpp;
+  const uint64_t total = per_sweep * uint64_t(sweeps);
+  double* bufs[2] = {const_cast<double*>(a.src), other};
+  // Static round-robin assignment (block b: tasks b, b + grid, ...): every
+  // block runs its tasks in increasing order, so the smallest unfinished task
+  // is always running and its dependencies (all smaller) are done.  Sweep s
+  // visits the planes starting at plane 2s: sweep s's i-th plane then needs
+  // sweep s-1's (i+1)..(i+3)-th planes, dispatched about a whole sweep
+  // earlier -- without the rotation the z wrap would make the first plane of
+  // every sweep wait for the last plane of the previous one.
+  auto where = [&](uint64_t task, uint32_t& s, uint32_t& z, uint32_t& chunk) {
+    s = static_cast<uint32_t>(task / per_sweep);
+    const uint32_t rem = static_cast<uint32_t>(task - uint64_t(s) * per_sweep);
+    const uint32_t zi = rem / cpp;
+    chunk = rem - zi * cpp;
+    z = static_cast<uint32_t>((zi + 2ull * s) % a.nzl);
+  };
+  // lanes 0-2 watch planes z-1, z, z+1 of the previous sweep
+  auto watched = [&](uint32_t z) {
+    return lane == 0 ? (z == 0 ? a.nzl - 1 : z - 1)
+         : lane == 1 ? z
+                     : (z + 1 == a.nzl ? 0 : z + 1);
+  };
+  // The counters a task needs are read one task ahead (relaxed; re-polled
+  // only if not yet enough); the acquire is a fence after the observing
+  // read, so in the common case (dependencies finished about a sweep ago)
+  // the check puts no L2 round trip on the critical path.
+  unsigned seen = 0;
+  if (lane < 3 && worker < total) {
+    uint32_t s, z, chunk;
+    where(worker, s, z, chunk);
+    seen = ld_relaxed(plane_done + watched(z));
+  }
+  for (uint64_t task = worker; task < total; task += workers) {
+    uint32_t s, z, chunk;
+    where(task, s, z, chunk);
+    if (s > 0) {
+      if (lane < 3) {
+        const unsigned need = base + s * cpp;  // wrap-safe comparisons
+        while (static_cast<int>(seen - need) < 0) {
+          __nanosleep(32);
+          seen = ld_relaxed(plane_done + watched(z));
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    }
+    if (lane < 3 && task + workers < total) {
+      uint32_t s2, z2, c2;
+      where(task + workers, s2, z2, c2);
+      seen = ld_relaxed(plane_done + watched(z2));
+    }
+    const uint32_t x = chunk * blockDim.x + lane;
+    if (x < a.P) {
+      const uint32_t n = z * a.P + x;
+      Coords c;
+      decode_node(a, n, c);
+      if (KIND == kFusedAA) {
+        if (s & 1)
+          aa_odd_node<SOA, false, true>(a, c, n);
+        else
+          aa_even_node<SOA, false, true>(a, c, n);
+      } else if (KIND == kFusedPush) {
+        a.src = bufs[s & 1];
+        a.dst = bufs[(s & 1) ^ 1];
+        push_node<SOA, false, true>(a, c, n);
+      } else if (s == 0) {  // pull: collide pass on the current grid
+        a.dst = bufs[0];
+        collide_node_pass<SOA, true>(a, c, n);
+      } else {
+        a.src = bufs[(s - 1) & 1];
+        a.dst = bufs[s & 1];
+        if (s + 1 < sweeps)
+          pull_node<SOA, true, false, true>(a, c, n);
+        else
+          pull_node<SOA, false, false, true>(a, c, n);
+      }
+    }
+    __syncthreads();  // orders the block's stores before thread 0's release
+    if (lane == 0) red_release_add(plane_done + z, 1u);
   }
 }
 
@@ -509,6 +641,27 @@ __global__ void k_part_flags(const uint8_t* __restrict__ gflags, int nx, int ny,
   }
 }
 
+// Push target mask of a whole-box part: bit d set iff the node x + c_d
+// (wrapped on every axis, as the push sweep stores) is solid.  One 4-byte
+// load per node instead of 18 neighbour flag loads.
+__global__ void k_push_tmask(const uint8_t* __restrict__ pflags, uint32_t nx, uint32_t ny,
+                             uint32_t nz, uint32_t* __restrict__ tmask) {
+  const uint64_t P = uint64_t(nx) * ny, V = P * nz;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < V;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t z = static_cast<uint32_t>(i / P);
+    const uint32_t r = static_cast<uint32_t>(i - z * P);
+    const uint32_t y = r / nx, x = r - y * nx;
+    uint32_t m = 0;
+    for (int d = 1; d < kQ; ++d) {
+      const uint32_t tx = (x + nx + cx(d)) % nx, ty = (y + ny + cy(d)) % ny,
+                     tz = (z + nz + cz(d)) % nz;
+      if (pflags[(uint64_t(tz) * ny + ty) * nx + tx]) m |= 1u << d;
+    }
+    tmask[i] = m;
+  }
+}
+
 // For each fluid box node in canonical order with z in [z0, z1): its
 // canonical index is crank[gi]; its position k within the part is
 // prank[gi] (scan of the part mask).  Writes node_of[k] and canon[k].
@@ -555,6 +708,7 @@ struct Part {
   uint32_t nzl = 0, zoff = 0, nzs = 0;
   DevBuf<double> buf[2];
   DevBuf<uint8_t> flags;
+  DevBuf<uint32_t> tmask;   // push: solid-target bits per node (k_push_tmask)
   DevBuf<uint32_t> node_of;
   DevBuf<uint64_t> canon;   // empty when the part holds the whole box
   uint64_t n_fluid = 0;
@@ -644,7 +798,15 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_TMA_STAGES")) tma_stages_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AA_CS")) cs_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_AA_THREADS")) aa_threads_ = std::atoi(e);
+      if (aa_threads_ < 32 || aa_threads_ > 256 || aa_threads_ % 32)
+        throw ConfigError("LBMGPU_AA_THREADS must be a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_FUSED_FLOW")) flow_threads_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_FUSED_SHAPE")) fused_shape_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_PUSH_TMASK")) use_tmask_ = std::atoi(e) != 0;
+      if (flow_threads_ < 0 || flow_threads_ > 256 || flow_threads_ % 32)
+        throw ConfigError("LBMGPU_FUSED_FLOW must be 0 or a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
         fused_bytes_ = uint64_t(std::atoll(e)) << 20;
       barrier_.alloc(2);
@@ -702,6 +864,12 @@ class DirectEngine final : public Engine {
       k_part_flags<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
           geo.flags.get(), nx_, ny_, nz_, pt.z0, pt.z1, pt.flags.get());
       LBM_CHECK_LAUNCH();
+      if (d.prop == Prop::OsPush && nparts_ == 1 && use_tmask_) {
+        pt.tmask.alloc(uint64_t(pt.nzl) * P_);
+        k_push_tmask<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
+            pt.flags.get(), nx_, ny_, pt.nzl, pt.tmask.get());
+        LBM_CHECK_LAUNCH();
+      }
       // the slab's fluid nodes in canonical order
       DevBuf<uint8_t> mask(V);
       DevBuf<uint32_t> prank(V);
@@ -766,6 +934,7 @@ class DirectEngine final : public Engine {
     a.src = pt.buf[src_buf].get();
     a.dst = pt.buf[dst_buf].get();
     a.flags = pt.flags.get();
+    a.tmask = pt.tmask.get();
     a.nx = nx_;
     a.ny = ny_;
     a.nzl = pt.nzl;
@@ -786,13 +955,20 @@ class DirectEngine final : public Engine {
     const long long D = geom_.pipe_diameter > 0 ? geom_.pipe_diameter
                                                 : (long long)std::min(ny_, nz_) - 2;
     a.d2 = D * D;
+    for (int d = 0; d < kQ; ++d) {
+      const long long dn = -(long long)cz(d) * (long long)P_ - (long long)cy(d) * nx_ - cx(d);
+      a.odd_off[d] = desc_.soa
+                         ? (-(long long)cz(d) * kQ + dslot(opp(d))) * (long long)P_ +
+                               (-(long long)cy(d) * nx_ - cx(d))
+                         : dn * kQ + dslot(opp(d));
+    }
     return a;
   }
 
   template <class K>
-  void launch(const char* name, K kern, const DirectArgs& a, cudaStream_t s) {
+  void launch(const char* name, K kern, const DirectArgs& a, cudaStream_t s,
+              int threads = 256) {
     if (a.count == 0) return;
-    const int threads = 256;
     const int tok = stats_.begin(name, s);
     kern<<<static_cast<unsigned>(ceil_div(a.count, threads)), threads, 0, s>>>(a);
     LBM_CHECK_LAUNCH();
@@ -839,16 +1015,16 @@ class DirectEngine final : public Engine {
     }
     switch (minb_) {
       case 2:
-        odd ? launch(name, k_full_aa_odd<true, false, 2>, a, stream_)
-            : launch(name, k_full_aa_even<true, false, 2>, a, stream_);
+        odd ? launch(name, k_full_aa_odd<true, false, 2>, a, stream_, aa_threads_)
+            : launch(name, k_full_aa_even<true, false, 2>, a, stream_, aa_threads_);
         break;
       case 3:
-        odd ? launch(name, k_full_aa_odd<true, false, 3>, a, stream_)
-            : launch(name, k_full_aa_even<true, false, 3>, a, stream_);
+        odd ? launch(name, k_full_aa_odd<true, false, 3>, a, stream_, aa_threads_)
+            : launch(name, k_full_aa_even<true, false, 3>, a, stream_, aa_threads_);
         break;
       case 4:
-        odd ? launch(name, k_full_aa_odd<true, false, 4>, a, stream_)
-            : launch(name, k_full_aa_even<true, false, 4>, a, stream_);
+        odd ? launch(name, k_full_aa_odd<true, false, 4>, a, stream_, aa_threads_)
+            : launch(name, k_full_aa_even<true, false, 4>, a, stream_, aa_threads_);
         break;
       default:
         odd ? launch(name, k_full_aa_odd<true, false>, a, stream_)
@@ -869,19 +1045,70 @@ class DirectEngine final : public Engine {
   template <bool SOA, int KIND>
   void launch_fused(const DirectArgs& a, double* other, long steps, const char* name,
                     long sweeps) {
-    auto kern = k_full_fused<SOA, KIND>;
+    if (flow_threads_ > 0) {
+      launch_flow<SOA, KIND>(a, other, sweeps, name);
+      return;
+    }
+    // block shape: measured on cfg 1 (B200), push (320, 2) 15.5k MFLUP/s,
+    // pull (160, 4) 18.3k, AA (160, 4) 18.0k; (256, 1) lands at 132-146
+    // registers, one block per SM, 11k
+    const int shape = fused_shape_ >= 0 ? fused_shape_ : KIND == kFusedPush ? 1 : 3;
+    switch (shape) {
+      case 1: launch_fused_as<SOA, KIND, 320, 2>(a, other, steps, name, sweeps); break;
+      case 2: launch_fused_as<SOA, KIND, 224, 3>(a, other, steps, name, sweeps); break;
+      case 3: launch_fused_as<SOA, KIND, 160, 4>(a, other, steps, name, sweeps); break;
+      case 4: launch_fused_as<SOA, KIND, 128, 5>(a, other, steps, name, sweeps); break;
+      case 5: launch_fused_as<SOA, KIND, 256, 2>(a, other, steps, name, sweeps); break;
+      default: launch_fused_as<SOA, KIND, 256, 1>(a, other, steps, name, sweeps);
+    }
+  }
+
+  template <bool SOA, int KIND, int TPB, int MINB>
+  void launch_fused_as(const DirectArgs& a, double* other, long steps, const char* name,
+                       long sweeps) {
+    auto kern = k_full_fused<SOA, KIND, TPB, MINB>;
     int per_sm = 0;
-    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
-    const uint64_t want = ceil_div(a.count, 256);
+    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, 0));
+    const uint64_t want = ceil_div(a.count, TPB);
     const int grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(per_sm, 1)) * sm_count_)));
     GridBarrier bar{barrier_.get(), barrier_.get() + 1};
     DirectArgs aa = a;
     void* params[] = {&aa, &other, &steps, &bar};
     const int tok = stats_.begin(name, stream_, sweeps);
-    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, params, 0,
+    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, TPB, params, 0,
                                          stream_));
     stats_.end(tok, stream_);
+  }
+
+  // Dataflow variant (k_full_flow): persistent co-resident blocks, plane
+  // counters instead of grid barriers.
+  template <bool SOA, int KIND>
+  void launch_flow(const DirectArgs& a, double* other, long sweeps, const char* name) {
+    auto kern = k_full_flow<SOA, KIND>;
+    const int threads = flow_threads_;
+    int per_sm = 0;
+    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+    const uint64_t tasks = uint64_t(parts_[0].nzl) * ceil_div(P_, threads);
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(tasks, uint64_t(std::max(per_sm, 1)) * sm_count_)));
+    const uint32_t nz = parts_[0].nzl;
+    if (flow_ctr_.size() < nz) {
+      flow_ctr_.alloc(nz);
+      LBM_CUDA(cudaMemsetAsync(flow_ctr_.get(), 0, nz * sizeof(unsigned), stream_));
+      flow_base_ = 0;
+    }
+    // the plane counters run on across launches (no reset memset per
+    // advance): this launch's sweep s is complete on z at flow_base_ + (s+1)*cpp
+    const int tok = stats_.begin(name, stream_, sweeps);
+    DirectArgs aa = a;
+    unsigned* planes = flow_ctr_.get();
+    unsigned base = flow_base_;
+    void* params[] = {&aa, &other, &sweeps, &planes, &base};
+    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, threads, params, 0,
+                                         stream_));
+    stats_.end(tok, stream_);
+    flow_base_ += static_cast<unsigned>(uint64_t(sweeps) * ceil_div(P_, threads));
   }
 
   bool advance_fused(const TrtArgs& t, long steps) {
@@ -1153,9 +1380,20 @@ class DirectEngine final : public Engine {
   // i.e. 16 resident warps/SM (measured best on B200: 1 -> 140 registers and
   // 8 warps runs 33% slower; 3 -> 80 registers spills and hits the power cap)
   int minb_ = 2;
+  // CTA size of the AA sweeps: 128 (4 CTAs x 4 warps per SM at 128
+  // registers) retires and refills warps in smaller groups than 2 x 8 warps;
+  // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830 (64: 6567/6695).
+  int aa_threads_ = 128;
   int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
   DevBuf<unsigned> barrier_;            // grid barrier {count, generation}
+  DevBuf<unsigned> flow_ctr_;           // k_full_flow: plane_done[nz] (monotone, wrapping)
+  unsigned flow_base_ = 0;              // plane_done value at the start of the next launch
+  // > 0: k_full_flow with this block size instead of the grid-barrier
+  // kernel (measured slower on cfg 1: 12.8k vs 14.8k MFLUP/s; opt-in)
+  int flow_threads_ = 0;
+  bool use_tmask_ = true;  // push: precomputed solid-target masks
+  int fused_shape_ = -1;  // grid-barrier kernel block shape (-1: per kind, see launch_fused)
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;

@@ -9,6 +9,7 @@ struct DirectArgs {
   const double* src;
   double* dst;
   const uint8_t* flags;  // own planes, (z*ny + y)*nx + x, 1 = solid
+  const uint32_t* tmask; // push only (may be null): bit d = target x + c_d solid
   uint32_t nx, ny, nzl;  // own extents
   uint32_t zoff;         // storage plane of own plane 0
   uint32_t zwrap;        // 1: single part, wrap z over own planes
@@ -23,6 +24,11 @@ struct DirectArgs {
   int gny, gnz, z0;      // global ny, nz and the slab's first global z
   int period, spacing;   // blocks
   long long d2;          // pipe: D^2
+  // AA odd step, interior nodes (no x/y/z wrap): element offset of
+  // direction d's gather/scatter slot, (x - c_d, opp d), from the node's own
+  // slot-0 element.  One 64-bit add per direction instead of the wrapped
+  // coordinate arithmetic; layout-specific, filled on the host.
+  long long odd_off[kQ];
 };
 
 // Solid flag of own node (x, y, own-plane z) without touching memory for the

@@ -684,6 +684,12 @@ class ListEngine final : public Engine {
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
       if (const char* e = std::getenv("LBMGPU_LIST_ODD_PIPE")) odd_pipe_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_RIA_MODE")) ria_mode_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_LIST_THREADS")) {
+        threads_ = std::atoi(e);
+        threads_env_ = true;
+      }
+      if (threads_ < 32 || threads_ > 256 || threads_ % 32)
+        throw ConfigError("LBMGPU_LIST_THREADS must be a multiple of 32 in [32, 256]");
       // adjacency L2 prefetch distance, in resident-grid waves (0 = off)
       int waves = 1;  // measured best on B200 (cfg 2 list-aa odd: 5946 -> 6530 GB/s)
       if (const char* e = std::getenv("LBMGPU_LIST_PF_WAVES")) waves = std::atoi(e);
@@ -929,7 +935,7 @@ class ListEngine final : public Engine {
 
   template <class K, class... Extra>
   void launch(const char* name, K kern, const ListArgs& a, Extra... extra) {
-    const int threads = 256;
+    const int threads = threads_;
     if (a.ne <= a.nb) return;
     const int tok = stats_.begin(name, stream_);
     kern<<<static_cast<unsigned>(ceil_div(a.ne - a.nb, threads)), threads, 0, stream_>>>(
@@ -953,12 +959,15 @@ class ListEngine final : public Engine {
             : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         if (desc_.ria && soa) {
           const int tok = stats_.begin("list_aa_odd_ria_soa", stream_);
-          const unsigned g = static_cast<unsigned>(ceil_div(a.N, 256));
+          // 128-thread CTAs: cfg 2 RIA odd 5228 -> 5431 GB/s (the indexed
+          // sweeps measured equal or better at 256)
+          const int rt = threads_env_ ? threads_ : 128;
+          const unsigned g = static_cast<unsigned>(ceil_div(a.N, rt));
           if (ria_mode_ == 1)
-            k_list_aa_odd_gpat<false><<<g, 256, 0, stream_>>>(a, ria_gpat_.get(), pf_);
+            k_list_aa_odd_gpat<false><<<g, rt, 0, stream_>>>(a, ria_gpat_.get(), pf_);
           else
-            k_list_aa_odd_ria<false><<<g, 256, 0, stream_>>>(a, ria_pat_.get(), ria_run0_.get(),
-                                                             ria_mask_.get(), pf_);
+            k_list_aa_odd_ria<false><<<g, rt, 0, stream_>>>(
+                a, ria_pat_.get(), ria_run0_.get(), ria_mask_.get(), pf_);
           LBM_CHECK_LAUNCH();
           stats_.end(tok, stream_);
         } else if (odd_pipe_) {
@@ -1183,6 +1192,8 @@ class ListEngine final : public Engine {
   DevBuf<uint32_t> ria_mask_;   // run starts within nodes 32w .. 32w+31
   DevBuf<int32_t> ria_gpat_;    // [group][18] inline pattern or kMixedGroup
   int ria_mode_ = 0;            // 0: run table, 1: group patterns (LBMGPU_RIA_MODE)
+  int threads_ = 256;           // CTA size of the sweeps
+  bool threads_env_ = false;    // threads_ set by LBMGPU_LIST_THREADS
   uint64_t pf_ = 0;             // adjacency L2 prefetch distance in nodes (AA odd)
   uint64_t pull_pf_ = 0;        // same for the one-step pull sweeps
 };

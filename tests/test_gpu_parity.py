@@ -56,16 +56,22 @@ def test_kernel_matches_golden_bitwise(idx, small_golden, small_snapshots):
     assert abs(k.total_mass() - case["mass"]) <= 1e-12 * abs(case["mass"])
 
 
-@pytest.mark.parametrize("fused", ["default", "per-sweep"])
+@pytest.mark.parametrize("fused", ["default", "per-sweep", "flow-256", "flow-64"])
 @pytest.mark.parametrize("name", NAMES)
 def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
     """Host load_state path + a second geometry, against our C restatement
     of the reference steppers (tests/support/reference.hpp:33-105).  Small
-    direct lattices normally run as one fused cooperative launch; the
+    direct lattices normally run as one fused grid-barrier launch; the
     per-sweep kernels (used for large lattices) are forced with
-    LBMGPU_FUSED_MB=0 so both code paths are checked bit for bit."""
+    LBMGPU_FUSED_MB=0 and the dataflow variant (k_full_flow) with
+    LBMGPU_FUSED_FLOW=256 / 64 (64: several chunks per plane, partial last
+    chunk), so every path is checked bit for bit."""
+    if fused != "default" and name.startswith("list-"):
+        pytest.skip("direct-addressing knob")
     if fused == "per-sweep":
         monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    elif fused.startswith("flow-"):
+        monkeypatch.setenv("LBMGPU_FUSED_FLOW", fused[5:])
     for kind, dims in [("blocks", (12, 12, 12)), ("channel", (33, 7, 9))]:
         _, _, nf = port.geometry(kind, *dims)
         init = port.perturbed(nf, 99)
@@ -83,6 +89,30 @@ def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
             expect2, _ = port.run(fam, kind, *dims, steps + 2, PARAMS.omega_plus, g=G_TEST,
                                   init=init)
             assert np.array_equal(k.snapshot(), expect2), (name, kind, steps + 2)
+
+
+@pytest.mark.parametrize("name", ["blk-push-soa", "blk-pull-soa", "aa-soa", "blk-push-aos",
+                                  "aa-aos"])
+@pytest.mark.parametrize("kind,dims", [("channel", (64, 64, 64)), ("blocks", (48, 40, 36))])
+def test_flow_launch_equals_per_sweep_at_scale(name, kind, dims, monkeypatch):
+    """The multi-sweep launches -- grid barrier (default) and dataflow (plane
+    counters, LBMGPU_FUSED_FLOW) -- at a cfg-1-sized lattice, where hundreds
+    of blocks race through 21 sweeps (odd count for push/pull), are bitwise
+    the per-sweep kernels' result."""
+    steps = 20 if name.startswith("aa") else 21
+    res = []
+    for env in ("0", "256", "128", None):
+        if env is None:
+            monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+        else:
+            monkeypatch.setenv("LBMGPU_FUSED_FLOW", env)
+        k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
+        k.load_perturbed(7)
+        k.advance(PARAMS, FORCE, steps)
+        k.advance(PARAMS, FORCE, 4)
+        res.append(k.fingerprint())
+        del k
+    assert len(set(res)) == 1, (name, kind, [f"{r:016x}" for r in res])
 
 
 def _list_kernel_for(layout, scatter):
