@@ -217,7 +217,8 @@ def main():
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
     ap.add_argument("--decompose", action="store_true",
-                    help="list-aa configs at N>1: node-range decomposition instead of replicas")
+                    help="at N>1: z-slab decomposition of direct push/pull and node-range "
+                         "decomposition of list AA instead of replicas")
     ap.add_argument("--virtual-parts", type=int, default=1,
                     help="1 GPU: emulate the multi-GPU decomposition with this many parts "
                          "(device-copy halos) -- an overhead probe, not a bench line")
@@ -261,8 +262,11 @@ def main():
     dspec = None
     # direct AA (cfg 5) is z-slab decomposed over the ranks (strong scaling);
     # every other kernel runs as independent replicas, one lattice per GPU
-    # (the list configs are replicas only) -> weak scaling
-    decomposable = aa and (desc.addr == "direct" or (args.decompose and not desc.ria))
+    # (the list configs are replicas only) -> weak scaling.
+    # --decompose also splits direct push/pull (z slabs) and list AA (node
+    # ranges) instead of replicating them.
+    decomposable = (aa and desc.addr == "direct") or (
+        args.decompose and not desc.ria and (desc.addr == "direct" or aa))
     replicas = world > 1 and not decomposable
     if world == 1 and args.virtual_parts > 1:
         dspec = {"virtual_parts": args.virtual_parts}

@@ -252,7 +252,10 @@ int lbmgpu_load_state_local(lbmgpu_ctx* ctx, const double* host,
 int lbmgpu_part_info(lbmgpu_ctx* ctx, int part, int* z0, int* z1,
                      uint64_t* n_fluid_part);
 /* Halo exchange plan as (phase, src part, dst part, src plane, dst plane,
- * group, elements) rows, 7 int64 per row; see DESIGN.md §multi-GPU. */
+ * group, elements) rows, 7 int64 per row; see DESIGN.md §multi-GPU.
+ * z_wrap: 0 = AA plan (phases 0/1), 1 = AA plan with the z ring,
+ * 2 = one-step push/pull plan (phases 2/3, always with the ring; dst plane
+ * -1 / -2 = the receiver's bottom / top staging plane). */
 int lbmgpu_halo_plan(int nz, int parts, int z_wrap, int64_t* rows, int cap,
                      int* n_rows);
 

@@ -805,7 +805,8 @@ int lbmgpu_halo_plan(int nz, int parts, int ring, int64_t* rows, int cap,
                      int* n_rows) {
   return guard([&] {
     if (nz < 1 || parts < 1 || parts > nz) throw ConfigError("halo_plan: bad nz/parts");
-    std::vector<HaloRow> plan = halo_plan(nz, parts, ring != 0);
+    if (ring < 0 || ring > 2) throw ConfigError("halo_plan: z_wrap must be 0, 1 or 2");
+    std::vector<HaloRow> plan = ring == 2 ? halo_plan_os(nz, parts) : halo_plan(nz, parts, ring != 0);
     if (n_rows) *n_rows = static_cast<int>(plan.size());
     for (int i = 0; i < cap && i < static_cast<int>(plan.size()); ++i) {
       const HaloRow& r = plan[i];

@@ -641,24 +641,48 @@ __global__ void k_part_flags(const uint8_t* __restrict__ gflags, int nx, int ny,
   }
 }
 
-// Push target mask of a whole-box part: bit d set iff the node x + c_d
-// (wrapped on every axis, as the push sweep stores) is solid.  One 4-byte
-// load per node instead of 18 neighbour flag loads.
-__global__ void k_push_tmask(const uint8_t* __restrict__ pflags, uint32_t nx, uint32_t ny,
-                             uint32_t nz, uint32_t* __restrict__ tmask) {
-  const uint64_t P = uint64_t(nx) * ny, V = P * nz;
+// Push target mask of a part's own planes: bit d set iff the node x + c_d
+// (wrapped on every axis of the whole box, as the single-part push sweep
+// stores) is solid.  One 4-byte load per node instead of 18 neighbour flag
+// loads; for a z slab it also covers the targets in the ghost planes.
+__global__ void k_push_tmask(const uint8_t* __restrict__ gflags, uint32_t nx, uint32_t ny,
+                             uint32_t nz, uint32_t z0, uint32_t nzl,
+                             uint32_t* __restrict__ tmask) {
+  const uint64_t P = uint64_t(nx) * ny, V = P * nzl;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < V;
        i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t z = static_cast<uint32_t>(i / P);
-    const uint32_t r = static_cast<uint32_t>(i - z * P);
+    const uint32_t z = static_cast<uint32_t>(i / P) + z0;
+    const uint32_t r = static_cast<uint32_t>(i % P);
     const uint32_t y = r / nx, x = r - y * nx;
     uint32_t m = 0;
     for (int d = 1; d < kQ; ++d) {
       const uint32_t tx = (x + nx + cx(d)) % nx, ty = (y + ny + cy(d)) % ny,
                      tz = (z + nz + cz(d)) % nz;
-      if (pflags[(uint64_t(tz) * ny + ty) * nx + tx]) m |= 1u << d;
+      if (gflags[(uint64_t(tx) * ny + ty) * nz + tz]) m |= 1u << d;  // x-major
     }
     tmask[i] = m;
+  }
+}
+
+// Push halo merge (halo.hpp phase 3) into a boundary plane of the
+// destination grid: the staged ghost plane of the neighbour holds, per node
+// and crossing direction d, slot d (node fluid) or the bounce-back slot
+// opp(d) (node solid); exactly that slot is copied.  `up` = the data came
+// from below (crossing slots are the c_z = +1 ones).
+__global__ void k_push_halo_merge(DirectArgs a, const double* __restrict__ stage,
+                                  uint32_t zown, bool up) {
+  const uint32_t P = a.P;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    const uint32_t y = i / a.nx, x = i - y * a.nx;
+    const bool solid = solid_node(a, x, y, zown, zown * P + i);
+    double* plane = a.dst + uint64_t(zown + a.zoff) * kQ * P + i;
+    const int s0 = up ? kUpSlot0 : kDownSlot0;
+#pragma unroll
+    for (int k = 0; k < kHaloSlots; ++k) {
+      const int sc = s0 + k;
+      const int s = solid ? dslot(opp(ddir(sc))) : sc;
+      plane[uint64_t(s) * P] = stage[uint64_t(s) * P + i];
+    }
   }
 }
 
@@ -709,19 +733,28 @@ struct Part {
   DevBuf<double> buf[2];
   DevBuf<uint8_t> flags;
   DevBuf<uint32_t> tmask;   // push: solid-target bits per node (k_push_tmask)
+  DevBuf<double> stage;     // push, several parts: bottom / top staging planes (2 x 19 x P)
   DevBuf<uint32_t> node_of;
   DevBuf<uint64_t> canon;   // empty when the part holds the whole box
   uint64_t n_fluid = 0;
   std::vector<uint64_t> canon_host;  // canonical index of each k (sorted)
 };
 
+// Address of a plan row's plane: storage plane >= 0 of grid `buf`, or one of
+// the part's two staging planes (halo.hpp kStageBottom / kStageTop).
+inline double* plane_ptr(const Part& pt, int buf, int plane, int slot0, uint64_t P) {
+  if (plane >= 0) return pt.buf[buf].get() + (uint64_t(plane) * kQ + slot0) * P;
+  return pt.stage.get() + (uint64_t(-plane - 1) * kQ + slot0) * P;
+}
+
 // Halo transport between slabs.  exchange() enqueues one phase of the plan
-// after the work already on `s`; wait() makes `s` wait for its completion.
+// on grid `buf` after the work already on `s`; wait() makes `s` wait for its
+// completion.
 class Transport {
  public:
   virtual ~Transport() = default;
   virtual void exchange(int phase, std::vector<Part>& parts, uint64_t P,
-                        cudaStream_t s) = 0;
+                        cudaStream_t s, int buf = 0) = 0;
   virtual void wait(int phase, cudaStream_t s) { (void)phase; (void)s; }
   virtual double sum(double v) { return v; }
 };
@@ -732,13 +765,11 @@ class LocalTransport final : public Transport {
  public:
   explicit LocalTransport(std::vector<HaloRow> plan) : plan_(std::move(plan)) {}
   void exchange(int phase, std::vector<Part>& parts, uint64_t P,
-                cudaStream_t s) override {
+                cudaStream_t s, int buf) override {
     for (const HaloRow& r : plan_) {
       if (r.phase != phase) continue;
-      const Part& a = parts[r.src_part];
-      const Part& b = parts[r.dst_part];
-      const double* src = a.buf[0].get() + (uint64_t(r.src_plane) * kQ + r.slot0) * P;
-      double* dst = b.buf[0].get() + (uint64_t(r.dst_plane) * kQ + r.slot0) * P;
+      const double* src = plane_ptr(parts[r.src_part], buf, r.src_plane, r.slot0, P);
+      double* dst = plane_ptr(parts[r.dst_part], buf, r.dst_plane, r.slot0, P);
       LBM_CUDA(cudaMemcpyAsync(dst, src, uint64_t(kHaloSlots) * P * sizeof(double),
                                cudaMemcpyDeviceToDevice, s));
     }
@@ -759,19 +790,24 @@ class NcclTransport final : public Transport {
  public:
   NcclTransport(std::vector<HaloRow> plan, int rank, int nranks, int nparts,
                 const uint8_t* id128)
-      : t_(nccl_create(std::move(plan), rank, nranks, id128)), bases_(nparts, nullptr) {}
+      : t_(nccl_create(std::move(plan), rank, nranks, id128)),
+        bases_(nparts, nullptr),
+        stages_(nparts, nullptr) {}
   ~NcclTransport() override { nccl_destroy(t_); }
   void exchange(int phase, std::vector<Part>& parts, uint64_t P,
-                cudaStream_t s) override {
-    for (Part& pt : parts) bases_[pt.index] = pt.buf[0].get();
-    nccl_exchange(t_, phase, bases_, P, s);
+                cudaStream_t s, int buf) override {
+    for (Part& pt : parts) {
+      bases_[pt.index] = pt.buf[buf].get();
+      stages_[pt.index] = pt.stage.get();
+    }
+    nccl_exchange(t_, phase, bases_, stages_, P, s);
   }
   void wait(int phase, cudaStream_t s) override { nccl_wait(t_, phase, s); }
   double sum(double v) override { return nccl_sum(t_, v); }
 
  private:
   NcclTransportImpl* t_;
-  std::vector<double*> bases_;
+  std::vector<double*> bases_, stages_;
 };
 
 class DirectEngine final : public Engine {
@@ -782,9 +818,6 @@ class DirectEngine final : public Engine {
     rank_ = dist.rank;
     nranks_ = dist.nranks;
     nparts_ = nranks_ > 1 ? nranks_ : std::max(1, dist.virtual_parts);
-    if (nparts_ > 1 && d.prop != Prop::Aa)
-      throw ConfigError("z-slab decomposition is implemented for the AA "
-                        "pattern only (kernel '" + d.name + "')");
     if (nparts_ > 1 && !d.soa)
       throw ConfigError("z-slab decomposition needs the SoA layout");
     if (nparts_ > g.nz) throw ConfigError("more z-slab parts than z planes");
@@ -864,12 +897,15 @@ class DirectEngine final : public Engine {
       k_part_flags<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
           geo.flags.get(), nx_, ny_, nz_, pt.z0, pt.z1, pt.flags.get());
       LBM_CHECK_LAUNCH();
-      if (d.prop == Prop::OsPush && nparts_ == 1 && use_tmask_) {
+      // push: solid-target masks (required with several parts: the
+      // targets in the ghost planes have no flags of their own here)
+      if (d.prop == Prop::OsPush && (nparts_ > 1 || use_tmask_)) {
         pt.tmask.alloc(uint64_t(pt.nzl) * P_);
         k_push_tmask<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
-            pt.flags.get(), nx_, ny_, pt.nzl, pt.tmask.get());
+            geo.flags.get(), nx_, ny_, nz_, pt.z0, pt.nzl, pt.tmask.get());
         LBM_CHECK_LAUNCH();
       }
+      if (d.prop == Prop::OsPush && nparts_ > 1) pt.stage.alloc(2 * kQ * P_);
       // the slab's fluid nodes in canonical order
       DevBuf<uint8_t> mask(V);
       DevBuf<uint32_t> prank(V);
@@ -902,7 +938,9 @@ class DirectEngine final : public Engine {
       bool end_fluid = false;
       for (uint64_t i = 0; i < V && !end_fluid; i += nz_)
         end_fluid = hf[i] == 0 || hf[i + nz_ - 1] == 0;
-      std::vector<HaloRow> plan = halo_plan(nz_, nparts_, end_fluid);
+      // one-step kernels stream solid nodes too: always the full ring
+      std::vector<HaloRow> plan = d.prop == Prop::Aa ? halo_plan(nz_, nparts_, end_fluid)
+                                                     : halo_plan_os(nz_, nparts_);
       // NCCL between processes; with one process the copies are local, and
       // an NCCL id selects NCCL self send/recv instead (tests the NCCL path on
       // one GPU).
@@ -1138,6 +1176,10 @@ class DirectEngine final : public Engine {
     const bool soa = desc_.soa;
     const bool cs = cs_;
     if (advance_fused(t, steps)) return;
+    if (desc_.prop != Prop::Aa && nparts_ > 1) {
+      os_sweeps_slabs(t, steps);
+      return;
+    }
     if (desc_.prop == Prop::OsPush) {
       const Part& pt = parts_[0];
       const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
@@ -1197,6 +1239,73 @@ class DirectEngine final : public Engine {
       } else {
         aa_pair_slabs(t);
       }
+    }
+  }
+
+  // One-step sweeps over z-slabs (halo.hpp phases 2 / 3), per lattice step:
+  //   pull: [exchange 2 (source ghost planes) || pull(interior)] -> pull(boundary)
+  //   push: push(boundary) -> [exchange 3 (ghosts -> staging) || push(interior)]
+  //         -> merge the staging planes into the boundary planes
+  // Interior sweeps never touch a ghost plane (pull reads, push writes own
+  // planes only), and the merge writes exactly the boundary-plane slots only
+  // the neighbour pushes into, so nothing races.  The pull's collide pass
+  // (kernels_full_os.cpp:173-190) is local to each slab.
+  void os_sweeps_slabs(const TrtArgs& t, long steps) {
+    const uint32_t P = static_cast<uint32_t>(P_);
+    auto each = [&](bool boundary, auto&& fn) {
+      for (Part& pt : parts_) {
+        const uint32_t last = (pt.nzl - 1) * P;
+        if (boundary) {
+          fn(pt, 0u, P);
+          if (pt.nzl > 1) fn(pt, last, P);
+        } else if (pt.nzl > 2) {
+          fn(pt, P, last - P);
+        }
+      }
+    };
+    const bool push = desc_.prop == Prop::OsPush;
+    if (!push)
+      for (Part& pt : parts_)
+        launch("full_collide_soa", k_full_collide<true>,
+               args(pt, 0, pt.nzl * P, t, cur_, cur_), stream_);
+    for (long s = 0; s < steps; ++s) {
+      const int src = cur_, dst = 1 - cur_;
+      if (push) {
+        auto sweep = [&](const char* name) {
+          return [&, name](Part& pt, uint32_t n0, uint32_t cnt) {
+            launch(name, k_full_push<true, false>, args(pt, n0, cnt, t, src, dst), stream_);
+          };
+        };
+        each(true, sweep("full_push_soa_halo"));
+        tr_->exchange(3, parts_, P_, stream_, dst);
+        each(false, sweep("full_push_soa"));
+        tr_->wait(3, stream_);
+        const int g = grid_for(P_, 256);
+        for (Part& pt : parts_) {
+          const DirectArgs a = args(pt, 0, 0, t, src, dst);
+          for (int face = 0; face < 2; ++face) {
+            const int tok = stats_.begin("push_halo_merge", stream_);
+            k_push_halo_merge<<<g, 256, 0, stream_>>>(
+                a, pt.stage.get() + uint64_t(face) * kQ * P_, face ? pt.nzl - 1 : 0, face == 0);
+            LBM_CHECK_LAUNCH();
+            stats_.end(tok, stream_);
+          }
+        }
+      } else {
+        const bool collide = s + 1 < steps;
+        auto sweep = [&](const char* name) {
+          return [&, name](Part& pt, uint32_t n0, uint32_t cnt) {
+            const DirectArgs a = args(pt, n0, cnt, t, src, dst);
+            collide ? launch(name, k_full_pull<true, true, false>, a, stream_)
+                    : launch(name, k_full_pull<true, false, false>, a, stream_);
+          };
+        };
+        tr_->exchange(2, parts_, P_, stream_, src);
+        each(false, sweep(collide ? "full_pull_soa" : "full_pull_stream_soa"));
+        tr_->wait(2, stream_);
+        each(true, sweep(collide ? "full_pull_soa_halo" : "full_pull_stream_soa_halo"));
+      }
+      cur_ ^= 1;
     }
   }
 

@@ -83,7 +83,7 @@ class NcclTransportImpl {
     std::memcpy(&id, id128, sizeof(id));
     nccl_check(api.CommInitRank(&comm_, nranks, id, rank), "ncclCommInitRank");
     LBM_CUDA(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kPhases; ++i) {
       LBM_CUDA(cudaEventCreateWithFlags(&ready_[i], cudaEventDisableTiming));
       LBM_CUDA(cudaEventCreateWithFlags(&done_[i], cudaEventDisableTiming));
     }
@@ -92,7 +92,7 @@ class NcclTransportImpl {
   ~NcclTransportImpl() {
     if (comm_) NcclApi::get().CommDestroy(comm_);
     if (comm_stream_) cudaStreamDestroy(comm_stream_);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kPhases; ++i) {
       if (ready_[i]) cudaEventDestroy(ready_[i]);
       if (done_[i]) cudaEventDestroy(done_[i]);
     }
@@ -103,23 +103,27 @@ class NcclTransportImpl {
   // in this process, else nullptr.  Slab p belongs to rank p, or to rank 0
   // when the communicator has a single rank (self send/recv: the NCCL code
   // path exercised on one GPU by the tests).
-  void exchange(int phase, const std::vector<double*>& bases, uint64_t P,
-                cudaStream_t s) {
+  void exchange(int phase, const std::vector<double*>& bases,
+                const std::vector<double*>& stages, uint64_t P, cudaStream_t s) {
     const NcclApi& api = NcclApi::get();
     LBM_CUDA(cudaEventRecord(ready_[phase], s));
     LBM_CUDA(cudaStreamWaitEvent(comm_stream_, ready_[phase], 0));
     const size_t count = size_t(kHaloSlots) * P;
     auto peer = [&](int part) { return nranks_ == 1 ? 0 : part; };
+    // storage plane >= 0 of the grid, or one of the two staging planes
+    auto at = [&](int part, int plane, int slot0) -> double* {
+      if (plane >= 0)
+        return bases[part] ? bases[part] + (uint64_t(plane) * kQ + slot0) * P : nullptr;
+      return stages[part] ? stages[part] + (uint64_t(-plane - 1) * kQ + slot0) * P : nullptr;
+    };
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (const HaloRow& r : plan_) {
       if (r.phase != phase) continue;
-      if (double* b = bases[r.src_part])
-        nccl_check(api.Send(b + (uint64_t(r.src_plane) * kQ + r.slot0) * P, count,
-                            ncclFloat64, peer(r.dst_part), comm_, comm_stream_),
+      if (double* b = at(r.src_part, r.src_plane, r.slot0))
+        nccl_check(api.Send(b, count, ncclFloat64, peer(r.dst_part), comm_, comm_stream_),
                    "ncclSend");
-      if (double* b = bases[r.dst_part])
-        nccl_check(api.Recv(b + (uint64_t(r.dst_plane) * kQ + r.slot0) * P, count,
-                            ncclFloat64, peer(r.src_part), comm_, comm_stream_),
+      if (double* b = at(r.dst_part, r.dst_plane, r.slot0))
+        nccl_check(api.Recv(b, count, ncclFloat64, peer(r.src_part), comm_, comm_stream_),
                    "ncclRecv");
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
@@ -172,7 +176,8 @@ class NcclTransportImpl {
   int rank_, nranks_;
   ncclComm_t comm_ = nullptr;
   cudaStream_t comm_stream_ = nullptr;
-  cudaEvent_t ready_[2] = {nullptr, nullptr}, done_[2] = {nullptr, nullptr};
+  static constexpr int kPhases = 4;  // halo.hpp phases 0-3
+  cudaEvent_t ready_[kPhases] = {}, done_[kPhases] = {};
   double* dsum_ = nullptr;
 };
 
@@ -181,8 +186,9 @@ NcclTransportImpl* nccl_create(std::vector<HaloRow> plan, int rank, int nranks,
   return new NcclTransportImpl(std::move(plan), rank, nranks, id128);
 }
 void nccl_exchange(NcclTransportImpl* t, int phase, const std::vector<double*>& bases,
+                   const std::vector<double*>& stages,
                    uint64_t P, cudaStream_t s) {
-  t->exchange(phase, bases, P, s);
+  t->exchange(phase, bases, stages, P, s);
 }
 void nccl_wait(NcclTransportImpl* t, int phase, cudaStream_t s) { t->wait(phase, s); }
 void nccl_begin(NcclTransportImpl* t, int phase, cudaStream_t s) { t->begin(phase, s); }

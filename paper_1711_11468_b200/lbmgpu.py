@@ -652,11 +652,15 @@ def verify_kernel(k, c: PoiseuilleCase = None, check_interval: int = 200, rel_to
 
 
 # ------------------------------------------------------------------ misc
-def halo_plan(nz: int, parts: int, ring: bool):
+def halo_plan(nz: int, parts: int, ring: bool, one_step: bool = False):
+    """z-slab halo rows (phase, src, dst, src plane, dst plane, slot0, slots):
+    the AA plan (phases 0/1, z ring optional) or, one_step=True, the
+    push/pull plan (phases 2/3, always with the ring)."""
     cap = 8 * parts + 8
     rows = np.zeros(7 * cap, np.int64)
     n = C.c_int()
-    _check(lib.lbmgpu_halo_plan(nz, parts, int(ring), rows.ctypes.data, cap, C.byref(n)))
+    _check(lib.lbmgpu_halo_plan(nz, parts, 2 if one_step else int(ring), rows.ctypes.data, cap,
+                                C.byref(n)))
     return rows[:7 * n.value].reshape(-1, 7)
 
 

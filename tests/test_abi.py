@@ -127,6 +127,37 @@ def test_halo_plan_invariants():
                 assert (ph == 0 and dp == 0) or (ph == 1 and sp == 0)
 
 
+def test_one_step_halo_plan_invariants():
+    """Push/pull z-slab plan (halo.hpp phases 2/3): every boundary incl. the
+    z ring; pull copies own boundary planes into the neighbour's ghost
+    planes (the slots its boundary nodes gather across the face), push
+    ships both 5-slot groups of a ghost plane into the neighbour's staging
+    plane (-1 bottom / -2 top)."""
+    for nz, parts in [(24, 2), (17, 5), (13, 13), (64, 8)]:
+        rows = L.halo_plan(nz, parts, True, one_step=True)
+        assert rows.shape == (6 * parts, 7)
+        nzl = [nz * (p + 1) // parts - nz * p // parts for p in range(parts)]
+        pull = rows[rows[:, 0] == 2]
+        push = rows[rows[:, 0] == 3]
+        assert len(pull) == 2 * parts and len(push) == 4 * parts
+        for _, src, dst, sp, dp, slot0, n in pull:
+            assert n == 5 and src != dst or parts == 1
+            if dp == 0:  # below -> my bottom ghost: the c_z=+1 slots of its top plane
+                assert slot0 == 14 and sp == nzl[src] and (dst - src) % parts == 1
+            else:        # above -> my top ghost: the c_z=-1 slots of its plane 1
+                assert dp == nzl[dst] + 1 and slot0 == 0 and sp == 1 and (src - dst) % parts == 1
+        recv = {}
+        for _, src, dst, sp, dp, slot0, n in push:
+            assert dp in (-1, -2) and slot0 in (0, 14)
+            if dp == -1:
+                assert sp == nzl[src] + 1 and (dst - src) % parts == 1
+            else:
+                assert sp == 0 and (src - dst) % parts == 1
+            recv.setdefault((int(dst), int(dp)), set()).add(int(slot0))
+        # each part's two staging planes receive both slot groups once
+        assert recv == {(p, f): {0, 14} for p in range(parts) for f in (-1, -2)}
+
+
 def test_compute_without_gpu_fails_loudly():
     """No CPU fallback: on a machine without a CUDA device every compute entry
     point raises DeviceError."""

@@ -259,43 +259,50 @@ def test_capabilities():
     assert lbm.make_kernel(lbm.make_descriptor("blk-push-soa"), spec).capabilities().nt_streams_effective == 0
 
 
+@pytest.mark.parametrize("name", ["aa-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims,parts", [
     ("channel", (16, 12, 24), 2), ("channel", (16, 12, 24), 3), ("channel", (16, 12, 24), 4),
     ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2), ("blocks", (12, 10, 16), 4),
-    ("slit", (6, 5, 9), 3)])
-def test_zslab_parts_bitwise_equal_single(kind, dims, parts):
+    ("slit", (6, 5, 9), 3), ("pipe", (9, 12, 13), 13)])
+def test_zslab_parts_bitwise_equal_single(name, kind, dims, parts):
     """z-slab decomposition (the multi-GPU plan, emulated on one device):
     fingerprint identical for 1..N parts -- the worker-count invariance of
-    tests/test_kernels.cpp:177-195 carried to the slab split."""
+    tests/test_kernels.cpp:177-195 carried to the slab split.  AA: halo
+    phases 0/1; one-step push / pull: phases 2/3 with the z ring (solid
+    nodes stream too), down to one plane per slab; odd step counts leave
+    push/pull on the second grid."""
     spec = lbm.GeometrySpec(kind, *dims)
-    ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    steps = (4, 6) if name.startswith("aa") else (3, 6)
+    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
     ref.load_perturbed(4242)
-    ref.advance(PARAMS, FORCE, 10)
-    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec, dist={"virtual_parts": parts})
+    ref.advance(PARAMS, FORCE, sum(steps))
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec, dist={"virtual_parts": parts})
     k.load_perturbed(4242)
     init = k.snapshot()
     assert np.array_equal(init, lbm.perturbed_equilibrium(k.n_fluid(), 4242))
-    k.advance(PARAMS, FORCE, 4)
-    k.advance(PARAMS, FORCE, 6)
-    assert np.array_equal(k.snapshot(), ref.snapshot())
+    for st in steps:
+        k.advance(PARAMS, FORCE, st)
+    assert np.array_equal(k.snapshot(), ref.snapshot()), name
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
+@pytest.mark.parametrize("name", ["aa-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims,parts", [("channel", (32, 12, 24), 3), ("blocks", (16, 16, 16), 2)])
-def test_zslab_nccl_transport_single_gpu(kind, dims, parts):
+def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     """The NCCL halo transport (grouped ncclSend/ncclRecv on a comm stream,
     event-ordered against the compute stream) exercised on one GPU: one NCCL
     rank owning all slabs, self send/recv per plan row.  Bitwise equal to the
     single-slab run."""
     spec = lbm.GeometrySpec(kind, *dims)
-    ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
     ref.load_perturbed(31)
     ref.advance(PARAMS, FORCE, 8)
-    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec,
                         dist={"virtual_parts": parts, "nccl_id": lbm.lbmgpu.nccl_unique_id()})
     k.load_perturbed(31)
     k.advance(PARAMS, FORCE, 8)
     assert np.array_equal(k.snapshot(), ref.snapshot())
+    assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
 @pytest.mark.parametrize("name", ["list-aa-soa", "list-aa-aos"])

@@ -143,3 +143,161 @@ def test_two_rank_zslab_protocol_gloo(kind, dims):
     assert all(p.exitcode == 0 for p in procs)
     equal, rel = q.get(timeout=5)
     assert equal, rel
+
+
+def _rank_main_one_step(rank, world, port_no, kind, dims, steps, push, q):
+    """blk-push / blk-pull over z slabs with the one-step plan (halo.hpp
+    phases 2/3): pull fills the source ghost planes before every sweep; push
+    ships its ghost planes into the neighbour's staging planes after every
+    sweep and the receiver merges them by its own node flags.  Every node
+    streams (solid ones too), so the plan always carries the z ring."""
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        from paper_1711_11468_b200 import lbmgpu as L
+        port = Port()
+        nx, ny, nz = dims
+        flags, per, nf = port.geometry(kind, nx, ny, nz)
+        solid = flags.reshape(nx, ny, nz).astype(bool)
+        z0, z1 = nz * rank // world, nz * (rank + 1) // world
+        nzl = z1 - z0
+        plan = L.halo_plan(nz, world, True, one_step=True)
+        wp = 1.0 / TAU
+        wm = port.omega_minus(wp)
+        w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+        bufs = [np.empty((nzl + 2, Q, ny, nx)) for _ in range(2)]
+        stage = np.zeros((2, Q, ny, nx))
+        for d in range(Q):
+            bufs[0][:, SLOT[d]] = w[d]
+            bufs[1][:, SLOT[d]] = w[d]
+        init = port.perturbed(nf, 78)
+        k = 0
+        for x in range(nx):
+            for y in range(ny):
+                for z in range(nz):
+                    if solid[x, y, z]:
+                        continue
+                    if z0 <= z < z1:
+                        for d in range(Q):
+                            bufs[0][z - z0 + 1, SLOT[d], y, x] = init[k * Q + d]
+                    k += 1
+        nodes = [(x, y, z) for z in range(nzl) for y in range(ny) for x in range(nx)]
+
+        def exchange(phase, buf):
+            reqs = []
+            for i, (ph, src, dst, sp, dp, s0, ns) in enumerate(plan):
+                if ph != phase:
+                    continue
+                if src == rank:
+                    t = torch.from_numpy(np.ascontiguousarray(buf[sp, s0:s0 + ns]))
+                    reqs.append(("s", dist.isend(t, int(dst), tag=i), None, None))
+                if dst == rank:
+                    t = torch.empty((ns, ny, nx), dtype=torch.float64)
+                    reqs.append(("r", dist.irecv(t, int(src), tag=i), t, (dp, s0, ns)))
+            for kind_, r, t, where in reqs:
+                r.wait()
+                if kind_ == "r":
+                    dp, s0, ns = where
+                    target = buf[dp] if dp >= 0 else stage[-dp - 1]
+                    target[s0:s0 + ns] = t.numpy()
+
+        def merge(buf):
+            # staging plane 0 (from below, c_z=+1 crossings) -> own plane 0,
+            # staging plane 1 (from above, c_z=-1 crossings) -> own plane nzl-1
+            for face, zo in ((0, 0), (1, nzl - 1)):
+                for y in range(ny):
+                    for x in range(nx):
+                        sol = solid[x, y, zo + z0]
+                        for d in range(1, Q):
+                            if CZ[d] != (1 if face == 0 else -1):
+                                continue
+                            s = SLOT[OPP[d]] if sol else SLOT[d]
+                            buf[zo + 1, s, y, x] = stage[face, s, y, x]
+
+        cur = 0
+        if not push:  # collide pass (kernels_full_os.cpp:173-190)
+            for (x, y, z) in nodes:
+                if not solid[x, y, z + z0]:
+                    f = np.array([bufs[0][z + 1, SLOT[d], y, x] for d in range(Q)])
+                    f = port.collide(f, wp, wm, G)
+                    for d in range(Q):
+                        bufs[0][z + 1, SLOT[d], y, x] = f[d]
+        for s in range(steps):
+            src, dst = bufs[cur], bufs[1 - cur]
+            if push:
+                for (x, y, z) in nodes:
+                    zs = z + 1
+                    f = np.array([src[zs, SLOT[d], y, x] for d in range(Q)])
+                    if not solid[x, y, z + z0]:
+                        f = port.collide(f, wp, wm, G)
+                    dst[zs, SLOT[0], y, x] = f[0]
+                    for d in range(1, Q):
+                        tx, ty = (x + CX[d]) % nx, (y + CY[d]) % ny
+                        tzg = (z + z0 + CZ[d]) % nz
+                        sl = SLOT[OPP[d]] if solid[tx, ty, tzg] else SLOT[d]
+                        dst[zs + CZ[d], sl, ty, tx] = f[d]
+                exchange(3, dst)
+                merge(dst)
+            else:
+                exchange(2, src)
+                for (x, y, z) in nodes:
+                    zs = z + 1
+                    f = np.empty(Q)
+                    f[0] = src[zs, SLOT[0], y, x]
+                    for d in range(1, Q):
+                        f[d] = src[zs - CZ[d], SLOT[d], (y - CY[d]) % ny, (x - CX[d]) % nx]
+                    sol = solid[x, y, z + z0]
+                    if s + 1 < steps and not sol:
+                        f = port.collide(f, wp, wm, G)
+                    dst[zs, SLOT[0], y, x] = f[0]
+                    for d in range(1, Q):
+                        dst[zs, SLOT[OPP[d]] if sol else SLOT[d], y, x] = f[d]
+            cur ^= 1
+        buf = bufs[cur]
+        rows = {}
+        k = 0
+        for x in range(nx):
+            for y in range(ny):
+                for z in range(nz):
+                    if solid[x, y, z]:
+                        continue
+                    if z0 <= z < z1:
+                        rows[k] = [buf[z - z0 + 1, SLOT[d], y, x] for d in range(Q)]
+                    k += 1
+        mass = float(sum(buf[zs, s].sum() for zs in range(1, nzl + 1) for s in range(Q)))
+        out = [None] * world
+        dist.all_gather_object(out, (rows, mass))
+        if rank == 0:
+            full = np.zeros(nf * Q)
+            for part, _ in out:
+                for kk, v in part.items():
+                    full[kk * Q:(kk + 1) * Q] = v
+            expect, emass = port.run("full", kind, nx, ny, nz, steps, wp, g=G, init=init)
+            q.put((bool(np.array_equal(full, expect)), float(port.max_rel_diff(full, expect)),
+                   sum(m for _, m in out), emass))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("push", [True, False])
+@pytest.mark.parametrize("kind,dims", [("channel", (6, 5, 8)), ("blocks", (8, 8, 8))])
+def test_two_rank_one_step_protocol_gloo(kind, dims, push):
+    """The push / pull halo protocol on 2 gloo ranks, bitwise equal to the
+    full-domain textbook full-way stepper (odd step count: result on the
+    second grid)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_rank_main_one_step,
+                         args=(r, 2, port_no, kind, dims, 3, push, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    equal, rel, mass, emass = q.get(timeout=5)
+    assert equal, rel
+    assert abs(mass - emass) <= 1e-12 * abs(emass)

@@ -22,7 +22,7 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
-@pytest.mark.parametrize("name", ["aa-soa", "list-aa-soa"])
+@pytest.mark.parametrize("name", ["aa-soa", "blk-push-soa", "blk-pull-soa", "list-aa-soa"])
 @pytest.mark.parametrize("kind,dims", [("channel", (64, 32, 48)), ("blocks", (32, 32, 32))])
 def test_nccl_decomposition_bitwise(n, kind, dims, name):
     if _ngpus() < n:
