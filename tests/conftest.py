@@ -32,3 +32,9 @@ def small_golden():
 def small_snapshots():
     import numpy as np
     return dict(np.load(os.path.join(GOLDEN, "small_snapshots.npz")))
+
+
+@pytest.fixture(scope="session")
+def edge_golden():
+    import json
+    return json.load(open(os.path.join(GOLDEN, "edge.json")))

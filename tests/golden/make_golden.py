@@ -6,6 +6,7 @@ build_structure, padding_offsets.  Run in this container (the GPU box has no
 /root/reference):
 
     python tests/golden/make_golden.py small      # seconds
+    python tests/golden/make_golden.py edge       # seconds
     python tests/golden/make_golden.py configs    # BASELINE configs 1-4, ~25 min
 """
 import json
@@ -142,10 +143,43 @@ def configs(ref: Ref, which):
               f"({time.time() - t0:.0f} s)", flush=True)
 
 
+def edge(ref: Ref):
+    """Degenerate and ragged shapes (the wrap onto itself of a 1- or 2-cell
+    periodic axis, one fluid node, box sizes that are not a multiple of the
+    blocks period, a pipe one cell long) for every kernel, and blk tilings
+    that do not divide the box: fingerprint + mass after 6 steps."""
+    out = {"cases": []}
+    cases = [("channel", (1, 3, 3), {}), ("channel", (2, 3, 4), {}), ("slit", (1, 1, 3), {}),
+             ("slit", (3, 2, 5), {}), ("pipe", (1, 4, 4), {}), ("pipe", (2, 7, 5), {}),
+             ("blocks", (9, 8, 8), dict(block=4, spacing=4)),
+             ("blocks", (11, 7, 13), dict(block=3, spacing=2)),
+             ("blocks", (5, 5, 5), dict(block=5, spacing=0))]
+    for kind, dims, kw in cases:
+        for name in ref.kernel_names():
+            for blk in ((0, 2, 3) if name.startswith("list-") else (0,)):
+                try:
+                    k = ref.kernel(name, kind, *dims, threads=2, blk=blk, **kw)
+                except Exception as e:  # e.g. no fluid node: ConfigError
+                    out["cases"].append({"kernel": name, "kind": kind, "dims": dims, **kw,
+                                         "blk": blk, "config_error": str(e)})
+                    continue
+                init = ref.perturbed(k.n_fluid, 99)
+                k.load_state(init)
+                k.advance(1.0 / TAU, 3.0 / 16.0, G_TEST, 6)
+                out["cases"].append({"kernel": name, "kind": kind, "dims": dims, **kw, "blk": blk,
+                                     "seed": 99, "steps": 6, "n_fluid": k.n_fluid,
+                                     "fingerprint": f"{k.fingerprint():016x}",
+                                     "mass": k.total_mass()})
+    json.dump(out, open(os.path.join(HERE, "edge.json"), "w"), indent=1)
+    print(len(out["cases"]), "edge cases")
+
+
 if __name__ == "__main__":
     ref = Ref()
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":
         small(ref)
+    elif what == "edge":
+        edge(ref)
     else:
         configs(ref, [int(a) for a in sys.argv[2:]])
