@@ -247,6 +247,73 @@ __global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
   aa_odd_node<SOA, CS, false>(a, c, n);
 }
 
+// Odd step with the x-shifted scatters realigned through shared memory.
+// In k_full_aa_odd every warp stores the 10 directions with c_x != 0 one
+// element off its own x range, so each such store instruction writes two
+// partial 32-byte sectors (one shared with the neighbouring warp).  Here a
+// 128-thread block covers 128 consecutive x of one row (nx % 128 == 0): the
+// producer of the value that lands on x_u parks it in shared memory, and
+// thread u stores it aligned; only the two elements that leave the block's x
+// range are stored by their producers directly.  Loads, collision and the
+// order of values are unchanged, so results are bitwise those of
+// k_full_aa_odd.
+constexpr int kSxThreads = 128;
+template <int MINB>
+__global__ void __launch_bounds__(kSxThreads, MINB) k_full_aa_odd_sx(const DirectArgs a) {
+  constexpr int kX = 10;  // directions with c_x != 0
+  __shared__ double sh[kX][kSxThreads];
+  __shared__ uint8_t fl[kSxThreads];
+  const int u = threadIdx.x;
+  const uint32_t n = a.node0 + blockIdx.x * kSxThreads + u;
+  Coords c;
+  decode_node(a, n, c);
+  const bool fluid = !solid_node(a, c.x, c.y, c.z, n);
+  fl[u] = fluid;
+  const Idx<true> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  if (fluid) {
+    // gather/scatter address of direction d: own slot-0 element + constant
+    // for interior warps (see aa_odd_node), the wrapped form otherwise
+    const bool inner = c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u &&
+                       (!a.zwrap || c.z - 1u < a.nzl - 2u);
+    const bool fast = __all_sync(__activemask(), inner);
+    double* own = buf + I(c.Z[1], 0, c.y, c.x);
+    auto addr = [&](int d) -> double* {
+      if (fast) return own + a.odd_off[d];
+      return d == 0 ? buf + I(c.Z[1], dslot(0), c.y, c.x)
+                    : buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+    };
+    double q[kQ];
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) q[d] = *addr(d);
+    collide(q, a.trt);
+    int k = 0;
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) {
+      if (cx(d) == 0) {
+        *addr(d) = q[opp(d)];
+      } else {
+        const int dst = u - cx(d);  // the thread whose x the value lands on
+        if (dst >= 0 && dst < kSxThreads)
+          sh[k][dst] = q[opp(d)];
+        else
+          *addr(d) = q[opp(d)];
+        ++k;
+      }
+    }
+  }
+  __syncthreads();
+  int k = 0;
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    if (cx(d) == 0) continue;
+    const int src = u + cx(d);
+    if (src >= 0 && src < kSxThreads && fl[src])
+      buf[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.x)] = sh[k][u];
+    ++k;
+  }
+}
+
 // ---- fused multi-step sweeps for small lattices ----------------------------
 // For lattices that live in L2 (cfg 1: 2 x 40 MB) a sweep takes ~15 us and
 // the per-launch fill/drain and launch gaps cost as much as the work.  One
@@ -832,6 +899,7 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_CS")) cs_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AA_THREADS")) aa_threads_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_AA_ODD_SX")) odd_sx_ = std::atoi(e);
       if (aa_threads_ < 32 || aa_threads_ > 256 || aa_threads_ % 32)
         throw ConfigError("LBMGPU_AA_THREADS must be a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
@@ -1049,6 +1117,12 @@ class DirectEngine final : public Engine {
     if (cs_) {
       odd ? launch(name, k_full_aa_odd<true, true>, a, stream_)
           : launch(name, k_full_aa_even<true, true>, a, stream_);
+      return;
+    }
+    if (odd && odd_sx_ && a.nx % kSxThreads == 0 && a.node0 % kSxThreads == 0 &&
+        a.count % kSxThreads == 0) {
+      odd_sx_ == 4 ? launch(name, k_full_aa_odd_sx<4>, a, stream_, kSxThreads)
+                   : launch(name, k_full_aa_odd_sx<3>, a, stream_, kSxThreads);
       return;
     }
     switch (minb_) {
@@ -1493,6 +1567,9 @@ class DirectEngine final : public Engine {
   // registers) retires and refills warps in smaller groups than 2 x 8 warps;
   // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830 (64: 6567/6695).
   int aa_threads_ = 128;
+  // odd step with shared-memory realigned x-shifted stores (k_full_aa_odd_sx):
+  // 0 off, 3 / 4 = min blocks per SM of its 128-thread blocks
+  int odd_sx_ = 0;
   int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
   DevBuf<unsigned> barrier_;            // grid barrier {count, generation}

@@ -91,6 +91,27 @@ def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
             assert np.array_equal(k.snapshot(), expect2), (name, kind, steps + 2)
 
 
+@pytest.mark.parametrize("kind,dims", [("channel", (128, 12, 10)), ("blocks", (256, 16, 16)),
+                                       ("slit", (128, 5, 9))])
+def test_aa_odd_shared_realigned_variant(kind, dims, monkeypatch):
+    """k_full_aa_odd_sx (x-shifted scatters realigned through shared memory,
+    rows of 128-node blocks incl. the x wrap at both row ends) is bitwise the
+    register odd step, on one slab and on three z slabs."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    res = []
+    for sx in ("0", "4"):
+        for parts in (1, 3):
+            monkeypatch.setenv("LBMGPU_AA_ODD_SX", sx)
+            monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+            k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
+                                dist={"virtual_parts": parts} if parts > 1 else None)
+            k.load_perturbed(5)
+            k.advance(PARAMS, FORCE, 8)
+            res.append(k.fingerprint())
+            del k
+    assert len(set(res)) == 1, [f"{r:016x}" for r in res]
+
+
 def test_edge_shapes_match_reference(edge_golden):
     """Degenerate and ragged shapes for every kernel (tests/golden/edge.json,
     generated by the reference): 1- and 2-cell periodic axes that wrap onto
