@@ -102,4 +102,23 @@ struct FastDiv {
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// ---- AoS tiles through shared memory ---------------------------------------
+// A block's `cnt` consecutive AoS records (19 doubles each) are one
+// contiguous range: moved between global and shared memory with 16-byte
+// accesses (8-byte ones for a ragged or unaligned tile), so an own-record
+// sweep issues full-sector loads and stores instead of one 32-byte sector
+// request per 8-byte element.
+template <int T>
+__device__ __forceinline__ void aos_tile_copy(double* dst, const double* src, uint32_t cnt) {
+  const uint32_t nd = cnt * kQ;
+  if (cnt == T && T % 2 == 0 &&
+      ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (uint32_t i = threadIdx.x; i < nd / 2; i += T) d2[i] = s2[i];
+  } else {
+    for (uint32_t i = threadIdx.x; i < nd; i += T) dst[i] = src[i];
+  }
+}
+
 }  // namespace lbmgpu

@@ -29,6 +29,10 @@ struct DirectArgs {
   // slot-0 element.  One 64-bit add per direction instead of the wrapped
   // coordinate arithmetic; layout-specific, filled on the host.
   long long odd_off[kQ];
+  // AoS gather/scatter sweeps: traverse rows in y-bands of `band` rows, z
+  // before y inside a band, so the z +- 1 rows whose records a row's
+  // gathers touch are processed close in time (L2 reuse); 0 = plain order.
+  uint32_t band;
 };
 
 // Solid flag of own node (x, y, own-plane z) without touching memory for the

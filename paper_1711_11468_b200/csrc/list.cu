@@ -26,6 +26,7 @@
 #include <tuple>
 
 #include "halo.hpp"
+#include "tma.cuh"
 #include "lbm.hpp"
 
 namespace lbmgpu {
@@ -77,6 +78,53 @@ __global__ void __launch_bounds__(256) k_list_pull(const ListArgs a, uint64_t pf
   if (COLLIDE) collide(q, a.trt);
 #pragma unroll
   for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
+}
+
+// AoS list sweeps with the node's own record staged through a shared-memory
+// tile of kLAosTile consecutive nodes (slots 19n + d are contiguous): full-
+// sector loads / stores instead of one sector request per element.
+//   k_list_aos_tile<true>:  AA even (own slots -> opposite slots), [nb, ne)
+//   k_list_aos_tile<false>: collide pass, in place
+//   k_list_pull_aos_tile:   pull; gathers as k_list_pull, own record stored
+//                           through the tile
+constexpr int kLAosTile = 128;
+template <bool EVEN>
+__global__ void __launch_bounds__(kLAosTile) k_list_aos_tile(const ListArgs a) {
+  __shared__ __align__(128) double sh[kLAosTile * kQ];
+  __shared__ __align__(8) uint64_t bar;
+  const uint64_t n0 = a.nb + blockIdx.x * uint64_t(kLAosTile);
+  const uint32_t cnt = static_cast<uint32_t>(min(uint64_t(kLAosTile), a.ne - n0));
+  double* g = a.dst + n0 * kQ;
+  aos_tile_load<kLAosTile>(sh, g, cnt, &bar);
+  if (threadIdx.x < cnt) {
+    double* r = sh + threadIdx.x * kQ;
+    double q[kQ];
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) q[d] = r[d];
+    collide(q, a.trt);
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) r[EVEN ? opp(d) : d] = q[d];
+  }
+  aos_tile_store<kLAosTile>(g, sh, cnt);
+}
+
+template <bool COLLIDE>
+__global__ void __launch_bounds__(kLAosTile) k_list_pull_aos_tile(const ListArgs a) {
+  __shared__ __align__(128) double sh[kLAosTile * kQ];
+  const uint64_t n0 = blockIdx.x * uint64_t(kLAosTile);
+  const uint32_t cnt = static_cast<uint32_t>(min(uint64_t(kLAosTile), a.N - n0));
+  if (threadIdx.x < cnt) {
+    const uint64_t n = n0 + threadIdx.x;
+    double q[kQ];
+    q[0] = a.src[n * kQ];
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) q[d] = a.src[__ldg(a.adj + (d - 1) * a.N + n)];
+    if (COLLIDE) collide(q, a.trt);
+    double* r = sh + threadIdx.x * kQ;
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) r[d] = q[d];
+  }
+  aos_tile_store<kLAosTile>(a.dst + n0 * kQ, sh, cnt);
 }
 
 // list-push (kernels_list_os.cpp:43-62, push): own loads, scatter stores.
@@ -684,6 +732,7 @@ class ListEngine final : public Engine {
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
       if (const char* e = std::getenv("LBMGPU_LIST_ODD_PIPE")) odd_pipe_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_RIA_MODE")) ria_mode_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_LIST_THREADS")) {
         threads_ = std::atoi(e);
         threads_env_ = true;
@@ -870,7 +919,9 @@ class ListEngine final : public Engine {
                 : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a, pf_);
           else
             soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
-                : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+                : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
+                            : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
+                        : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         };
         if (boundary) {
           run(p.n0, p.n0 + p.head);
@@ -933,6 +984,16 @@ class ListEngine final : public Engine {
     return a;
   }
 
+  // AoS own-record tile kernels: kLAosTile-node blocks over [nb, ne)
+  template <class K>
+  void launch_tile(const char* name, K kern, const ListArgs& a) {
+    if (a.ne <= a.nb) return;
+    const int tok = stats_.begin(name, stream_);
+    kern<<<static_cast<unsigned>(ceil_div(a.ne - a.nb, kLAosTile)), kLAosTile, 0, stream_>>>(a);
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, stream_);
+  }
+
   template <class K, class... Extra>
   void launch(const char* name, K kern, const ListArgs& a, Extra... extra) {
     const int threads = threads_;
@@ -956,7 +1017,8 @@ class ListEngine final : public Engine {
       a.src = a.dst = buf_[0].get();
       for (long s = 0; s < steps; s += 2) {
         soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
-            : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+            : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
+                        : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         if (desc_.ria && soa) {
           const int tok = stats_.begin("list_aa_odd_ria_soa", stream_);
           // 128-thread CTAs: cfg 2 RIA odd 5228 -> 5431 GB/s (the indexed
@@ -1001,7 +1063,8 @@ class ListEngine final : public Engine {
     // (kernels_list_os.cpp:74-91, kernels_list_nt.cpp:146-158)
     a.src = a.dst = buf_[cur_].get();
     soa ? launch("list_collide_soa", k_list_collide<true>, a)
-        : launch("list_collide_aos", k_list_collide<false>, a);
+        : aos_tile_ ? launch_tile("list_collide_aos", k_list_aos_tile<false>, a)
+                    : launch("list_collide_aos", k_list_collide<false>, a);
     for (long s = 0; s < steps; ++s) {
       a.src = buf_[cur_].get();
       a.dst = buf_[1 - cur_].get();
@@ -1014,8 +1077,12 @@ class ListEngine final : public Engine {
         else
           launch("list_pull_soa", k_list_pull<true, true, false>, a, pull_pf_);
       } else {
-        last ? launch("list_pull_stream_aos", k_list_pull<false, false, false>, a, pull_pf_)
-             : launch("list_pull_aos", k_list_pull<false, true, false>, a, pull_pf_);
+        if (last)
+          launch("list_pull_stream_aos", k_list_pull<false, false, false>, a, pull_pf_);
+        else if (aos_tile_)
+          launch_tile("list_pull_aos", k_list_pull_aos_tile<true>, a);
+        else
+          launch("list_pull_aos", k_list_pull<false, true, false>, a, pull_pf_);
       }
       cur_ ^= 1;
     }
@@ -1193,6 +1260,7 @@ class ListEngine final : public Engine {
   DevBuf<int32_t> ria_gpat_;    // [group][18] inline pattern or kMixedGroup
   int ria_mode_ = 0;            // 0: run table, 1: group patterns (LBMGPU_RIA_MODE)
   int threads_ = 256;           // CTA size of the sweeps
+  bool aos_tile_ = true;        // AoS own-record sweeps through shared-memory tiles
   bool threads_env_ = false;    // threads_ set by LBMGPU_LIST_THREADS
   uint64_t pf_ = 0;             // adjacency L2 prefetch distance in nodes (AA odd)
   uint64_t pull_pf_ = 0;        // same for the one-step pull sweeps
