@@ -83,8 +83,10 @@ typedef struct {
   int vector_width;
 } lbmgpu_descriptor;
 
-/* Multi-GPU z-slab decomposition of the direct AA sweep (new; the reference
- * has no distributed path).  nranks == 1 and virtual_parts <= 1: one slab.
+/* Multi-GPU decomposition (new; the reference has no distributed path):
+ * z slabs for the direct SoA kernels (AA: halo phases 0/1; blk-push /
+ * blk-pull: phases 2/3), contiguous node ranges for list-aa-soa/aos with
+ * blk = 0.  nranks == 1 and virtual_parts <= 1: one part.
  * virtual_parts > 1 (nranks == 1): the box is cut into that many z-slabs on
  * ONE device and the halo exchange runs as device copies -- the same plan and
  * kernels as the NCCL path, used for single-GPU parity tests.  nranks > 1:
