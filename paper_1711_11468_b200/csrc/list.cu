@@ -39,11 +39,12 @@ struct ListArgs {
   uint64_t starts[kQ];  // SoA direction starts (unused for AoS)
   TrtArgs trt;
   uint64_t nb, ne;      // node range of this launch (AA sweeps); [0, N) by default
+  uint64_t node_base;   // canonical sweeps over a part's local arrays: node n is local n - base
 };
 
 template <bool SOA>
 __device__ __forceinline__ uint64_t lslot(const ListArgs& a, uint64_t n, int d) {
-  return SOA ? a.starts[d] + n : n * kQ + d;
+  return SOA ? a.starts[d] + (n - a.node_base) : (n - a.node_base) * kQ + d;
 }
 
 template <bool CS>
@@ -551,13 +552,19 @@ __global__ void k_list_mass_terms(const ListArgs a, const double* buf,
 
 // ---- node-range decomposition of list AA (multi-GPU) ----
 // Part p owns the contiguous list nodes [n0_p, n1_p) (blk = 0: x-major, so
-// parts are x-slabs) and keeps the full slot array; its odd step gathers from
-// and scatters to the slots of neighbour-owned nodes listed in its links.
-// Link (r <- s) = the slots of s's nodes that r's scatter entries point to;
-// every slot is referenced by exactly one node, so r's odd step is the only
-// reader/writer of those slots in that sub-step.  Exchange per AA pair:
-// phase 0 (after even) s -> r, phase 1 (after odd) r -> s, of exactly these
-// slots -- the list analogue of the direct z-slab plan (halo.hpp).
+// parts are x-slabs) and holds only its own slots plus ghost copies of the
+// remote slots its nodes' scatter entries point to, in a local numbering:
+//   own slot (node n, direction slot d):  SoA d * nloc + (n - n0),
+//                                         AoS (n - n0) * 19 + d
+//   ghost slots:                          19 * nloc + gofs[s] + k
+// where k is the rank of the global slot in the sorted list of link (p <- s)
+// = the slots of s's nodes that p's entries point to.  The part's adjacency
+// is remapped to local indices (boundary adjacency remap), so its sweeps are
+// the single-lattice kernels on an nloc-node lattice.  Every slot is
+// referenced by exactly one node, so p's odd step is the only reader/writer
+// of a link's slots in that sub-step.  Exchange per AA pair: phase 0 (after
+// even) s -> r, phase 1 (after odd) r -> s, of exactly these slots -- the
+// list analogue of the direct z-slab plan (halo.hpp).
 
 // node owning the slot that entry (n, column d) points to (SlotMap::slot,
 // list_lattice.hpp:66-75: a fluid neighbour's slot d, else n's own opp slot)
@@ -568,6 +575,34 @@ __device__ __forceinline__ uint64_t entry_owner(const ListArgs& a, int soa, uint
     return (e >= s && e < s + a.N) ? e - s : n;
   }
   return e / kQ;
+}
+
+// (owner node, direction slot) of a global slot
+__device__ __forceinline__ void slot_node(const ListArgs& a, int soa, uint32_t e, uint64_t& m,
+                                          int& dd) {
+  if (!soa) {
+    m = e / kQ;
+    dd = static_cast<int>(e - m * kQ);
+    return;
+  }
+  dd = 0;
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    if (e >= a.starts[d]) dd = d;  // starts ascend (padding_offsets)
+  m = e - a.starts[dd];
+}
+
+__device__ __forceinline__ uint64_t local_own(int soa, uint64_t m, int dd, uint64_t n0,
+                                              uint64_t nloc) {
+  return soa ? uint64_t(dd) * nloc + (m - n0) : (m - n0) * kQ + dd;
+}
+
+// part owning node m under the cut [N*p/P, N*(p+1)/P)
+__device__ __forceinline__ int part_of_node(uint64_t m, uint64_t N, int parts) {
+  int p = static_cast<int>(m * uint64_t(parts) / N);
+  while (p > 0 && m < N * uint64_t(p) / parts) --p;
+  while (p + 1 < parts && m >= N * uint64_t(p + 1) / parts) ++p;
+  return p;
 }
 
 __global__ void k_link_flags(const ListArgs a, int soa, uint64_t nb, uint64_t ne, uint64_t olo,
@@ -585,38 +620,92 @@ __global__ void k_link_flags(const ListArgs a, int soa, uint64_t nb, uint64_t ne
   }
 }
 
-__global__ void k_boundary_mask(const ListArgs a, int soa, uint64_t nb, uint64_t ne,
-                                uint8_t* __restrict__ mask) {
-  for (uint64_t n = nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < ne;
-       n += uint64_t(gridDim.x) * blockDim.x) {
-    bool remote = false;
-    for (int d = 1; d < kQ && !remote; ++d) {
-      const uint64_t m = entry_owner(a, soa, n, d, a.adj[uint64_t(d - 1) * a.N + n]);
-      remote = m < nb || m >= ne;
+// Local adjacency of part [n0, n0 + nloc): own entries -> local own index,
+// remote entries -> ghost index (binary search in the sorted link list).
+__global__ void k_local_adj(const ListArgs g, int soa, uint64_t n0, uint64_t nloc, int parts,
+                            const uint32_t* __restrict__ gslots,
+                            const uint64_t* __restrict__ gofs, const uint64_t* __restrict__ gcnt,
+                            uint32_t* __restrict__ ladj) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nloc * 18;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const int d = static_cast<int>(i / nloc) + 1;
+    const uint64_t j = i - uint64_t(d - 1) * nloc, n = n0 + j;
+    const uint32_t e = g.adj[uint64_t(d - 1) * g.N + n];
+    const uint64_t m = entry_owner(g, soa, n, d, e);
+    uint64_t loc;
+    if (m >= n0 && m < n0 + nloc) {
+      uint64_t mm;
+      int dd;
+      slot_node(g, soa, e, mm, dd);
+      loc = local_own(soa, mm, dd, n0, nloc);
+    } else {
+      const int s = part_of_node(m, g.N, parts);
+      const uint32_t* l = gslots + gofs[s];
+      uint64_t lo = 0, hi = gcnt[s];
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (l[mid] < e) lo = mid + 1; else hi = mid;
+      }
+      loc = nloc * kQ + gofs[s] + lo;
     }
-    mask[n - nb] = remote;
+    ladj[i] = static_cast<uint32_t>(loc);
   }
 }
 
-__global__ void k_slots_copy(const uint32_t* __restrict__ slots, uint64_t cnt,
-                             const double* __restrict__ src, double* __restrict__ dst) {
+// local own index of each (global) slot of a link, on the owning part
+__global__ void k_own_local_idx(const ListArgs g, int soa, uint64_t n0, uint64_t nloc,
+                                const uint32_t* __restrict__ slots, uint64_t cnt,
+                                uint32_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    dst[slots[i]] = src[slots[i]];
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t m;
+    int dd;
+    slot_node(g, soa, slots[i], m, dd);
+    out[i] = static_cast<uint32_t>(local_own(soa, m, dd, n0, nloc));
+  }
 }
 
-__global__ void k_slots_pack(const uint32_t* __restrict__ slots, uint64_t cnt,
+// initial local array of a part from the global one: own slots, then ghosts
+__global__ void k_local_init(const ListArgs g, int soa, const double* __restrict__ gbuf,
+                             uint64_t n0, uint64_t nloc, const uint32_t* __restrict__ gslots,
+                             uint64_t nghost, double* __restrict__ lbuf) {
+  const uint64_t own = nloc * kQ;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < own + nghost;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (i < own) {
+      const uint64_t j = soa ? i % nloc : i / kQ;
+      const int d = static_cast<int>(soa ? i / nloc : i % kQ);
+      lbuf[i] = soa ? gbuf[g.starts[d] + n0 + j] : gbuf[(n0 + j) * kQ + d];
+    } else {
+      lbuf[i] = gbuf[gslots[i - own]];
+    }
+  }
+}
+
+// boundary nodes of a part: any local entry in the ghost range
+__global__ void k_ghost_mask(const uint32_t* __restrict__ ladj, uint64_t nloc,
+                             uint8_t* __restrict__ mask) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < nloc;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    bool ghost = false;
+    for (int d = 0; d < 18 && !ghost; ++d) ghost = ladj[uint64_t(d) * nloc + j] >= nloc * kQ;
+    mask[j] = ghost;
+  }
+}
+
+// link transfers: gather by index / scatter by index / indexed copy
+__global__ void k_slots_pack(const uint32_t* __restrict__ idx, uint64_t cnt,
                              const double* __restrict__ buf, double* __restrict__ out) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
        i += uint64_t(gridDim.x) * blockDim.x)
-    out[i] = buf[slots[i]];
+    out[i] = buf[idx[i]];
 }
 
-__global__ void k_slots_unpack(const uint32_t* __restrict__ slots, uint64_t cnt,
+__global__ void k_slots_unpack(const uint32_t* __restrict__ idx, uint64_t cnt,
                                const double* __restrict__ in, double* __restrict__ buf) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
        i += uint64_t(gridDim.x) * blockDim.x)
-    buf[slots[i]] = in[i];
+    buf[idx[i]] = in[i];
 }
 
 // ------------------------------------------------------------------ engine
@@ -628,18 +717,32 @@ int grid_for(uint64_t n, int threads) {
 
 class ListEngine final : public Engine {
  public:
-  // node-range part of a decomposed list lattice
+  // node-range part of a decomposed list lattice (local numbering, see the
+  // kernels above): 19 * nloc own slots + nghost ghost slots
   struct LPart {
     int index = 0;
-    uint64_t n0 = 0, n1 = 0, head = 0, tail = 0;
-    DevBuf<double> own;  // full slot array (parts other than the first)
+    uint64_t n0 = 0, n1 = 0, nloc = 0, nghost = 0, head = 0, tail = 0;
+    DevBuf<double> own;
+    DevBuf<uint32_t> adj;  // local d-major adjacency [(d-1) * nloc + j]
     double* buf = nullptr;
+    ListArgs args(const TrtArgs& t, bool soa) const {
+      ListArgs a{};
+      a.src = a.dst = buf;
+      a.adj = adj.get();
+      a.N = nloc;
+      for (int q = 0; q < kQ; ++q) a.starts[q] = soa ? uint64_t(q) * nloc : 0;
+      a.trt = t;
+      a.nb = 0;
+      a.ne = nloc;
+      return a;
+    }
   };
   struct LLink {
     int r = 0, s = 0;      // slots of s's nodes referenced by r's nodes
     uint64_t count = 0;
-    DevBuf<uint32_t> slots;
-    DevBuf<double> send, recv;  // NCCL staging
+    uint64_t ghost0 = 0;   // first ghost index of these slots on r (local)
+    DevBuf<uint32_t> sidx; // local own index of each slot on s
+    DevBuf<double> stage;  // NCCL staging of the gathered (s side) values
   };
 
   ListEngine(const Descriptor& d, const GeomSpec& g, const Padding& pad,
@@ -757,6 +860,9 @@ class ListEngine final : public Engine {
   }
 
   // ---- node-range decomposition -------------------------------------------
+  // Links and local structures are derived from the global adjacency, which
+  // (with the global PDF array) is released afterwards: each part keeps
+  // 19 * nloc + nghost doubles and 18 * nloc indices.
   void setup_parts(const DistSpec& dist, int parts) {
     if (desc_.prop != Prop::Aa || desc_.ria)
       throw ConfigError("list decomposition is implemented for list-aa-soa / list-aa-aos "
@@ -770,34 +876,99 @@ class ListEngine final : public Engine {
     lrank_ = dist.rank;
     lnranks_ = dist.nranks;
     const bool multi_process = dist.nranks > 1;
+    const int soa = desc_.soa ? 1 : 0;
     auto range = [&](int p) {
       return std::pair<uint64_t, uint64_t>(n_fluid_ * uint64_t(p) / parts,
                                            n_fluid_ * uint64_t(p + 1) / parts);
     };
-    ListArgs a = base_args();
-    // parts living in this process; part 0 (or this rank's part) reuses buf_[0]
+    auto is_local = [&](int p) { return !multi_process || p == lrank_; };
+    const ListArgs g = base_args();
+    // links (r <- s) this process takes part in: sorted global slot lists
+    std::vector<DevBuf<uint32_t>> slots;  // parallel to links_
+    for (int r = 0; r < parts; ++r)
+      for (int s = 0; s < parts; ++s) {
+        if (r == s || !(is_local(r) || is_local(s))) continue;
+        const auto [rn0, rn1] = range(r);
+        const auto [sn0, sn1] = range(s);
+        const uint64_t cnt = (rn1 - rn0) * 18;
+        DevBuf<uint8_t> flags(cnt);
+        DevBuf<uint32_t> vals(cnt);
+        k_link_flags<<<grid_for(cnt, 256), 256, 0, stream_>>>(g, soa, rn0, rn1, sn0, sn1,
+                                                              flags.get(), vals.get());
+        LBM_CHECK_LAUNCH();
+        DevBuf<uint32_t> sel(cnt);
+        DevBuf<unsigned long long> nsel(1);
+        size_t tmp = 0;
+        LBM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, vals.get(), flags.get(), sel.get(),
+                                            nsel.get(), static_cast<int64_t>(cnt), stream_));
+        DevBuf<uint8_t> t(tmp);
+        LBM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, vals.get(), flags.get(), sel.get(),
+                                            nsel.get(), static_cast<int64_t>(cnt), stream_));
+        unsigned long long k = 0;
+        LBM_CUDA(cudaMemcpyAsync(&k, nsel.get(), 8, cudaMemcpyDeviceToHost, stream_));
+        LBM_CUDA(cudaStreamSynchronize(stream_));
+        if (k == 0) continue;
+        DevBuf<uint32_t> sorted(k);
+        tmp = 0;
+        LBM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, sel.get(), sorted.get(),
+                                                static_cast<int64_t>(k), 0, 32, stream_));
+        DevBuf<uint8_t> t2(tmp);
+        LBM_CUDA(cub::DeviceRadixSort::SortKeys(t2.get(), tmp, sel.get(), sorted.get(),
+                                                static_cast<int64_t>(k), 0, 32, stream_));
+        LLink l;
+        l.r = r;
+        l.s = s;
+        l.count = k;
+        links_.push_back(std::move(l));
+        slots.push_back(std::move(sorted));
+      }
+    // parts living in this process
     for (int p = 0; p < parts; ++p) {
-      if (multi_process && p != lrank_) continue;
+      if (!is_local(p)) continue;
       LPart lp;
       lp.index = p;
       std::tie(lp.n0, lp.n1) = range(p);
-      if (lparts_.empty()) {
-        lp.buf = buf_[0].get();
-      } else {
-        lp.own.alloc(total_slots_);
-        LBM_CUDA(cudaMemcpyAsync(lp.own.get(), buf_[0].get(), total_slots_ * 8,
-                                 cudaMemcpyDeviceToDevice, stream_));
-        lp.buf = lp.own.get();
-      }
-      // boundary nodes (any entry owned by another part) -> head / tail spans
-      const uint64_t cnt = lp.n1 - lp.n0;
-      DevBuf<uint8_t> mask(cnt);
-      k_boundary_mask<<<grid_for(cnt, 256), 256, 0, stream_>>>(a, desc_.soa, lp.n0, lp.n1,
-                                                                mask.get());
+      lp.nloc = lp.n1 - lp.n0;
+      // ghost list = the sorted link lists (p <- s) concatenated in s order
+      std::vector<uint64_t> gofs(parts, 0), gcnt(parts, 0);
+      for (size_t i = 0; i < links_.size(); ++i)
+        if (links_[i].r == p) {
+          links_[i].ghost0 = lp.nloc * kQ + lp.nghost;
+          gofs[links_[i].s] = lp.nghost;
+          gcnt[links_[i].s] = links_[i].count;
+          lp.nghost += links_[i].count;
+        }
+      const uint64_t nslots = lp.nloc * kQ + lp.nghost;
+      if (nslots >= (1ull << 32))
+        throw ConfigError("list decomposition: more than 2^32 local slots in one part");
+      DevBuf<uint32_t> gslots(std::max<uint64_t>(lp.nghost, 1));
+      for (size_t i = 0; i < links_.size(); ++i)
+        if (links_[i].r == p)
+          LBM_CUDA(cudaMemcpyAsync(gslots.get() + gofs[links_[i].s], slots[i].get(),
+                                   links_[i].count * 4, cudaMemcpyDeviceToDevice, stream_));
+      DevBuf<uint64_t> dofs(parts), dcnt(parts);
+      LBM_CUDA(cudaMemcpyAsync(dofs.get(), gofs.data(), parts * 8, cudaMemcpyHostToDevice,
+                               stream_));
+      LBM_CUDA(cudaMemcpyAsync(dcnt.get(), gcnt.data(), parts * 8, cudaMemcpyHostToDevice,
+                               stream_));
+      lp.adj.alloc(18 * lp.nloc);
+      k_local_adj<<<grid_for(18 * lp.nloc, 256), 256, 0, stream_>>>(
+          g, soa, lp.n0, lp.nloc, parts, gslots.get(), dofs.get(), dcnt.get(), lp.adj.get());
       LBM_CHECK_LAUNCH();
-      std::vector<uint8_t> h(cnt);
-      LBM_CUDA(cudaMemcpyAsync(h.data(), mask.get(), cnt, cudaMemcpyDeviceToHost, stream_));
+      lp.own.alloc(nslots);
+      lp.buf = lp.own.get();
+      k_local_init<<<grid_for(nslots, 256), 256, 0, stream_>>>(
+          g, soa, buf_[0].get(), lp.n0, lp.nloc, gslots.get(), lp.nghost, lp.buf);
+      LBM_CHECK_LAUNCH();
+      // boundary nodes (any ghost entry) -> head / tail spans (x-slab ends)
+      DevBuf<uint8_t> mask(lp.nloc);
+      k_ghost_mask<<<grid_for(lp.nloc, 256), 256, 0, stream_>>>(lp.adj.get(), lp.nloc,
+                                                                 mask.get());
+      LBM_CHECK_LAUNCH();
+      std::vector<uint8_t> h(lp.nloc);
+      LBM_CUDA(cudaMemcpyAsync(h.data(), mask.get(), lp.nloc, cudaMemcpyDeviceToHost, stream_));
       LBM_CUDA(cudaStreamSynchronize(stream_));
+      const uint64_t cnt = lp.nloc;
       uint64_t head = 0, tail = 0;
       for (uint64_t i = 0; i < cnt / 2; ++i)
         if (h[i]) head = i + 1;
@@ -810,48 +981,25 @@ class ListEngine final : public Engine {
       lp.tail = std::min(tail, cnt - head);
       lparts_.push_back(std::move(lp));
     }
-    // links (r <- s) this process takes part in
-    for (int r = 0; r < parts; ++r)
-      for (int s = 0; s < parts; ++s) {
-        if (r == s) continue;
-        if (multi_process && r != lrank_ && s != lrank_) continue;
-        const auto [rn0, rn1] = range(r);
-        const auto [sn0, sn1] = range(s);
-        const uint64_t cnt = (rn1 - rn0) * 18;
-        DevBuf<uint8_t> flags(cnt);
-        DevBuf<uint32_t> vals(cnt);
-        k_link_flags<<<grid_for(cnt, 256), 256, 0, stream_>>>(a, desc_.soa, rn0, rn1, sn0, sn1,
-                                                              flags.get(), vals.get());
+    // sender-side local indices; NCCL staging
+    for (size_t i = 0; i < links_.size(); ++i) {
+      LLink& l = links_[i];
+      if (is_local(l.s)) {
+        const auto [sn0, sn1] = range(l.s);
+        l.sidx.alloc(l.count);
+        k_own_local_idx<<<grid_for(l.count, 256), 256, 0, stream_>>>(
+            g, soa, sn0, sn1 - sn0, slots[i].get(), l.count, l.sidx.get());
         LBM_CHECK_LAUNCH();
-        DevBuf<uint32_t> out(cnt);
-        DevBuf<unsigned long long> nsel(1);
-        size_t tmp = 0;
-        LBM_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, vals.get(), flags.get(), out.get(),
-                                            nsel.get(), static_cast<int64_t>(cnt), stream_));
-        DevBuf<uint8_t> t(tmp);
-        LBM_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, vals.get(), flags.get(), out.get(),
-                                            nsel.get(), static_cast<int64_t>(cnt), stream_));
-        unsigned long long k = 0;
-        LBM_CUDA(cudaMemcpyAsync(&k, nsel.get(), 8, cudaMemcpyDeviceToHost, stream_));
-        LBM_CUDA(cudaStreamSynchronize(stream_));
-        if (k == 0) continue;
-        LLink l;
-        l.r = r;
-        l.s = s;
-        l.count = k;
-        l.slots.alloc(k);
-        LBM_CUDA(cudaMemcpyAsync(l.slots.get(), out.get(), k * 4, cudaMemcpyDeviceToDevice,
-                                 stream_));
-        if (multi_process || dist.have_id) {
-          l.send.alloc(k);
-          l.recv.alloc(k);
-        }
-        links_.push_back(std::move(l));
       }
+      if (multi_process || dist.have_id) l.stage.alloc(l.count);
+    }
     if (multi_process || dist.have_id)
       lnccl_ = nccl_create({}, multi_process ? lrank_ : 0, multi_process ? lnranks_ : 1,
                            dist.nccl_id.data());
     LBM_CUDA(cudaStreamSynchronize(stream_));
+    // memory scaling: the global arrays are not needed any more
+    buf_[0].release();
+    adj_.release();
   }
 
   LPart* part_of(int index) {
@@ -860,41 +1008,54 @@ class ListEngine final : public Engine {
     return nullptr;
   }
 
-  // phase 0 (after even): slots flow s -> r; phase 1 (after odd): r -> s.
+  // phase 0 (after even): slots flow s -> r (s's own slots -> r's ghosts);
+  // phase 1 (after odd): r -> s.  r's ghosts of one link are contiguous.
   void list_exchange(int phase) {
-    if (!lnccl_) {  // all parts in this process: direct slot copies
+    if (!lnccl_) {  // all parts in this process: indexed device copies
       for (LLink& l : links_) {
-        LPart* from = part_of(phase == 0 ? l.s : l.r);
-        LPart* to = part_of(phase == 0 ? l.r : l.s);
-        k_slots_copy<<<grid_for(l.count, 256), 256, 0, stream_>>>(l.slots.get(), l.count,
-                                                                   from->buf, to->buf);
+        LPart* sp = part_of(l.s);
+        LPart* rp = part_of(l.r);
+        if (phase == 0)
+          k_slots_pack<<<grid_for(l.count, 256), 256, 0, stream_>>>(
+              l.sidx.get(), l.count, sp->buf, rp->buf + l.ghost0);
+        else
+          k_slots_unpack<<<grid_for(l.count, 256), 256, 0, stream_>>>(
+              l.sidx.get(), l.count, rp->buf + l.ghost0, sp->buf);
         LBM_CHECK_LAUNCH();
       }
       return;
     }
-    std::vector<NcclP2P> ops;
-    for (LLink& l : links_) {  // pack what this process sends
-      LPart* from = part_of(phase == 0 ? l.s : l.r);
-      if (!from) continue;
-      k_slots_pack<<<grid_for(l.count, 256), 256, 0, stream_>>>(l.slots.get(), l.count,
-                                                                 from->buf, l.send.get());
-      LBM_CHECK_LAUNCH();
-    }
+    // phase 0: s packs its slots into the staging buffer, sends it, r
+    // receives straight into its ghost range.  phase 1: r sends its ghost
+    // range, s receives into staging and scatters.
+    for (LLink& l : links_)
+      if (phase == 0 && part_of(l.s)) {
+        k_slots_pack<<<grid_for(l.count, 256), 256, 0, stream_>>>(
+            l.sidx.get(), l.count, part_of(l.s)->buf, l.stage.get());
+        LBM_CHECK_LAUNCH();
+      }
     nccl_begin(lnccl_, phase, stream_);
+    std::vector<NcclP2P> ops;
     for (LLink& l : links_) {  // global link order on every rank -> matched pairs
-      const int src = phase == 0 ? l.s : l.r, dst = phase == 0 ? l.r : l.s;
-      if (part_of(src)) ops.push_back({dst, l.send.get(), nullptr, l.count});
-      if (part_of(dst)) ops.push_back({src, nullptr, l.recv.get(), l.count});
+      LPart* sp = part_of(l.s);
+      LPart* rp = part_of(l.r);
+      if (phase == 0) {
+        if (sp) ops.push_back({l.r, l.stage.get(), nullptr, l.count});
+        if (rp) ops.push_back({l.s, nullptr, rp->buf + l.ghost0, l.count});
+      } else {
+        if (rp) ops.push_back({l.s, rp->buf + l.ghost0, nullptr, l.count});
+        if (sp) ops.push_back({l.r, nullptr, l.stage.get(), l.count});
+      }
     }
     nccl_p2p(lnccl_, ops);
     cudaStream_t cs = nccl_comm_stream(lnccl_);
-    for (LLink& l : links_) {
-      LPart* to = part_of(phase == 0 ? l.r : l.s);
-      if (!to) continue;
-      k_slots_unpack<<<grid_for(l.count, 256), 256, 0, cs>>>(l.slots.get(), l.count,
-                                                             l.recv.get(), to->buf);
-      LBM_CHECK_LAUNCH();
-    }
+    if (phase == 1)
+      for (LLink& l : links_)
+        if (LPart* sp = part_of(l.s)) {
+          k_slots_unpack<<<grid_for(l.count, 256), 256, 0, cs>>>(l.sidx.get(), l.count,
+                                                                 l.stage.get(), sp->buf);
+          LBM_CHECK_LAUNCH();
+        }
     nccl_end(lnccl_, phase);
   }
 
@@ -908,9 +1069,7 @@ class ListEngine final : public Engine {
     const bool soa = desc_.soa;
     auto sweep = [&](bool odd, bool boundary) {
       for (LPart& p : lparts_) {
-        ListArgs a = base_args();
-        a.trt = t;
-        a.src = a.dst = p.buf;
+        ListArgs a = p.args(t, soa);
         auto run = [&](uint64_t b0, uint64_t b1) {
           a.nb = b0;
           a.ne = b1;
@@ -920,14 +1079,13 @@ class ListEngine final : public Engine {
           else
             soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
                 : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
-                            : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
-                        : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+                            : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         };
         if (boundary) {
-          run(p.n0, p.n0 + p.head);
-          run(p.n1 - p.tail, p.n1);
+          run(0, p.head);
+          run(p.nloc - p.tail, p.nloc);
         } else {
-          run(p.n0 + p.head, p.n1 - p.tail);
+          run(p.head, p.nloc - p.tail);
         }
       }
     };
@@ -1112,8 +1270,12 @@ class ListEngine final : public Engine {
       return;
     }
     // node-range parts (blk = 0: canonical index == list index): each node's
-    // PDFs live in its owner part's buffer
-    for (LPart& p : lparts_) run(p.buf, std::max(c0, p.n0), std::min(c1, p.n1));
+    // PDFs live in its owner part's local array (node n is local n - n0)
+    for (LPart& p : lparts_) {
+      a = p.args(TrtArgs{}, desc_.soa);
+      a.node_base = p.n0;
+      run(p.buf, std::max(c0, p.n0), std::min(c1, p.n1));
+    }
   }
 
   void gather_canonical(uint64_t c0, uint64_t count, double* out) override {
@@ -1130,10 +1292,14 @@ class ListEngine final : public Engine {
   }
 
   double total_mass() override {
-    auto part_mass = [&](double* buf, uint64_t b0, uint64_t b1) {
+    auto part_mass = [&](double* buf, uint64_t b0, uint64_t b1, const LPart* p) {
       if (b1 <= b0) return 0.0;
       DevBuf<double> tmp((b1 - b0) * kQ);
       ListArgs a = base_args();
+      if (p) {
+        a = p->args(TrtArgs{}, desc_.soa);
+        a.node_base = p->n0;
+      }
       a.nb = b0;
       a.ne = b1;
       desc_.soa ? k_list_mass_terms<true><<<grid_for(b1 - b0, 256), 256, 0, stream_>>>(
@@ -1143,9 +1309,9 @@ class ListEngine final : public Engine {
       LBM_CHECK_LAUNCH();
       return device_sum(tmp.get(), tmp.size(), stream_);
     };
-    if (lparts_.empty()) return part_mass(buf_[cur_].get(), 0, n_fluid_);
+    if (lparts_.empty()) return part_mass(buf_[cur_].get(), 0, n_fluid_, nullptr);
     double m = 0.0;
-    for (LPart& p : lparts_) m += part_mass(p.buf, p.n0, p.n1);
+    for (LPart& p : lparts_) m += part_mass(p.buf, p.n0, p.n1, &p);
     return lnccl_ && lnranks_ > 1 ? nccl_sum(lnccl_, m) : m;
   }
 
@@ -1155,6 +1321,9 @@ class ListEngine final : public Engine {
       LBM_CUDA(cudaMemcpyAsync(nodes, nodes_.get(), nodes_.bytes(),
                                cudaMemcpyDeviceToHost, stream_));
     if (adj) {
+      if (!lparts_.empty())
+        throw ConfigError("export_structure: the adjacency of a decomposed list lattice "
+                          "lives in per-part local numbering");
       DevBuf<uint32_t> canon(18 * n_fluid_);
       k_adj_canonical<<<grid_for(18 * n_fluid_, 256), 256, 0, stream_>>>(
           adj_.get(), n_fluid_, canon.get());
