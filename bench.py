@@ -323,7 +323,11 @@ def main():
         # every sweep launch of the timed region touches each fluid node once:
         # 19 reads + 19 writes of 8 B (+ 72 B of adjacency for list one-step,
         # 72 B for the odd AA list sub-step only)
-        if "ria" in name:
+        if "ria_pid" in name:
+            # pattern-id coding: 304 B of PDFs + a 1-byte pattern id per node
+            # (the <= 256-row pattern table stays in L1)
+            per_node = 304 + 1
+        elif "ria" in name:
             # run-coded odd step: 304 B of PDFs + 8 B of run table per 32
             # nodes (the pattern rows are L1/L2 resident)
             per_node = 304 + 0.25

@@ -23,7 +23,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <tuple>
+#include <unordered_map>
 
 #include "halo.hpp"
 #include "tma.cuh"
@@ -423,6 +425,52 @@ __global__ void __launch_bounds__(256) k_list_aa_odd_ria(const ListArgs a,
   const uint32_t below = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
   const uint32_t r = __ldg(warp_run0 + (n >> 5)) + __popc(__ldg(warp_mask + (n >> 5)) & below);
   const int32_t* p = pat + uint64_t(r) * 18;
+  double* buf = a.dst;
+  // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
+  int64_t off[18];
+#pragma unroll
+  for (int k = 0; k < 18; ++k) off[k] = __ldg(p + k);
+  double q[kQ];
+  q[0] = buf[a.starts[0] + n];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = buf[int64_t(a.starts[opp(d)] + n) + off[opp(d) - 1]];
+  collide(q, a.trt);
+  lst<CS>(buf + a.starts[0] + n, q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) lst<CS>(buf + int64_t(a.starts[d] + n) + off[d - 1], q[d]);
+}
+
+// Pattern-id form of the run coding, for lattices whose runs share few
+// distinct patterns (a channel: interior, walls, edges): the <= 256 distinct
+// rows live in a small table that stays in L1, and every node carries the
+// one-byte id of its run's row.  The dependent chain in front of the gathers
+// is then one coalesced byte load (prefetched into L2 a wave ahead) and an
+// L1 hit, instead of the run-table word and the run's row from L2.
+__global__ void k_ria_node_ids(const uint32_t* __restrict__ warp_run0,
+                               const uint32_t* __restrict__ warp_mask,
+                               const uint8_t* __restrict__ run_pid, uint64_t N,
+                               uint8_t* __restrict__ nid) {
+  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < N;
+       n += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t lane = static_cast<uint32_t>(n & 31);
+    const uint32_t below = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
+    const uint32_t r = warp_run0[n >> 5] + __popc(warp_mask[n >> 5] & below);
+    nid[n] = run_pid[r];
+  }
+}
+
+template <bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_odd_pid(const ListArgs a,
+                                                         const int32_t* __restrict__ ptab,
+                                                         const uint8_t* __restrict__ nid,
+                                                         uint64_t pf) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  if (pf && (threadIdx.x & 31) == 0) {  // ids of a later wave -> L2
+    const uint64_t m = n + pf;
+    if (m < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(nid + m));
+  }
+  const int32_t* p = ptab + uint32_t(__ldg(nid + n)) * 18;
   double* buf = a.dst;
   // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
   int64_t off[18];
@@ -1178,12 +1226,18 @@ class ListEngine final : public Engine {
             : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
                         : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         if (desc_.ria && soa) {
-          const int tok = stats_.begin("list_aa_odd_ria_soa", stream_);
+          const int mode = ria_mode_ >= 0 ? ria_mode_ : (ria_npat_ > 0 ? 2 : 0);
+          const int tok = stats_.begin(mode == 2 && ria_npat_ > 0 ? "list_aa_odd_ria_pid_soa"
+                                                                  : "list_aa_odd_ria_soa",
+                                       stream_);
           // 128-thread CTAs: cfg 2 RIA odd 5228 -> 5431 GB/s (the indexed
           // sweeps measured equal or better at 256)
           const int rt = threads_env_ ? threads_ : 128;
           const unsigned g = static_cast<unsigned>(ceil_div(a.N, rt));
-          if (ria_mode_ == 1)
+          if (mode == 2 && ria_npat_ > 0)
+            k_list_aa_odd_pid<false><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(), ria_nid_.get(),
+                                                            pf_);
+          else if (mode == 1)
             k_list_aa_odd_gpat<false><<<g, rt, 0, stream_>>>(a, ria_gpat_.get(), pf_);
           else
             k_list_aa_odd_ria<false><<<g, rt, 0, stream_>>>(
@@ -1377,6 +1431,43 @@ class ListEngine final : public Engine {
     k_ria_group_patterns<<<grid_for(warps * 18, 256), 256, 0, stream_>>>(
         ria_pat_.get(), ria_run0_.get(), ria_mask_.get(), n_fluid_, ria_gpat_.get());
     LBM_CHECK_LAUNCH();
+    // distinct run patterns (host dedup, stops at 257): <= 256 -> pattern ids
+    {
+      std::vector<int32_t> hp(uint64_t(R) * 18);
+      LBM_CUDA(cudaMemcpyAsync(hp.data(), ria_pat_.get(), hp.size() * 4, cudaMemcpyDeviceToHost,
+                               stream_));
+      LBM_CUDA(cudaStreamSynchronize(stream_));
+      std::unordered_map<std::string, uint8_t> ids;
+      std::vector<uint8_t> run_pid(R);
+      std::vector<int32_t> tab;
+      bool ok = true;
+      for (uint32_t r = 0; r < R && ok; ++r) {
+        std::string key(reinterpret_cast<const char*>(hp.data() + uint64_t(r) * 18), 72);
+        auto it = ids.find(key);
+        if (it == ids.end()) {
+          if (ids.size() == 256) {
+            ok = false;
+            break;
+          }
+          it = ids.emplace(key, static_cast<uint8_t>(ids.size())).first;
+          tab.insert(tab.end(), hp.begin() + uint64_t(r) * 18, hp.begin() + uint64_t(r) * 18 + 18);
+        }
+        run_pid[r] = it->second;
+      }
+      ria_npat_ = ok ? static_cast<int>(ids.size()) : -1;
+      if (ok) {
+        ria_ptab_.alloc(tab.size());
+        LBM_CUDA(cudaMemcpyAsync(ria_ptab_.get(), tab.data(), tab.size() * 4,
+                                 cudaMemcpyHostToDevice, stream_));
+        DevBuf<uint8_t> dpid(R);
+        LBM_CUDA(cudaMemcpyAsync(dpid.get(), run_pid.data(), R, cudaMemcpyHostToDevice, stream_));
+        ria_nid_.alloc(n_fluid_);
+        k_ria_node_ids<<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
+            ria_run0_.get(), ria_mask_.get(), dpid.get(), n_fluid_, ria_nid_.get());
+        LBM_CHECK_LAUNCH();
+        LBM_CUDA(cudaStreamSynchronize(stream_));
+      }
+    }
     // run lengths -> vectorizable fraction (list_lattice.cpp:228-236)
     std::vector<uint32_t> h(R);
     LBM_CUDA(cudaMemcpyAsync(h.data(), run_start.get(), uint64_t(R) * 4,
@@ -1427,7 +1518,13 @@ class ListEngine final : public Engine {
   DevBuf<uint32_t> ria_run0_;   // run id of node 32w
   DevBuf<uint32_t> ria_mask_;   // run starts within nodes 32w .. 32w+31
   DevBuf<int32_t> ria_gpat_;    // [group][18] inline pattern or kMixedGroup
-  int ria_mode_ = 0;            // 0: run table, 1: group patterns (LBMGPU_RIA_MODE)
+  // odd-step coding: -1 auto (pattern ids when <= 256 distinct run
+  // patterns, else the run table), 0 run table, 1 group patterns, 2 pattern
+  // ids (LBMGPU_RIA_MODE)
+  int ria_mode_ = -1;
+  int ria_npat_ = -1;           // distinct run patterns (-1: more than 256)
+  DevBuf<int32_t> ria_ptab_;    // [pattern id][18]
+  DevBuf<uint8_t> ria_nid_;     // pattern id of every node
   int threads_ = 256;           // CTA size of the sweeps
   bool aos_tile_ = true;        // AoS own-record sweeps through shared-memory tiles
   bool threads_env_ = false;    // threads_ set by LBMGPU_LIST_THREADS

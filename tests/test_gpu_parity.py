@@ -112,6 +112,26 @@ def test_aa_odd_shared_realigned_variant(kind, dims, monkeypatch):
     assert len(set(res)) == 1, [f"{r:016x}" for r in res]
 
 
+@pytest.mark.parametrize("kind,dims", [("channel", (16, 12, 10)), ("blocks", (24, 20, 20)),
+                                       ("pipe", (9, 12, 13))])
+def test_ria_codings_bitwise_equal(kind, dims, monkeypatch):
+    """Every coding of the run-coded odd step -- run table (0), group
+    patterns (1), per-node pattern ids (2, used when <= 256 distinct run
+    patterns), auto (-1) -- is bitwise list-aa-soa."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    ref = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec)
+    ref.load_perturbed(21)
+    ref.advance(PARAMS, FORCE, 10)
+    for mode in ("0", "1", "2", "-1"):
+        monkeypatch.setenv("LBMGPU_RIA_MODE", mode)
+        for name in ("list-aa-ria-soa", "list-aa-pv-soa"):
+            k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+            k.load_perturbed(21)
+            k.advance(PARAMS, FORCE, 10)
+            assert k.fingerprint() == ref.fingerprint(), (mode, name)
+            del k
+
+
 def test_edge_shapes_match_reference(edge_golden):
     """Degenerate and ragged shapes for every kernel (tests/golden/edge.json,
     generated by the reference): 1- and 2-cell periodic axes that wrap onto
