@@ -108,14 +108,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic(kernel_name):
-    """dram bytes per launch for `kernel_name` from the committed ncu summary
-    (profiles/ncu_summary.json, written by tools/ncu_summary.py)."""
+def ncu_traffic(kernel_name, cid=5, dims=None):
+    """dram bytes per launch for `kernel_name` on BASELINE config `cid` from
+    the committed ncu summary (profiles/ncu_summary.json: cfg 5 under
+    "kernels", the list configs under "configs"); None for other boxes."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if dims is not None:
+        return None
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("kernels", {}).get(kernel_name, {}).get("dram_bytes_per_launch")
+        table = d.get("kernels", {}) if cid == 5 else d.get("configs", {}).get(str(cid), {})
+        return table.get(kernel_name, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -341,7 +345,7 @@ def main():
                              "share": st["ms"] / ms if ms else None,
                              "alg_bytes_per_launch": alg, "achieved_GBps": ach}
         if roof is None:
-            traffic = ncu_traffic(name)
+            traffic = ncu_traffic(name, cid, args.dims)
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": ach / hbm, "traffic": traffic, "kernel": name,
                     "alg_bytes_per_launch": alg, "peak_source": peak_src,
