@@ -345,7 +345,9 @@ def main():
                              "share": st["ms"] / ms if ms else None,
                              "alg_bytes_per_launch": alg, "achieved_GBps": ach}
         if roof is None:
-            traffic = ncu_traffic(name, cid, args.dims)
+            # the committed ncu numbers are whole-box launches on one GPU
+            whole = world == 1 and args.virtual_parts <= 1
+            traffic = ncu_traffic(name, cid, args.dims) if whole else None
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": ach / hbm, "traffic": traffic, "kernel": name,
                     "alg_bytes_per_launch": alg, "peak_source": peak_src,
