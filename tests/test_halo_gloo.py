@@ -1,4 +1,5 @@
-"""CPU, world_size 2 (gloo): the multi-GPU z-slab protocol end to end.
+"""CPU, world_size 2 (gloo): the multi-GPU decomposition protocols end to end
+(z-slab AA, z-slab push/pull, list node ranges with local numbering).
 
 Each rank holds its slab in the device layout the CUDA path uses
 ([storage plane][slot][y][x], one ghost plane per side, slots grouped by c_z),
@@ -301,3 +302,150 @@ def test_two_rank_one_step_protocol_gloo(kind, dims, push):
     equal, rel, mass, emass = q.get(timeout=5)
     assert equal, rel
     assert abs(mass - emass) <= 1e-12 * abs(emass)
+
+
+def _rank_main_list(rank, world, port_no, kind, dims, steps, q):
+    """list-aa-soa over node ranges with the per-part local numbering the
+    CUDA path uses (list.cu, 'node-range decomposition'): own slots
+    d * nloc + j, ghost copies of the incoming links' sorted slot lists, the
+    scatter table remapped to local indices; per AA pair phase 0 (after
+    even) s's link slots -> r's ghosts, phase 1 (after odd) back."""
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        port = Port()
+        nx, ny, nz = dims
+        st = port.structure(kind, nx, ny, nz, scatter=True)
+        N = st["n_fluid"]
+        starts = np.asarray(st["starts"], np.int64)
+        adj = st["adj"].reshape(N, 18).astype(np.int64)
+        rng = [(N * p // world, N * (p + 1) // world) for p in range(world)]
+        wp = 1.0 / TAU
+        wm = port.omega_minus(wp)
+
+        def owner(n, d, e):  # entry_owner
+            s0 = starts[d]
+            return e - s0 if s0 <= e < s0 + N else n
+
+        def slot_node(e):
+            dd = max(d for d in range(Q) if e >= starts[d])
+            return e - starts[dd], dd
+
+        def part_of(m):
+            return next(p for p, (a, b) in enumerate(rng) if a <= m < b)
+
+        links = {}  # (r, s) -> sorted global slots
+        for r in range(world):
+            a, b = rng[r]
+            for n in range(a, b):
+                for d in range(1, Q):
+                    e = int(adj[n, d - 1])
+                    s = part_of(owner(n, d, e))
+                    if s != r:
+                        links.setdefault((r, s), set()).add(e)
+        links = {k: sorted(v) for k, v in links.items()}
+        n0, n1 = rng[rank]
+        nloc = n1 - n0
+        gofs, ghosts = {}, []
+        for (r, s), sl in sorted(links.items()):
+            if r == rank:
+                gofs[s] = len(ghosts)
+                ghosts += sl
+
+        def local(e, n):
+            mm, dd = slot_node(e)
+            if n0 <= mm < n1:
+                return dd * nloc + (mm - n0)
+            s = part_of(mm)
+            return Q * nloc + gofs[s] + links[(rank, s)].index(e)
+
+        ladj = np.array([[local(int(adj[n, d - 1]), n) for d in range(1, Q)]
+                         for n in range(n0, n1)], np.int64).reshape(nloc, 18)
+        init = port.perturbed(N, 55)
+        gbuf = np.zeros(int(st["total_slots"]))
+        for n in range(N):
+            for d in range(Q):
+                gbuf[starts[d] + n] = init[n * Q + d]
+        buf = np.zeros(Q * nloc + len(ghosts))
+        for j in range(nloc):
+            for d in range(Q):
+                buf[d * nloc + j] = gbuf[starts[d] + n0 + j]
+        buf[Q * nloc:] = gbuf[np.asarray(ghosts, np.int64)] if ghosts else 0
+        sidx = {k: [slot_node(e)[1] * nloc + (slot_node(e)[0] - n0) for e in sl]
+                for k, sl in links.items() if k[1] == rank}
+
+        def exchange(phase):
+            reqs = []
+            for i, ((r, s), sl) in enumerate(sorted(links.items())):
+                if phase == 0 and s == rank:
+                    t = torch.from_numpy(buf[np.asarray(sidx[(r, s)])].copy())
+                    reqs.append(("s", dist.isend(t, r, tag=i), None, None))
+                if phase == 0 and r == rank:
+                    t = torch.empty(len(sl), dtype=torch.float64)
+                    reqs.append(("r", dist.irecv(t, s, tag=i), t, Q * nloc + gofs[s]))
+                if phase == 1 and r == rank:
+                    g0 = Q * nloc + gofs[s]
+                    t = torch.from_numpy(buf[g0:g0 + len(sl)].copy())
+                    reqs.append(("s", dist.isend(t, s, tag=i), None, None))
+                if phase == 1 and s == rank:
+                    t = torch.empty(len(sl), dtype=torch.float64)
+                    reqs.append(("r", dist.irecv(t, r, tag=i), t, ("scatter", (r, s))))
+            for kind_, rq, t, where in reqs:
+                rq.wait()
+                if kind_ == "r":
+                    if isinstance(where, tuple):
+                        buf[np.asarray(sidx[where[1]])] = t.numpy()
+                    else:
+                        buf[where:where + len(t)] = t.numpy()
+
+        for _ in range(steps // 2):
+            for j in range(nloc):  # even: own slots -> opposite slots
+                f = np.array([buf[d * nloc + j] for d in range(Q)])
+                f = port.collide(f, wp, wm, G)
+                for d in range(Q):
+                    buf[OPP[d] * nloc + j] = f[d]
+            exchange(0)
+            for j in range(nloc):  # odd: gather column opp(d), scatter column d
+                f = np.empty(Q)
+                f[0] = buf[j]
+                for d in range(1, Q):
+                    f[d] = buf[ladj[j, OPP[d] - 1]]
+                f = port.collide(f, wp, wm, G)
+                buf[j] = f[0]
+                for d in range(1, Q):
+                    buf[ladj[j, d - 1]] = f[d]
+            exchange(1)
+        rows = {n0 + j: [buf[d * nloc + j] for d in range(Q)] for j in range(nloc)}
+        out = [None] * world
+        dist.all_gather_object(out, rows)
+        if rank == 0:
+            full = np.zeros(N * Q)
+            for part in out:
+                for kk, v in part.items():
+                    full[kk * Q:(kk + 1) * Q] = v
+            expect, _ = port.run("half", kind, nx, ny, nz, steps, wp, g=G, init=init)
+            q.put((bool(np.array_equal(full, expect)), float(port.max_rel_diff(full, expect))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,dims", [("channel", (6, 5, 8)), ("blocks", (8, 8, 8))])
+def test_two_rank_list_node_range_protocol_gloo(kind, dims):
+    """list-aa-soa node-range decomposition with local numbering on 2 gloo
+    ranks (blocks: the x wrap makes both part boundaries active), bitwise
+    equal to the oracle's full-domain half-way stepper."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_rank_main_list, args=(r, 2, port_no, kind, dims, 4, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    equal, rel = q.get(timeout=5)
+    assert equal, rel
