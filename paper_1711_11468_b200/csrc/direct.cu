@@ -239,8 +239,27 @@ __global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
   collide_node_pass<SOA, false>(a, c, n);
 }
 
+// SoA AA sweeps: lanes 0..18 of a warp prefetch into L2 the two 128-byte
+// lines of slot `lane` of the 32 nodes `a.pf` nodes ahead (blocks dispatch in
+// index order, so that warp runs about one wave later; the odd step's
+// +-1-row gathers hit lines the neighbouring rows' warps prefetched).
+__device__ __forceinline__ void aa_prefetch(const DirectArgs& a) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (a.pf == 0 || lane >= kQ) return;
+  const uint32_t m = a.node0 + blockIdx.x * blockDim.x + (threadIdx.x & ~31u) + a.pf;
+  if (m >= a.node0 + a.count) return;
+  const uint32_t z = a.fdP.div(m);
+  const uint32_t r = m - z * a.P;
+  const uint32_t y = a.fdx.div(r);
+  const double* p =
+      a.dst + (uint64_t(z + a.zoff) * kQ + lane) * a.P + uint64_t(y) * a.nx + (r - y * a.nx);
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
+}
+
 template <bool SOA, bool CS, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
+  if (SOA) aa_prefetch(a);
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
@@ -249,6 +268,7 @@ __global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) 
 
 template <bool SOA, bool CS, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
+  if (SOA) aa_prefetch(a);
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
@@ -943,6 +963,7 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_ODD_SX")) odd_sx_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AOS_BAND")) aos_band_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_AA_PF_WAVES")) aa_pf_waves_ = std::atof(e);
       if (aa_threads_ < 32 || aa_threads_ > 256 || aa_threads_ % 32)
         throw ConfigError("LBMGPU_AA_THREADS must be a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
@@ -1105,6 +1126,7 @@ class DirectEngine final : public Engine {
                                                 : (long long)std::min(ny_, nz_) - 2;
     a.d2 = D * D;
     a.band = 0;
+    a.pf = 0;
     for (int d = 0; d < kQ; ++d) {
       const long long dn = -(long long)cz(d) * (long long)P_ - (long long)cy(d) * nx_ - cx(d);
       a.odd_off[d] = desc_.soa
@@ -1175,6 +1197,9 @@ class DirectEngine final : public Engine {
           : launch(name, k_full_aa_even<true, true>, a, stream_);
       return;
     }
+    DirectArgs ap = a;
+    ap.pf = static_cast<uint32_t>(aa_pf_waves_ * sm_count_ * 16 * 32);
+    const DirectArgs& a2 = ap;
     if (odd && odd_sx_ && a.nx % kSxThreads == 0 && a.node0 % kSxThreads == 0 &&
         a.count % kSxThreads == 0) {
       odd_sx_ == 4 ? launch(name, k_full_aa_odd_sx<4>, a, stream_, kSxThreads)
@@ -1183,8 +1208,8 @@ class DirectEngine final : public Engine {
     }
     switch (minb_) {
       case 2:
-        odd ? launch(name, k_full_aa_odd<true, false, 2>, a, stream_, aa_threads_)
-            : launch(name, k_full_aa_even<true, false, 2>, a, stream_, aa_threads_);
+        odd ? launch(name, k_full_aa_odd<true, false, 2>, a2, stream_, aa_threads_)
+            : launch(name, k_full_aa_even<true, false, 2>, a2, stream_, aa_threads_);
         break;
       case 3:
         odd ? launch(name, k_full_aa_odd<true, false, 3>, a, stream_, aa_threads_)
@@ -1634,6 +1659,7 @@ class DirectEngine final : public Engine {
   // AoS push / pull sweeps: y-band height (0/1: plain order); cfg-5-sized
   // box: push 959 -> 1507 GB/s, pull 2014 -> 2115 at 16
   int aos_band_ = 16;
+  double aa_pf_waves_ = 0.0;  // SoA AA sweeps: L2 prefetch distance in waves (0 = off)
   int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
   DevBuf<unsigned> barrier_;            // grid barrier {count, generation}

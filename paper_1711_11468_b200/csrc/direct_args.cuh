@@ -33,6 +33,9 @@ struct DirectArgs {
   // before y inside a band, so the z +- 1 rows whose records a row's
   // gathers touch are processed close in time (L2 reuse); 0 = plain order.
   uint32_t band;
+  // AA sweeps: L2 prefetch of the 19 slot lines of the warp `pf` nodes ahead
+  // (one resident-grid wave = SMs x warps/SM x 32); 0 = off
+  uint32_t pf;
 };
 
 // Solid flag of own node (x, y, own-plane z) without touching memory for the
