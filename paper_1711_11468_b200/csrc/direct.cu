@@ -308,6 +308,94 @@ __global__ void __launch_bounds__(kAosTile) k_full_aos_tile(const DirectArgs a) 
   aos_tile_store<kAosTile>(g, sh, cnt);
 }
 
+// AoS pull through 3-D halo tiles.  A block owns a 16 x 4 x 4 (x, y, z) tile
+// of nodes; the 6 x 6 source rows around it, each as 20 whole records
+// (x0-2 .. x0+17, i.e. 16-byte aligned), arrive by 1-D TMA bulk copies into
+// shared memory (rows wrapped on y and z, row segments split at the periodic
+// x wrap), every node gathers its 19 values there, and the tile's own
+// destination records leave by 16 bulk stores after the block barrier.  Each
+// source record is fetched by the ~2.25 tiles around it instead of as 19
+// separate 32-byte sectors; destination records are written whole.  Needs a
+// single part with nx % 16 == 0, ny % 4 == 0, nz % 4 == 0.
+constexpr int kPtX = 16;
+constexpr int kPtW = kPtX + 4;                           // records per halo row
+constexpr uint32_t kPtRowBytes = kPtW * kQ * 8;         // 3040
+template <int kPtY, int kPtZ>
+constexpr size_t pt_smem() {
+  return size_t((kPtY + 2) * (kPtZ + 2)) * kPtRowBytes + 16;
+}
+template <bool COLLIDE, int kPtY, int kPtZ>
+__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(const DirectArgs a) {
+  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);  // halo rows
+  extern __shared__ __align__(128) unsigned char pt_smem[];
+  double* sh = reinterpret_cast<double*>(pt_smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
+  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
+  const uint32_t b = blockIdx.x;
+  const uint32_t x0 = (b % tilesx) * kPtX;
+  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
+  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
+  const uint64_t nx = a.nx;
+  auto rec = [&](uint32_t zs, uint32_t y, uint32_t x) {  // record pointer (AoS)
+    return a.src + ((uint64_t(zs) * a.ny + y) * nx + x) * kQ;
+  };
+  const uint32_t t = threadIdx.x;
+  if (t == 0) {
+    tma::mbar_init(bar, 1);
+    tma::fence_barrier_init();
+  }
+  __syncthreads();
+  // warp 0 issues the row copies: lane l handles halo rows l and l + 32
+  if (t < 32) {
+    if (t == 0) tma::mbar_arrive_expect_tx(bar, kPtRows * kPtRowBytes);
+    __syncwarp();
+    for (uint32_t row = t; row < uint32_t(kPtRows); row += 32) {
+      const uint32_t hy = row % (kPtY + 2), hz = row / (kPtY + 2);
+      const uint32_t y = (y0 + a.ny + hy - 1) % a.ny;
+      const uint32_t z = (z0 + a.nzl + hz - 1) % a.nzl;  // single part: zwrap
+      double* dst = sh + size_t(row) * kPtW * kQ;
+      if (x0 >= 2 && x0 + kPtX + 2 <= nx) {
+        tma::bulk_g2s(dst, rec(z, y, x0 - 2), kPtRowBytes, bar);
+      } else {  // split at the x wrap: pieces of records [x0-2, x0+18) mod nx
+        uint32_t h = 0;
+        while (h < uint32_t(kPtW)) {
+          const uint32_t x = uint32_t((int64_t(x0) - 2 + h + nx) % nx);
+          const uint32_t len = min(uint32_t(kPtW) - h, uint32_t(nx - x));
+          tma::bulk_g2s(dst + size_t(h) * kQ, rec(z, y, x), len * kQ * 8, bar);
+          h += len;
+        }
+      }
+    }
+  }
+  const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
+  const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
+  const bool solid = solid_node(a, x0 + tx, y0 + ty, z0 + tz, n);
+  tma::mbar_wait(bar, 0);
+  auto at = [&](int hx, int hy, int hz) {
+    return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
+  };
+  double q[kQ];
+  q[0] = at(tx + 2, ty + 1, tz + 1)[dslot(0)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(d)];
+  if (COLLIDE && !solid) collide(q, a.trt);
+  __syncthreads();  // every gather done: the centre records may be overwritten
+  double* own = at(tx + 2, ty + 1, tz + 1);
+  own[dslot(0)] = q[0];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) own[solid ? dslot(opp(d)) : dslot(d)] = q[d];
+  tma::fence_proxy_async();
+  __syncthreads();
+  if (t < uint32_t(kPtY * kPtZ)) {  // one bulk store per centre row
+    const uint32_t ry = t % kPtY, rz = t / kPtY;
+    double* g = a.dst + ((uint64_t(z0 + rz) * a.ny + (y0 + ry)) * nx + x0) * kQ;
+    tma::bulk_s2g(g, at(2, ry + 1, rz + 1), kPtX * kQ * 8);
+    tma::bulk_commit();
+    tma::bulk_wait_read0();
+  }
+}
+
 // Odd step with the x-shifted scatters realigned through shared memory.
 // In k_full_aa_odd every warp stores the 10 directions with c_x != 0 one
 // element off its own x range, so each such store instruction writes two
@@ -963,6 +1051,7 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_ODD_SX")) odd_sx_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AOS_BAND")) aos_band_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_PULL_TILE")) pull_tile_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AA_PF_WAVES")) aa_pf_waves_ = std::atof(e);
       if (aa_threads_ < 32 || aa_threads_ > 256 || aa_threads_ % 32)
         throw ConfigError("LBMGPU_AA_THREADS must be a multiple of 32 in [32, 256]");
@@ -1135,6 +1224,19 @@ class DirectEngine final : public Engine {
                          : dn * kQ + dslot(opp(d));
     }
     return a;
+  }
+
+  template <int TY, int TZ>
+  void pull_aos_tile3d(const DirectArgs& a, bool last, const char* name) {
+    const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
+    auto kern = last ? k_full_pull_aos_tile3d<false, TY, TZ> : k_full_pull_aos_tile3d<true, TY, TZ>;
+    constexpr size_t smem = pt_smem<TY, TZ>();
+    LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    const int tok = stats_.begin(name, stream_);
+    kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(a);
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, stream_);
   }
 
   // AoS gather/scatter sweep over a whole part in y-band order (see
@@ -1369,6 +1471,13 @@ class DirectEngine final : public Engine {
           else
             cs ? launch("full_pull_soa", k_full_pull<true, true, true>, a, stream_)
                : launch("full_pull_soa", k_full_pull<true, true, false>, a, stream_);
+        } else if (aos_tile_ && pull_tile_ && nparts_ == 1 && nx_ % kPtX == 0 &&
+                   ny_ % pull_tile_ == 0 && nz_ % pull_tile_ == 0) {
+          const char* name = last ? "full_pull_stream_aos" : "full_pull_aos";
+          switch (pull_tile_) {
+            case 2: pull_aos_tile3d<2, 2>(a, last, name); break;
+            default: pull_aos_tile3d<4, 4>(a, last, name);
+          }
         } else {
           if (last)
             launch("full_pull_stream_aos", k_full_pull<false, false, false>, banded(a), stream_);
@@ -1659,6 +1768,7 @@ class DirectEngine final : public Engine {
   // AoS push / pull sweeps: y-band height (0/1: plain order); cfg-5-sized
   // box: push 959 -> 1507 GB/s, pull 2014 -> 2115 at 16
   int aos_band_ = 16;
+  int pull_tile_ = 4;  // AoS pull halo tiles: 16 x T x T nodes (0: per-node kernel)
   double aa_pf_waves_ = 0.0;  // SoA AA sweeps: L2 prefetch distance in waves (0 = off)
   int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
