@@ -324,20 +324,16 @@ template <int kPtY, int kPtZ>
 constexpr size_t pt_smem() {
   return size_t((kPtY + 2) * (kPtZ + 2)) * kPtRowBytes + 16;
 }
-template <bool COLLIDE, int kPtY, int kPtZ>
-__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(const DirectArgs a) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);  // halo rows
-  extern __shared__ __align__(128) unsigned char pt_smem[];
-  double* sh = reinterpret_cast<double*>(pt_smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
-  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
-  const uint32_t b = blockIdx.x;
-  const uint32_t x0 = (b % tilesx) * kPtX;
-  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
-  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
+// Halo rows of a 16 x TY x TZ tile at (x0, y0, z0) from AoS grid `src` into
+// shared memory `sh` (block-wide; ends with the copies in flight on `bar`).
+template <int kPtY, int kPtZ>
+__device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* src, double* sh,
+                                             uint64_t* bar, uint32_t x0, uint32_t y0,
+                                             uint32_t z0) {
+  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
   const uint64_t nx = a.nx;
   auto rec = [&](uint32_t zs, uint32_t y, uint32_t x) {  // record pointer (AoS)
-    return a.src + ((uint64_t(zs) * a.ny + y) * nx + x) * kQ;
+    return src + ((uint64_t(zs) * a.ny + y) * nx + x) * kQ;
   };
   const uint32_t t = threadIdx.x;
   if (t == 0) {
@@ -367,6 +363,22 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(con
       }
     }
   }
+}
+
+template <bool COLLIDE, int kPtY, int kPtZ>
+__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(const DirectArgs a) {
+  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);  // halo rows
+  extern __shared__ __align__(128) unsigned char pt_smem[];
+  double* sh = reinterpret_cast<double*>(pt_smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
+  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
+  const uint32_t b = blockIdx.x;
+  const uint32_t x0 = (b % tilesx) * kPtX;
+  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
+  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
+  const uint64_t nx = a.nx;
+  const uint32_t t = threadIdx.x;
+  pt_load_halo<kPtY, kPtZ>(a, a.src, sh, bar, x0, y0, z0);
   const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
   const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
   const bool solid = solid_node(a, x0 + tx, y0 + ty, z0 + tz, n);
@@ -394,6 +406,46 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(con
     tma::bulk_commit();
     tma::bulk_wait_read0();
   }
+}
+
+// AoS AA odd step with the gathers through the same 3-D halo tiles: the
+// tile's source rows arrive by TMA as whole records, each node reads its 18
+// neighbour values (x - c_d, opp d) in shared memory, and writes them back to
+// global memory slot by slot (every slot is read and written by exactly one
+// node in this sub-step, so the other, possibly stale, slots of the staged
+// records are never used).
+template <int kPtY, int kPtZ>
+__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(const DirectArgs a) {
+  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
+  extern __shared__ __align__(128) unsigned char pt_smem[];
+  double* sh = reinterpret_cast<double*>(pt_smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
+  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
+  const uint32_t b = blockIdx.x;
+  const uint32_t x0 = (b % tilesx) * kPtX;
+  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
+  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
+  const uint32_t t = threadIdx.x;
+  pt_load_halo<kPtY, kPtZ>(a, a.dst, sh, bar, x0, y0, z0);
+  const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
+  const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
+  Coords c;
+  decode_node(a, n, c);
+  const bool solid = solid_node(a, c.x, c.y, c.z, n);
+  tma::mbar_wait(bar, 0);
+  if (solid) return;
+  auto at = [&](int hx, int hy, int hz) {
+    return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
+  };
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d)
+    q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(opp(d))];
+  collide(q, a.trt);
+  const Idx<false> I{a.P, a.nx, a.ny};
+#pragma unroll
+  for (int d = 0; d < kQ; ++d)
+    a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])] = q[opp(d)];
 }
 
 // Odd step with the x-shifted scatters realigned through shared memory.
@@ -1052,6 +1104,7 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AOS_BAND")) aos_band_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_PULL_TILE")) pull_tile_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_ODD_TILE")) odd_tile_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AA_PF_WAVES")) aa_pf_waves_ = std::atof(e);
       if (aa_threads_ < 32 || aa_threads_ > 256 || aa_threads_ % 32)
         throw ConfigError("LBMGPU_AA_THREADS must be a multiple of 32 in [32, 256]");
@@ -1502,7 +1555,20 @@ class DirectEngine final : public Engine {
                     : launch("full_aa_even_aos", k_full_aa_even<false, false>, a, stream_);
           // (y-band order measured slower for the AA odd step: 1922 -> 1103
           // GB/s at band 16, although it halves the DRAM traffic)
-          launch("full_aa_odd_aos", k_full_aa_odd<false, false>, a, stream_);
+          if (aos_tile_ && odd_tile_ && nx_ % kPtX == 0 && ny_ % 4 == 0 && nz_ % 4 == 0) {
+            const unsigned grid =
+                static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / 4) * (nz_ / 4));
+            auto kern = k_full_aa_odd_aos_tile3d<4, 4>;
+            constexpr size_t smem = pt_smem<4, 4>();
+            LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            const int tok = stats_.begin("full_aa_odd_aos", stream_);
+            kern<<<grid, kPtX * 16, smem, stream_>>>(a);
+            LBM_CHECK_LAUNCH();
+            stats_.end(tok, stream_);
+          } else {
+            launch("full_aa_odd_aos", k_full_aa_odd<false, false>, a, stream_);
+          }
         }
       } else {
         aa_pair_slabs(t);
@@ -1769,6 +1835,7 @@ class DirectEngine final : public Engine {
   // box: push 959 -> 1507 GB/s, pull 2014 -> 2115 at 16
   int aos_band_ = 16;
   int pull_tile_ = 4;  // AoS pull halo tiles: 16 x T x T nodes (0: per-node kernel)
+  bool odd_tile_ = true;  // AoS AA odd step: gathers through 16 x 4 x 4 halo tiles
   double aa_pf_waves_ = 0.0;  // SoA AA sweeps: L2 prefetch distance in waves (0 = off)
   int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold

@@ -155,6 +155,25 @@ def test_aos_pull_halo_tiles_bitwise(kind, dims, monkeypatch):
     assert abs(res[0][1] - res[2][1]) <= 1e-12 * abs(res[2][1])
 
 
+@pytest.mark.parametrize("kind,dims", [("channel", (16, 8, 8)), ("channel", (32, 12, 8)),
+                                       ("blocks", (32, 16, 16)), ("slit", (48, 4, 12)),
+                                       ("pipe", (16, 12, 12))])
+def test_aos_aa_odd_halo_tiles_bitwise(kind, dims, monkeypatch):
+    """aa-aos with the odd step's gathers through 3-D halo tiles equals the
+    per-node AoS odd step and aa-soa bit for bit."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    res = []
+    for name, tile in (("aa-aos", "1"), ("aa-aos", "0"), ("aa-soa", "1")):
+        monkeypatch.setenv("LBMGPU_ODD_TILE", tile)
+        k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        k.load_perturbed(19)
+        k.advance(PARAMS, FORCE, 6)
+        res.append(k.fingerprint())
+        del k
+    assert len(set(res)) == 1, [f"{r:016x}" for r in res]
+
+
 def test_edge_shapes_match_reference(edge_golden):
     """Degenerate and ragged shapes for every kernel (tests/golden/edge.json,
     generated by the reference): 1- and 2-cell periodic axes that wrap onto
