@@ -20,7 +20,16 @@ struct lbmgpu_ctx {
   GeomSpec geom;
   DevBuf<double> rho, u, uprev;  // steady-state scratch
   cudaStream_t copy = nullptr;   // host<->device staging copies
+  // staging buffers and events of pipelined(), kept across calls (a
+  // load/snapshot of a small lattice would otherwise pay for the
+  // allocations more than for the transfer)
+  DevBuf<double> stage[2];
+  cudaEvent_t ready[2] = {}, freed[2] = {};
   ~lbmgpu_ctx() {
+    for (int b = 0; b < 2; ++b) {
+      if (ready[b]) cudaEventDestroy(ready[b]);
+      if (freed[b]) cudaEventDestroy(freed[b]);
+    }
     if (copy) cudaStreamDestroy(copy);
   }
 };
@@ -133,21 +142,21 @@ void pipelined(lbmgpu_ctx* c, double* host, uint64_t rows, bool to_host, Dev dev
   if (rows == 0) return;
   if (!c->copy) LBM_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   const uint64_t chunk = std::min(rows, kChunkNodes);
-  DevBuf<double> st[2];
-  st[0].alloc(chunk * kQ);
-  if (rows > chunk) st[1].alloc(chunk * kQ);
-  cudaStream_t s = c->eng->stream(), cs = c->copy;
-  cudaEvent_t ready[2], freed[2];
-  for (int b = 0; b < 2; ++b) {
-    LBM_CUDA(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
-    LBM_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+  const int nb = rows > chunk ? 2 : 1;
+  for (int b = 0; b < nb; ++b) {
+    if (c->stage[b].size() < chunk * kQ) c->stage[b].alloc(chunk * kQ);
+    if (!c->ready[b]) LBM_CUDA(cudaEventCreateWithFlags(&c->ready[b], cudaEventDisableTiming));
+    if (!c->freed[b]) LBM_CUDA(cudaEventCreateWithFlags(&c->freed[b], cudaEventDisableTiming));
   }
+  cudaStream_t s = c->eng->stream(), cs = c->copy;
+  cudaEvent_t* ready = c->ready;
+  cudaEvent_t* freed = c->freed;
   try {
     uint64_t k = 0;
     for (uint64_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
       const int b = static_cast<int>(k & 1);
       const uint64_t n = std::min(chunk, rows - r0);
-      double* sb = st[b].get();
+      double* sb = c->stage[b].get();
       if (to_host) {
         if (k >= 2) LBM_CUDA(cudaStreamWaitEvent(s, freed[b], 0));
         dev(r0, n, sb, true);
@@ -156,6 +165,8 @@ void pipelined(lbmgpu_ctx* c, double* host, uint64_t rows, bool to_host, Dev dev
         LBM_CUDA(cudaMemcpyAsync(host + r0 * kQ, sb, n * kQ * 8, cudaMemcpyDeviceToHost, cs));
         LBM_CUDA(cudaEventRecord(freed[b], cs));
       } else {
+        // (every call ends with both streams synchronised, so a buffer's
+        // first use in a call needs no wait)
         if (k >= 2) LBM_CUDA(cudaStreamWaitEvent(cs, freed[b], 0));
         LBM_CUDA(cudaMemcpyAsync(sb, host + r0 * kQ, n * kQ * 8, cudaMemcpyHostToDevice, cs));
         LBM_CUDA(cudaEventRecord(ready[b], cs));
@@ -169,15 +180,7 @@ void pipelined(lbmgpu_ctx* c, double* host, uint64_t rows, bool to_host, Dev dev
   } catch (...) {
     cudaStreamSynchronize(cs);
     cudaStreamSynchronize(s);
-    for (int b = 0; b < 2; ++b) {
-      cudaEventDestroy(ready[b]);
-      cudaEventDestroy(freed[b]);
-    }
     throw;
-  }
-  for (int b = 0; b < 2; ++b) {
-    cudaEventDestroy(ready[b]);
-    cudaEventDestroy(freed[b]);
   }
 }
 
