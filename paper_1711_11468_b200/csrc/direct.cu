@@ -30,781 +30,12 @@
 #include "tma.cuh"
 #include "lbm.hpp"
 
+#include "direct_node.cuh"
+#include "direct_aos.cuh"
+#include "direct_fused.cuh"
+#include "direct_experimental.cuh"
+
 namespace lbmgpu {
-
-template <bool SOA>
-struct Idx {
-  uint64_t P;
-  uint32_t nx, ny;
-  __device__ __forceinline__ uint64_t operator()(uint32_t zs, int slot,
-                                                 uint32_t y, uint32_t x) const {
-    if (SOA)
-      return (uint64_t(zs) * kQ + slot) * P + uint64_t(y) * nx + x;
-    return ((uint64_t(zs) * ny + y) * nx + x) * kQ + slot;
-  }
-};
-
-struct Coords {
-  uint32_t x, y, z;        // own-plane coordinates
-  uint32_t X[3], Y[3];     // wrapped x-1,x,x+1 / y-1,y,y+1
-  uint32_t Z[3];           // storage planes of z-1, z, z+1
-};
-
-// own-node id n -> coordinates, wrapped x/y neighbours and storage planes
-__device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coords& c) {
-  const uint32_t z = a.fdP.div(n);
-  const uint32_t r = n - z * a.P;
-  const uint32_t y = a.fdx.div(r);
-  const uint32_t x = r - y * a.nx;
-  c.x = x;
-  c.y = y;
-  c.z = z;
-  c.X[0] = x == 0 ? a.nx - 1 : x - 1;
-  c.X[1] = x;
-  c.X[2] = x + 1 == a.nx ? 0 : x + 1;
-  c.Y[0] = y == 0 ? a.ny - 1 : y - 1;
-  c.Y[1] = y;
-  c.Y[2] = y + 1 == a.ny ? 0 : y + 1;
-  const uint32_t zs = z + a.zoff;
-  if (a.zwrap) {
-    c.Z[0] = z == 0 ? a.nzl - 1 : z - 1;
-    c.Z[2] = z + 1 == a.nzl ? 0 : z + 1;
-  } else {
-    c.Z[0] = zs - 1;
-    c.Z[2] = zs + 1;
-  }
-  c.Z[1] = zs;
-}
-
-__device__ __forceinline__ bool decode(const DirectArgs& a, Coords& c,
-                                       uint32_t& n) {
-  n = a.node0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= a.node0 + a.count) return false;
-  if (a.band) {  // y-band order (a whole part: node0 == 0, ny % band == 0)
-    const uint32_t x = n % a.nx, r = n / a.nx;
-    const uint32_t per_band = a.band * a.nzl;
-    const uint32_t b = r / per_band, t = r - b * per_band;
-    const uint32_t z = t / a.band;
-    n = (z * a.ny + b * a.band + (t - z * a.band)) * a.nx + x;
-  }
-  decode_node(a, n, c);
-  return true;
-}
-
-// Loads of lattice data: plain (L1-cached) in the one-sweep-per-launch
-// kernels; L2-only (ld.global.cg) in the fused multi-step kernel, whose later
-// sweeps read lines other SMs wrote after a grid barrier.
-template <bool CG>
-__device__ __forceinline__ double ldp(const double* p) {
-  if (CG) return __ldcg(p);
-  return *p;
-}
-template <bool CS>
-__device__ __forceinline__ void st(double* p, double v) {
-  if (CS)
-    __stcs(p, v);
-  else
-    *p = v;
-}
-
-// ---- per-node bodies (shared by the sweep kernels and the fused kernel) ----
-// kernels_full_os.cpp:56-89 + full_lattice.cpp:42-56 (push, correction on dst)
-template <bool SOA, bool CS, bool CG>
-__device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, uint32_t n) {
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double q[kQ];
-  const uint32_t tm = a.tmask ? a.tmask[n] : 0u;
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.src + I(c.Z[1], dslot(d), c.y, c.x));
-  if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
-  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) {
-    const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
-    // solid target: the precomputed mask, else the neighbour's flag from L1
-    // (measured faster than the arithmetic test here: cfg 1 fused 15.5k vs
-    // 13.9k MFLUP/s)
-    const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
-    const bool ts = a.tmask ? ((tm >> d) & 1u) != 0 : a.flags[tn] != 0;
-    const int s = ts ? dslot(opp(d)) : dslot(d);
-    st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
-  }
-}
-
-// kernels_full_os.cpp:56-89 (PULL); COLLIDE=false is the stream-only pass
-template <bool SOA, bool COLLIDE, bool CS, bool CG>
-__device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, uint32_t n) {
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double q[kQ];
-  q[0] = ldp<CG>(a.src + I(c.Z[1], dslot(0), c.y, c.x));
-#pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    q[d] = ldp<CG>(a.src + I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)]));
-  const bool solid = solid_node(a, c.x, c.y, c.z, n);
-  if (COLLIDE && !solid) collide(q, a.trt);
-  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) {
-    const int s = solid ? dslot(opp(d)) : dslot(d);
-    st<CS>(a.dst + I(c.Z[1], s, c.y, c.x), q[d]);
-  }
-}
-
-// collide_pass (kernels_full_os.cpp:149-159): fluid nodes, in place on dst
-template <bool SOA, bool CG>
-__device__ __forceinline__ void collide_node_pass(const DirectArgs& a, const Coords& c, uint32_t n) {
-  if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.dst + I(c.Z[1], dslot(d), c.y, c.x));
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) a.dst[I(c.Z[1], dslot(d), c.y, c.x)] = q[d];
-}
-
-// AA pattern (kernels_full_aa.cpp:46-94), corrections dropped.  Built-in
-// geometries test solidity arithmetically (no flag load ahead of the PDF
-// loads; solid nodes issue no loads at all).
-template <bool SOA, bool CS, bool CG>
-__device__ __forceinline__ void aa_even_node(const DirectArgs& a, const Coords& c, uint32_t n) {
-  if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double* buf = a.dst;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(buf + I(c.Z[1], dslot(d), c.y, c.x));
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) st<CS>(buf + I(c.Z[1], dslot(opp(d)), c.y, c.x), q[d]);
-}
-
-template <bool SOA, bool CS, bool CG>
-__device__ __forceinline__ void aa_odd_node(const DirectArgs& a, const Coords& c, uint32_t n) {
-  if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
-  double* buf = a.dst;
-  // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
-  // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
-  // per direction serves both the load and the store.
-  double q[kQ];
-  // Warp-uniform fast path: no active lane touches a wrapped neighbour, so
-  // every address is the own slot-0 element plus a per-direction constant
-  // (recomputed for the stores: only `own` stays live across the collision).
-  const bool inner = c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u &&
-                     (!a.zwrap || c.z - 1u < a.nzl - 2u);
-  if (__all_sync(__activemask(), inner)) {
-    double* own = buf + I(c.Z[1], 0, c.y, c.x);
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(own + a.odd_off[d]);
-    collide(q, a.trt);
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) st<CS>(own + a.odd_off[d], q[opp(d)]);
-    return;
-  }
-  double* p[kQ];
-  p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(p[d]);
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
-}
-
-// ---- one sweep per launch, one node per thread ------------------------------
-template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_full_push(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  push_node<SOA, CS, false>(a, c, n);
-}
-
-template <bool SOA, bool COLLIDE, bool CS>
-__global__ void __launch_bounds__(256) k_full_pull(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  pull_node<SOA, COLLIDE, CS, false>(a, c, n);
-}
-
-template <bool SOA>
-__global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  collide_node_pass<SOA, false>(a, c, n);
-}
-
-// SoA AA sweeps: lanes 0..18 of a warp prefetch into L2 the two 128-byte
-// lines of slot `lane` of the 32 nodes `a.pf` nodes ahead (blocks dispatch in
-// index order, so that warp runs about one wave later; the odd step's
-// +-1-row gathers hit lines the neighbouring rows' warps prefetched).
-__device__ __forceinline__ void aa_prefetch(const DirectArgs& a) {
-  const uint32_t lane = threadIdx.x & 31;
-  if (a.pf == 0 || lane >= kQ) return;
-  const uint32_t m = a.node0 + blockIdx.x * blockDim.x + (threadIdx.x & ~31u) + a.pf;
-  if (m >= a.node0 + a.count) return;
-  const uint32_t z = a.fdP.div(m);
-  const uint32_t r = m - z * a.P;
-  const uint32_t y = a.fdx.div(r);
-  const double* p =
-      a.dst + (uint64_t(z + a.zoff) * kQ + lane) * a.P + uint64_t(y) * a.nx + (r - y * a.nx);
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
-}
-
-template <bool SOA, bool CS, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
-  if (SOA) aa_prefetch(a);
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  aa_even_node<SOA, CS, false>(a, c, n);
-}
-
-template <bool SOA, bool CS, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
-  if (SOA) aa_prefetch(a);
-  Coords c;
-  uint32_t n;
-  if (!decode(a, c, n)) return;
-  aa_odd_node<SOA, CS, false>(a, c, n);
-}
-
-// AoS own-record sweeps (AA even: own slots -> opposite slots; the pull's
-// collide pass: in place) on a tile of kAosTile consecutive nodes staged
-// through shared memory.  A thread's record lives at sh[t*19 .. t*19+18] and
-// only that thread touches it between the barriers; solid records are
-// written back unchanged.  Same per-node arithmetic as aa_even_node /
-// collide_node_pass.
-constexpr int kAosTile = 128;
-template <bool EVEN>
-__global__ void __launch_bounds__(kAosTile) k_full_aos_tile(const DirectArgs a) {
-  __shared__ __align__(128) double sh[kAosTile * kQ];
-  __shared__ __align__(8) uint64_t bar;
-  const uint32_t n0 = a.node0 + blockIdx.x * kAosTile;
-  const uint32_t cnt = min(uint32_t(kAosTile), a.node0 + a.count - n0);
-  // record of own node n: storage plane z + zoff, i.e. n + zoff * P
-  double* g = a.dst + (uint64_t(n0) + uint64_t(a.zoff) * a.P) * kQ;
-  aos_tile_load<kAosTile>(sh, g, cnt, &bar);
-  if (threadIdx.x < cnt) {
-    const uint32_t n = n0 + threadIdx.x;
-    Coords c;
-    decode_node(a, n, c);
-    if (!solid_node(a, c.x, c.y, c.z, n)) {
-      double* r = sh + threadIdx.x * kQ;
-      double q[kQ];
-#pragma unroll
-      for (int d = 0; d < kQ; ++d) q[d] = r[dslot(d)];
-      collide(q, a.trt);
-#pragma unroll
-      for (int d = 0; d < kQ; ++d) r[dslot(EVEN ? opp(d) : d)] = q[d];
-    }
-  }
-  aos_tile_store<kAosTile>(g, sh, cnt);
-}
-
-// AoS pull through 3-D halo tiles.  A block owns a 16 x 4 x 4 (x, y, z) tile
-// of nodes; the 6 x 6 source rows around it, each as 20 whole records
-// (x0-2 .. x0+17, i.e. 16-byte aligned), arrive by 1-D TMA bulk copies into
-// shared memory (rows wrapped on y and z, row segments split at the periodic
-// x wrap), every node gathers its 19 values there, and the tile's own
-// destination records leave by 16 bulk stores after the block barrier.  Each
-// source record is fetched by the ~2.25 tiles around it instead of as 19
-// separate 32-byte sectors; destination records are written whole.  Needs a
-// single part with nx % 16 == 0, ny % 4 == 0, nz % 4 == 0.
-constexpr int kPtX = 16;
-constexpr int kPtW = kPtX + 4;                           // records per halo row
-constexpr uint32_t kPtRowBytes = kPtW * kQ * 8;         // 3040
-template <int kPtY, int kPtZ>
-constexpr size_t pt_smem() {
-  return size_t((kPtY + 2) * (kPtZ + 2)) * kPtRowBytes + 16;
-}
-// Halo rows of a 16 x TY x TZ tile at (x0, y0, z0) from AoS grid `src` into
-// shared memory `sh` (block-wide; ends with the copies in flight on `bar`).
-template <int kPtY, int kPtZ>
-__device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* src, double* sh,
-                                             uint64_t* bar, uint32_t x0, uint32_t y0,
-                                             uint32_t z0) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
-  const uint64_t nx = a.nx;
-  auto rec = [&](uint32_t zs, uint32_t y, uint32_t x) {  // record pointer (AoS)
-    return src + ((uint64_t(zs) * a.ny + y) * nx + x) * kQ;
-  };
-  const uint32_t t = threadIdx.x;
-  if (t == 0) {
-    tma::mbar_init(bar, 1);
-    tma::fence_barrier_init();
-  }
-  __syncthreads();
-  // warp 0 issues the row copies: lane l handles halo rows l and l + 32
-  if (t < 32) {
-    if (t == 0) tma::mbar_arrive_expect_tx(bar, kPtRows * kPtRowBytes);
-    __syncwarp();
-    for (uint32_t row = t; row < uint32_t(kPtRows); row += 32) {
-      const uint32_t hy = row % (kPtY + 2), hz = row / (kPtY + 2);
-      const uint32_t y = (y0 + a.ny + hy - 1) % a.ny;
-      const uint32_t z = (z0 + a.nzl + hz - 1) % a.nzl;  // single part: zwrap
-      double* dst = sh + size_t(row) * kPtW * kQ;
-      if (x0 >= 2 && x0 + kPtX + 2 <= nx) {
-        tma::bulk_g2s(dst, rec(z, y, x0 - 2), kPtRowBytes, bar);
-      } else {  // split at the x wrap: pieces of records [x0-2, x0+18) mod nx
-        uint32_t h = 0;
-        while (h < uint32_t(kPtW)) {
-          const uint32_t x = uint32_t((int64_t(x0) - 2 + h + nx) % nx);
-          const uint32_t len = min(uint32_t(kPtW) - h, uint32_t(nx - x));
-          tma::bulk_g2s(dst + size_t(h) * kQ, rec(z, y, x), len * kQ * 8, bar);
-          h += len;
-        }
-      }
-    }
-  }
-}
-
-template <bool COLLIDE, int kPtY, int kPtZ>
-__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(const DirectArgs a) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);  // halo rows
-  extern __shared__ __align__(128) unsigned char pt_smem[];
-  double* sh = reinterpret_cast<double*>(pt_smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
-  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
-  const uint32_t b = blockIdx.x;
-  const uint32_t x0 = (b % tilesx) * kPtX;
-  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
-  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
-  const uint64_t nx = a.nx;
-  const uint32_t t = threadIdx.x;
-  pt_load_halo<kPtY, kPtZ>(a, a.src, sh, bar, x0, y0, z0);
-  const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
-  const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
-  const bool solid = solid_node(a, x0 + tx, y0 + ty, z0 + tz, n);
-  tma::mbar_wait(bar, 0);
-  auto at = [&](int hx, int hy, int hz) {
-    return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
-  };
-  double q[kQ];
-  q[0] = at(tx + 2, ty + 1, tz + 1)[dslot(0)];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(d)];
-  if (COLLIDE && !solid) collide(q, a.trt);
-  __syncthreads();  // every gather done: the centre records may be overwritten
-  double* own = at(tx + 2, ty + 1, tz + 1);
-  own[dslot(0)] = q[0];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) own[solid ? dslot(opp(d)) : dslot(d)] = q[d];
-  tma::fence_proxy_async();
-  __syncthreads();
-  if (t < uint32_t(kPtY * kPtZ)) {  // one bulk store per centre row
-    const uint32_t ry = t % kPtY, rz = t / kPtY;
-    double* g = a.dst + ((uint64_t(z0 + rz) * a.ny + (y0 + ry)) * nx + x0) * kQ;
-    tma::bulk_s2g(g, at(2, ry + 1, rz + 1), kPtX * kQ * 8);
-    tma::bulk_commit();
-    tma::bulk_wait_read0();
-  }
-}
-
-// AoS AA odd step with the gathers through the same 3-D halo tiles: the
-// tile's source rows arrive by TMA as whole records, each node reads its 18
-// neighbour values (x - c_d, opp d) in shared memory, and writes them back to
-// global memory slot by slot (every slot is read and written by exactly one
-// node in this sub-step, so the other, possibly stale, slots of the staged
-// records are never used).
-template <int kPtY, int kPtZ>
-__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(const DirectArgs a) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
-  extern __shared__ __align__(128) unsigned char pt_smem[];
-  double* sh = reinterpret_cast<double*>(pt_smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
-  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
-  const uint32_t b = blockIdx.x;
-  const uint32_t x0 = (b % tilesx) * kPtX;
-  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
-  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
-  const uint32_t t = threadIdx.x;
-  pt_load_halo<kPtY, kPtZ>(a, a.dst, sh, bar, x0, y0, z0);
-  const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
-  const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
-  Coords c;
-  decode_node(a, n, c);
-  const bool solid = solid_node(a, c.x, c.y, c.z, n);
-  tma::mbar_wait(bar, 0);
-  if (solid) return;
-  auto at = [&](int hx, int hy, int hz) {
-    return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
-  };
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d)
-    q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(opp(d))];
-  collide(q, a.trt);
-  const Idx<false> I{a.P, a.nx, a.ny};
-#pragma unroll
-  for (int d = 0; d < kQ; ++d)
-    a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])] = q[opp(d)];
-}
-
-// Odd step with the x-shifted scatters realigned through shared memory.
-// In k_full_aa_odd every warp stores the 10 directions with c_x != 0 one
-// element off its own x range, so each such store instruction writes two
-// partial 32-byte sectors (one shared with the neighbouring warp).  Here a
-// 128-thread block covers 128 consecutive x of one row (nx % 128 == 0): the
-// producer of the value that lands on x_u parks it in shared memory, and
-// thread u stores it aligned; only the two elements that leave the block's x
-// range are stored by their producers directly.  Loads, collision and the
-// order of values are unchanged, so results are bitwise those of
-// k_full_aa_odd.
-constexpr int kSxThreads = 128;
-template <int MINB>
-__global__ void __launch_bounds__(kSxThreads, MINB) k_full_aa_odd_sx(const DirectArgs a) {
-  constexpr int kX = 10;  // directions with c_x != 0
-  __shared__ double sh[kX][kSxThreads];
-  __shared__ uint8_t fl[kSxThreads];
-  const int u = threadIdx.x;
-  const uint32_t n = a.node0 + blockIdx.x * kSxThreads + u;
-  Coords c;
-  decode_node(a, n, c);
-  const bool fluid = !solid_node(a, c.x, c.y, c.z, n);
-  fl[u] = fluid;
-  const Idx<true> I{a.P, a.nx, a.ny};
-  double* buf = a.dst;
-  if (fluid) {
-    // gather/scatter address of direction d: own slot-0 element + constant
-    // for interior warps (see aa_odd_node), the wrapped form otherwise
-    const bool inner = c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u &&
-                       (!a.zwrap || c.z - 1u < a.nzl - 2u);
-    const bool fast = __all_sync(__activemask(), inner);
-    double* own = buf + I(c.Z[1], 0, c.y, c.x);
-    auto addr = [&](int d) -> double* {
-      if (fast) return own + a.odd_off[d];
-      return d == 0 ? buf + I(c.Z[1], dslot(0), c.y, c.x)
-                    : buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
-    };
-    double q[kQ];
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) q[d] = *addr(d);
-    collide(q, a.trt);
-    int k = 0;
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) {
-      if (cx(d) == 0) {
-        *addr(d) = q[opp(d)];
-      } else {
-        const int dst = u - cx(d);  // the thread whose x the value lands on
-        if (dst >= 0 && dst < kSxThreads)
-          sh[k][dst] = q[opp(d)];
-        else
-          *addr(d) = q[opp(d)];
-        ++k;
-      }
-    }
-  }
-  __syncthreads();
-  int k = 0;
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) {
-    if (cx(d) == 0) continue;
-    const int src = u + cx(d);
-    if (src >= 0 && src < kSxThreads && fl[src])
-      buf[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.x)] = sh[k][u];
-    ++k;
-  }
-}
-
-// ---- fused multi-step sweeps for small lattices ----------------------------
-// For lattices that live in L2 (cfg 1: 2 x 40 MB) a sweep takes ~15 us and
-// the per-launch fill/drain and launch gaps cost as much as the work.  One
-// cooperative launch runs all T sweeps with a grid barrier between them;
-// every block walks the nodes grid-stride.  Same per-node bodies, so the
-// results are bitwise those of the per-sweep kernels.
-struct GridBarrier {
-  unsigned* count;
-  unsigned* gen;
-};
-
-__device__ __forceinline__ void grid_sync(const GridBarrier& b) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = b.gen;
-    const unsigned g = *vgen;
-    __threadfence();
-    if (atomicAdd(b.count, 1u) == gridDim.x - 1) {
-      atomicExch(b.count, 0u);
-      __threadfence();
-      atomicAdd(b.gen, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-enum FusedKind { kFusedPush = 0, kFusedPull = 1, kFusedAA = 2 };
-
-template <bool SOA, int KIND, int TPB = 256, int MINB = 1>
-__global__ void __launch_bounds__(TPB, MINB) k_full_fused(DirectArgs a, double* other,
-                                                          long steps, GridBarrier bar) {
-  const uint32_t G = gridDim.x * blockDim.x;
-  auto sweep = [&](auto body) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.count; i += G) {
-      const uint32_t n = a.node0 + i;
-      Coords c;
-      decode_node(a, n, c);
-      body(c, n);
-    }
-  };
-  if (KIND == kFusedAA) {
-    for (long s = 0; s < steps; s += 2) {
-      sweep([&](const Coords& c, uint32_t n) { aa_even_node<SOA, false, true>(a, c, n); });
-      grid_sync(bar);
-      sweep([&](const Coords& c, uint32_t n) { aa_odd_node<SOA, false, true>(a, c, n); });
-      grid_sync(bar);
-    }
-    return;
-  }
-  // two grids: a.src -> a.dst, then swap (the host tracks the parity)
-  double* bufs[2] = {const_cast<double*>(a.src), other};
-  int cur = 0;
-  if (KIND == kFusedPull) {
-    a.dst = bufs[0];
-    sweep([&](const Coords& c, uint32_t n) { collide_node_pass<SOA, true>(a, c, n); });
-    grid_sync(bar);
-  }
-  for (long s = 0; s < steps; ++s) {
-    a.src = bufs[cur];
-    a.dst = bufs[1 - cur];
-    if (KIND == kFusedPush)
-      sweep([&](const Coords& c, uint32_t n) { push_node<SOA, false, true>(a, c, n); });
-    else if (s + 1 < steps)
-      sweep([&](const Coords& c, uint32_t n) { pull_node<SOA, true, false, true>(a, c, n); });
-    else
-      sweep([&](const Coords& c, uint32_t n) { pull_node<SOA, false, false, true>(a, c, n); });
-    grid_sync(bar);
-    cur ^= 1;
-  }
-}
-
-// ---- the same multi-sweep run as a plane-level dataflow --------------------
-// No grid barrier: the T sweeps are cut into tasks (sweep s, plane z, chunk i)
-// of blockDim nodes.  A task of sweep s > 0 waits until sweep s-1 has
-// finished planes z-1, z, z+1 (z wrapped); that covers every read and write
-// hazard of push, pull and AA (each sweep touches only the planes next to its
-// own, and the chains close transitively -- DESIGN.md section 4).
-// plane_done[z] counts finished chunks of plane z over all sweeps, so "sweep
-// s-1 done on z" is plane_done[z] >= s * chunks_per_plane (release add by the
-// finishing block, acquire load by the waiting one; lattice loads are
-// ld.global.cg, so no stale L1 line is read).  All blocks are co-resident
-// (cooperative launch).  Blocks that finish their part of a sweep start the
-// next one instead of idling at a barrier.
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <bool SOA, int KIND>
-__global__ void __launch_bounds__(256) k_full_flow(DirectArgs a, double* other, long sweeps,
-                                                   unsigned* plane_done, unsigned base) {
-  // Tasks are blockDim-node chunks run by whole blocks.  (32-node warp
-  // tasks without block barriers measured 2x slower: the release/acquire
-  // fences per task dominate.)
-  const uint32_t lane = threadIdx.x;
-  const uint64_t worker = blockIdx.x;
-  const uint64_t workers = gridDim.x;
-  const uint32_t cpp = (a.P + blockDim.x - 1) / blockDim.x;  // chunks per plane
-  const uint64_t per_sweep = uint64_t(a.nzl) * cpp;
-  const uint64_t total = per_sweep * uint64_t(sweeps);
-  double* bufs[2] = {const_cast<double*>(a.src), other};
-  // Static round-robin assignment (block b: tasks b, b + grid, ...): every
-  // block runs its tasks in increasing order, so the smallest unfinished task
-  // is always running and its dependencies (all smaller) are done.  Sweep s
-  // visits the planes starting at plane 2s: sweep s's i-th plane then needs
-  // sweep s-1's (i+1)..(i+3)-th planes, dispatched about a whole sweep
-  // earlier -- without the rotation the z wrap would make the first plane of
-  // every sweep wait for the last plane of the previous one.
-  auto where = [&](uint64_t task, uint32_t& s, uint32_t& z, uint32_t& chunk) {
-    s = static_cast<uint32_t>(task / per_sweep);
-    const uint32_t rem = static_cast<uint32_t>(task - uint64_t(s) * per_sweep);
-    const uint32_t zi = rem / cpp;
-    chunk = rem - zi * cpp;
-    z = static_cast<uint32_t>((zi + 2ull * s) % a.nzl);
-  };
-  // lanes 0-2 watch planes z-1, z, z+1 of the previous sweep
-  auto watched = [&](uint32_t z) {
-    return lane == 0 ? (z == 0 ? a.nzl - 1 : z - 1)
-         : lane == 1 ? z
-                     : (z + 1 == a.nzl ? 0 : z + 1);
-  };
-  // The counters a task needs are read one task ahead (relaxed; re-polled
-  // only if not yet enough); the acquire is a fence after the observing
-  // read, so in the common case (dependencies finished about a sweep ago)
-  // the check puts no L2 round trip on the critical path.
-  unsigned seen = 0;
-  if (lane < 3 && worker < total) {
-    uint32_t s, z, chunk;
-    where(worker, s, z, chunk);
-    seen = ld_relaxed(plane_done + watched(z));
-  }
-  for (uint64_t task = worker; task < total; task += workers) {
-    uint32_t s, z, chunk;
-    where(task, s, z, chunk);
-    if (s > 0) {
-      if (lane < 3) {
-        const unsigned need = base + s * cpp;  // wrap-safe comparisons
-        while (static_cast<int>(seen - need) < 0) {
-          __nanosleep(32);
-          seen = ld_relaxed(plane_done + watched(z));
-        }
-        __threadfence();
-      }
-      __syncthreads();
-    }
-    if (lane < 3 && task + workers < total) {
-      uint32_t s2, z2, c2;
-      where(task + workers, s2, z2, c2);
-      seen = ld_relaxed(plane_done + watched(z2));
-    }
-    const uint32_t x = chunk * blockDim.x + lane;
-    if (x < a.P) {
-      const uint32_t n = z * a.P + x;
-      Coords c;
-      decode_node(a, n, c);
-      if (KIND == kFusedAA) {
-        if (s & 1)
-          aa_odd_node<SOA, false, true>(a, c, n);
-        else
-          aa_even_node<SOA, false, true>(a, c, n);
-      } else if (KIND == kFusedPush) {
-        a.src = bufs[s & 1];
-        a.dst = bufs[(s & 1) ^ 1];
-        push_node<SOA, false, true>(a, c, n);
-      } else if (s == 0) {  // pull: collide pass on the current grid
-        a.dst = bufs[0];
-        collide_node_pass<SOA, true>(a, c, n);
-      } else {
-        a.src = bufs[(s - 1) & 1];
-        a.dst = bufs[s & 1];
-        if (s + 1 < sweeps)
-          pull_node<SOA, true, false, true>(a, c, n);
-        else
-          pull_node<SOA, false, false, true>(a, c, n);
-      }
-    }
-    __syncthreads();  // orders the block's stores before thread 0's release
-    if (lane == 0) red_release_add(plane_done + z, 1u);
-  }
-}
-
-// ---- AA sub-steps, software-pipelined through shared memory ---------------
-// Persistent variant of the two kernels above.  Each thread walks nodes
-// n, n + G, n + 2G, ... (G = grid size) and, while it collides node n, the
-// 19 populations of its next node are already in flight as per-thread
-// cp.async (LDGSTS) copies into its own shared-memory column: the load
-// latency of node n+G overlaps the collision of node n inside every warp
-// instead of depending on other resident warps.  Each thread only ever
-// reads the shared-memory slots it filled itself, so no block barrier is
-// needed -- cp.async.wait_group orders it.
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-
-// Address of the slot a node gathers direction d from (odd: (x - c_d, opp d);
-// even: (x, d)); in the odd step it is also where direction opp(d) is stored.
-template <bool ODD>
-__device__ __forceinline__ uint64_t aa_src(const Idx<true>& I, const Coords& c, int d) {
-  if (ODD && d != 0)
-    return I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
-  return I(c.Z[1], dslot(d), c.y, c.x);
-}
-
-constexpr int kPipeThreads = 256;
-
-template <bool ODD, int STAGES, int MINB>
-__global__ void __launch_bounds__(kPipeThreads, MINB) k_full_aa_pipe(const DirectArgs a) {
-  extern __shared__ double sm_pipe[];  // [STAGES][19][kPipeThreads]
-  const uint32_t tid = threadIdx.x;
-  const uint32_t G = gridDim.x * kPipeThreads;
-  const uint32_t end = a.node0 + a.count;
-  const Idx<true> I{a.P, a.nx, a.ny};
-  double* buf = a.dst;
-  uint8_t solid[STAGES];
-  auto prefetch = [&](uint32_t n, int s) {
-    if (n < end) {
-      Coords c;
-      decode_node(a, n, c);
-      solid[s] = a.flags[n];
-      double* col = sm_pipe + size_t(s) * kQ * kPipeThreads + tid;
-#pragma unroll
-      for (int d = 0; d < kQ; ++d) cp_async8(col + d * kPipeThreads, buf + aa_src<ODD>(I, c, d));
-    }
-    cp_async_commit();
-  };
-  uint32_t n = a.node0 + blockIdx.x * kPipeThreads + tid;
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) prefetch(n + s * G, s);
-  while (n < end) {
-    // unrolled by STAGES so the ring index (and solid[]) is a constant
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) {
-      if (n < end) {
-        prefetch(n + (STAGES - 1) * G, (s + STAGES - 1) % STAGES);
-        cp_async_wait<STAGES - 1>();
-        if (!solid[s]) {
-          const double* col = sm_pipe + size_t(s) * kQ * kPipeThreads + tid;
-          double q[kQ];
-#pragma unroll
-          for (int d = 0; d < kQ; ++d) q[d] = col[d * kPipeThreads];
-          collide(q, a.trt);
-          Coords c;
-          decode_node(a, n, c);
-          if (ODD) {
-#pragma unroll
-            for (int d = 0; d < kQ; ++d) buf[aa_src<true>(I, c, d)] = q[opp(d)];
-          } else {
-#pragma unroll
-            for (int d = 0; d < kQ; ++d) buf[I(c.Z[1], dslot(opp(d)), c.y, c.x)] = q[d];
-          }
-        }
-        n += G;
-      }
-    }
-  }
-  cp_async_wait<0>();
-}
-
-template <bool ODD, int STAGES, int MINB>
-void launch_aa_pipe(const DirectArgs& a, int sm_count, cudaStream_t s) {
-  const size_t smem = size_t(STAGES) * kQ * kPipeThreads * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    LBM_CUDA(cudaFuncSetAttribute(k_full_aa_pipe<ODD, STAGES, MINB>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    configured = true;
-  }
-  const uint64_t blocks = ceil_div(a.count, kPipeThreads);
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(blocks, uint64_t(sm_count) * MINB));
-  k_full_aa_pipe<ODD, STAGES, MINB><<<grid, kPipeThreads, smem, s>>>(a);
-  LBM_CHECK_LAUNCH();
-}
 
 // ---- init / canonical transfer / perturbation / macro --------------------
 template <bool SOA>

@@ -1,0 +1,252 @@
+// Direct lattices: indexing, node decode, per-node bodies and the one-sweep kernels.
+// (part of the direct-addressing translation unit, included by direct.cu)
+#pragma once
+
+#include "direct_args.cuh"
+
+namespace lbmgpu {
+
+template <bool SOA>
+struct Idx {
+  uint64_t P;
+  uint32_t nx, ny;
+  __device__ __forceinline__ uint64_t operator()(uint32_t zs, int slot,
+                                                 uint32_t y, uint32_t x) const {
+    if (SOA)
+      return (uint64_t(zs) * kQ + slot) * P + uint64_t(y) * nx + x;
+    return ((uint64_t(zs) * ny + y) * nx + x) * kQ + slot;
+  }
+};
+
+struct Coords {
+  uint32_t x, y, z;        // own-plane coordinates
+  uint32_t X[3], Y[3];     // wrapped x-1,x,x+1 / y-1,y,y+1
+  uint32_t Z[3];           // storage planes of z-1, z, z+1
+};
+
+// own-node id n -> coordinates, wrapped x/y neighbours and storage planes
+__device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coords& c) {
+  const uint32_t z = a.fdP.div(n);
+  const uint32_t r = n - z * a.P;
+  const uint32_t y = a.fdx.div(r);
+  const uint32_t x = r - y * a.nx;
+  c.x = x;
+  c.y = y;
+  c.z = z;
+  c.X[0] = x == 0 ? a.nx - 1 : x - 1;
+  c.X[1] = x;
+  c.X[2] = x + 1 == a.nx ? 0 : x + 1;
+  c.Y[0] = y == 0 ? a.ny - 1 : y - 1;
+  c.Y[1] = y;
+  c.Y[2] = y + 1 == a.ny ? 0 : y + 1;
+  const uint32_t zs = z + a.zoff;
+  if (a.zwrap) {
+    c.Z[0] = z == 0 ? a.nzl - 1 : z - 1;
+    c.Z[2] = z + 1 == a.nzl ? 0 : z + 1;
+  } else {
+    c.Z[0] = zs - 1;
+    c.Z[2] = zs + 1;
+  }
+  c.Z[1] = zs;
+}
+
+__device__ __forceinline__ bool decode(const DirectArgs& a, Coords& c,
+                                       uint32_t& n) {
+  n = a.node0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.node0 + a.count) return false;
+  if (a.band) {  // y-band order (a whole part: node0 == 0, ny % band == 0)
+    const uint32_t x = n % a.nx, r = n / a.nx;
+    const uint32_t per_band = a.band * a.nzl;
+    const uint32_t b = r / per_band, t = r - b * per_band;
+    const uint32_t z = t / a.band;
+    n = (z * a.ny + b * a.band + (t - z * a.band)) * a.nx + x;
+  }
+  decode_node(a, n, c);
+  return true;
+}
+
+// Loads of lattice data: plain (L1-cached) in the one-sweep-per-launch
+// kernels; L2-only (ld.global.cg) in the fused multi-step kernel, whose later
+// sweeps read lines other SMs wrote after a grid barrier.
+template <bool CG>
+__device__ __forceinline__ double ldp(const double* p) {
+  if (CG) return __ldcg(p);
+  return *p;
+}
+template <bool CS>
+__device__ __forceinline__ void st(double* p, double v) {
+  if (CS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+// ---- per-node bodies (shared by the sweep kernels and the fused kernel) ----
+// kernels_full_os.cpp:56-89 + full_lattice.cpp:42-56 (push, correction on dst)
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+  const uint32_t tm = a.tmask ? a.tmask[n] : 0u;
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.src + I(c.Z[1], dslot(d), c.y, c.x));
+  if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
+  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)], tz = c.Z[1 + cz(d)];
+    // solid target: the precomputed mask, else the neighbour's flag from L1
+    // (measured faster than the arithmetic test here: cfg 1 fused 15.5k vs
+    // 13.9k MFLUP/s)
+    const uint32_t tn = (tz - a.zoff) * a.P + ty * a.nx + tx;
+    const bool ts = a.tmask ? ((tm >> d) & 1u) != 0 : a.flags[tn] != 0;
+    const int s = ts ? dslot(opp(d)) : dslot(d);
+    st<CS>(a.dst + I(tz, s, ty, tx), q[d]);
+  }
+}
+
+// kernels_full_os.cpp:56-89 (PULL); COLLIDE=false is the stream-only pass
+template <bool SOA, bool COLLIDE, bool CS, bool CG>
+__device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+  q[0] = ldp<CG>(a.src + I(c.Z[1], dslot(0), c.y, c.x));
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    q[d] = ldp<CG>(a.src + I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)]));
+  const bool solid = solid_node(a, c.x, c.y, c.z, n);
+  if (COLLIDE && !solid) collide(q, a.trt);
+  st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const int s = solid ? dslot(opp(d)) : dslot(d);
+    st<CS>(a.dst + I(c.Z[1], s, c.y, c.x), q[d]);
+  }
+}
+
+// collide_pass (kernels_full_os.cpp:149-159): fluid nodes, in place on dst
+template <bool SOA, bool CG>
+__device__ __forceinline__ void collide_node_pass(const DirectArgs& a, const Coords& c, uint32_t n) {
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.dst + I(c.Z[1], dslot(d), c.y, c.x));
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) a.dst[I(c.Z[1], dslot(d), c.y, c.x)] = q[d];
+}
+
+// AA pattern (kernels_full_aa.cpp:46-94), corrections dropped.  Built-in
+// geometries test solidity arithmetically (no flag load ahead of the PDF
+// loads; solid nodes issue no loads at all).
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void aa_even_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(buf + I(c.Z[1], dslot(d), c.y, c.x));
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) st<CS>(buf + I(c.Z[1], dslot(opp(d)), c.y, c.x), q[d]);
+}
+
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void aa_odd_node(const DirectArgs& a, const Coords& c, uint32_t n) {
+  if (solid_node(a, c.x, c.y, c.z, n)) return;
+  const Idx<SOA> I{a.P, a.nx, a.ny};
+  double* buf = a.dst;
+  // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
+  // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
+  // per direction serves both the load and the store.
+  double q[kQ];
+  // Warp-uniform fast path: no active lane touches a wrapped neighbour, so
+  // every address is the own slot-0 element plus a per-direction constant
+  // (recomputed for the stores: only `own` stays live across the collision).
+  const bool inner = c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u &&
+                     (!a.zwrap || c.z - 1u < a.nzl - 2u);
+  if (__all_sync(__activemask(), inner)) {
+    double* own = buf + I(c.Z[1], 0, c.y, c.x);
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(own + a.odd_off[d]);
+    collide(q, a.trt);
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) st<CS>(own + a.odd_off[d], q[opp(d)]);
+    return;
+  }
+  double* p[kQ];
+  p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(p[d]);
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
+}
+
+// ---- one sweep per launch, one node per thread ------------------------------
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_full_push(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  push_node<SOA, CS, false>(a, c, n);
+}
+
+template <bool SOA, bool COLLIDE, bool CS>
+__global__ void __launch_bounds__(256) k_full_pull(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  pull_node<SOA, COLLIDE, CS, false>(a, c, n);
+}
+
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  collide_node_pass<SOA, false>(a, c, n);
+}
+
+// SoA AA sweeps: lanes 0..18 of a warp prefetch into L2 the two 128-byte
+// lines of slot `lane` of the 32 nodes `a.pf` nodes ahead (blocks dispatch in
+// index order, so that warp runs about one wave later; the odd step's
+// +-1-row gathers hit lines the neighbouring rows' warps prefetched).
+__device__ __forceinline__ void aa_prefetch(const DirectArgs& a) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (a.pf == 0 || lane >= kQ) return;
+  const uint32_t m = a.node0 + blockIdx.x * blockDim.x + (threadIdx.x & ~31u) + a.pf;
+  if (m >= a.node0 + a.count) return;
+  const uint32_t z = a.fdP.div(m);
+  const uint32_t r = m - z * a.P;
+  const uint32_t y = a.fdx.div(r);
+  const double* p =
+      a.dst + (uint64_t(z + a.zoff) * kQ + lane) * a.P + uint64_t(y) * a.nx + (r - y * a.nx);
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
+}
+
+template <bool SOA, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
+  if (SOA) aa_prefetch(a);
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  aa_even_node<SOA, CS, false>(a, c, n);
+}
+
+template <bool SOA, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
+  if (SOA) aa_prefetch(a);
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  aa_odd_node<SOA, CS, false>(a, c, n);
+}
+
+}  // namespace lbmgpu

@@ -31,730 +31,12 @@
 #include "tma.cuh"
 #include "lbm.hpp"
 
+#include "list_sweeps.cuh"
+#include "list_build.cuh"
+#include "list_ria.cuh"
+#include "list_parts.cuh"
+
 namespace lbmgpu {
-
-struct ListArgs {
-  const double* src;
-  double* dst;
-  const uint32_t* adj;  // d-major [(d-1)*N + n]
-  uint64_t N;
-  uint64_t starts[kQ];  // SoA direction starts (unused for AoS)
-  TrtArgs trt;
-  uint64_t nb, ne;      // node range of this launch (AA sweeps); [0, N) by default
-  uint64_t node_base;   // canonical sweeps over a part's local arrays: node n is local n - base
-};
-
-template <bool SOA>
-__device__ __forceinline__ uint64_t lslot(const ListArgs& a, uint64_t n, int d) {
-  return SOA ? a.starts[d] + (n - a.node_base) : (n - a.node_base) * kQ + d;
-}
-
-template <bool CS>
-__device__ __forceinline__ void lst(double* p, double v) {
-  if (CS)
-    __stcs(p, v);
-  else
-    *p = v;
-}
-
-// list-pull (kernels_list_os.cpp:43-62, PULL): gather through the Gather
-// table, collide, coalesced stores to own slots.  COLLIDE=false is the
-// stream-only exit pass.  CS selects st.global.cs (the GPU's counterpart of
-// the nt split-store variants, kernels_list_nt.cpp).
-template <bool SOA, bool COLLIDE, bool CS>
-__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a, uint64_t pf) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
-  if (pf) {  // adjacency L2 prefetch for a later wave (see k_list_aa_odd)
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t m = (n & ~uint64_t(31)) + pf;
-    if (lane < 18 && m < a.N)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
-  }
-  uint32_t an[18];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
-  double q[kQ];
-  q[0] = a.src[lslot<SOA>(a, n, 0)];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = a.src[an[d - 1]];
-  if (COLLIDE) collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
-}
-
-// AoS list sweeps with the node's own record staged through a shared-memory
-// tile of kLAosTile consecutive nodes (slots 19n + d are contiguous): full-
-// sector loads / stores instead of one sector request per element.
-//   k_list_aos_tile<true>:  AA even (own slots -> opposite slots), [nb, ne)
-//   k_list_aos_tile<false>: collide pass, in place
-//   k_list_pull_aos_tile:   pull; gathers as k_list_pull, own record stored
-//                           through the tile
-constexpr int kLAosTile = 128;
-template <bool EVEN>
-__global__ void __launch_bounds__(kLAosTile) k_list_aos_tile(const ListArgs a) {
-  __shared__ __align__(128) double sh[kLAosTile * kQ];
-  __shared__ __align__(8) uint64_t bar;
-  const uint64_t n0 = a.nb + blockIdx.x * uint64_t(kLAosTile);
-  const uint32_t cnt = static_cast<uint32_t>(min(uint64_t(kLAosTile), a.ne - n0));
-  double* g = a.dst + n0 * kQ;
-  aos_tile_load<kLAosTile>(sh, g, cnt, &bar);
-  if (threadIdx.x < cnt) {
-    double* r = sh + threadIdx.x * kQ;
-    double q[kQ];
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) q[d] = r[d];
-    collide(q, a.trt);
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) r[EVEN ? opp(d) : d] = q[d];
-  }
-  aos_tile_store<kLAosTile>(g, sh, cnt);
-}
-
-template <bool COLLIDE>
-__global__ void __launch_bounds__(kLAosTile) k_list_pull_aos_tile(const ListArgs a) {
-  __shared__ __align__(128) double sh[kLAosTile * kQ];
-  const uint64_t n0 = blockIdx.x * uint64_t(kLAosTile);
-  const uint32_t cnt = static_cast<uint32_t>(min(uint64_t(kLAosTile), a.N - n0));
-  if (threadIdx.x < cnt) {
-    const uint64_t n = n0 + threadIdx.x;
-    double q[kQ];
-    q[0] = a.src[n * kQ];
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) q[d] = a.src[__ldg(a.adj + (d - 1) * a.N + n)];
-    if (COLLIDE) collide(q, a.trt);
-    double* r = sh + threadIdx.x * kQ;
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) r[d] = q[d];
-  }
-  aos_tile_store<kLAosTile>(a.dst + n0 * kQ, sh, cnt);
-}
-
-// list-push (kernels_list_os.cpp:43-62, push): own loads, scatter stores.
-template <bool SOA>
-__global__ void __launch_bounds__(256) k_list_push(const ListArgs a) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = a.src[lslot<SOA>(a, n, d)];
-  collide(q, a.trt);
-  a.dst[lslot<SOA>(a, n, 0)] = q[0];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) a.dst[__ldg(a.adj + (d - 1) * a.N + n)] = q[d];
-}
-
-// collide_pass (kernels_list_os.cpp:64-72), in place on dst.
-template <bool SOA>
-__global__ void __launch_bounds__(256) k_list_collide(const ListArgs a) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = a.dst[lslot<SOA>(a, n, d)];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) a.dst[lslot<SOA>(a, n, d)] = q[d];
-}
-
-// aa_even_node (kernels_list_aa.cpp:10-16): own slots -> opposite slots.
-template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
-  const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.ne) return;
-  double* buf = a.dst;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = buf[lslot<SOA>(a, n, d)];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) lst<CS>(buf + lslot<SOA>(a, n, opp(d)), q[d]);
-}
-
-// aa_odd_node (kernels_list_aa.cpp:22-31): one scatter table serves both
-// sides -- gather d through column opp(d), scatter d through column d.
-template <bool SOA, bool CS>
-__global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a, uint64_t pf) {
-  const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.ne) return;
-  double* buf = a.dst;
-  // L2 prefetch of the adjacency lines a block about `pf` nodes ahead will
-  // need (blocks are dispatched in index order): the index load of later
-  // blocks then hits L2 and the index -> gather chain shortens.  Lanes 0..17
-  // of each warp each touch one 128 B column line of that warp.
-  if (pf) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t m = (n & ~uint64_t(31)) + pf;
-    if (lane < 18 && m < a.N)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
-  }
-  uint32_t an[18];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
-  double q[kQ];
-  q[0] = buf[lslot<SOA>(a, n, 0)];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
-  collide(q, a.trt);
-  lst<CS>(buf + lslot<SOA>(a, n, 0), q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) lst<CS>(buf + an[d - 1], q[d]);
-}
-
-// Persistent variant of k_list_aa_odd: every thread walks n, n+G, ... and
-// loads the 18 adjacency entries of its NEXT node while the current node's
-// gathers and collision are in flight, so the index-load latency no longer
-// sits in series in front of the dependent PDF gathers.
-template <bool SOA>
-__global__ void __launch_bounds__(256, 2) k_list_aa_odd_pipe(const ListArgs a) {
-  const uint64_t G = uint64_t(gridDim.x) * blockDim.x;
-  uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  double* buf = a.dst;
-  uint32_t an[18];
-  if (n < a.N) {
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
-  }
-  for (; n < a.N; n += G) {
-    double q[kQ];
-    q[0] = buf[lslot<SOA>(a, n, 0)];
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
-    uint32_t nx[18];
-    const uint64_t m = n + G;
-    if (m < a.N) {
-#pragma unroll
-      for (int d = 1; d < kQ; ++d) nx[d - 1] = __ldg(a.adj + (d - 1) * a.N + m);
-    }
-    collide(q, a.trt);
-    buf[lslot<SOA>(a, n, 0)] = q[0];
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) buf[an[d - 1]] = q[d];
-#pragma unroll
-    for (int d = 0; d < 18; ++d) an[d] = nx[d];
-  }
-}
-
-// ---- structure construction -------------------------------------------------
-// Traversal position of box node (x,y,z) in order_nodes (list_lattice.cpp:
-// 127-140).  blk > 0: tiles (ty, tz) in row-major order, inside a tile x, then
-// y, then z; the tile at (ty, tz) with extents th x tw starts after
-// nx*(ty*nz + th*tz) positions.
-__device__ __forceinline__ uint64_t trav_pos(int x, int y, int z, int nx,
-                                             int ny, int nz, int blk) {
-  if (blk == 0) return (uint64_t(x) * ny + y) * nz + z;
-  const int ty = y / blk * blk, tz = z / blk * blk;
-  const int th = min(blk, ny - ty), tw = min(blk, nz - tz);
-  return uint64_t(nx) * (uint64_t(ty) * nz + uint64_t(th) * tz) +
-         uint64_t(x) * th * tw + uint64_t(y - ty) * tw + (z - tz);
-}
-
-__global__ void k_trav_flags(const uint8_t* __restrict__ flags, int nx, int ny,
-                             int nz, int blk, uint8_t* __restrict__ ft) {
-  const uint64_t V = uint64_t(nx) * ny * nz;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < V;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const int z = static_cast<int>(i % nz);
-    const uint64_t r = i / nz;
-    const int y = static_cast<int>(r % ny), x = static_cast<int>(r / ny);
-    ft[trav_pos(x, y, z, nx, ny, nz, blk)] = flags[i];
-  }
-}
-
-// rank (list_lattice.cpp:160-164), nodes, canonical <-> list maps.
-__global__ void k_rank_nodes(const uint8_t* __restrict__ flags,
-                             const uint32_t* __restrict__ trank,
-                             const uint32_t* __restrict__ crank, int nx, int ny,
-                             int nz, int blk, uint32_t* __restrict__ rank,
-                             int32_t* __restrict__ nodes,
-                             uint32_t* __restrict__ list_of_canon) {
-  const uint64_t V = uint64_t(nx) * ny * nz;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < V;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    if (flags[i]) {
-      rank[i] = 0xffffffffu;
-      continue;
-    }
-    const int z = static_cast<int>(i % nz);
-    const uint64_t r = i / nz;
-    const int y = static_cast<int>(r % ny), x = static_cast<int>(r / ny);
-    const uint32_t n = blk == 0 ? crank[i] : trank[trav_pos(x, y, z, nx, ny, nz, blk)];
-    rank[i] = n;
-    nodes[3 * uint64_t(n)] = x;
-    nodes[3 * uint64_t(n) + 1] = y;
-    nodes[3 * uint64_t(n) + 2] = z;
-    if (list_of_canon) list_of_canon[crank[i]] = n;
-  }
-}
-
-struct AdjBuild {
-  const uint8_t* flags;
-  const uint32_t* rank;
-  const int32_t* nodes;
-  uint32_t* adj;  // d-major
-  uint64_t N;
-  int nx, ny, nz;
-  int per[3];
-  int soa, scatter;
-  uint64_t starts[kQ];
-};
-
-// build_structure adjacency loop (list_lattice.cpp:177-191) with the
-// neighbor() rule (geometry.cpp:119-131).
-__global__ void k_build_adj(const AdjBuild b) {
-  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < b.N;
-       n += uint64_t(gridDim.x) * blockDim.x) {
-    const int x = b.nodes[3 * n], y = b.nodes[3 * n + 1], z = b.nodes[3 * n + 2];
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) {
-      const int look = b.scatter ? d : opp(d);
-      int t0 = x + cx(look), t1 = y + cy(look), t2 = z + cz(look);
-      bool outside = false;
-      if (t0 < 0 || t0 >= b.nx) {
-        if (!b.per[0]) outside = true; else t0 = (t0 + b.nx) % b.nx;
-      }
-      if (!outside && (t1 < 0 || t1 >= b.ny)) {
-        if (!b.per[1]) outside = true; else t1 = (t1 + b.ny) % b.ny;
-      }
-      if (!outside && (t2 < 0 || t2 >= b.nz)) {
-        if (!b.per[2]) outside = true; else t2 = (t2 + b.nz) % b.nz;
-      }
-      uint64_t slot;
-      const uint64_t ti = (uint64_t(t0) * b.ny + t1) * b.nz + t2;
-      if (!outside && b.flags[ti] == 0) {
-        const uint64_t m = b.rank[ti];
-        slot = b.soa ? b.starts[d] + m : m * kQ + d;
-      } else {
-        slot = b.soa ? b.starts[opp(d)] + n : n * kQ + opp(d);
-      }
-      b.adj[(d - 1) * b.N + n] = static_cast<uint32_t>(slot);
-    }
-  }
-}
-
-__global__ void k_adj_canonical(const uint32_t* __restrict__ adj, uint64_t N,
-                                uint32_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < N * 18;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t n = i / 18;
-    const int dm1 = static_cast<int>(i - n * 18);
-    out[i] = adj[dm1 * N + n];
-  }
-}
-
-// RIA run starts (build_ria, list_lattice.cpp:206-226): node n starts a run
-// if n == 0 or its pattern of 18 relative offsets differs from node n-1's.
-__global__ void k_ria_starts(const uint32_t* __restrict__ adj, uint64_t N,
-                             int soa, const ListArgs a,
-                             uint8_t* __restrict__ is_start) {
-  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < N;
-       n += uint64_t(gridDim.x) * blockDim.x) {
-    bool start = n == 0;
-    if (!start)
-      for (int d = 1; d < kQ && !start; ++d) {
-        const uint64_t sn = soa ? a.starts[d] + n : n * kQ + d;
-        const uint64_t sp = soa ? a.starts[d] + n - 1 : (n - 1) * kQ + d;
-        const int32_t pn = static_cast<int32_t>(int64_t(adj[(d - 1) * N + n]) - int64_t(sn));
-        const int32_t pp = static_cast<int32_t>(int64_t(adj[(d - 1) * N + n - 1]) - int64_t(sp));
-        start = pn != pp;
-      }
-    is_start[n] = start;
-  }
-}
-
-// ---- RIA: run-coded odd step (list-aa-ria-soa / list-aa-pv-soa) -------------
-struct IsStart {
-  __host__ __device__ __forceinline__ uint32_t operator()(uint8_t f) const { return f; }
-};
-
-// The reference (kernels_list_aa.cpp:185-224) walks runs of consecutive nodes
-// that share one pattern of 18 relative offsets (entry - own slot) and
-// resolves the slot bases once per run.  GPU form: the run of node n is found
-// from a per-32-node table (first run id + a bitmask of run starts, 8 B per
-// 32 nodes) and the run's 18 offsets are read from a small pattern table that
-// stays in L1/L2 (warps mostly share one run).  Index traffic drops from
-// 72 B per odd update to ~0.25 B + the amortised pattern rows; results are
-// bitwise those of list-aa-soa (same loads, same collide, same stores).
-__global__ void k_ria_tables(const uint8_t* __restrict__ is_start,
-                             const uint32_t* __restrict__ run_incl, uint64_t N,
-                             uint32_t* __restrict__ run_start,
-                             uint32_t* __restrict__ warp_run0,
-                             uint32_t* __restrict__ warp_mask) {
-  // launched with blockDim a multiple of 32 and N padded to whole warps
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  const bool valid = n < N;
-  const bool st = valid && is_start[n];
-  const uint32_t r = valid ? run_incl[n] - 1 : 0;
-  if (st) run_start[r] = static_cast<uint32_t>(n);
-  const uint32_t mask = __ballot_sync(0xffffffffu, st);
-  if ((threadIdx.x & 31) == 0 && valid) {
-    warp_run0[n >> 5] = r;
-    warp_mask[n >> 5] = mask;
-  }
-}
-
-__global__ void k_ria_patterns(const uint32_t* __restrict__ adj,
-                               const uint32_t* __restrict__ run_start, uint64_t R,
-                               const ListArgs a, int32_t* __restrict__ pat) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < R * 18;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / 18;
-    const int d = static_cast<int>(i - r * 18) + 1;
-    const uint64_t s = run_start[r];
-    pat[i] = static_cast<int32_t>(int64_t(adj[(d - 1) * a.N + s]) -
-                                  int64_t(a.starts[d] + s));
-  }
-}
-
-template <bool CS>
-__global__ void __launch_bounds__(256) k_list_aa_odd_ria(const ListArgs a,
-                                                         const int32_t* __restrict__ pat,
-                                                         const uint32_t* __restrict__ warp_run0,
-                                                         const uint32_t* __restrict__ warp_mask,
-                                                         uint64_t pf) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
-  const uint32_t lane = threadIdx.x & 31;
-  if (pf && lane == 0) {  // L2 prefetch of a later wave's run-table words
-    const uint64_t w = (n >> 5) + pf / 32;
-    if (w * 32 < a.N) {
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(warp_run0 + w));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(warp_mask + w));
-    }
-  }
-  const uint32_t below = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
-  const uint32_t r = __ldg(warp_run0 + (n >> 5)) + __popc(__ldg(warp_mask + (n >> 5)) & below);
-  const int32_t* p = pat + uint64_t(r) * 18;
-  double* buf = a.dst;
-  // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
-  int64_t off[18];
-#pragma unroll
-  for (int k = 0; k < 18; ++k) off[k] = __ldg(p + k);
-  double q[kQ];
-  q[0] = buf[a.starts[0] + n];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = buf[int64_t(a.starts[opp(d)] + n) + off[opp(d) - 1]];
-  collide(q, a.trt);
-  lst<CS>(buf + a.starts[0] + n, q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) lst<CS>(buf + int64_t(a.starts[d] + n) + off[d - 1], q[d]);
-}
-
-// Pattern-id form of the run coding, for lattices whose runs share few
-// distinct patterns (a channel: interior, walls, edges): the <= 256 distinct
-// rows live in a small table that stays in L1, and every node carries the
-// one-byte id of its run's row.  The dependent chain in front of the gathers
-// is then one coalesced byte load (prefetched into L2 a wave ahead) and an
-// L1 hit, instead of the run-table word and the run's row from L2.
-__global__ void k_ria_node_ids(const uint32_t* __restrict__ warp_run0,
-                               const uint32_t* __restrict__ warp_mask,
-                               const uint8_t* __restrict__ run_pid, uint64_t N,
-                               uint8_t* __restrict__ nid) {
-  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < N;
-       n += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t lane = static_cast<uint32_t>(n & 31);
-    const uint32_t below = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
-    const uint32_t r = warp_run0[n >> 5] + __popc(warp_mask[n >> 5] & below);
-    nid[n] = run_pid[r];
-  }
-}
-
-template <bool CS>
-__global__ void __launch_bounds__(256) k_list_aa_odd_pid(const ListArgs a,
-                                                         const int32_t* __restrict__ ptab,
-                                                         const uint8_t* __restrict__ nid,
-                                                         uint64_t pf) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
-  if (pf && (threadIdx.x & 31) == 0) {  // ids of a later wave -> L2
-    const uint64_t m = n + pf;
-    if (m < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(nid + m));
-  }
-  const int32_t* p = ptab + uint32_t(__ldg(nid + n)) * 18;
-  double* buf = a.dst;
-  // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
-  int64_t off[18];
-#pragma unroll
-  for (int k = 0; k < 18; ++k) off[k] = __ldg(p + k);
-  double q[kQ];
-  q[0] = buf[a.starts[0] + n];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = buf[int64_t(a.starts[opp(d)] + n) + off[opp(d) - 1]];
-  collide(q, a.trt);
-  lst<CS>(buf + a.starts[0] + n, q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) lst<CS>(buf + int64_t(a.starts[d] + n) + off[d - 1], q[d]);
-}
-
-// Group-pattern form of the run coding: a 32-node group (one warp) that lies
-// inside a single run carries that run's 18 offsets inline (72 B per 32
-// nodes, loaded as warp broadcasts with no dependent lookup in front); a
-// group that straddles run boundaries is marked (first offset = INT32_MIN)
-// and its nodes read their own scatter-table entries.  Same loads, collide
-// and stores as list-aa-soa, so bitwise identical.
-constexpr int32_t kMixedGroup = INT32_MIN;
-
-__global__ void k_ria_group_patterns(const int32_t* __restrict__ pat,
-                                     const uint32_t* __restrict__ warp_run0,
-                                     const uint32_t* __restrict__ warp_mask, uint64_t N,
-                                     int32_t* __restrict__ gpat) {
-  const uint64_t groups = (N + 31) / 32;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < groups * 18;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t g = i / 18;
-    const int k = static_cast<int>(i - g * 18);
-    const bool full = (g + 1) * 32 <= N;
-    const bool uniform = full && (warp_mask[g] & ~1u) == 0;
-    gpat[i] = uniform ? pat[uint64_t(warp_run0[g]) * 18 + k] : (k == 0 ? kMixedGroup : 0);
-  }
-}
-
-template <bool CS>
-__global__ void __launch_bounds__(256) k_list_aa_odd_gpat(const ListArgs a,
-                                                          const int32_t* __restrict__ gpat,
-                                                          uint64_t pf) {
-  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (n >= a.N) return;
-  if (pf) {  // L2 prefetch of the group row a later wave needs (see k_list_aa_odd)
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t g = (n >> 5) + pf / 32;
-    if (lane < 2 && g * 32 < a.N)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(gpat + g * 18 + lane * 16));
-  }
-  const int32_t* row = gpat + (n >> 5) * 18;
-  double* buf = a.dst;
-  int64_t ent[18];  // scatter-table entries of node n
-  const int32_t first = __ldg(row);
-  if (first != kMixedGroup) {
-    // entry(n, k) = starts[k] + n + pattern[k-1]  (list_lattice.cpp:206-226)
-    ent[0] = int64_t(a.starts[1] + n) + first;
-#pragma unroll
-    for (int k = 1; k < 18; ++k) ent[k] = int64_t(a.starts[k + 1] + n) + __ldg(row + k);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 18; ++k) ent[k] = __ldg(a.adj + uint64_t(k) * a.N + n);
-  }
-  double q[kQ];
-  q[0] = buf[a.starts[0] + n];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = buf[ent[opp(d) - 1]];
-  collide(q, a.trt);
-  lst<CS>(buf + a.starts[0] + n, q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) lst<CS>(buf + ent[d - 1], q[d]);
-}
-
-template <bool SOA>
-__global__ void k_list_init(double* buf, const ListArgs a) {
-  for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.N;
-       n += uint64_t(gridDim.x) * blockDim.x)
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) buf[lslot<SOA>(a, n, d)] = weight(d);
-}
-
-// canonical gather / scatter / perturbation / macro fields over c in
-// [c0, c1): list node n = list_of_canon[c] (identity for blk = 0).
-template <bool SOA, int MODE>  // 0 gather, 1 scatter, 2 perturb, 3 macro
-__global__ void k_list_canon(const ListArgs a, double* buf,
-                             const uint32_t* __restrict__ loc, uint64_t c0,
-                             uint64_t c1, double* stage, uint64_t seed,
-                             double amp, double* rho, double* u) {
-  for (uint64_t c = c0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-       c < c1; c += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t n = loc ? loc[c] : c;
-    if (MODE == 0) {
-#pragma unroll
-      for (int d = 0; d < kQ; ++d) stage[(c - c0) * kQ + d] = buf[lslot<SOA>(a, n, d)];
-    } else if (MODE == 1) {
-#pragma unroll
-      for (int d = 0; d < kQ; ++d) buf[lslot<SOA>(a, n, d)] = stage[(c - c0) * kQ + d];
-    } else if (MODE == 2) {
-#pragma unroll
-      for (int d = 0; d < kQ; ++d)
-        buf[lslot<SOA>(a, n, d)] = perturbed_value(c, d, seed, amp);
-    } else {
-      double f[kQ];
-#pragma unroll
-      for (int d = 0; d < kQ; ++d) f[d] = buf[lslot<SOA>(a, n, d)];
-      double r, ux, uy, uz;
-      macroscopic(f, r, ux, uy, uz);
-      rho[c] = r;
-      u[3 * c] = ux;
-      u[3 * c + 1] = uy;
-      u[3 * c + 2] = uz;
-    }
-  }
-}
-
-template <bool SOA>
-__global__ void k_list_mass_terms(const ListArgs a, const double* buf,
-                                  double* out) {
-  // contiguous copy of the fluid populations (pads excluded) of nodes
-  // [nb, ne) for the compensated sum
-  const uint64_t cnt = a.ne - a.nb;
-  for (uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < a.ne;
-       n += uint64_t(gridDim.x) * blockDim.x)
-#pragma unroll
-    for (int d = 0; d < kQ; ++d) out[d * cnt + (n - a.nb)] = buf[lslot<SOA>(a, n, d)];
-}
-
-// ---- node-range decomposition of list AA (multi-GPU) ----
-// Part p owns the contiguous list nodes [n0_p, n1_p) (blk = 0: x-major, so
-// parts are x-slabs) and holds only its own slots plus ghost copies of the
-// remote slots its nodes' scatter entries point to, in a local numbering:
-//   own slot (node n, direction slot d):  SoA d * nloc + (n - n0),
-//                                         AoS (n - n0) * 19 + d
-//   ghost slots:                          19 * nloc + gofs[s] + k
-// where k is the rank of the global slot in the sorted list of link (p <- s)
-// = the slots of s's nodes that p's entries point to.  The part's adjacency
-// is remapped to local indices (boundary adjacency remap), so its sweeps are
-// the single-lattice kernels on an nloc-node lattice.  Every slot is
-// referenced by exactly one node, so p's odd step is the only reader/writer
-// of a link's slots in that sub-step.  Exchange per AA pair: phase 0 (after
-// even) s -> r, phase 1 (after odd) r -> s, of exactly these slots -- the
-// list analogue of the direct z-slab plan (halo.hpp).
-
-// node owning the slot that entry (n, column d) points to (SlotMap::slot,
-// list_lattice.hpp:66-75: a fluid neighbour's slot d, else n's own opp slot)
-__device__ __forceinline__ uint64_t entry_owner(const ListArgs& a, int soa, uint64_t n, int d,
-                                                uint32_t e) {
-  if (soa) {
-    const uint64_t s = a.starts[d];
-    return (e >= s && e < s + a.N) ? e - s : n;
-  }
-  return e / kQ;
-}
-
-// (owner node, direction slot) of a global slot
-__device__ __forceinline__ void slot_node(const ListArgs& a, int soa, uint32_t e, uint64_t& m,
-                                          int& dd) {
-  if (!soa) {
-    m = e / kQ;
-    dd = static_cast<int>(e - m * kQ);
-    return;
-  }
-  dd = 0;
-#pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    if (e >= a.starts[d]) dd = d;  // starts ascend (padding_offsets)
-  m = e - a.starts[dd];
-}
-
-__device__ __forceinline__ uint64_t local_own(int soa, uint64_t m, int dd, uint64_t n0,
-                                              uint64_t nloc) {
-  return soa ? uint64_t(dd) * nloc + (m - n0) : (m - n0) * kQ + dd;
-}
-
-// part owning node m under the cut [N*p/P, N*(p+1)/P)
-__device__ __forceinline__ int part_of_node(uint64_t m, uint64_t N, int parts) {
-  int p = static_cast<int>(m * uint64_t(parts) / N);
-  while (p > 0 && m < N * uint64_t(p) / parts) --p;
-  while (p + 1 < parts && m >= N * uint64_t(p + 1) / parts) ++p;
-  return p;
-}
-
-__global__ void k_link_flags(const ListArgs a, int soa, uint64_t nb, uint64_t ne, uint64_t olo,
-                             uint64_t ohi, uint8_t* __restrict__ flags,
-                             uint32_t* __restrict__ vals) {
-  const uint64_t cnt = ne - nb;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt * 18;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const int d = static_cast<int>(i / cnt) + 1;
-    const uint64_t n = nb + (i - uint64_t(d - 1) * cnt);
-    const uint32_t e = a.adj[uint64_t(d - 1) * a.N + n];
-    const uint64_t m = entry_owner(a, soa, n, d, e);
-    flags[i] = m >= olo && m < ohi;
-    vals[i] = e;
-  }
-}
-
-// Local adjacency of part [n0, n0 + nloc): own entries -> local own index,
-// remote entries -> ghost index (binary search in the sorted link list).
-__global__ void k_local_adj(const ListArgs g, int soa, uint64_t n0, uint64_t nloc, int parts,
-                            const uint32_t* __restrict__ gslots,
-                            const uint64_t* __restrict__ gofs, const uint64_t* __restrict__ gcnt,
-                            uint32_t* __restrict__ ladj) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nloc * 18;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const int d = static_cast<int>(i / nloc) + 1;
-    const uint64_t j = i - uint64_t(d - 1) * nloc, n = n0 + j;
-    const uint32_t e = g.adj[uint64_t(d - 1) * g.N + n];
-    const uint64_t m = entry_owner(g, soa, n, d, e);
-    uint64_t loc;
-    if (m >= n0 && m < n0 + nloc) {
-      uint64_t mm;
-      int dd;
-      slot_node(g, soa, e, mm, dd);
-      loc = local_own(soa, mm, dd, n0, nloc);
-    } else {
-      const int s = part_of_node(m, g.N, parts);
-      const uint32_t* l = gslots + gofs[s];
-      uint64_t lo = 0, hi = gcnt[s];
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi) / 2;
-        if (l[mid] < e) lo = mid + 1; else hi = mid;
-      }
-      loc = nloc * kQ + gofs[s] + lo;
-    }
-    ladj[i] = static_cast<uint32_t>(loc);
-  }
-}
-
-// local own index of each (global) slot of a link, on the owning part
-__global__ void k_own_local_idx(const ListArgs g, int soa, uint64_t n0, uint64_t nloc,
-                                const uint32_t* __restrict__ slots, uint64_t cnt,
-                                uint32_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    uint64_t m;
-    int dd;
-    slot_node(g, soa, slots[i], m, dd);
-    out[i] = static_cast<uint32_t>(local_own(soa, m, dd, n0, nloc));
-  }
-}
-
-// initial local array of a part from the global one: own slots, then ghosts
-__global__ void k_local_init(const ListArgs g, int soa, const double* __restrict__ gbuf,
-                             uint64_t n0, uint64_t nloc, const uint32_t* __restrict__ gslots,
-                             uint64_t nghost, double* __restrict__ lbuf) {
-  const uint64_t own = nloc * kQ;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < own + nghost;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    if (i < own) {
-      const uint64_t j = soa ? i % nloc : i / kQ;
-      const int d = static_cast<int>(soa ? i / nloc : i % kQ);
-      lbuf[i] = soa ? gbuf[g.starts[d] + n0 + j] : gbuf[(n0 + j) * kQ + d];
-    } else {
-      lbuf[i] = gbuf[gslots[i - own]];
-    }
-  }
-}
-
-// boundary nodes of a part: any local entry in the ghost range
-__global__ void k_ghost_mask(const uint32_t* __restrict__ ladj, uint64_t nloc,
-                             uint8_t* __restrict__ mask) {
-  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < nloc;
-       j += uint64_t(gridDim.x) * blockDim.x) {
-    bool ghost = false;
-    for (int d = 0; d < 18 && !ghost; ++d) ghost = ladj[uint64_t(d) * nloc + j] >= nloc * kQ;
-    mask[j] = ghost;
-  }
-}
-
-// link transfers: gather by index / scatter by index / indexed copy
-__global__ void k_slots_pack(const uint32_t* __restrict__ idx, uint64_t cnt,
-                             const double* __restrict__ buf, double* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    out[i] = buf[idx[i]];
-}
-
-__global__ void k_slots_unpack(const uint32_t* __restrict__ idx, uint64_t cnt,
-                               const double* __restrict__ in, double* __restrict__ buf) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < cnt;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    buf[idx[i]] = in[i];
-}
 
 // ------------------------------------------------------------------ engine
 namespace {

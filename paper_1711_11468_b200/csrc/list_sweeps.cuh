@@ -1,0 +1,212 @@
+// List lattices: kernel arguments and the sweep kernels (pull, push, collide, AA, AoS tiles).
+// (part of the list-addressing translation unit, included by list.cu)
+#pragma once
+
+#include "lbm.hpp"
+#include "tma.cuh"
+
+namespace lbmgpu {
+
+struct ListArgs {
+  const double* src;
+  double* dst;
+  const uint32_t* adj;  // d-major [(d-1)*N + n]
+  uint64_t N;
+  uint64_t starts[kQ];  // SoA direction starts (unused for AoS)
+  TrtArgs trt;
+  uint64_t nb, ne;      // node range of this launch (AA sweeps); [0, N) by default
+  uint64_t node_base;   // canonical sweeps over a part's local arrays: node n is local n - base
+};
+
+template <bool SOA>
+__device__ __forceinline__ uint64_t lslot(const ListArgs& a, uint64_t n, int d) {
+  return SOA ? a.starts[d] + (n - a.node_base) : (n - a.node_base) * kQ + d;
+}
+
+template <bool CS>
+__device__ __forceinline__ void lst(double* p, double v) {
+  if (CS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+// list-pull (kernels_list_os.cpp:43-62, PULL): gather through the Gather
+// table, collide, coalesced stores to own slots.  COLLIDE=false is the
+// stream-only exit pass.  CS selects st.global.cs (the GPU's counterpart of
+// the nt split-store variants, kernels_list_nt.cpp).
+template <bool SOA, bool COLLIDE, bool CS>
+__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a, uint64_t pf) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  if (pf) {  // adjacency L2 prefetch for a later wave (see k_list_aa_odd)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t m = (n & ~uint64_t(31)) + pf;
+    if (lane < 18 && m < a.N)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
+  }
+  uint32_t an[18];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  double q[kQ];
+  q[0] = a.src[lslot<SOA>(a, n, 0)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = a.src[an[d - 1]];
+  if (COLLIDE) collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
+}
+
+// AoS list sweeps with the node's own record staged through a shared-memory
+// tile of kLAosTile consecutive nodes (slots 19n + d are contiguous): full-
+// sector loads / stores instead of one sector request per element.
+//   k_list_aos_tile<true>:  AA even (own slots -> opposite slots), [nb, ne)
+//   k_list_aos_tile<false>: collide pass, in place
+//   k_list_pull_aos_tile:   pull; gathers as k_list_pull, own record stored
+//                           through the tile
+constexpr int kLAosTile = 128;
+template <bool EVEN>
+__global__ void __launch_bounds__(kLAosTile) k_list_aos_tile(const ListArgs a) {
+  __shared__ __align__(128) double sh[kLAosTile * kQ];
+  __shared__ __align__(8) uint64_t bar;
+  const uint64_t n0 = a.nb + blockIdx.x * uint64_t(kLAosTile);
+  const uint32_t cnt = static_cast<uint32_t>(min(uint64_t(kLAosTile), a.ne - n0));
+  double* g = a.dst + n0 * kQ;
+  aos_tile_load<kLAosTile>(sh, g, cnt, &bar);
+  if (threadIdx.x < cnt) {
+    double* r = sh + threadIdx.x * kQ;
+    double q[kQ];
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) q[d] = r[d];
+    collide(q, a.trt);
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) r[EVEN ? opp(d) : d] = q[d];
+  }
+  aos_tile_store<kLAosTile>(g, sh, cnt);
+}
+
+template <bool COLLIDE>
+__global__ void __launch_bounds__(kLAosTile) k_list_pull_aos_tile(const ListArgs a) {
+  __shared__ __align__(128) double sh[kLAosTile * kQ];
+  const uint64_t n0 = blockIdx.x * uint64_t(kLAosTile);
+  const uint32_t cnt = static_cast<uint32_t>(min(uint64_t(kLAosTile), a.N - n0));
+  if (threadIdx.x < cnt) {
+    const uint64_t n = n0 + threadIdx.x;
+    double q[kQ];
+    q[0] = a.src[n * kQ];
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) q[d] = a.src[__ldg(a.adj + (d - 1) * a.N + n)];
+    if (COLLIDE) collide(q, a.trt);
+    double* r = sh + threadIdx.x * kQ;
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) r[d] = q[d];
+  }
+  aos_tile_store<kLAosTile>(a.dst + n0 * kQ, sh, cnt);
+}
+
+// list-push (kernels_list_os.cpp:43-62, push): own loads, scatter stores.
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_list_push(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.src[lslot<SOA>(a, n, d)];
+  collide(q, a.trt);
+  a.dst[lslot<SOA>(a, n, 0)] = q[0];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) a.dst[__ldg(a.adj + (d - 1) * a.N + n)] = q[d];
+}
+
+// collide_pass (kernels_list_os.cpp:64-72), in place on dst.
+template <bool SOA>
+__global__ void __launch_bounds__(256) k_list_collide(const ListArgs a) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.dst[lslot<SOA>(a, n, d)];
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) a.dst[lslot<SOA>(a, n, d)] = q[d];
+}
+
+// aa_even_node (kernels_list_aa.cpp:10-16): own slots -> opposite slots.
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
+  const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.ne) return;
+  double* buf = a.dst;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = buf[lslot<SOA>(a, n, d)];
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(buf + lslot<SOA>(a, n, opp(d)), q[d]);
+}
+
+// aa_odd_node (kernels_list_aa.cpp:22-31): one scatter table serves both
+// sides -- gather d through column opp(d), scatter d through column d.
+template <bool SOA, bool CS>
+__global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a, uint64_t pf) {
+  const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.ne) return;
+  double* buf = a.dst;
+  // L2 prefetch of the adjacency lines a block about `pf` nodes ahead will
+  // need (blocks are dispatched in index order): the index load of later
+  // blocks then hits L2 and the index -> gather chain shortens.  Lanes 0..17
+  // of each warp each touch one 128 B column line of that warp.
+  if (pf) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t m = (n & ~uint64_t(31)) + pf;
+    if (lane < 18 && m < a.N)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
+  }
+  uint32_t an[18];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  double q[kQ];
+  q[0] = buf[lslot<SOA>(a, n, 0)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
+  collide(q, a.trt);
+  lst<CS>(buf + lslot<SOA>(a, n, 0), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) lst<CS>(buf + an[d - 1], q[d]);
+}
+
+// Persistent variant of k_list_aa_odd: every thread walks n, n+G, ... and
+// loads the 18 adjacency entries of its NEXT node while the current node's
+// gathers and collision are in flight, so the index-load latency no longer
+// sits in series in front of the dependent PDF gathers.
+template <bool SOA>
+__global__ void __launch_bounds__(256, 2) k_list_aa_odd_pipe(const ListArgs a) {
+  const uint64_t G = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  double* buf = a.dst;
+  uint32_t an[18];
+  if (n < a.N) {
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  }
+  for (; n < a.N; n += G) {
+    double q[kQ];
+    q[0] = buf[lslot<SOA>(a, n, 0)];
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
+    uint32_t nx[18];
+    const uint64_t m = n + G;
+    if (m < a.N) {
+#pragma unroll
+      for (int d = 1; d < kQ; ++d) nx[d - 1] = __ldg(a.adj + (d - 1) * a.N + m);
+    }
+    collide(q, a.trt);
+    buf[lslot<SOA>(a, n, 0)] = q[0];
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) buf[an[d - 1]] = q[d];
+#pragma unroll
+    for (int d = 0; d < 18; ++d) an[d] = nx[d];
+  }
+}
+
+}  // namespace lbmgpu
