@@ -664,8 +664,15 @@ class DirectEngine final : public Engine {
   // counters instead of grid barriers.
   template <bool SOA, int KIND>
   void launch_flow(const DirectArgs& a, double* other, long sweeps, const char* name) {
-    auto kern = k_full_flow<SOA, KIND>;
-    const int threads = flow_threads_;
+    // block shapes as for the barrier kernel: (threads, min blocks per SM)
+    // (cfg 1, 160 threads x 4 blocks/SM: push 15.8k, pull 16.4k, AA 16.8k
+    // MFLUP/s against 16.5k / 18.1k / 18.0k for the barrier kernel)
+    auto kern = flow_threads_ == 160   ? k_full_flow<SOA, KIND, 160, 4>
+                : flow_threads_ == 128 ? k_full_flow<SOA, KIND, 128, 5>
+                : flow_threads_ == 64  ? k_full_flow<SOA, KIND, 64, 8>
+                                       : k_full_flow<SOA, KIND, 256, 2>;
+    const int threads =
+        flow_threads_ == 160 || flow_threads_ == 128 || flow_threads_ == 64 ? flow_threads_ : 256;
     int per_sm = 0;
     LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
     const uint64_t tasks = uint64_t(parts_[0].nzl) * ceil_div(P_, threads);

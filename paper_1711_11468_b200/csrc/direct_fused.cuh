@@ -103,8 +103,8 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <bool SOA, int KIND>
-__global__ void __launch_bounds__(256) k_full_flow(DirectArgs a, double* other, long sweeps,
+template <bool SOA, int KIND, int TPB = 256, int MINB = 1>
+__global__ void __launch_bounds__(TPB, MINB) k_full_flow(DirectArgs a, double* other, long sweeps,
                                                    unsigned* plane_done, unsigned base) {
   // Tasks are blockDim-node chunks run by whole blocks.  (32-node warp
   // tasks without block barriers measured 2x slower: the release/acquire
