@@ -431,6 +431,11 @@ def test_list_node_range_parts_bitwise(name, kind, dims, parts):
     k.advance(PARAMS, FORCE, 4)
     assert np.array_equal(k.snapshot(), ref.snapshot())
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
+    # macro fields and the fingerprint go through the per-part local arrays
+    assert k.fingerprint() == ref.fingerprint()
+    # the global adjacency is released after the local numbering is built
+    with pytest.raises(lbm.ConfigError):
+        k.export_structure()
 
 
 def test_list_parts_nccl_transport_single_gpu():
