@@ -342,6 +342,7 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_FUSED_FLOW")) flow_threads_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_FUSED_SHAPE")) fused_shape_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_GRID_SYNC")) barrier_mode_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_PUSH_TMASK")) use_tmask_ = std::atoi(e) != 0;
       if (flow_threads_ < 0 || flow_threads_ > 256 || flow_threads_ % 32)
         throw ConfigError("LBMGPU_FUSED_FLOW must be 0 or a multiple of 32 in [32, 256]");
@@ -628,10 +629,12 @@ class DirectEngine final : public Engine {
       launch_flow<SOA, KIND>(a, other, sweeps, name);
       return;
     }
-    // block shape: measured on cfg 1 (B200), push (320, 2) 15.5k MFLUP/s,
-    // pull (160, 4) 18.3k, AA (160, 4) 18.0k; (256, 1) lands at 132-146
-    // registers, one block per SM, 11k
-    const int shape = fused_shape_ >= 0 ? fused_shape_ : KIND == kFusedPush ? 1 : 3;
+    // block shape, measured on cfg 1 (B200, cooperative-groups grid sync,
+    // 20 sweeps per launch): push (160, 4) 18.1k MFLUP/s [(320, 2) 17.4k],
+    // pull (160, 4) 19.6k, AA SoA (256, 2) 24.6k [(160, 4) 19.6k], AA AoS
+    // (160, 4); the unconstrained (256, 1) compile lands at 132-146
+    // registers, one block per SM
+    const int shape = fused_shape_ >= 0 ? fused_shape_ : (KIND == kFusedAA && SOA) ? 5 : 3;
     switch (shape) {
       case 1: launch_fused_as<SOA, KIND, 320, 2>(a, other, steps, name, sweeps); break;
       case 2: launch_fused_as<SOA, KIND, 224, 3>(a, other, steps, name, sweeps); break;
@@ -651,7 +654,7 @@ class DirectEngine final : public Engine {
     const uint64_t want = ceil_div(a.count, TPB);
     const int grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(per_sm, 1)) * sm_count_)));
-    GridBarrier bar{barrier_.get(), barrier_.get() + 1};
+    GridBarrier bar{barrier_.get(), barrier_.get() + 1, barrier_mode_};
     DirectArgs aa = a;
     void* params[] = {&aa, &other, &steps, &bar};
     const int tok = stats_.begin(name, stream_, sweeps);
@@ -1084,6 +1087,10 @@ class DirectEngine final : public Engine {
   // kernel (measured slower on cfg 1: 12.8k vs 14.8k MFLUP/s; opt-in)
   int flow_threads_ = 0;
   bool use_tmask_ = true;  // push: precomputed solid-target masks
+  // fused kernel grid barrier: 1 = cooperative_groups grid sync (cfg 1: push
+  // 16.5k -> 17.3k, pull 18.1k -> 19.5k, AA 18.0k -> 19.7k MFLUP/s against
+  // the counter + generation barrier, mode 0)
+  int barrier_mode_ = 1;
   int fused_shape_ = -1;  // grid-barrier kernel block shape (-1: per kind, see launch_fused)
   int sm_count_ = 148;
   std::vector<Part> parts_;

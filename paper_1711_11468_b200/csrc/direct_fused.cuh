@@ -3,6 +3,8 @@
 #pragma once
 
 #include "direct_args.cuh"
+#include <cooperative_groups.h>
+
 #include "direct_node.cuh"
 
 namespace lbmgpu {
@@ -16,9 +18,14 @@ namespace lbmgpu {
 struct GridBarrier {
   unsigned* count;
   unsigned* gen;
+  int mode;  // 0: counter + generation below, 1: cooperative_groups grid sync
 };
 
 __device__ __forceinline__ void grid_sync(const GridBarrier& b) {
+  if (b.mode == 1) {
+    cooperative_groups::this_grid().sync();
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* vgen = b.gen;
