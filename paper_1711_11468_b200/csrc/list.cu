@@ -166,6 +166,8 @@ class ListEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_LIST_ODD_PIPE")) odd_pipe_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_RIA_MODE")) ria_mode_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
+      if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
+        fused_bytes_ = uint64_t(std::atoll(e)) << 20;
       if (const char* e = std::getenv("LBMGPU_LIST_THREADS")) {
         threads_ = std::atoi(e);
         threads_env_ = true;
@@ -493,7 +495,50 @@ class ListEngine final : public Engine {
     stats_.end(tok, stream_);
   }
 
+  // One cooperative launch for all sweeps when the PDFs and the adjacency
+  // live in L2 (<= fused_bytes_), a single part, no run coding.
+  template <bool SOA, int KIND>
+  void launch_list_fused(ListArgs a, double* other, long sweeps, const char* name) {
+    constexpr int TPB = 256, MINB = 2;
+    auto kern = k_list_fused<SOA, KIND, TPB, MINB>;
+    int per_sm = 0;
+    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, 0));
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(a.N, TPB), uint64_t(std::max(per_sm, 1)) * sm_count_)));
+    void* params[] = {&a, &other, &sweeps};
+    const int tok = stats_.begin(name, stream_, sweeps);
+    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, TPB, params, 0,
+                                         stream_));
+    stats_.end(tok, stream_);
+  }
+
+  bool advance_fused(const TrtArgs& t, long steps) {
+    if (!lparts_.empty() || desc_.ria || steps < 2 || fused_bytes_ == 0) return false;
+    const uint64_t nbuf = desc_.prop == Prop::Aa ? 1 : 2;
+    if (nbuf * total_slots_ * 8 + 72 * n_fluid_ > fused_bytes_) return false;
+    ListArgs a = base_args();
+    a.trt = t;
+    const bool soa = desc_.soa;
+    if (desc_.prop == Prop::Aa) {
+      a.src = a.dst = buf_[0].get();
+      soa ? launch_list_fused<true, kListFusedAA>(a, nullptr, steps, "list_aa_soa_fused")
+          : launch_list_fused<false, kListFusedAA>(a, nullptr, steps, "list_aa_aos_fused");
+      return true;
+    }
+    a.src = a.dst = buf_[cur_].get();
+    double* other = buf_[1 - cur_].get();
+    if (desc_.prop == Prop::OsPush)
+      soa ? launch_list_fused<true, kListFusedPush>(a, other, steps, "list_push_soa_fused")
+          : launch_list_fused<false, kListFusedPush>(a, other, steps, "list_push_aos_fused");
+    else
+      soa ? launch_list_fused<true, kListFusedPull>(a, other, steps + 1, "list_pull_soa_fused")
+          : launch_list_fused<false, kListFusedPull>(a, other, steps + 1, "list_pull_aos_fused");
+    if (steps & 1) cur_ ^= 1;
+    return true;
+  }
+
   void advance(const TrtArgs& t, long steps) override {
+    if (advance_fused(t, steps)) return;
     ListArgs a = base_args();
     a.trt = t;
     const bool soa = desc_.soa;
@@ -809,6 +854,7 @@ class ListEngine final : public Engine {
   DevBuf<uint8_t> ria_nid_;     // pattern id of every node
   int threads_ = 256;           // CTA size of the sweeps
   bool aos_tile_ = true;        // AoS own-record sweeps through shared-memory tiles
+  uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold (PDFs + adjacency)
   bool threads_env_ = false;    // threads_ set by LBMGPU_LIST_THREADS
   uint64_t pf_ = 0;             // adjacency L2 prefetch distance in nodes (AA odd)
   uint64_t pull_pf_ = 0;        // same for the one-step pull sweeps

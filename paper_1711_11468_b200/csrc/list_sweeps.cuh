@@ -2,6 +2,8 @@
 // (part of the list-addressing translation unit, included by list.cu)
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "lbm.hpp"
 #include "tma.cuh"
 
@@ -31,6 +33,84 @@ __device__ __forceinline__ void lst(double* p, double v) {
     *p = v;
 }
 
+// PDF loads: plain in the one-sweep-per-launch kernels, L2-only
+// (ld.global.cg) in the fused multi-sweep kernel, whose later sweeps read
+// lines other SMs rewrote after a grid barrier.
+template <bool CG>
+__device__ __forceinline__ double lld(const double* p) {
+  if (CG) return __ldcg(p);
+  return *p;
+}
+
+// ---- per-node bodies (one-sweep kernels and the fused kernel) --------------
+// list-pull (kernels_list_os.cpp:43-62, PULL)
+template <bool SOA, bool COLLIDE, bool CS, bool CG>
+__device__ __forceinline__ void list_pull_node(const ListArgs& a, uint64_t n) {
+  uint32_t an[18];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  double q[kQ];
+  q[0] = lld<CG>(a.src + lslot<SOA>(a, n, 0));
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = lld<CG>(a.src + an[d - 1]);
+  if (COLLIDE) collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
+}
+
+// list-push (kernels_list_os.cpp:43-62, push): own loads, scatter stores
+template <bool SOA, bool CG>
+__device__ __forceinline__ void list_push_node(const ListArgs& a, uint64_t n) {
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = lld<CG>(a.src + lslot<SOA>(a, n, d));
+  collide(q, a.trt);
+  a.dst[lslot<SOA>(a, n, 0)] = q[0];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) a.dst[__ldg(a.adj + (d - 1) * a.N + n)] = q[d];
+}
+
+// collide_pass (kernels_list_os.cpp:64-72), in place on dst
+template <bool SOA, bool CG>
+__device__ __forceinline__ void list_collide_node(const ListArgs& a, uint64_t n) {
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = lld<CG>(a.dst + lslot<SOA>(a, n, d));
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) a.dst[lslot<SOA>(a, n, d)] = q[d];
+}
+
+// aa_even_node (kernels_list_aa.cpp:10-16): own slots -> opposite slots
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void list_aa_even_node(const ListArgs& a, uint64_t n) {
+  double* buf = a.dst;
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = lld<CG>(buf + lslot<SOA>(a, n, d));
+  collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(buf + lslot<SOA>(a, n, opp(d)), q[d]);
+}
+
+// aa_odd_node (kernels_list_aa.cpp:22-31): one scatter table serves both
+// sides -- gather d through column opp(d), scatter d through column d
+template <bool SOA, bool CS, bool CG>
+__device__ __forceinline__ void list_aa_odd_node(const ListArgs& a, uint64_t n) {
+  double* buf = a.dst;
+  uint32_t an[18];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
+  double q[kQ];
+  q[0] = lld<CG>(buf + lslot<SOA>(a, n, 0));
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = lld<CG>(buf + an[opp(d) - 1]);
+  collide(q, a.trt);
+  lst<CS>(buf + lslot<SOA>(a, n, 0), q[0]);
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) lst<CS>(buf + an[d - 1], q[d]);
+}
+
 // list-pull (kernels_list_os.cpp:43-62, PULL): gather through the Gather
 // table, collide, coalesced stores to own slots.  COLLIDE=false is the
 // stream-only exit pass.  CS selects st.global.cs (the GPU's counterpart of
@@ -45,16 +125,7 @@ __global__ void __launch_bounds__(256) k_list_pull(const ListArgs a, uint64_t pf
     if (lane < 18 && m < a.N)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
   }
-  uint32_t an[18];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
-  double q[kQ];
-  q[0] = a.src[lslot<SOA>(a, n, 0)];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = a.src[an[d - 1]];
-  if (COLLIDE) collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
+  list_pull_node<SOA, COLLIDE, CS, false>(a, n);
 }
 
 // AoS list sweeps with the node's own record staged through a shared-memory
@@ -109,13 +180,7 @@ template <bool SOA>
 __global__ void __launch_bounds__(256) k_list_push(const ListArgs a) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = a.src[lslot<SOA>(a, n, d)];
-  collide(q, a.trt);
-  a.dst[lslot<SOA>(a, n, 0)] = q[0];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) a.dst[__ldg(a.adj + (d - 1) * a.N + n)] = q[d];
+  list_push_node<SOA, false>(a, n);
 }
 
 // collide_pass (kernels_list_os.cpp:64-72), in place on dst.
@@ -123,12 +188,7 @@ template <bool SOA>
 __global__ void __launch_bounds__(256) k_list_collide(const ListArgs a) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = a.dst[lslot<SOA>(a, n, d)];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) a.dst[lslot<SOA>(a, n, d)] = q[d];
+  list_collide_node<SOA, false>(a, n);
 }
 
 // aa_even_node (kernels_list_aa.cpp:10-16): own slots -> opposite slots.
@@ -136,13 +196,7 @@ template <bool SOA, bool CS>
 __global__ void __launch_bounds__(256) k_list_aa_even(const ListArgs a) {
   const uint64_t n = a.nb + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.ne) return;
-  double* buf = a.dst;
-  double q[kQ];
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = buf[lslot<SOA>(a, n, d)];
-  collide(q, a.trt);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) lst<CS>(buf + lslot<SOA>(a, n, opp(d)), q[d]);
+  list_aa_even_node<SOA, CS, false>(a, n);
 }
 
 // aa_odd_node (kernels_list_aa.cpp:22-31): one scatter table serves both
@@ -162,17 +216,8 @@ __global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a, uint64_t 
     if (lane < 18 && m < a.N)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
   }
-  uint32_t an[18];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
-  double q[kQ];
-  q[0] = buf[lslot<SOA>(a, n, 0)];
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
-  collide(q, a.trt);
-  lst<CS>(buf + lslot<SOA>(a, n, 0), q[0]);
-#pragma unroll
-  for (int d = 1; d < kQ; ++d) lst<CS>(buf + an[d - 1], q[d]);
+  (void)buf;
+  list_aa_odd_node<SOA, CS, false>(a, n);
 }
 
 // Persistent variant of k_list_aa_odd: every thread walks n, n+G, ... and
@@ -206,6 +251,42 @@ __global__ void __launch_bounds__(256, 2) k_list_aa_odd_pipe(const ListArgs a) {
     for (int d = 1; d < kQ; ++d) buf[an[d - 1]] = q[d];
 #pragma unroll
     for (int d = 0; d < 18; ++d) an[d] = nx[d];
+  }
+}
+
+// ---- fused multi-sweep launch for L2-resident list lattices ---------------
+// As k_full_fused (direct_fused.cuh): one cooperative launch runs all sweeps,
+// cooperative-groups grid sync between them, grid-stride node loops, PDF
+// loads ld.global.cg, the per-node bodies above -- bitwise the per-sweep
+// kernels' results.
+enum ListFusedKind { kListFusedAA = 0, kListFusedPush = 1, kListFusedPull = 2 };
+template <bool SOA, int KIND, int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) k_list_fused(ListArgs a, double* other, long sweeps) {
+  const uint64_t G = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t i0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  double* bufs[2] = {a.dst, other};
+  for (long s = 0; s < sweeps; ++s) {
+    if (KIND == kListFusedAA) {
+      for (uint64_t n = i0; n < a.N; n += G)
+        (s & 1) ? list_aa_odd_node<SOA, false, true>(a, n)
+                : list_aa_even_node<SOA, false, true>(a, n);
+    } else if (KIND == kListFusedPush) {
+      a.src = bufs[s & 1];
+      a.dst = bufs[(s & 1) ^ 1];
+      for (uint64_t n = i0; n < a.N; n += G) list_push_node<SOA, true>(a, n);
+    } else if (s == 0) {  // pull: collide pass on the current grid
+      a.dst = bufs[0];
+      for (uint64_t n = i0; n < a.N; n += G) list_collide_node<SOA, true>(a, n);
+    } else {
+      a.src = bufs[(s - 1) & 1];
+      a.dst = bufs[s & 1];
+      if (s + 1 < sweeps)
+        for (uint64_t n = i0; n < a.N; n += G) list_pull_node<SOA, true, false, true>(a, n);
+      else
+        for (uint64_t n = i0; n < a.N; n += G) list_pull_node<SOA, false, false, true>(a, n);
+    }
+    if (s + 1 < sweeps) grid.sync();
   }
 }
 

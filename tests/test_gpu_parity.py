@@ -66,7 +66,7 @@ def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
     LBMGPU_FUSED_MB=0 and the dataflow variant (k_full_flow) with
     LBMGPU_FUSED_FLOW=256 / 64 (64: several chunks per plane, partial last
     chunk), so every path is checked bit for bit."""
-    if fused != "default" and name.startswith("list-"):
+    if fused.startswith("flow-") and name.startswith("list-"):
         pytest.skip("direct-addressing knob")
     if fused == "per-sweep":
         monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
