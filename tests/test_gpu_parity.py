@@ -222,6 +222,27 @@ def test_flow_launch_equals_per_sweep_at_scale(name, kind, dims, monkeypatch):
     assert len(set(res)) == 1, (name, kind, [f"{r:016x}" for r in res])
 
 
+@pytest.mark.parametrize("name", ["list-aa-soa", "list-pull-soa", "list-push-soa", "list-aa-aos",
+                                  "list-pull-aos"])
+@pytest.mark.parametrize("kind,dims", [("channel", (64, 64, 64)), ("blocks", (48, 40, 36))])
+def test_list_fused_launch_equals_per_sweep_at_scale(name, kind, dims, monkeypatch):
+    """The fused multi-sweep list launch on a cfg-1-sized lattice (hundreds
+    of blocks racing through 21 sweeps, grid sync between them) is bitwise
+    the per-sweep kernels' result."""
+    steps = 20 if "-aa-" in name else 21
+    res = []
+    for mb in (None, "0"):
+        if mb is not None:
+            monkeypatch.setenv("LBMGPU_FUSED_MB", mb)
+        k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
+        k.load_perturbed(8)
+        k.advance(PARAMS, FORCE, steps)
+        k.advance(PARAMS, FORCE, 4)
+        res.append(k.fingerprint())
+        del k
+    assert res[0] == res[1], (name, kind, [f"{r:016x}" for r in res])
+
+
 def _list_kernel_for(layout, scatter):
     if scatter:
         return "list-aa-soa" if layout == "soa" else "list-aa-aos"
