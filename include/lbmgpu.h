@@ -268,6 +268,16 @@ uint64_t lbmgpu_fnv1a(const void* data, uint64_t nbytes);
 const char* lbmgpu_last_error(void);
 int lbmgpu_abi_version(void);
 
+/* Debug aid (no reference equivalent): with LBMGPU_GUARD=1 in the
+ * environment when buffers are allocated, every device buffer carries 4 KiB
+ * guard zones of a fixed byte pattern on both sides; this counts the live
+ * buffers whose guards were overwritten (out-of-bounds device writes).  The
+ * description of the first corruptions is left in lbmgpu_last_error(). */
+int lbmgpu_guard_check(int* corrupted);
+/* Negative control: writes 8 bytes past a fresh guarded buffer and reports
+ * how many corrupted buffers lbmgpu_guard_check would see (1 expected). */
+int lbmgpu_guard_selftest(int* detected);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

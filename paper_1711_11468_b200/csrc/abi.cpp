@@ -227,6 +227,22 @@ uint64_t lbmgpu_fnv1a(const void* data, uint64_t nbytes) {
 }
 int lbmgpu_abi_version(void) { return LBMGPU_ABI_VERSION; }
 
+int lbmgpu_guard_check(int* corrupted) {
+  return guard([&] {
+    need(corrupted, "corrupted");
+    std::string rep;
+    *corrupted = guard_check(&rep);
+    if (*corrupted) g_err = "guard zones overwritten: " + rep;
+  });
+}
+
+int lbmgpu_guard_selftest(int* detected) {
+  return guard([&] {
+    need(detected, "detected");
+    *detected = guard_selftest();
+  });
+}
+
 int lbmgpu_kernel_names(char* buf, size_t cap) {
   return guard([&] {
     std::string s;

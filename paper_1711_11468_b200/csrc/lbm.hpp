@@ -62,6 +62,18 @@ std::array<uint64_t, kQ> padding_offsets(uint64_t n_fluid, const Padding& p,
                                          uint64_t* total);
 
 // ------------------------------------------------------- device buffers
+// Guard zones (debug aid, LBMGPU_GUARD=1 at allocation time; the pool has no
+// compute-sanitizer): every device buffer gets kGuardBytes of a known byte
+// pattern on both sides, and guard_check() reports buffers whose guards a
+// kernel overwrote.  Off by default (plain cudaMalloc).
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_enabled();
+void* guarded_malloc(size_t bytes);   // returns the user pointer
+void guarded_free(void* user);
+int guard_check(std::string* report);  // number of corrupted buffers
+int guard_selftest();                  // negative control: 1 expected
+
 template <class T>
 class DevBuf {
  public:
@@ -70,20 +82,45 @@ class DevBuf {
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), guarded_(o.guarded_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+    o.guarded_ = false;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      guarded_ = o.guarded_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+      o.guarded_ = false;
+    }
     return *this;
   }
   void alloc(size_t n) {
     release();
-    if (n) LBM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    if (n) {
+      if (guard_enabled()) {
+        p_ = static_cast<T*>(guarded_malloc(n * sizeof(T)));
+        guarded_ = true;
+      } else {
+        LBM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+      }
+    }
     n_ = n;
   }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) {
+      if (guarded_)
+        guarded_free(p_);
+      else
+        cudaFree(p_);
+    }
     p_ = nullptr;
     n_ = 0;
+    guarded_ = false;
   }
   T* get() const { return p_; }
   size_t size() const { return n_; }
@@ -92,6 +129,7 @@ class DevBuf {
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
+  bool guarded_ = false;
 };
 
 // Device-resident FlagField (geometry.hpp:16-29): canonical x-major order.

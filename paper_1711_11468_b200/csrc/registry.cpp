@@ -5,6 +5,10 @@
 
 #include "lbm.hpp"
 
+#include <cstdlib>
+#include <map>
+#include <mutex>
+
 namespace lbmgpu {
 
 // kernel_names() (reference src/kernels.cpp:22-43), canonical order.
@@ -188,6 +192,79 @@ std::array<bool, 3> validate_geometry(const GeomSpec& s) {
     default:
       throw ConfigError("unknown geometry kind (valid: channel, slit, pipe, blocks)");
   }
+}
+
+// ---- guard zones around device buffers (lbm.hpp) ---------------------------
+namespace {
+struct GuardRegistry {
+  std::mutex m;
+  std::map<void*, size_t> live;  // user pointer -> user bytes
+  static GuardRegistry& get() {
+    static GuardRegistry r;
+    return r;
+  }
+};
+}  // namespace
+
+bool guard_enabled() {
+  const char* e = std::getenv("LBMGPU_GUARD");
+  return e && std::atoi(e) != 0;
+}
+
+void* guarded_malloc(size_t bytes) {
+  const size_t user = (bytes + 255) / 256 * 256;  // keep the 256-byte alignment
+  unsigned char* raw = nullptr;
+  LBM_CUDA(cudaMalloc(reinterpret_cast<void**>(&raw), user + 2 * kGuardBytes));
+  LBM_CUDA(cudaMemset(raw, kGuardByte, kGuardBytes));
+  LBM_CUDA(cudaMemset(raw + kGuardBytes + user, kGuardByte, kGuardBytes));
+  void* p = raw + kGuardBytes;
+  GuardRegistry& r = GuardRegistry::get();
+  std::lock_guard<std::mutex> lk(r.m);
+  r.live[p] = user;
+  return p;
+}
+
+void guarded_free(void* user) {
+  GuardRegistry& r = GuardRegistry::get();
+  {
+    std::lock_guard<std::mutex> lk(r.m);
+    r.live.erase(user);
+  }
+  cudaFree(static_cast<unsigned char*>(user) - kGuardBytes);
+}
+
+// Negative control of the guard zones: a guarded buffer written 8 bytes past
+// its end must be reported (returns the count guard_check saw, then frees).
+int guard_selftest() {
+  unsigned char* p = static_cast<unsigned char*>(guarded_malloc(1000));
+  LBM_CUDA(cudaMemset(p + 1024, 0, 8));  // user size rounds up to 1024
+  const int bad = guard_check(nullptr);
+  guarded_free(p);
+  return bad;
+}
+
+int guard_check(std::string* report) {
+  LBM_CUDA(cudaDeviceSynchronize());
+  GuardRegistry& r = GuardRegistry::get();
+  std::lock_guard<std::mutex> lk(r.m);
+  std::vector<unsigned char> h(kGuardBytes);
+  int bad = 0;
+  for (const auto& [p, bytes] : r.live) {
+    unsigned char* user = static_cast<unsigned char*>(p);
+    for (int side = 0; side < 2; ++side) {
+      const unsigned char* g = side ? user + bytes : user - kGuardBytes;
+      LBM_CUDA(cudaMemcpy(h.data(), g, kGuardBytes, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < kGuardBytes; ++i)
+        if (h[i] != kGuardByte) {
+          ++bad;
+          if (report)
+            *report += std::string(side ? "after" : "before") + " buffer of " +
+                       std::to_string(bytes) + " bytes at offset " + std::to_string(i) + "; ";
+          break;
+        }
+    }
+  }
+  return bad;
 }
 
 }  // namespace lbmgpu

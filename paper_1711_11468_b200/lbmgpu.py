@@ -101,6 +101,8 @@ def _load():
     L.lbmgpu_snapshot_local.argtypes = [vp, vp, u64]
     L.lbmgpu_load_state_local.argtypes = [vp, vp, u64]
     L.lbmgpu_halo_plan.argtypes = [i, i, i, vp, i, P(i)]
+    L.lbmgpu_guard_check.argtypes = [P(i)]
+    L.lbmgpu_guard_selftest.argtypes = [P(i)]
     return L
 
 
@@ -662,6 +664,24 @@ def halo_plan(nz: int, parts: int, ring: bool, one_step: bool = False):
     _check(lib.lbmgpu_halo_plan(nz, parts, 2 if one_step else int(ring), rows.ctypes.data, cap,
                                 C.byref(n)))
     return rows[:7 * n.value].reshape(-1, 7)
+
+
+def guard_check():
+    """Debug aid: (number of live device buffers whose 4 KiB guard zones were
+    overwritten, description).  Buffers get guard zones only when
+    LBMGPU_GUARD=1 is set at allocation time."""
+    n = C.c_int()
+    rc = lib.lbmgpu_guard_check(C.byref(n))
+    msg = lib.lbmgpu_last_error().decode() if n.value else ""
+    _check(rc)
+    return n.value, msg
+
+
+def guard_selftest() -> int:
+    """Negative control of guard_check (1 = the planted overrun was seen)."""
+    n = C.c_int()
+    _check(lib.lbmgpu_guard_selftest(C.byref(n)))
+    return n.value
 
 
 def microbench(kind: str, working_set_bytes: int = 8 << 30, reps: int = 5) -> float:

@@ -174,6 +174,54 @@ def test_aos_aa_odd_halo_tiles_bitwise(kind, dims, monkeypatch):
     assert len(set(res)) == 1, [f"{r:016x}" for r in res]
 
 
+def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
+    """Memory-safety check in place of compute-sanitizer (closed on this
+    pool): with LBMGPU_GUARD=1 every device buffer carries 4 KiB guard zones
+    of a fixed byte pattern; after every kernel family has run -- each name
+    per-sweep and fused, the TMA tiles and 3-D halo tiles, RIA codings,
+    z-slab and node-range decompositions with both transports, snapshot /
+    load / verify -- no guard byte may have changed."""
+    monkeypatch.setenv("LBMGPU_GUARD", "1")
+    assert lbm.lbmgpu.guard_selftest() == 1  # a planted 8-byte overrun is seen
+    small = lbm.GeometrySpec("blocks", 12, 10, 10)
+    tiled = lbm.GeometrySpec("channel", 32, 12, 8)  # nx % 16, ny/nz % 4: halo tiles
+    keep = []
+    for fused in ("96", "0"):
+        monkeypatch.setenv("LBMGPU_FUSED_MB", fused)
+        for name in lbm.kernel_names():
+            for spec in (small, tiled):
+                k = lbm.make_kernel(lbm.make_descriptor(name, blk=2 if "list" in name else 0), spec)
+                k.load_perturbed(3)
+                k.advance(PARAMS, FORCE, 6)
+                k.load_state(k.snapshot())
+                k.total_mass()
+                keep.append(k)
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("LBMGPU_RIA_MODE", mode)
+        k = lbm.make_kernel(lbm.make_descriptor("list-aa-ria-soa"), small)
+        k.advance(PARAMS, FORCE, 4)
+        keep.append(k)
+    for name in ("aa-soa", "blk-push-soa", "blk-pull-soa"):
+        for extra in ({}, {"nccl_id": lbm.lbmgpu.nccl_unique_id()}):
+            k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec("channel", 16, 12, 24),
+                                dist={"virtual_parts": 3, **extra})
+            k.advance(PARAMS, FORCE, 4)
+            k.snapshot_local()
+            keep.append(k)
+    for extra in ({}, {"nccl_id": lbm.lbmgpu.nccl_unique_id()}):
+        k = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), lbm.GeometrySpec("blocks", 16, 16, 16),
+                            dist={"virtual_parts": 3, **extra})
+        k.advance(PARAMS, FORCE, 4)
+        k.snapshot()
+        keep.append(k)
+    rep = lbm.verify_kernel(lbm.make_descriptor("aa-soa"))
+    assert rep["passed"]
+    bad, msg = lbm.lbmgpu.guard_check()
+    assert bad == 0, msg
+    del keep
+
+
 def test_edge_shapes_match_reference(edge_golden):
     """Degenerate and ragged shapes for every kernel (tests/golden/edge.json,
     generated by the reference): 1- and 2-cell periodic axes that wrap onto
