@@ -226,6 +226,9 @@ def main():
     ap.add_argument("--virtual-parts", type=int, default=1,
                     help="1 GPU: emulate the multi-GPU decomposition with this many parts "
                          "(device-copy halos) -- an overhead probe, not a bench line")
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="with --virtual-parts: halos through the NCCL transport (one rank "
+                         "owning every part, self send/recv) instead of device copies")
     ap.add_argument("--kernel", default=None,
                     help="run another kernel name on the config's geometry (extra lines)")
     ap.add_argument("--dims", default=None,
@@ -274,6 +277,8 @@ def main():
     replicas = world > 1 and not decomposable
     if world == 1 and args.virtual_parts > 1:
         dspec = {"virtual_parts": args.virtual_parts}
+        if args.nccl_self:
+            dspec["nccl_id"] = lbm.nccl_unique_id()
     if world > 1 and not replicas:
         obj = [lbm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -378,7 +383,9 @@ def main():
         line["config"]["parallelism"] = f"node-range (x-slab) decomposition x{world}, NCCL index-list halos"
     if world == 1 and args.virtual_parts > 1:
         line["config"]["parallelism"] = (f"EMULATED {args.virtual_parts}-part decomposition on 1 GPU "
-                                         "(device-copy halos; overhead probe)")
+                                         + ("(NCCL self send/recv halos" if args.nccl_self
+                                            else "(device-copy halos")
+                                         + "; overhead probe)")
     line.update({
         "value": mflups,
         "ms_per_step": ms / args.steps,
