@@ -1,0 +1,65 @@
+"""Seeded random parity fuzzing on the GPU against the oracle's textbook
+steppers (test infrastructure; the 32-case subset runs in
+tests/test_gpu_parity.py::test_randomized_against_oracle).
+
+    python tools/fuzz_parity.py [cases] [seed0]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_1711_11468_b200 as lbm  # noqa: E402
+from oracle.oracle import Port  # noqa: E402
+
+port = Port()
+names = lbm.kernel_names()
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 500
+seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
+bad = 0
+for case in range(cases):
+    rng = np.random.default_rng(seed0 + case)
+    while True:
+        kind = str(rng.choice(["channel", "slit", "pipe", "blocks"]))
+        nx = int(rng.choice([16, 32, 48, 64])) if rng.random() < 0.5 else int(rng.integers(1, 40))
+        ny, nz = int(rng.integers(3, 26)), int(rng.integers(3, 26))
+        block, spacing = int(rng.integers(1, 5)), int(rng.integers(0, 4))
+        try:
+            _, _, nf = port.geometry(kind, nx, ny, nz, block, spacing)
+        except ValueError:
+            continue
+        if nf > 0:
+            break
+    name = str(rng.choice(names))
+    blk = int(rng.integers(0, 5)) if name.startswith("list-") else 0
+    tau = float(rng.uniform(0.52, 1.95))
+    g = tuple(float(v) for v in rng.uniform(-3e-5, 3e-5, 3))
+    steps = int(rng.integers(1, 6)) * 2 if "aa" in name.split("-") else int(rng.integers(1, 11))
+    os.environ["LBMGPU_FUSED_MB"] = str(rng.choice(["96", "0"]))
+    parts = int(rng.choice([1, 1, 2, 3]))
+    dist = None
+    if parts > 1 and nz >= parts and (name in ("aa-soa", "aa-vec-soa", "blk-push-soa", "blk-pull-soa")
+                                      or (name in ("list-aa-soa", "list-aa-aos") and blk == 0)):
+        dist = {"virtual_parts": parts}
+    init = port.perturbed(nf, seed0 + case)
+    fam = "half" if name.startswith("list-") else "full"
+    params = lbm.TrtParams.from_tau(tau)
+    expect, _ = port.run(fam, kind, nx, ny, nz, steps, params.omega_plus, g=g, init=init,
+                         block=block, spacing=spacing)
+    try:
+        k = lbm.make_kernel(lbm.make_descriptor(name, blk=blk),
+                            lbm.GeometrySpec(kind, nx, ny, nz, block, spacing), dist=dist)
+        k.load_state(init)
+        k.advance(params, lbm.BodyForce(g), steps)
+        ok = np.array_equal(k.snapshot(), expect)
+        del k
+    except lbm.ConfigError as e:  # e.g. more parts than fluid nodes
+        print("config", case, name, kind, (nx, ny, nz), dist, e)
+        continue
+    if not ok:
+        bad += 1
+        print("MISMATCH", case, name, kind, (nx, ny, nz), block, spacing, blk, tau, steps,
+              os.environ["LBMGPU_FUSED_MB"], dist, flush=True)
+print(f"{cases} cases, {bad} mismatches", flush=True)
+sys.exit(1 if bad else 0)
