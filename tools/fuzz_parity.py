@@ -2,7 +2,7 @@
 steppers (test infrastructure; the 32-case subset runs in
 tests/test_gpu_parity.py::test_randomized_against_oracle).
 
-    python tools/fuzz_parity.py [cases] [seed0]
+    [FUZZ_BIG=1] python tools/fuzz_parity.py [cases] [seed0]
 """
 import os
 import sys
@@ -22,8 +22,10 @@ for case in range(cases):
     rng = np.random.default_rng(seed0 + case)
     while True:
         kind = str(rng.choice(["channel", "slit", "pipe", "blocks"]))
-        nx = int(rng.choice([16, 32, 48, 64])) if rng.random() < 0.5 else int(rng.integers(1, 40))
-        ny, nz = int(rng.integers(3, 26)), int(rng.integers(3, 26))
+        big = os.environ.get("FUZZ_BIG") == "1"  # boxes up to 128 x 48 x 48
+        nx = (int(rng.choice([16, 32, 48, 64, 128] if big else [16, 32, 48, 64]))
+              if rng.random() < 0.5 else int(rng.integers(1, 130 if big else 40)))
+        ny, nz = int(rng.integers(3, 49 if big else 26)), int(rng.integers(3, 49 if big else 26))
         block, spacing = int(rng.integers(1, 5)), int(rng.integers(0, 4))
         try:
             _, _, nf = port.geometry(kind, nx, ny, nz, block, spacing)
