@@ -47,8 +47,8 @@ int grid_for(uint64_t n, int threads) {
 
 class ListEngine final : public Engine {
  public:
-  // node-range part of a decomposed list lattice (local numbering, see the
-  // kernels above): 19 * nloc own slots + nghost ghost slots
+  // node-range part of a decomposed list lattice (local numbering, see
+  // list_parts.cuh): 19 * nloc own slots + nghost ghost slots
   struct LPart {
     int index = 0;
     uint64_t n0 = 0, n1 = 0, nloc = 0, nghost = 0, head = 0, tail = 0;
