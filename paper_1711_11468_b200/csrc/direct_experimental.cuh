@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kSxThreads, MINB) k_full_aa_odd_sx(const Direc
 }
 
 // ---- AA sub-steps, software-pipelined through shared memory ---------------
-// Persistent variant of the two kernels above.  Each thread walks nodes
+// Persistent variant of k_full_aa_even / k_full_aa_odd (direct_node.cuh).  Each thread walks nodes
 // n, n + G, n + 2G, ... (G = grid size) and, while it collides node n, the
 // 19 populations of its next node are already in flight as per-thread
 // cp.async (LDGSTS) copies into its own shared-memory column: the load
