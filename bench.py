@@ -220,6 +220,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
+    ap.add_argument("--transport", default="copy", choices=["copy", "peer"],
+                    help="z-slab AA halo transport: copy = NCCL send/recv (device copies "
+                         "with --virtual-parts), peer = boundary odd sub-steps load/store the "
+                         "neighbour slab in peer memory (CUDA IPC), epoch flags")
     ap.add_argument("--decompose", action="store_true",
                     help="at N>1: z-slab decomposition of direct push/pull and node-range "
                          "decomposition of list AA instead of replicas")
@@ -276,14 +280,20 @@ def main():
         args.decompose and not desc.ria and (desc.addr == "direct" or aa))
     replicas = world > 1 and not decomposable
     if world == 1 and args.virtual_parts > 1:
-        dspec = {"virtual_parts": args.virtual_parts}
+        dspec = {"virtual_parts": args.virtual_parts, "transport": args.transport}
         if args.nccl_self:
             dspec["nccl_id"] = lbm.nccl_unique_id()
     if world > 1 and not replicas:
         obj = [lbm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        dspec = {"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0]}
+        dspec = {"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0],
+                 "transport": args.transport}
     k = lbm.make_kernel(desc, spec, lbm.PaddingPolicy.automatic(), dist=dspec)
+    if dspec and dspec.get("transport") == "peer" and world > 1:
+        recs = [None] * world
+        dist.all_gather_object(recs, k.peer_export())
+        k.peer_attach(recs)
+        dist.barrier()
     N = k.n_fluid() * (world if replicas else 1)  # fluid updates per lattice step, all ranks
     params = lbm.TrtParams(OMEGA_PLUS, LAMBDA)
     force = lbm.BodyForce(G)
@@ -379,11 +389,16 @@ def main():
     if replicas:
         line["scaling"] = "weak"
         line["config"]["parallelism"] = f"{world} independent replicas (list kernels do not shard)"
+    elif world > 1 and args.transport == "peer":
+        line["config"]["parallelism"] = (f"z-slab x{world}, peer-memory boundary sweeps "
+                                         "(CUDA IPC over NVLink, epoch flags)")
     elif world > 1 and desc.addr == "indirect":
         line["config"]["parallelism"] = f"node-range (x-slab) decomposition x{world}, NCCL index-list halos"
     if world == 1 and args.virtual_parts > 1:
         line["config"]["parallelism"] = (f"EMULATED {args.virtual_parts}-part decomposition on 1 GPU "
-                                         + ("(NCCL self send/recv halos" if args.nccl_self
+                                         + ("(peer-memory boundary sweeps, epoch flags"
+                                            if args.transport == "peer"
+                                            else "(NCCL self send/recv halos" if args.nccl_self
                                             else "(device-copy halos")
                                          + "; overhead probe)")
     line.update({

@@ -32,7 +32,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define LBMGPU_ABI_VERSION 1
+#define LBMGPU_ABI_VERSION 2
 #define LBMGPU_Q 19
 
 typedef enum {
@@ -91,12 +91,18 @@ typedef struct {
  * ONE device and the halo exchange runs as device copies -- the same plan and
  * kernels as the NCCL path, used for single-GPU parity tests.  nranks > 1:
  * one process per GPU, NCCL point-to-point over NVLink; nccl_id is the
- * 128-byte id from lbmgpu_nccl_unique_id() broadcast by rank 0. */
+ * 128-byte id from lbmgpu_nccl_unique_id() broadcast by rank 0.
+ * transport = 1 (AA z slabs only): no halo copies -- the boundary planes'
+ * odd sub-step loads and stores the neighbour slab's slots in peer memory
+ * (CUDA IPC over NVLink between processes: lbmgpu_peer_export / _attach
+ * before the first advance; device pointers with virtual_parts), with
+ * per-sub-step epoch flags in peer memory as the only synchronisation. */
 typedef struct {
   int rank, nranks;
   int device;        /* CUDA ordinal; -1 = current */
   int virtual_parts; /* >1: emulate that many slabs on one device */
   const void* nccl_id;
+  int transport;     /* 0: halo copies (NCCL / device copies), 1: peer memory */
 } lbmgpu_dist;
 
 typedef struct lbmgpu_ctx lbmgpu_ctx;
@@ -250,6 +256,14 @@ int lbmgpu_local_canonical_index(lbmgpu_ctx* ctx, uint64_t* out_rows);
 int lbmgpu_snapshot_local(lbmgpu_ctx* ctx, double* host, uint64_t count);
 int lbmgpu_load_state_local(lbmgpu_ctx* ctx, const double* host,
                             uint64_t count);
+/* Peer-memory transport (dist.transport = 1, nranks > 1): this rank's
+ * record (CUDA IPC handles of its lattice and epoch flags; *len bytes, at
+ * most cap), and the attach of all ranks' records concatenated in rank order
+ * (every rank calls both, export before any attach; the caller moves the
+ * records, e.g. an all-gather).  advance() before attach is a ConfigError. */
+int lbmgpu_peer_export(lbmgpu_ctx* ctx, void* out, size_t cap, size_t* len);
+int lbmgpu_peer_attach(lbmgpu_ctx* ctx, const void* records, size_t record_len,
+                       int nranks);
 /* This process's slab(s): part index < number of local parts. */
 int lbmgpu_part_info(lbmgpu_ctx* ctx, int part, int* z0, int* z1,
                      uint64_t* n_fluid_part);

@@ -327,6 +327,7 @@ int lbmgpu_create(const char* name, int blk, int W, const lbmgpu_geometry* geom,
       ds.nranks = dist->nranks;
       ds.device = dist->device;
       ds.virtual_parts = dist->virtual_parts;
+      ds.transport = dist->transport;
       if (dist->nccl_id) {
         std::memcpy(ds.nccl_id.data(), dist->nccl_id, 128);
         ds.have_id = true;
@@ -804,6 +805,28 @@ int lbmgpu_nccl_unique_id(void* out128) {
     auto fn = reinterpret_cast<Fn>(dlsym(h, "ncclGetUniqueId"));
     if (!fn) throw DeviceError("libnccl.so.2 has no ncclGetUniqueId");
     if (fn(out128) != 0) throw DeviceError("ncclGetUniqueId failed");
+  });
+}
+
+int lbmgpu_peer_export(lbmgpu_ctx* c, void* out, size_t cap, size_t* len) {
+  return guard([&] {
+    need(c, "ctx");
+    need(len, "len");
+    std::vector<uint8_t> rec;
+    c->eng->peer_export(rec);
+    *len = rec.size();
+    if (out) {
+      if (cap < rec.size()) throw ConfigError("peer transport: record buffer too small");
+      std::memcpy(out, rec.data(), rec.size());
+    }
+  });
+}
+
+int lbmgpu_peer_attach(lbmgpu_ctx* c, const void* recs, size_t rec_len, int nranks) {
+  return guard([&] {
+    need(c, "ctx");
+    need(recs, "records");
+    c->eng->peer_attach(static_cast<const uint8_t*>(recs), rec_len, nranks);
   });
 }
 

@@ -34,6 +34,7 @@
 #include "direct_aos.cuh"
 #include "direct_fused.cuh"
 #include "direct_experimental.cuh"
+#include "direct_peer.cuh"
 
 namespace lbmgpu {
 
@@ -235,6 +236,7 @@ struct Part {
   DevBuf<double> stage;     // push, several parts: bottom / top staging planes (2 x 19 x P)
   DevBuf<uint32_t> node_of;
   DevBuf<uint64_t> canon;   // empty when the part holds the whole box
+  DevBuf<unsigned long long> pflag;  // peer transport: epoch flags (direct_peer.cuh)
   uint64_t n_fluid = 0;
   std::vector<uint64_t> canon_host;  // canonical index of each k (sorted)
 };
@@ -320,6 +322,11 @@ class DirectEngine final : public Engine {
     if (nparts_ > 1 && !d.soa)
       throw ConfigError("z-slab decomposition needs the SoA layout");
     if (nparts_ > g.nz) throw ConfigError("more z-slab parts than z planes");
+    if (dist.transport != 0 && dist.transport != 1)
+      throw ConfigError("dist: transport must be 0 (halo copies) or 1 (peer memory)");
+    if (dist.transport == 1 && (d.prop != Prop::Aa || nparts_ < 2))
+      throw ConfigError("peer transport: implemented for the AA z-slab decomposition "
+                        "(aa-soa / aa-vec-soa over >= 2 slabs)");
     if (nranks_ > 1 && !dist.have_id)
       throw ConfigError("dist: nranks > 1 needs the NCCL unique id");
     {
@@ -455,11 +462,16 @@ class DirectEngine final : public Engine {
                                               nparts_, dist.nccl_id.data());
       else
         tr_ = std::make_unique<LocalTransport>(std::move(plan));
+      ring_ = end_fluid;
+      if (dist.transport == 1) setup_peer();
     }
     LBM_CUDA(cudaStreamSynchronize(stream_));
   }
 
   ~DirectEngine() override {
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
+    if (peer_err_) cudaFreeHost(peer_err_);
     tr_.reset();
     if (stream_) cudaStreamDestroy(stream_);
   }
@@ -724,6 +736,7 @@ class DirectEngine final : public Engine {
   }
 
   void advance(const TrtArgs& t, long steps) override {
+    if (peer_) peer_check();
     const bool soa = desc_.soa;
     const bool cs = cs_;
     if (advance_fused(t, steps)) return;
@@ -812,7 +825,7 @@ class DirectEngine final : public Engine {
           }
         }
       } else {
-        aa_pair_slabs(t);
+        peer_ ? aa_pair_peer(t) : aa_pair_slabs(t);
       }
     }
   }
@@ -918,6 +931,218 @@ class DirectEngine final : public Engine {
     tr_->exchange(1, parts_, P_, stream_);
     sweep(true, false);
     tr_->wait(1, stream_);
+  }
+
+  // ---- peer-memory transport (direct_peer.cuh) --------------
+  // Per AA pair, epoch e:
+  //   even(boundary) -> signal(even) -> even(interior) -> wait(even) ->
+  //   odd(boundary, peer loads/stores) -> signal(odd) -> odd(interior) ->
+  //   wait(odd)
+  // The slots a neighbour's odd(boundary) touches in this slab (the top
+  // plane's down-slots, the bottom plane's up-slots) are written by this
+  // slab's even(boundary) and by nothing else in the pair, so:
+  //  * wait(even) before odd(boundary): the neighbour's even(boundary) has
+  //    written the slots this odd step reads from its planes;
+  //  * wait(odd) before the next even(boundary): the neighbour's
+  //    odd(boundary) has finished with this slab's slots (and its scatters
+  //    into them are visible).
+  // The two odd(boundary) steps of a face touch disjoint slot sets (down-
+  // slots of the lower plane, up-slots of the upper plane), and interior
+  // sweeps touch no boundary slot of another slab.
+  struct PeerLink {
+    double* lo = nullptr;  // lower neighbour's lattice (its storage plane lo_plane = global z0-1)
+    double* hi = nullptr;  // upper neighbour's lattice (its storage plane hi_plane = global z1)
+    uint32_t lo_plane = 0, hi_plane = 0;
+    unsigned long long* lo_flags = nullptr;  // the neighbours' epoch flags (4 each)
+    unsigned long long* hi_flags = nullptr;
+  };
+  // CUDA IPC record one rank exports (lbmgpu_peer_export)
+  struct PeerRecord {
+    uint32_t magic, rank, nzl, zoff;
+    uint64_t buf_off, flag_off;
+    cudaIpcMemHandle_t buf, flag;
+  };
+  static constexpr uint32_t kPeerMagic = 0x4c424d50u;  // "LBMP"
+
+  void neighbours(int p, int& lo, int& hi) const {
+    lo = p > 0 ? p - 1 : (ring_ ? nparts_ - 1 : -1);
+    hi = p + 1 < nparts_ ? p + 1 : (ring_ ? 0 : -1);
+  }
+
+  void setup_peer() {
+    peer_ = true;
+    if (const char* e = std::getenv("LBMGPU_PEER_TIMEOUT_MS"))
+      peer_timeout_ns_ = 1000000ull * std::strtoull(e, nullptr, 10);
+    LBM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&peer_err_), sizeof(int),
+                           cudaHostAllocMapped));
+    *peer_err_ = 0;
+    LBM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&peer_err_dev_), peer_err_, 0));
+    for (Part& pt : parts_) {
+      pt.pflag.alloc(4);
+      LBM_CUDA(cudaMemsetAsync(pt.pflag.get(), 0, 4 * sizeof(unsigned long long), stream_));
+    }
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    if (nranks_ > 1) return;  // lbmgpu_peer_attach links the neighbours
+    // all slabs in this process: the neighbours' device pointers directly
+    links_.assign(parts_.size(), PeerLink{});
+    for (size_t i = 0; i < parts_.size(); ++i) {
+      int lo, hi;
+      neighbours(parts_[i].index, lo, hi);
+      PeerLink& L = links_[i];
+      if (lo >= 0) {
+        const Part& q = parts_[lo];
+        L.lo = q.buf[0].get();
+        L.lo_plane = q.zoff + q.nzl - 1;
+        L.lo_flags = q.pflag.get();
+      }
+      if (hi >= 0) {
+        const Part& q = parts_[hi];
+        L.hi = q.buf[0].get();
+        L.hi_plane = q.zoff;
+        L.hi_flags = q.pflag.get();
+      }
+    }
+    peer_ready_ = true;
+  }
+
+  void peer_export(std::vector<uint8_t>& rec) override {
+    if (!peer_ || nranks_ < 2)
+      throw ConfigError("peer transport: export needs nranks > 1 and transport = 1");
+    const Part& pt = parts_[0];
+    PeerRecord r;
+    std::memset(&r, 0, sizeof r);
+    r.magic = kPeerMagic;
+    r.rank = static_cast<uint32_t>(rank_);
+    r.nzl = pt.nzl;
+    r.zoff = pt.zoff;
+    r.buf_off = pt.buf[0].alloc_offset();
+    r.flag_off = pt.pflag.alloc_offset();
+    LBM_CUDA(cudaIpcGetMemHandle(&r.buf, reinterpret_cast<char*>(pt.buf[0].get()) - r.buf_off));
+    LBM_CUDA(cudaIpcGetMemHandle(&r.flag, reinterpret_cast<char*>(pt.pflag.get()) - r.flag_off));
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(&r);
+    rec.assign(b, b + sizeof r);
+  }
+
+  void peer_attach(const uint8_t* recs, size_t rec_len, int n) override {
+    if (!peer_ || nranks_ < 2)
+      throw ConfigError("peer transport: attach needs nranks > 1 and transport = 1");
+    if (peer_ready_) throw ConfigError("peer transport: already attached");
+    if (rec_len != sizeof(PeerRecord) || n != nranks_)
+      throw ConfigError("peer transport: expected " + std::to_string(nranks_) +
+                        " records of " + std::to_string(sizeof(PeerRecord)) + " bytes");
+    auto record = [&](int r) {
+      PeerRecord x;
+      std::memcpy(&x, recs + size_t(r) * rec_len, sizeof x);
+      if (x.magic != kPeerMagic || x.rank != static_cast<uint32_t>(r))
+        throw ConfigError("peer transport: bad record for rank " + std::to_string(r));
+      return x;
+    };
+    struct Mapped { char* buf; char* flag; };
+    std::vector<std::pair<int, Mapped>> opened;
+    auto map = [&](int r) -> Mapped {
+      for (auto& o : opened)
+        if (o.first == r) return o.second;  // two ranks with the z ring: lo == hi
+      const PeerRecord x = record(r);
+      void* b = nullptr;
+      void* f = nullptr;
+      LBM_CUDA(cudaIpcOpenMemHandle(&b, x.buf, cudaIpcMemLazyEnablePeerAccess));
+      ipc_open_.push_back(b);
+      LBM_CUDA(cudaIpcOpenMemHandle(&f, x.flag, cudaIpcMemLazyEnablePeerAccess));
+      ipc_open_.push_back(f);
+      Mapped m{static_cast<char*>(b) + x.buf_off, static_cast<char*>(f) + x.flag_off};
+      opened.emplace_back(r, m);
+      return m;
+    };
+    int lo, hi;
+    neighbours(rank_, lo, hi);
+    links_.assign(1, PeerLink{});
+    PeerLink& L = links_[0];
+    if (lo >= 0) {
+      const PeerRecord x = record(lo);
+      const Mapped m = map(lo);
+      L.lo = reinterpret_cast<double*>(m.buf);
+      L.lo_plane = x.zoff + x.nzl - 1;
+      L.lo_flags = reinterpret_cast<unsigned long long*>(m.flag);
+    }
+    if (hi >= 0) {
+      const PeerRecord x = record(hi);
+      const Mapped m = map(hi);
+      L.hi = reinterpret_cast<double*>(m.buf);
+      L.hi_plane = x.zoff;
+      L.hi_flags = reinterpret_cast<unsigned long long*>(m.flag);
+    }
+    peer_ready_ = true;
+  }
+
+  void peer_check() const {
+    if (!peer_ready_)
+      throw ConfigError("peer transport: lbmgpu_peer_attach has not been called");
+    if (*static_cast<volatile int*>(peer_err_))
+      throw DeviceError("peer transport: a neighbour's sub-step signal timed out");
+  }
+
+  void peer_signal(int kind, unsigned long long e) {
+    for (const PeerLink& L : links_) {
+      const int tok = stats_.begin("peer_signal", stream_);
+      k_peer_signal<<<1, 32, 0, stream_>>>(L.lo_flags ? L.lo_flags + 2 * kind + 1 : nullptr,
+                                           L.hi_flags ? L.hi_flags + 2 * kind : nullptr, e);
+      LBM_CHECK_LAUNCH();
+      stats_.end(tok, stream_);
+    }
+  }
+
+  void peer_wait(int kind, unsigned long long e) {
+    for (size_t i = 0; i < parts_.size(); ++i) {
+      const PeerLink& L = links_[i];
+      unsigned long long* own = parts_[i].pflag.get();
+      const int tok = stats_.begin("peer_wait", stream_);
+      k_peer_wait<<<1, 32, 0, stream_>>>(L.lo_flags ? own + 2 * kind : nullptr,
+                                         L.hi_flags ? own + 2 * kind + 1 : nullptr, e,
+                                         peer_err_dev_, peer_timeout_ns_);
+      LBM_CHECK_LAUNCH();
+      stats_.end(tok, stream_);
+    }
+  }
+
+  void aa_pair_peer(const TrtArgs& t) {
+    const uint32_t P = static_cast<uint32_t>(P_);
+    const unsigned long long e = ++epoch_;
+    auto sweep = [&](bool odd, bool boundary) {
+      for (size_t i = 0; i < parts_.size(); ++i) {
+        Part& pt = parts_[i];
+        const uint32_t last = (pt.nzl - 1) * P;
+        auto run = [&](uint32_t n0, uint32_t cnt) {
+          DirectArgs a = args(pt, n0, cnt, t, 0, 0);
+          if (!boundary) {
+            aa_sub(odd, a, odd ? "full_aa_odd_soa" : "full_aa_even_soa");
+          } else if (!odd) {
+            aa_sub(false, a, "full_aa_even_soa_halo");
+          } else {
+            const PeerLink& L = links_[i];
+            const PeerArgs pa{L.lo, L.hi, L.lo_plane, L.hi_plane};
+            const int tok = stats_.begin("full_aa_odd_soa_peer", stream_);
+            k_full_aa_odd_peer<<<static_cast<unsigned>(ceil_div(cnt, 128)), 128, 0, stream_>>>(
+                a, pa);
+            LBM_CHECK_LAUNCH();
+            stats_.end(tok, stream_);
+          }
+        };
+        if (boundary) {
+          run(0, P);
+          if (pt.nzl > 1) run(last, P);
+        } else if (pt.nzl > 2) {
+          run(P, last - P);
+        }
+      }
+    };
+    sweep(false, true);
+    peer_signal(0, e);
+    sweep(false, false);
+    peer_wait(0, e);
+    sweep(true, true);
+    peer_signal(1, e);
+    sweep(true, false);
+    peer_wait(1, e);
   }
 
   CanonArgs canon_args(const Part& pt, int buf) const {
@@ -1095,6 +1320,14 @@ class DirectEngine final : public Engine {
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;
+  bool ring_ = false;                   // the halo plan includes the z ring
+  bool peer_ = false, peer_ready_ = false;
+  unsigned long long epoch_ = 0;        // AA pairs run with the peer transport
+  unsigned long long peer_timeout_ns_ = 30000000000ull;
+  std::vector<PeerLink> links_;         // per local part
+  int* peer_err_ = nullptr;             // host-mapped wait-timeout flag
+  int* peer_err_dev_ = nullptr;
+  std::vector<void*> ipc_open_;         // CUDA IPC mappings to close
   GeomSpec geom_;  // kind/parameters for the analytic solid test (custom: flags)
 };
 

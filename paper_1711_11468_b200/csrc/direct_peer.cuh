@@ -1,0 +1,125 @@
+// Peer-memory transport of the z-slab AA decomposition:
+// the odd sub-step of a slab's two boundary planes gathers from and scatters
+// into the NEIGHBOUR's boundary plane directly (NVLink loads/stores through
+// CUDA-IPC-mapped pointers, or plain device pointers when the slabs share one
+// GPU), so no halo copy exists at all; a per-sub-step epoch flag written
+// into the neighbour's memory replaces the copy's completion.
+// (part of the direct-addressing translation unit, included by direct.cu)
+#pragma once
+
+#include "direct_args.cuh"
+#include "direct_node.cuh"
+
+namespace lbmgpu {
+
+// Which slots cross a face (kernels_full_aa.cpp:83-92 access sets, SURVEY.md
+// 8(e)): the odd sub-step of node (x, y, z) reads and writes slot opp(d) of
+// node x - c_d.  For the slab's bottom plane and c_z(d) = +1 that node is the
+// lower neighbour's top plane (its down-slots); for the top plane and
+// c_z(d) = -1 it is the upper neighbour's bottom plane (its up-slots).  The
+// even sub-step touches own slots only.
+struct PeerArgs {
+  double* lo;         // lower neighbour's lattice; null = own storage plane z-1
+  double* hi;         // upper neighbour's lattice; null = own storage plane z+1
+  uint32_t lo_plane;  // lower neighbour's storage plane of global z0 - 1
+  uint32_t hi_plane;  // upper neighbour's storage plane of global z1
+};
+
+// AA odd sub-step (kernels_full_aa.cpp:83-92, same expression as
+// aa_odd_node) over boundary planes whose out-of-slab neighbours live in
+// peer memory.  Each of the three z-planes a node touches has its own base
+// (own lattice, or the neighbour's for the crossing plane); warps without
+// an x/y wrap address every slot as base + a per-direction constant (the
+// fast path of aa_odd_node).  Its remote stores are complete when the
+// kernel is (kernel boundary), and k_peer_signal -- the next launch on the
+// stream -- publishes them with a system-scope fence + release store.  (A
+// per-block system fence here measured 1.7x slower on the boundary planes.)
+__global__ void __launch_bounds__(128) k_full_aa_odd_peer(const DirectArgs a, const PeerArgs pa) {
+  Coords c;
+  uint32_t n;
+  if (decode(a, c, n) && !solid_node(a, c.x, c.y, c.z, n)) {
+    const Idx<true> I{a.P, a.nx, a.ny};
+    double* zb[3] = {a.dst, a.dst, a.dst};
+    uint32_t zp[3] = {c.Z[0], c.Z[1], c.Z[2]};
+    if (c.z == 0 && pa.lo) {
+      zb[0] = pa.lo;
+      zp[0] = pa.lo_plane;
+    }
+    if (c.z + 1 == a.nzl && pa.hi) {
+      zb[2] = pa.hi;
+      zp[2] = pa.hi_plane;
+    }
+    double q[kQ];
+    const bool inner = c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u;
+    if (__all_sync(__activemask(), inner)) {
+      // slot 0 of (plane k, y, x); direction d's slot is a constant away
+      double* b[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) b[k] = zb[k] + I(zp[k], 0, c.y, c.x);
+      const long long plane = static_cast<long long>(kQ) * a.P;
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) q[d] = b[1 - cz(d)][a.odd_off[d] + cz(d) * plane];
+      collide(q, a.trt);
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) b[1 - cz(d)][a.odd_off[d] + cz(d) * plane] = q[opp(d)];
+    } else {
+      double* p[kQ];
+      p[0] = a.dst + I(c.Z[1], dslot(0), c.y, c.x);
+#pragma unroll
+      for (int d = 1; d < kQ; ++d)
+        p[d] = zb[1 - cz(d)] + I(zp[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) q[d] = p[d][0];
+      collide(q, a.trt);
+#pragma unroll
+      for (int d = 0; d < kQ; ++d) p[d][0] = q[opp(d)];
+    }
+  }
+}
+
+// Epoch flags: each part owns 4 u64 flags, [0] even done by the lower
+// neighbour, [1] even done by the upper, [2] / [3] the same for odd.
+// Signal: system-scope release store of `epoch` into the neighbours' flags
+// (null = no neighbour on that side).
+__global__ void k_peer_signal(unsigned long long* to_lo, unsigned long long* to_hi,
+                              unsigned long long epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  if (to_lo) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_lo), "l"(epoch) : "memory");
+  if (to_hi) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_hi), "l"(epoch) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait until the own flags f0 / f1 (null = skip) reach `epoch`.  Bounded:
+// after timeout_ns the kernel records the failure in *err (host-mapped) and
+// returns, so a dead neighbour cannot hang the device; the engine raises
+// the error at its next host call.
+__global__ void k_peer_wait(const unsigned long long* f0, const unsigned long long* f1,
+                            unsigned long long epoch, int* err, unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = global_ns();
+  const unsigned long long* fs[2] = {f0, f1};
+  for (int i = 0; i < 2; ++i) {
+    if (!fs[i]) continue;
+    while (ld_acquire_sys(fs[i]) < epoch) {
+      if (global_ns() - t0 > timeout_ns) {
+        atomicExch_system(err, 1);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+}  // namespace lbmgpu

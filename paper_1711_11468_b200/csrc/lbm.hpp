@@ -125,6 +125,9 @@ class DevBuf {
   T* get() const { return p_; }
   size_t size() const { return n_; }
   size_t bytes() const { return n_ * sizeof(T); }
+  // byte offset of get() inside its cudaMalloc allocation (CUDA IPC handles
+  // name the allocation base)
+  size_t alloc_offset() const { return guarded_ ? kGuardBytes : 0; }
 
  private:
   T* p_ = nullptr;
@@ -181,6 +184,7 @@ struct DistSpec {
   int rank = 0, nranks = 1, device = -1, virtual_parts = 1;
   std::array<uint8_t, 128> nccl_id{};
   bool have_id = false;
+  int transport = 0;  // 0: halo copies (NCCL / device), 1: peer memory (AA z slabs)
 };
 
 // One GPU-resident sweep implementation of the reference's Kernel
@@ -218,6 +222,16 @@ class Engine {
   virtual bool ria_stats(int64_t* runs, double* vfrac) {
     (void)runs; (void)vfrac;
     return false;
+  }
+  // Peer-memory transport (nranks > 1): this rank's CUDA IPC record, and
+  // the attach of every rank's record (rank order).
+  virtual void peer_export(std::vector<uint8_t>& rec) {
+    (void)rec;
+    throw ConfigError("peer transport: not enabled for this lattice");
+  }
+  virtual void peer_attach(const uint8_t* recs, size_t rec_len, int nranks) {
+    (void)recs; (void)rec_len; (void)nranks;
+    throw ConfigError("peer transport: not enabled for this lattice");
   }
   virtual int parts() const { return 1; }
   virtual void part_info(int p, int* z0, int* z1, uint64_t* nf) const {

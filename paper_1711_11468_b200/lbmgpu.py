@@ -103,6 +103,8 @@ def _load():
     L.lbmgpu_halo_plan.argtypes = [i, i, i, vp, i, P(i)]
     L.lbmgpu_guard_check.argtypes = [P(i)]
     L.lbmgpu_guard_selftest.argtypes = [P(i)]
+    L.lbmgpu_peer_export.argtypes = [vp, vp, C.c_size_t, P(C.c_size_t)]
+    L.lbmgpu_peer_attach.argtypes = [vp, vp, C.c_size_t, i]
     return L
 
 
@@ -139,7 +141,8 @@ class _Descriptor(C.Structure):
 
 class _Dist(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("device", C.c_int),
-                ("virtual_parts", C.c_int), ("nccl_id", C.c_void_p)]
+                ("virtual_parts", C.c_int), ("nccl_id", C.c_void_p),
+                ("transport", C.c_int)]
 
 
 class _VerifyReport(C.Structure):
@@ -424,6 +427,7 @@ class Kernel:
             ds.nranks = dist.get("nranks", 1)
             ds.device = dist.get("device", -1)
             ds.virtual_parts = dist.get("virtual_parts", 1)
+            ds.transport = {"copy": 0, "peer": 1}[dist.get("transport", "copy")]
             if dist.get("nccl_id") is not None:
                 self._nccl_keep = C.create_string_buffer(bytes(dist["nccl_id"]), 128)
                 ds.nccl_id = C.cast(self._nccl_keep, C.c_void_p)
@@ -584,6 +588,22 @@ class Kernel:
 
     def synchronize(self):
         _check(lib.lbmgpu_synchronize(self._h))
+
+    def peer_export(self) -> bytes:
+        """This rank's peer-transport record (CUDA IPC handles); all-gather
+        the records of every rank and pass them to peer_attach()."""
+        n = C.c_size_t()
+        _check(lib.lbmgpu_peer_export(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib.lbmgpu_peer_export(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def peer_attach(self, records) -> None:
+        """Map the neighbour slabs' lattices and flags (records in rank order)."""
+        records = [bytes(r) for r in records]
+        blob = b"".join(records)
+        _check(lib.lbmgpu_peer_attach(self._h, blob, len(records[0]) if records else 0,
+                                      len(records)))
 
     def part_info(self, part: int):
         z0, z1, nf = C.c_int(), C.c_int(), C.c_uint64()

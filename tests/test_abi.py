@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     so = ctypes.CDLL(L.LIB_PATH)
     missing = [s for s in syms if not hasattr(so, s)]
     assert not missing, missing
-    assert so.lbmgpu_abi_version() == 1
+    assert so.lbmgpu_abi_version() == 2
 
 
 def test_kernel_names_order():

@@ -481,6 +481,49 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
+@pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa"])
+@pytest.mark.parametrize("kind,dims,parts", [
+    ("channel", (16, 12, 24), 2), ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2),
+    ("blocks", (12, 10, 16), 4), ("slit", (6, 5, 9), 3), ("pipe", (9, 12, 13), 13),
+    ("blocks", (16, 16, 16), 16)])
+def test_zslab_peer_transport_bitwise_equal_single(name, kind, dims, parts):
+    """Peer-memory transport (direct_peer.cuh): the boundary planes' odd
+    sub-step loads and stores the neighbour slab's slots directly, epoch
+    flags in the neighbour's memory order the sub-steps, no halo copy at
+    all.  Emulated with all slabs on one device (device pointers instead of
+    CUDA IPC mappings; the flag protocol runs unchanged).  Covers the z ring
+    (blocks: fluid on z = 0), two slabs with the ring (lower == upper
+    neighbour) and one plane per slab (pipe 13, blocks 16).  Bitwise equal
+    to the single-slab run, over several advance() calls."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    ref.load_perturbed(777)
+    ref.advance(PARAMS, FORCE, 10)
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec,
+                        dist={"virtual_parts": parts, "transport": "peer"})
+    k.load_perturbed(777)
+    k.kernel_stats_enable(True)
+    for st in (4, 2, 4):
+        k.advance(PARAMS, FORCE, st)
+    assert np.array_equal(k.snapshot(), ref.snapshot()), name
+    assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
+    names = set(k.kernel_stats())
+    assert "full_aa_odd_soa_peer" in names and "peer_wait" in names
+
+
+def test_zslab_peer_transport_errors():
+    spec = lbm.GeometrySpec("channel", 16, 12, 24)
+    with pytest.raises(lbm.ConfigError, match="peer transport"):
+        lbm.make_kernel(lbm.make_descriptor("blk-push-soa"), spec,
+                        dist={"virtual_parts": 2, "transport": "peer"})
+    with pytest.raises(lbm.ConfigError, match="peer transport"):
+        lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec, dist={"transport": "peer"})
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
+                        dist={"virtual_parts": 3, "transport": "peer"})
+    with pytest.raises(lbm.ConfigError, match="nranks > 1"):
+        k.peer_export()
+
+
 @pytest.mark.parametrize("name", ["list-aa-soa", "list-aa-aos"])
 @pytest.mark.parametrize("kind,dims,parts", [
     ("channel", (20, 12, 10), 2), ("channel", (20, 12, 10), 3), ("blocks", (16, 16, 16), 2),

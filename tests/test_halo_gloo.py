@@ -449,3 +449,142 @@ def test_two_rank_list_node_range_protocol_gloo(kind, dims):
     assert all(p.exitcode == 0 for p in procs)
     equal, rel = q.get(timeout=5)
     assert equal, rel
+
+
+def _rank_main_peer(rank, world, kind, dims, steps, shared, flags, q):
+    """The peer-memory transport's protocol (direct_peer.cuh, DirectEngine::
+    aa_pair_peer) with real concurrency: every slab lives in shared memory
+    (the stand-in for CUDA-IPC-mapped peer memory), the boundary planes' odd
+    sub-step gathers from and scatters into the NEIGHBOUR's slab directly,
+    and the only synchronisation is the epoch flags written into the
+    neighbour's flag row (signal) and spun on in one's own (wait).  Random
+    delays between the stages shuffle the interleavings; the result must
+    equal the full-domain oracle bit for bit."""
+    import random
+    import time
+    from oracle.oracle import Port
+    port = Port()
+    rng = random.Random(1000 + rank)
+    nx, ny, nz = dims
+    flags_g, per, nf = port.geometry(kind, nx, ny, nz)
+    solid = flags_g.reshape(nx, ny, nz)
+    zr = [nz * r // world for r in range(world + 1)]
+    z0, z1 = zr[rank], zr[rank + 1]
+    nzl = z1 - z0
+    ring = bool(solid[:, :, 0].min() == 0 or solid[:, :, nz - 1].min() == 0)
+    lo = rank - 1 if rank > 0 else (world - 1 if ring else -1)
+    hi = rank + 1 if rank + 1 < world else (0 if ring else -1)
+    bufs = [t.numpy() for t in shared]   # every slab: (nzl_r + 2, Q, ny, nx)
+    fl = flags.numpy()                   # (world, 4): even from lo / hi, odd from lo / hi
+    buf = bufs[rank]
+    wp = 1.0 / TAU
+    wm = port.omega_minus(wp)
+    own = [(x, y, z) for z in range(nzl) for y in range(ny) for x in range(nx)
+           if not solid[x, y, z + z0]]
+    boundary = [n for n in own if n[2] == 0 or n[2] == nzl - 1]
+    interior = [n for n in own if 0 < n[2] < nzl - 1]
+
+    def at(zs):  # storage plane zs of this slab -> (array, plane), peer planes resolved
+        if zs == 0 and lo >= 0:
+            return bufs[lo], zr[lo + 1] - zr[lo]        # lower neighbour's top own plane
+        if zs == nzl + 1 and hi >= 0:
+            return bufs[hi], 1                          # upper neighbour's bottom own plane
+        return buf, zs
+
+    def even(nodes):
+        for (x, y, z) in nodes:
+            zs = z + 1
+            f = np.array([buf[zs, SLOT[d], y, x] for d in range(Q)])
+            f = port.collide(f, wp, wm, G)
+            for d in range(Q):
+                buf[zs, SLOT[OPP[d]], y, x] = f[d]
+
+    def odd(nodes):
+        for (x, y, z) in nodes:
+            zs = z + 1
+            f = np.empty(Q)
+            for d in range(Q):
+                a, p = at(zs - CZ[d])
+                f[d] = a[p, SLOT[OPP[d]], (y - CY[d]) % ny, (x - CX[d]) % nx]
+            f = port.collide(f, wp, wm, G)
+            for d in range(Q):  # scatter written independently of the gather address
+                a, p = at(zs + CZ[d])
+                a[p, SLOT[d], (y + CY[d]) % ny, (x + CX[d]) % nx] = f[d]
+
+    def signal(kind_, e):
+        if lo >= 0:
+            fl[lo, 2 * kind_ + 1] = e   # I am the lower neighbour's upper neighbour
+        if hi >= 0:
+            fl[hi, 2 * kind_] = e
+
+    def wait(kind_, e):
+        t0 = time.time()
+        for j, nb in ((2 * kind_, lo), (2 * kind_ + 1, hi)):
+            while nb >= 0 and fl[rank, j] < e:
+                assert time.time() - t0 < 120, "peer wait timed out"
+                time.sleep(0.0005)
+
+    def jitter():
+        time.sleep(rng.random() * 0.01)
+
+    for e in range(1, steps // 2 + 1):
+        jitter(); even(boundary); signal(0, e)
+        jitter(); even(interior); wait(0, e)
+        jitter(); odd(boundary); signal(1, e)
+        jitter(); odd(interior); wait(1, e)
+    q.put(rank)
+
+
+@pytest.mark.parametrize("kind,dims,world", [("channel", (6, 5, 8), 2), ("blocks", (8, 8, 8), 2),
+                                             ("blocks", (8, 8, 9), 3), ("channel", (5, 4, 6), 3)])
+def test_peer_transport_protocol_shared_memory(kind, dims, world):
+    import torch
+    from oracle.oracle import Port
+    port = Port()
+    nx, ny, nz = dims
+    flags_g, per, nf = port.geometry(kind, nx, ny, nz)
+    solid = flags_g.reshape(nx, ny, nz)
+    init = port.perturbed(nf, 91)
+    zr = [nz * r // world for r in range(world + 1)]
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    shared = []
+    for r in range(world):
+        b = np.empty((zr[r + 1] - zr[r] + 2, Q, ny, nx))
+        for d in range(Q):
+            b[:, SLOT[d]] = w[d]
+        shared.append(b)
+    k = 0
+    for x in range(nx):
+        for y in range(ny):
+            for z in range(nz):
+                if solid[x, y, z]:
+                    continue
+                r = max(i for i in range(world) if zr[i] <= z)
+                for d in range(Q):
+                    shared[r][z - zr[r] + 1, SLOT[d], y, x] = init[k * Q + d]
+                k += 1
+    shared = [torch.from_numpy(b).share_memory_() for b in shared]
+    flags = torch.zeros((world, 4), dtype=torch.int64).share_memory_()
+    steps = 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main_peer,
+                         args=(r, world, kind, dims, steps, shared, flags, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    full = np.zeros(nf * Q)
+    k = 0
+    for x in range(nx):
+        for y in range(ny):
+            for z in range(nz):
+                if solid[x, y, z]:
+                    continue
+                r = max(i for i in range(world) if zr[i] <= z)
+                full[k * Q:(k + 1) * Q] = [shared[r][z - zr[r] + 1, SLOT[d], y, x].item()
+                                           for d in range(Q)]
+                k += 1
+    expect, _ = port.run("full", kind, nx, ny, nz, steps, 1.0 / TAU, g=G, init=init)
+    assert np.array_equal(full, expect), port.max_rel_diff(full, expect)

@@ -1,8 +1,9 @@
-"""Multi-GPU parity check for the NCCL z-slab AA path (run under torchrun,
+"""Multi-GPU parity check for the z-slab / node-range paths (NCCL halo copies,
+or transport "peer": CUDA IPC peer memory for direct AA) (run under torchrun,
 one process per GPU):
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-        tools/mgpu_check.py [nx ny nz steps kind]
+        tools/mgpu_check.py [nx ny nz steps kind name transport]
 
 Every rank advances its slab; rank 0 gathers the local rows (canonical
 indices + PDFs) and compares the assembled state with a single-GPU run of the
@@ -22,6 +23,7 @@ def main():
     nx, ny, nz, steps = (int(v) for v in (sys.argv[1:5] if len(sys.argv) > 4 else (64, 32, 48, 10)))
     kind = sys.argv[5] if len(sys.argv) > 5 else "channel"
     name = sys.argv[6] if len(sys.argv) > 6 else "aa-soa"
+    transport = sys.argv[7] if len(sys.argv) > 7 else "copy"  # "peer": CUDA IPC peer memory
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -31,7 +33,13 @@ def main():
     spec = lbm.GeometrySpec(kind, nx, ny, nz)
     params, force = lbm.TrtParams.from_tau(0.9), lbm.BodyForce((1e-5, 2e-6, -3e-6))
     k = lbm.make_kernel(lbm.make_descriptor(name), spec,
-                        dist={"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0]})
+                        dist={"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0],
+                              "transport": transport})
+    if transport == "peer":
+        recs = [None] * world
+        dist.all_gather_object(recs, k.peer_export())
+        k.peer_attach(recs)
+        dist.barrier()
     k.load_perturbed(4242)
     k.advance(params, force, steps)
     mass = k.total_mass()
@@ -49,7 +57,8 @@ def main():
             got[idx.astype(np.int64)] = snap.reshape(-1, 19)
         ok = bool(np.array_equal(got, expect))
         ok = ok and abs(mass - ref.total_mass()) <= 1e-12 * abs(ref.total_mass())
-        print(("PASS" if ok else "FAIL"), f"world={world} {kind} {nx}x{ny}x{nz} steps={steps}",
+        print(("PASS" if ok else "FAIL"),
+              f"world={world} {name} {transport} {kind} {nx}x{ny}x{nz} steps={steps}",
               flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.broadcast(flag, 0)
