@@ -554,14 +554,22 @@ class ListEngine final : public Engine {
                         : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
         if (desc_.ria && soa) {
           const int mode = ria_mode_ >= 0 ? ria_mode_ : (ria_npat_ > 0 ? 2 : 0);
-          const int tok = stats_.begin(mode == 2 && ria_npat_ > 0 ? "list_aa_odd_ria_pid_soa"
-                                                                  : "list_aa_odd_ria_soa",
+          const int tok = stats_.begin(mode == 2 && ria_npat_ > 65536 ? "list_aa_odd_ria_pid32_soa"
+                                       : mode == 2 && ria_npat_ > 256 ? "list_aa_odd_ria_pid16_soa"
+                                       : mode == 2 && ria_npat_ > 0 ? "list_aa_odd_ria_pid_soa"
+                                                                    : "list_aa_odd_ria_soa",
                                        stream_);
           // 128-thread CTAs: cfg 2 RIA odd 5228 -> 5431 GB/s (the indexed
           // sweeps measured equal or better at 256)
           const int rt = threads_env_ ? threads_ : 128;
           const unsigned g = static_cast<unsigned>(ceil_div(a.N, rt));
-          if (mode == 2 && ria_npat_ > 0)
+          if (mode == 2 && ria_npat_ > 65536)
+            k_list_aa_odd_pid<false, uint32_t><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(),
+                                                                      ria_nid32_.get(), pf_);
+          else if (mode == 2 && ria_npat_ > 256)
+            k_list_aa_odd_pid<false, uint16_t><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(),
+                                                                      ria_nid16_.get(), pf_);
+          else if (mode == 2 && ria_npat_ > 0)
             k_list_aa_odd_pid<false><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(), ria_nid_.get(),
                                                             pf_);
           else if (mode == 1)
@@ -758,25 +766,27 @@ class ListEngine final : public Engine {
     k_ria_group_patterns<<<grid_for(warps * 18, 256), 256, 0, stream_>>>(
         ria_pat_.get(), ria_run0_.get(), ria_mask_.get(), n_fluid_, ria_gpat_.get());
     LBM_CHECK_LAUNCH();
-    // distinct run patterns (host dedup, stops at 257): <= 256 -> pattern ids
+    // distinct run patterns (host dedup, stops above kMaxPatterns): pattern
+    // ids of 8 / 16 / 32 bits for <= 256 / 65,536 / kMaxPatterns rows
     {
+      constexpr uint32_t kMaxPatterns = 1u << 20;  // table <= 72 MiB (L2-sized)
       std::vector<int32_t> hp(uint64_t(R) * 18);
       LBM_CUDA(cudaMemcpyAsync(hp.data(), ria_pat_.get(), hp.size() * 4, cudaMemcpyDeviceToHost,
                                stream_));
       LBM_CUDA(cudaStreamSynchronize(stream_));
-      std::unordered_map<std::string, uint8_t> ids;
-      std::vector<uint8_t> run_pid(R);
+      std::unordered_map<std::string, uint32_t> ids;
+      std::vector<uint32_t> run_pid(R);
       std::vector<int32_t> tab;
       bool ok = true;
       for (uint32_t r = 0; r < R && ok; ++r) {
         std::string key(reinterpret_cast<const char*>(hp.data() + uint64_t(r) * 18), 72);
         auto it = ids.find(key);
         if (it == ids.end()) {
-          if (ids.size() == 256) {
+          if (ids.size() == kMaxPatterns) {
             ok = false;
             break;
           }
-          it = ids.emplace(key, static_cast<uint8_t>(ids.size())).first;
+          it = ids.emplace(key, static_cast<uint32_t>(ids.size())).first;
           tab.insert(tab.end(), hp.begin() + uint64_t(r) * 18, hp.begin() + uint64_t(r) * 18 + 18);
         }
         run_pid[r] = it->second;
@@ -786,13 +796,24 @@ class ListEngine final : public Engine {
         ria_ptab_.alloc(tab.size());
         LBM_CUDA(cudaMemcpyAsync(ria_ptab_.get(), tab.data(), tab.size() * 4,
                                  cudaMemcpyHostToDevice, stream_));
-        DevBuf<uint8_t> dpid(R);
-        LBM_CUDA(cudaMemcpyAsync(dpid.get(), run_pid.data(), R, cudaMemcpyHostToDevice, stream_));
-        ria_nid_.alloc(n_fluid_);
-        k_ria_node_ids<<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
-            ria_run0_.get(), ria_mask_.get(), dpid.get(), n_fluid_, ria_nid_.get());
-        LBM_CHECK_LAUNCH();
-        LBM_CUDA(cudaStreamSynchronize(stream_));
+        auto node_ids = [&](auto tag, auto& out) {
+          using ID = decltype(tag);
+          std::vector<ID> p(run_pid.begin(), run_pid.end());
+          DevBuf<ID> dpid(R);
+          LBM_CUDA(cudaMemcpyAsync(dpid.get(), p.data(), uint64_t(R) * sizeof(ID),
+                                   cudaMemcpyHostToDevice, stream_));
+          out.alloc(n_fluid_);
+          k_ria_node_ids<ID><<<grid_for(n_fluid_, 256), 256, 0, stream_>>>(
+              ria_run0_.get(), ria_mask_.get(), dpid.get(), n_fluid_, out.get());
+          LBM_CHECK_LAUNCH();
+          LBM_CUDA(cudaStreamSynchronize(stream_));
+        };
+        if (ria_npat_ <= 256)
+          node_ids(uint8_t{}, ria_nid_);
+        else if (ria_npat_ <= 65536)
+          node_ids(uint16_t{}, ria_nid16_);
+        else
+          node_ids(uint32_t{}, ria_nid32_);
       }
     }
     // run lengths -> vectorizable fraction (list_lattice.cpp:228-236)
@@ -849,9 +870,11 @@ class ListEngine final : public Engine {
   // patterns, else the run table), 0 run table, 1 group patterns, 2 pattern
   // ids (LBMGPU_RIA_MODE)
   int ria_mode_ = -1;
-  int ria_npat_ = -1;           // distinct run patterns (-1: more than 256)
+  int ria_npat_ = -1;           // distinct run patterns (-1: more than 2^20)
   DevBuf<int32_t> ria_ptab_;    // [pattern id][18]
-  DevBuf<uint8_t> ria_nid_;     // pattern id of every node
+  DevBuf<uint8_t> ria_nid_;     // pattern id of every node (<= 256 patterns)
+  DevBuf<uint16_t> ria_nid16_;  // pattern id of every node (257 .. 65,536 patterns)
+  DevBuf<uint32_t> ria_nid32_;  // pattern id of every node (more than 65,536 patterns)
   int threads_ = 256;           // CTA size of the sweeps
   bool aos_tile_ = true;        // AoS own-record sweeps through shared-memory tiles
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold (PDFs + adjacency)

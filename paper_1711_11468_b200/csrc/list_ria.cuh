@@ -90,10 +90,11 @@ __global__ void __launch_bounds__(256) k_list_aa_odd_ria(const ListArgs a,
 // one-byte id of its run's row.  The dependent chain in front of the gathers
 // is then one coalesced byte load (prefetched into L2 a wave ahead) and an
 // L1 hit, instead of the run-table word and the run's row from L2.
+template <typename ID>
 __global__ void k_ria_node_ids(const uint32_t* __restrict__ warp_run0,
                                const uint32_t* __restrict__ warp_mask,
-                               const uint8_t* __restrict__ run_pid, uint64_t N,
-                               uint8_t* __restrict__ nid) {
+                               const ID* __restrict__ run_pid, uint64_t N,
+                               ID* __restrict__ nid) {
   for (uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; n < N;
        n += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t lane = static_cast<uint32_t>(n & 31);
@@ -103,10 +104,16 @@ __global__ void k_ria_node_ids(const uint32_t* __restrict__ warp_run0,
   }
 }
 
-template <bool CS>
+// ID = uint8_t: <= 256 distinct rows (<= 18 KB, L1-resident; a channel);
+// ID = uint16_t / uint32_t: <= 65,536 / 2^20 rows (<= 4.7 / 72 MiB,
+// L2-resident; cfg 4 blocks: 144,084 distinct rows of 6,422,500 runs,
+// 10 MB) -- the rows then come from L2 instead of the per-run pattern table
+// in DRAM (72 B per run, 8.7 nodes per run on cfg 4), for 2-4 B of id per
+// node.
+template <bool CS, typename ID = uint8_t>
 __global__ void __launch_bounds__(256) k_list_aa_odd_pid(const ListArgs a,
                                                          const int32_t* __restrict__ ptab,
-                                                         const uint8_t* __restrict__ nid,
+                                                         const ID* __restrict__ nid,
                                                          uint64_t pf) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;

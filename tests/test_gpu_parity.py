@@ -116,8 +116,9 @@ def test_aa_odd_shared_realigned_variant(kind, dims, monkeypatch):
                                        ("pipe", (9, 12, 13))])
 def test_ria_codings_bitwise_equal(kind, dims, monkeypatch):
     """Every coding of the run-coded odd step -- run table (0), group
-    patterns (1), per-node pattern ids (2, used when <= 256 distinct run
-    patterns), auto (-1) -- is bitwise list-aa-soa."""
+    patterns (1), per-node pattern ids (2: 8/16/32-bit ids for <= 256 /
+    65,536 / 2^20 distinct run patterns), auto (-1) -- is bitwise
+    list-aa-soa."""
     spec = lbm.GeometrySpec(kind, *dims)
     ref = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec)
     ref.load_perturbed(21)
@@ -130,6 +131,27 @@ def test_ria_codings_bitwise_equal(kind, dims, monkeypatch):
             k.advance(PARAMS, FORCE, 10)
             assert k.fingerprint() == ref.fingerprint(), (mode, name)
             del k
+
+
+@pytest.mark.parametrize("dims,expect", [((16, 12, 10, 4, 4), "list_aa_odd_ria_pid_soa"),
+                                         ((24, 24, 24, 4, 4), "list_aa_odd_ria_pid16_soa"),
+                                         ((192, 192, 192, 4, 4), "list_aa_odd_ria_pid32_soa")])
+def test_ria_pattern_id_widths(dims, expect):
+    """Pattern ids of every width: blocks 24^3 has 1,386 distinct run
+    patterns (16-bit ids), blocks 192^3 has 77,553 (32-bit ids; cfg 4 has
+    144,084 -- counts from tools/ria_patterns.py).  Auto mode picks the
+    width; bitwise list-aa-soa."""
+    kind = "channel" if dims[0] == 16 else "blocks"
+    spec = lbm.GeometrySpec(kind, *dims)
+    ref = lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec)
+    ref.load_perturbed(23)
+    ref.advance(PARAMS, FORCE, 6)
+    k = lbm.make_kernel(lbm.make_descriptor("list-aa-ria-soa"), spec)
+    k.load_perturbed(23)
+    k.kernel_stats_enable(True)
+    k.advance(PARAMS, FORCE, 6)
+    assert expect in k.kernel_stats()
+    assert k.fingerprint() == ref.fingerprint()
 
 
 @pytest.mark.parametrize("kind,dims", [("channel", (16, 8, 8)), ("channel", (32, 12, 8)),
