@@ -343,9 +343,9 @@ def main():
         # 19 reads + 19 writes of 8 B (+ 72 B of adjacency for list one-step,
         # 72 B for the odd AA list sub-step only)
         if "ria_pid" in name:
-            # pattern-id coding: 304 B of PDFs + a 1-byte pattern id per node
-            # (the <= 256-row pattern table stays in L1)
-            per_node = 304 + 1
+            # pattern-id coding: 304 B of PDFs + a 1/2/4-byte pattern id per
+            # node (the pattern table stays in L1 / L2)
+            per_node = 304 + (4 if "pid32" in name else 2 if "pid16" in name else 1)
         elif "ria" in name:
             # run-coded odd step: 304 B of PDFs + 8 B of run table per 32
             # nodes (the pattern rows are L1/L2 resident)

@@ -564,14 +564,11 @@ class ListEngine final : public Engine {
           const int rt = threads_env_ ? threads_ : 128;
           const unsigned g = static_cast<unsigned>(ceil_div(a.N, rt));
           if (mode == 2 && ria_npat_ > 65536)
-            k_list_aa_odd_pid<false, uint32_t><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(),
-                                                                      ria_nid32_.get(), pf_);
+            launch_pid(g, rt, a, ria_nid32_.get());
           else if (mode == 2 && ria_npat_ > 256)
-            k_list_aa_odd_pid<false, uint16_t><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(),
-                                                                      ria_nid16_.get(), pf_);
+            launch_pid(g, rt, a, ria_nid16_.get());
           else if (mode == 2 && ria_npat_ > 0)
-            k_list_aa_odd_pid<false><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(), ria_nid_.get(),
-                                                            pf_);
+            launch_pid(g, rt, a, ria_nid_.get());
           else if (mode == 1)
             k_list_aa_odd_gpat<false><<<g, rt, 0, stream_>>>(a, ria_gpat_.get(), pf_);
           else
@@ -725,6 +722,11 @@ class ListEngine final : public Engine {
       for (int q = 0; q < kQ; ++q) starts[q] = desc_.soa ? starts_[q] : 0;
     if (total) *total = total_slots_;
     LBM_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  template <typename ID>
+  void launch_pid(unsigned g, int rt, const ListArgs& a, const ID* nid) {
+    k_list_aa_odd_pid<false, ID><<<g, rt, 0, stream_>>>(a, ria_ptab_.get(), nid, pf_);
   }
 
   // ria_stats / vector_fraction (kernels_list_aa.cpp:95-140) for the ria/pv

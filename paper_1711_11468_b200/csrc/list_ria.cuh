@@ -110,11 +110,14 @@ __global__ void k_ria_node_ids(const uint32_t* __restrict__ warp_run0,
 // 10 MB) -- the rows then come from L2 instead of the per-run pattern table
 // in DRAM (72 B per run, 8.7 nodes per run on cfg 4), for 2-4 B of id per
 // node.
+// __launch_bounds__(256, 2): <= 128 registers (4 CTAs of 128 threads per
+// SM).  Measured alternatives: (128, 5) -- 96 registers, small spill -- 1-2 %
+// slower; re-reading the row's offsets after the collision instead of
+// keeping them live 3-5 % slower (the loads get hoisted, registers rise).
 template <bool CS, typename ID = uint8_t>
-__global__ void __launch_bounds__(256) k_list_aa_odd_pid(const ListArgs a,
-                                                         const int32_t* __restrict__ ptab,
-                                                         const ID* __restrict__ nid,
-                                                         uint64_t pf) {
+__global__ void __launch_bounds__(256, 2)
+    k_list_aa_odd_pid(const ListArgs a, const int32_t* __restrict__ ptab,
+                      const ID* __restrict__ nid, uint64_t pf) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
   if (pf && (threadIdx.x & 31) == 0) {  // ids of a later wave -> L2
