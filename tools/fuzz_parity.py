@@ -44,6 +44,9 @@ for case in range(cases):
     if parts > 1 and nz >= parts and (name in ("aa-soa", "aa-vec-soa", "blk-push-soa", "blk-pull-soa")
                                       or (name in ("list-aa-soa", "list-aa-aos") and blk == 0)):
         dist = {"virtual_parts": parts}
+        if name.startswith("aa") and rng.random() < 0.5:
+            dist["transport"] = "peer"  # boundary odd sweeps in the neighbour slab, epoch flags
+    os.environ["LBMGPU_RIA_MODE"] = str(rng.choice(["-1", "0", "1", "2"]))  # ria / pv names
     init = port.perturbed(nf, seed0 + case)
     fam = "half" if name.startswith("list-") else "full"
     params = lbm.TrtParams.from_tau(tau)
@@ -62,6 +65,6 @@ for case in range(cases):
     if not ok:
         bad += 1
         print("MISMATCH", case, name, kind, (nx, ny, nz), block, spacing, blk, tau, steps,
-              os.environ["LBMGPU_FUSED_MB"], dist, flush=True)
+              os.environ["LBMGPU_FUSED_MB"], os.environ["LBMGPU_RIA_MODE"], dist, flush=True)
 print(f"{cases} cases, {bad} mismatches", flush=True)
 sys.exit(1 if bad else 0)
