@@ -296,6 +296,20 @@ class Kernel {
     if (pv < 0) return std::nullopt;
     return pv;
   }
+  // Peer-memory transport (lbmgpu_dist.transport = 1, nranks > 1): this
+  // rank's CUDA IPC record; all-gather them and pass all ranks' records
+  // (rank order) to peer_attach before the first advance.
+  std::vector<std::uint8_t> peer_export() const {
+    std::size_t len = 0;
+    check(lbmgpu_peer_export(ctx_.get(), nullptr, 0, &len));
+    std::vector<std::uint8_t> rec(len);
+    check(lbmgpu_peer_export(ctx_.get(), rec.data(), rec.size(), &len));
+    return rec;
+  }
+  void peer_attach(std::span<const std::uint8_t> records, int nranks) {
+    check(lbmgpu_peer_attach(ctx_.get(), records.data(),
+                             nranks > 0 ? records.size() / nranks : 0, nranks));
+  }
 
  private:
   struct Del {
