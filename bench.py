@@ -221,8 +221,8 @@ def main():
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
     ap.add_argument("--transport", default="copy", choices=["copy", "peer"],
-                    help="z-slab AA halo transport: copy = NCCL send/recv (device copies "
-                         "with --virtual-parts), peer = boundary odd sub-steps load/store the "
+                    help="z-slab halo transport: copy = NCCL send/recv (device copies "
+                         "with --virtual-parts), peer = boundary sweeps load/store the "
                          "neighbour slab in peer memory (CUDA IPC), epoch flags")
     ap.add_argument("--decompose", action="store_true",
                     help="at N>1: z-slab decomposition of direct push/pull and node-range "

@@ -92,8 +92,8 @@ typedef struct {
  * kernels as the NCCL path, used for single-GPU parity tests.  nranks > 1:
  * one process per GPU, NCCL point-to-point over NVLink; nccl_id is the
  * 128-byte id from lbmgpu_nccl_unique_id() broadcast by rank 0.
- * transport = 1 (AA z slabs only): no halo copies -- the boundary planes'
- * odd sub-step loads and stores the neighbour slab's slots in peer memory
+ * transport = 1 (direct SoA z slabs): no halo copies -- the boundary planes'
+ * sweeps (AA odd, pull, push) load / store the neighbour slab in peer memory
  * (CUDA IPC over NVLink between processes: lbmgpu_peer_export / _attach
  * before the first advance; device pointers with virtual_parts), with
  * per-sub-step epoch flags in peer memory as the only synchronisation. */

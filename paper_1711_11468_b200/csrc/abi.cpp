@@ -339,6 +339,9 @@ int lbmgpu_create(const char* name, int blk, int W, const lbmgpu_geometry* geom,
     }
     if (ds.device >= 0) LBM_CUDA(cudaSetDevice(ds.device));
     if (c->desc.indirect) {
+      if (ds.transport == 1)
+        throw ConfigError("peer transport: implemented for the direct SoA z slabs (kernel '" +
+                          c->desc.name + "')");
       if ((ds.nranks > 1 || ds.virtual_parts > 1) &&
           (c->desc.prop != Prop::Aa || c->desc.ria || c->desc.blk != 0))
         throw ConfigError("list decomposition is implemented for list-aa-soa / list-aa-aos "

@@ -324,9 +324,8 @@ class DirectEngine final : public Engine {
     if (nparts_ > g.nz) throw ConfigError("more z-slab parts than z planes");
     if (dist.transport != 0 && dist.transport != 1)
       throw ConfigError("dist: transport must be 0 (halo copies) or 1 (peer memory)");
-    if (dist.transport == 1 && (d.prop != Prop::Aa || nparts_ < 2))
-      throw ConfigError("peer transport: implemented for the AA z-slab decomposition "
-                        "(aa-soa / aa-vec-soa over >= 2 slabs)");
+    if (dist.transport == 1 && nparts_ < 2)
+      throw ConfigError("peer transport: needs a z-slab decomposition (>= 2 slabs)");
     if (nranks_ > 1 && !dist.have_id)
       throw ConfigError("dist: nranks > 1 needs the NCCL unique id");
     {
@@ -462,7 +461,7 @@ class DirectEngine final : public Engine {
                                               nparts_, dist.nccl_id.data());
       else
         tr_ = std::make_unique<LocalTransport>(std::move(plan));
-      ring_ = end_fluid;
+      ring_ = end_fluid || d.prop != Prop::Aa;  // one-step plans always carry the ring
       if (dist.transport == 1) setup_peer();
     }
     LBM_CUDA(cudaStreamSynchronize(stream_));
@@ -741,7 +740,7 @@ class DirectEngine final : public Engine {
     const bool cs = cs_;
     if (advance_fused(t, steps)) return;
     if (desc_.prop != Prop::Aa && nparts_ > 1) {
-      os_sweeps_slabs(t, steps);
+      peer_ ? os_sweeps_peer(t, steps) : os_sweeps_slabs(t, steps);
       return;
     }
     if (desc_.prop == Prop::OsPush) {
@@ -950,17 +949,17 @@ class DirectEngine final : public Engine {
   // slots of the lower plane, up-slots of the upper plane), and interior
   // sweeps touch no boundary slot of another slab.
   struct PeerLink {
-    double* lo = nullptr;  // lower neighbour's lattice (its storage plane lo_plane = global z0-1)
-    double* hi = nullptr;  // upper neighbour's lattice (its storage plane hi_plane = global z1)
+    double* lo[2] = {nullptr, nullptr};  // lower neighbour's grids (storage plane lo_plane = global z0-1)
+    double* hi[2] = {nullptr, nullptr};  // upper neighbour's grids (storage plane hi_plane = global z1)
     uint32_t lo_plane = 0, hi_plane = 0;
     unsigned long long* lo_flags = nullptr;  // the neighbours' epoch flags (4 each)
     unsigned long long* hi_flags = nullptr;
   };
   // CUDA IPC record one rank exports (lbmgpu_peer_export)
   struct PeerRecord {
-    uint32_t magic, rank, nzl, zoff;
-    uint64_t buf_off, flag_off;
-    cudaIpcMemHandle_t buf, flag;
+    uint32_t magic, rank, nzl, zoff, nbuf, pad;
+    uint64_t buf_off[2], flag_off;
+    cudaIpcMemHandle_t buf[2], flag;
   };
   static constexpr uint32_t kPeerMagic = 0x4c424d50u;  // "LBMP"
 
@@ -991,13 +990,13 @@ class DirectEngine final : public Engine {
       PeerLink& L = links_[i];
       if (lo >= 0) {
         const Part& q = parts_[lo];
-        L.lo = q.buf[0].get();
+        for (int b = 0; b < 2; ++b) L.lo[b] = q.buf[b].get();
         L.lo_plane = q.zoff + q.nzl - 1;
         L.lo_flags = q.pflag.get();
       }
       if (hi >= 0) {
         const Part& q = parts_[hi];
-        L.hi = q.buf[0].get();
+        for (int b = 0; b < 2; ++b) L.hi[b] = q.buf[b].get();
         L.hi_plane = q.zoff;
         L.hi_flags = q.pflag.get();
       }
@@ -1015,9 +1014,13 @@ class DirectEngine final : public Engine {
     r.rank = static_cast<uint32_t>(rank_);
     r.nzl = pt.nzl;
     r.zoff = pt.zoff;
-    r.buf_off = pt.buf[0].alloc_offset();
+    r.nbuf = desc_.prop == Prop::Aa ? 1 : 2;
+    for (uint32_t b = 0; b < r.nbuf; ++b) {
+      r.buf_off[b] = pt.buf[b].alloc_offset();
+      LBM_CUDA(cudaIpcGetMemHandle(&r.buf[b],
+                                   reinterpret_cast<char*>(pt.buf[b].get()) - r.buf_off[b]));
+    }
     r.flag_off = pt.pflag.alloc_offset();
-    LBM_CUDA(cudaIpcGetMemHandle(&r.buf, reinterpret_cast<char*>(pt.buf[0].get()) - r.buf_off));
     LBM_CUDA(cudaIpcGetMemHandle(&r.flag, reinterpret_cast<char*>(pt.pflag.get()) - r.flag_off));
     const uint8_t* b = reinterpret_cast<const uint8_t*>(&r);
     rec.assign(b, b + sizeof r);
@@ -1037,19 +1040,23 @@ class DirectEngine final : public Engine {
         throw ConfigError("peer transport: bad record for rank " + std::to_string(r));
       return x;
     };
-    struct Mapped { char* buf; char* flag; };
+    struct Mapped { char* buf[2]; char* flag; };
     std::vector<std::pair<int, Mapped>> opened;
     auto map = [&](int r) -> Mapped {
       for (auto& o : opened)
         if (o.first == r) return o.second;  // two ranks with the z ring: lo == hi
       const PeerRecord x = record(r);
-      void* b = nullptr;
+      Mapped m{{nullptr, nullptr}, nullptr};
+      for (uint32_t b = 0; b < x.nbuf && b < 2; ++b) {
+        void* p = nullptr;
+        LBM_CUDA(cudaIpcOpenMemHandle(&p, x.buf[b], cudaIpcMemLazyEnablePeerAccess));
+        ipc_open_.push_back(p);
+        m.buf[b] = static_cast<char*>(p) + x.buf_off[b];
+      }
       void* f = nullptr;
-      LBM_CUDA(cudaIpcOpenMemHandle(&b, x.buf, cudaIpcMemLazyEnablePeerAccess));
-      ipc_open_.push_back(b);
       LBM_CUDA(cudaIpcOpenMemHandle(&f, x.flag, cudaIpcMemLazyEnablePeerAccess));
       ipc_open_.push_back(f);
-      Mapped m{static_cast<char*>(b) + x.buf_off, static_cast<char*>(f) + x.flag_off};
+      m.flag = static_cast<char*>(f) + x.flag_off;
       opened.emplace_back(r, m);
       return m;
     };
@@ -1060,14 +1067,14 @@ class DirectEngine final : public Engine {
     if (lo >= 0) {
       const PeerRecord x = record(lo);
       const Mapped m = map(lo);
-      L.lo = reinterpret_cast<double*>(m.buf);
+      for (int b = 0; b < 2; ++b) L.lo[b] = reinterpret_cast<double*>(m.buf[b]);
       L.lo_plane = x.zoff + x.nzl - 1;
       L.lo_flags = reinterpret_cast<unsigned long long*>(m.flag);
     }
     if (hi >= 0) {
       const PeerRecord x = record(hi);
       const Mapped m = map(hi);
-      L.hi = reinterpret_cast<double*>(m.buf);
+      for (int b = 0; b < 2; ++b) L.hi[b] = reinterpret_cast<double*>(m.buf[b]);
       L.hi_plane = x.zoff;
       L.hi_flags = reinterpret_cast<unsigned long long*>(m.flag);
     }
@@ -1119,7 +1126,7 @@ class DirectEngine final : public Engine {
             aa_sub(false, a, "full_aa_even_soa_halo");
           } else {
             const PeerLink& L = links_[i];
-            const PeerArgs pa{L.lo, L.hi, L.lo_plane, L.hi_plane};
+            const PeerArgs pa{L.lo[0], L.hi[0], L.lo_plane, L.hi_plane};
             const int tok = stats_.begin("full_aa_odd_soa_peer", stream_);
             k_full_aa_odd_peer<<<static_cast<unsigned>(ceil_div(cnt, 128)), 128, 0, stream_>>>(
                 a, pa);
@@ -1143,6 +1150,83 @@ class DirectEngine final : public Engine {
     peer_signal(1, e);
     sweep(true, false);
     peer_wait(1, e);
+  }
+
+  // One-step sweeps with the peer transport.  Every op (the pull's collide
+  // pass, each sweep) touching boundary planes runs as
+  //   wait(neighbours' op e-1) -> op(boundary planes) -> signal(e) -> op(interior)
+  // A neighbour's op e+1 touches only this slab's boundary planes of the grid
+  // this op does not write (pull: reads our source of e+1 = destination of
+  // e, written by our boundary sweep before the signal; push: writes our
+  // destination of e+1 = source of e, read by our boundary sweep before the
+  // signal) and each slot has one writer per sweep, so one flag per op
+  // orders everything.
+  void os_sweeps_peer(const TrtArgs& t, long steps) {
+    const uint32_t P = static_cast<uint32_t>(P_);
+    const bool push = desc_.prop == Prop::OsPush;
+    auto each = [&](bool boundary, auto&& fn) {
+      for (size_t i = 0; i < parts_.size(); ++i) {
+        Part& pt = parts_[i];
+        const uint32_t last = (pt.nzl - 1) * P;
+        if (boundary) {
+          fn(i, pt, 0u, P);
+          if (pt.nzl > 1) fn(i, pt, last, P);
+        } else if (pt.nzl > 2) {
+          fn(i, pt, P, last - P);
+        }
+      }
+    };
+    auto op = [&](auto&& boundary_fn, auto&& interior_fn) {
+      const unsigned long long e = ++epoch_;
+      peer_wait(0, e - 1);
+      each(true, boundary_fn);
+      peer_signal(0, e);
+      each(false, interior_fn);
+    };
+    if (!push) {
+      auto coll = [&](size_t, Part& pt, uint32_t n0, uint32_t cnt) {
+        launch("full_collide_soa", k_full_collide<true>, args(pt, n0, cnt, t, cur_, cur_),
+               stream_);
+      };
+      op(coll, coll);
+    }
+    for (long s = 0; s < steps; ++s) {
+      const int src = cur_, dst = 1 - cur_;
+      const bool collide = push || s + 1 < steps;
+      auto interior = [&](size_t, Part& pt, uint32_t n0, uint32_t cnt) {
+        const DirectArgs a = args(pt, n0, cnt, t, src, dst);
+        if (push)
+          launch("full_push_soa", k_full_push<true, false>, a, stream_);
+        else if (collide)
+          launch("full_pull_soa", k_full_pull<true, true, false>, a, stream_);
+        else
+          launch("full_pull_stream_soa", k_full_pull<true, false, false>, a, stream_);
+      };
+      auto boundary = [&](size_t i, Part& pt, uint32_t n0, uint32_t cnt) {
+        const DirectArgs a = args(pt, n0, cnt, t, src, dst);
+        const PeerLink& L = links_[i];
+        const int g = push ? dst : src;  // the neighbour grid the boundary touches
+        const PeerArgs pa{L.lo[g], L.hi[g], L.lo_plane, L.hi_plane};
+        const unsigned grid = static_cast<unsigned>(ceil_div(cnt, 256));
+        const int tok = stats_.begin(push ? "full_push_soa_peer"
+                                     : collide ? "full_pull_soa_peer"
+                                               : "full_pull_stream_soa_peer",
+                                     stream_);
+        if (push)
+          k_full_push_peer<<<grid, 256, 0, stream_>>>(a, pa);
+        else if (collide)
+          k_full_pull_peer<true><<<grid, 256, 0, stream_>>>(a, pa);
+        else
+          k_full_pull_peer<false><<<grid, 256, 0, stream_>>>(a, pa);
+        LBM_CHECK_LAUNCH();
+        stats_.end(tok, stream_);
+      };
+      op(boundary, interior);
+      cur_ ^= 1;
+    }
+    // the last op's neighbours must be done with this slab before the host
+    // touches it (snapshot / load_state) or the next advance starts
+    peer_wait(0, epoch_);
   }
 
   CanonArgs canon_args(const Part& pt, int buf) const {

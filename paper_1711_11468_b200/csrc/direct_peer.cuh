@@ -19,8 +19,8 @@ namespace lbmgpu {
 // c_z(d) = -1 it is the upper neighbour's bottom plane (its up-slots).  The
 // even sub-step touches own slots only.
 struct PeerArgs {
-  double* lo;         // lower neighbour's lattice; null = own storage plane z-1
-  double* hi;         // upper neighbour's lattice; null = own storage plane z+1
+  double* lo;         // lower neighbour's lattice (grid); null = own storage plane z-1
+  double* hi;         // upper neighbour's lattice (grid); null = own storage plane z+1
   uint32_t lo_plane;  // lower neighbour's storage plane of global z0 - 1
   uint32_t hi_plane;  // upper neighbour's storage plane of global z1
 };
@@ -74,6 +74,74 @@ __global__ void __launch_bounds__(128) k_full_aa_odd_peer(const DirectArgs a, co
 #pragma unroll
       for (int d = 0; d < kQ; ++d) p[d][0] = q[opp(d)];
     }
+  }
+}
+
+// One-step sweeps over z slabs with the peer transport (halo.hpp phases 2 / 3
+// without the copies).  Pull (kernels_full_os.cpp:56-89, PULL): a boundary
+// plane's gathers from z - 1 / z + 1 read the neighbour's source grid
+// directly (remote loads only).  Push: a boundary plane's crossing stores go
+// straight into the neighbour's destination grid, into slot d or -- solid
+// target, from the solid-target mask built with the global flags -- the
+// bounce-back slot opp(d): exactly the slot k_push_halo_merge would select,
+// so the staging planes and the merge disappear.  Same arithmetic as
+// pull_node / push_node.
+template <bool COLLIDE>
+__global__ void __launch_bounds__(256) k_full_pull_peer(const DirectArgs a, const PeerArgs pa) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  const Idx<true> I{a.P, a.nx, a.ny};
+  const double* zb[3] = {a.src, a.src, a.src};
+  uint32_t zp[3] = {c.Z[0], c.Z[1], c.Z[2]};
+  if (c.z == 0 && pa.lo) {
+    zb[0] = pa.lo;
+    zp[0] = pa.lo_plane;
+  }
+  if (c.z + 1 == a.nzl && pa.hi) {
+    zb[2] = pa.hi;
+    zp[2] = pa.hi_plane;
+  }
+  double q[kQ];
+  q[0] = a.src[I(c.Z[1], dslot(0), c.y, c.x)];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    q[d] = zb[1 - cz(d)][I(zp[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+  const bool solid = solid_node(a, c.x, c.y, c.z, n);
+  if (COLLIDE && !solid) collide(q, a.trt);
+  a.dst[I(c.Z[1], dslot(0), c.y, c.x)] = q[0];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d)
+    a.dst[I(c.Z[1], solid ? dslot(opp(d)) : dslot(d), c.y, c.x)] = q[d];
+}
+
+__global__ void __launch_bounds__(256) k_full_push_peer(const DirectArgs a, const PeerArgs pa) {
+  Coords c;
+  uint32_t n;
+  if (!decode(a, c, n)) return;
+  const Idx<true> I{a.P, a.nx, a.ny};
+  const uint32_t tm = a.tmask[n];  // always built for several parts
+  double q[kQ];
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) q[d] = a.src[I(c.Z[1], dslot(d), c.y, c.x)];
+  if (!solid_node(a, c.x, c.y, c.z, n)) collide(q, a.trt);
+  a.dst[I(c.Z[1], dslot(0), c.y, c.x)] = q[0];
+  const bool lo = c.z == 0 && pa.lo, hi = c.z + 1 == a.nzl && pa.hi;
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) {
+    const uint32_t tx = c.X[1 + cx(d)], ty = c.Y[1 + cy(d)];
+    double* base = a.dst;
+    uint32_t tz = c.Z[1 + cz(d)];
+    if (cz(d) < 0 && lo) {
+      base = pa.lo;
+      tz = pa.lo_plane;
+    }
+    if (cz(d) > 0 && hi) {
+      base = pa.hi;
+      tz = pa.hi_plane;
+    }
+    const int s = ((tm >> d) & 1u) ? dslot(opp(d)) : dslot(d);
+    base[I(tz, s, ty, tx)] = q[d];
   }
 }
 

@@ -503,43 +503,52 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
-@pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa"])
+@pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims,parts", [
     ("channel", (16, 12, 24), 2), ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2),
     ("blocks", (12, 10, 16), 4), ("slit", (6, 5, 9), 3), ("pipe", (9, 12, 13), 13),
     ("blocks", (16, 16, 16), 16)])
 def test_zslab_peer_transport_bitwise_equal_single(name, kind, dims, parts):
-    """Peer-memory transport (direct_peer.cuh): the boundary planes' odd
-    sub-step loads and stores the neighbour slab's slots directly, epoch
-    flags in the neighbour's memory order the sub-steps, no halo copy at
-    all.  Emulated with all slabs on one device (device pointers instead of
-    CUDA IPC mappings; the flag protocol runs unchanged).  Covers the z ring
-    (blocks: fluid on z = 0), two slabs with the ring (lower == upper
-    neighbour) and one plane per slab (pipe 13, blocks 16).  Bitwise equal
-    to the single-slab run, over several advance() calls."""
+    """Peer-memory transport (direct_peer.cuh): no halo copy at all -- the
+    AA boundary planes' odd sub-step loads and stores the neighbour slab's
+    slots, the pull's boundary gathers read the neighbour's source grid,
+    the push's boundary stores land in the neighbour's destination grid
+    (slot chosen by the solid-target mask, no staging / merge); epoch flags
+    in the neighbour's memory order the sub-steps.  Emulated with all slabs
+    on one device (device pointers instead of CUDA IPC mappings; the flag
+    protocol runs unchanged).  Covers the z ring (blocks: fluid on z = 0;
+    one-step kernels always), two slabs with the ring (lower == upper
+    neighbour), one plane per slab (pipe 13, blocks 16) and odd step counts
+    (push / pull end on the second grid).  Bitwise equal to the single-slab
+    run, over several advance() calls, total mass included."""
     spec = lbm.GeometrySpec(kind, *dims)
+    aa = name.startswith("aa")
+    steps = (4, 2, 4) if aa else (3, 2, 4)
     ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
     ref.load_perturbed(777)
-    ref.advance(PARAMS, FORCE, 10)
+    ref.advance(PARAMS, FORCE, sum(steps))
     k = lbm.make_kernel(lbm.make_descriptor(name), spec,
                         dist={"virtual_parts": parts, "transport": "peer"})
     k.load_perturbed(777)
     k.kernel_stats_enable(True)
-    for st in (4, 2, 4):
+    for st in steps:
         k.advance(PARAMS, FORCE, st)
     assert np.array_equal(k.snapshot(), ref.snapshot()), name
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
     names = set(k.kernel_stats())
-    assert "full_aa_odd_soa_peer" in names and "peer_wait" in names
+    peer_kernel = {"aa-soa": "full_aa_odd_soa_peer", "aa-vec-soa": "full_aa_odd_soa_peer",
+                   "blk-push-soa": "full_push_soa_peer", "blk-pull-soa": "full_pull_soa_peer"}
+    assert peer_kernel[name] in names and "peer_wait" in names
+    assert "push_halo_merge" not in names
 
 
 def test_zslab_peer_transport_errors():
     spec = lbm.GeometrySpec("channel", 16, 12, 24)
     with pytest.raises(lbm.ConfigError, match="peer transport"):
-        lbm.make_kernel(lbm.make_descriptor("blk-push-soa"), spec,
-                        dist={"virtual_parts": 2, "transport": "peer"})
-    with pytest.raises(lbm.ConfigError, match="peer transport"):
         lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec, dist={"transport": "peer"})
+    with pytest.raises(lbm.ConfigError, match="peer transport"):
+        lbm.make_kernel(lbm.make_descriptor("list-aa-soa"), spec,
+                        dist={"virtual_parts": 2, "transport": "peer"})
     k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
                         dist={"virtual_parts": 3, "transport": "peer"})
     with pytest.raises(lbm.ConfigError, match="nranks > 1"):

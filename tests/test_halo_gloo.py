@@ -588,3 +588,169 @@ def test_peer_transport_protocol_shared_memory(kind, dims, world):
                 k += 1
     expect, _ = port.run("full", kind, nx, ny, nz, steps, 1.0 / TAU, g=G, init=init)
     assert np.array_equal(full, expect), port.max_rel_diff(full, expect)
+
+
+def _rank_main_peer_one_step(rank, world, kind, dims, steps, push, shared, flags, q):
+    """The one-step peer protocol (DirectEngine::os_sweeps_peer) run
+    concurrently: every op (the pull's collide pass, each sweep) is
+    wait(neighbours' op e-1) -> op(boundary planes) -> signal(e) ->
+    op(interior planes); pull boundary nodes gather from the neighbour's
+    source grid, push boundary nodes store into the neighbour's destination
+    grid (slot by the target's global solid flag).  Slabs in shared memory,
+    random delays, flags as the only synchronisation."""
+    import random
+    import time
+    from oracle.oracle import Port
+    port = Port()
+    rng = random.Random(2000 + rank)
+    nx, ny, nz = dims
+    flags_g, per, nf = port.geometry(kind, nx, ny, nz)
+    solid = flags_g.reshape(nx, ny, nz).astype(bool)
+    zr = [nz * r // world for r in range(world + 1)]
+    z0, z1 = zr[rank], zr[rank + 1]
+    nzl = z1 - z0
+    lo, hi = (rank - 1) % world, (rank + 1) % world  # one-step plans always carry the ring
+    bufs = [[t.numpy() for t in pair] for pair in shared]  # [slab][grid]: (nzl_r + 2, Q, ny, nx)
+    fl = flags.numpy()
+    wp = 1.0 / TAU
+    wm = port.omega_minus(wp)
+    nodes = [(x, y, z) for z in range(nzl) for y in range(ny) for x in range(nx)]
+    boundary = [n for n in nodes if n[2] == 0 or n[2] == nzl - 1]
+    interior = [n for n in nodes if 0 < n[2] < nzl - 1]
+
+    def at(g, zs):  # storage plane of this slab's grid g -> (array, plane); ghosts -> peer
+        if zs == 0:
+            return bufs[lo][g], zr[lo + 1] - zr[lo]
+        if zs == nzl + 1:
+            return bufs[hi][g], 1
+        return bufs[rank][g], zs
+
+    def signal(e):
+        fl[lo, 1] = e   # I am the lower neighbour's upper neighbour
+        fl[hi, 0] = e
+
+    def wait(e):
+        t0 = time.time()
+        for j in (0, 1):
+            while fl[rank, j] < e:
+                assert time.time() - t0 < 120, "peer wait timed out"
+                time.sleep(0.0005)
+
+    def op(e, fn):
+        wait(e - 1)
+        time.sleep(rng.random() * 0.01)
+        fn(boundary)
+        signal(e)
+        time.sleep(rng.random() * 0.01)
+        fn(interior)
+
+    cur = 0
+    e = 0
+    if not push:
+        def coll(ns):
+            b = bufs[rank][0]
+            for (x, y, z) in ns:
+                if not solid[x, y, z + z0]:
+                    f = np.array([b[z + 1, SLOT[d], y, x] for d in range(Q)])
+                    f = port.collide(f, wp, wm, G)
+                    for d in range(Q):
+                        b[z + 1, SLOT[d], y, x] = f[d]
+        e += 1
+        op(e, coll)
+    for s in range(steps):
+        src, dst = cur, 1 - cur
+
+        def sweep(ns):
+            for (x, y, z) in ns:
+                zs = z + 1
+                if push:
+                    b = bufs[rank][src]
+                    f = np.array([b[zs, SLOT[d], y, x] for d in range(Q)])
+                    if not solid[x, y, z + z0]:
+                        f = port.collide(f, wp, wm, G)
+                    bufs[rank][dst][zs, SLOT[0], y, x] = f[0]
+                    for d in range(1, Q):
+                        tx, ty = (x + CX[d]) % nx, (y + CY[d]) % ny
+                        tzg = (z + z0 + CZ[d]) % nz
+                        a, p = at(dst, zs + CZ[d])
+                        a[p, SLOT[OPP[d]] if solid[tx, ty, tzg] else SLOT[d], ty, tx] = f[d]
+                else:
+                    f = np.empty(Q)
+                    f[0] = bufs[rank][src][zs, SLOT[0], y, x]
+                    for d in range(1, Q):
+                        a, p = at(src, zs - CZ[d])
+                        f[d] = a[p, SLOT[d], (y - CY[d]) % ny, (x - CX[d]) % nx]
+                    sol = solid[x, y, z + z0]
+                    if s + 1 < steps and not sol:
+                        f = port.collide(f, wp, wm, G)
+                    b = bufs[rank][dst]
+                    b[zs, SLOT[0], y, x] = f[0]
+                    for d in range(1, Q):
+                        b[zs, SLOT[OPP[d]] if sol else SLOT[d], y, x] = f[d]
+        e += 1
+        op(e, sweep)
+        cur ^= 1
+    wait(e)
+    q.put((rank, cur))
+
+
+@pytest.mark.parametrize("push", [True, False])
+@pytest.mark.parametrize("kind,dims,world", [("channel", (6, 5, 8), 2), ("blocks", (8, 8, 9), 3)])
+def test_peer_transport_one_step_protocol_shared_memory(kind, dims, world, push):
+    import torch
+    from oracle.oracle import Port
+    port = Port()
+    nx, ny, nz = dims
+    flags_g, per, nf = port.geometry(kind, nx, ny, nz)
+    solid = flags_g.reshape(nx, ny, nz)
+    init = port.perturbed(nf, 92)
+    zr = [nz * r // world for r in range(world + 1)]
+    w = np.array([1 / 3] + [1 / 18] * 6 + [1 / 36] * 12)
+    shared = []
+    for r in range(world):
+        pair = []
+        for g in range(2):
+            b = np.empty((zr[r + 1] - zr[r] + 2, Q, ny, nx))
+            for d in range(Q):
+                b[:, SLOT[d]] = w[d]
+            pair.append(b)
+        shared.append(pair)
+    k = 0
+    for x in range(nx):
+        for y in range(ny):
+            for z in range(nz):
+                if solid[x, y, z]:
+                    continue
+                r = max(i for i in range(world) if zr[i] <= z)
+                for d in range(Q):
+                    shared[r][0][z - zr[r] + 1, SLOT[d], y, x] = init[k * Q + d]
+                k += 1
+    shared = [[torch.from_numpy(b).share_memory_() for b in pair] for pair in shared]
+    flags = torch.zeros((world, 2), dtype=torch.int64).share_memory_()
+    steps = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_main_peer_one_step,
+                         args=(r, world, kind, dims, steps, push, shared, flags, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    cur = q.get(timeout=5)[1]
+    full = np.zeros(nf * Q)
+    mass = 0.0
+    k = 0
+    for x in range(nx):
+        for y in range(ny):
+            for z in range(nz):
+                r = max(i for i in range(world) if zr[i] <= z)
+                vals = [shared[r][cur][z - zr[r] + 1, SLOT[d], y, x].item() for d in range(Q)]
+                if not solid[x, y, z]:
+                    full[k * Q:(k + 1) * Q] = vals
+                    k += 1
+    mass = float(sum(shared[r][cur][1:-1].sum().item() for r in range(world)))
+    expect, emass = port.run("full", kind, nx, ny, nz, steps, 1.0 / TAU, g=G, init=init)
+    assert np.array_equal(full, expect), port.max_rel_diff(full, expect)
+    assert abs(mass - emass) <= 1e-12 * abs(emass)

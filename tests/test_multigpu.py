@@ -35,15 +35,16 @@ def test_nccl_decomposition_bitwise(n, kind, dims, name):
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("name", ["aa-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims", [("channel", (64, 32, 48)), ("blocks", (32, 32, 32))])
-def test_peer_transport_bitwise(n, kind, dims):
-    """aa-soa z slabs over CUDA IPC peer memory (direct_peer.cuh): no halo
-    copies, epoch flags in the neighbours' memory; bitwise vs one GPU."""
+def test_peer_transport_bitwise(n, kind, dims, name):
+    """Direct SoA z slabs over CUDA IPC peer memory (direct_peer.cuh): no
+    halo copies, epoch flags in the neighbours' memory; bitwise vs one GPU."""
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + n),
-           os.path.join(ROOT, "tools", "mgpu_check.py"), *map(str, dims), "10", kind, "aa-soa",
+           os.path.join(ROOT, "tools", "mgpu_check.py"), *map(str, dims), "10", kind, name,
            "peer"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr

@@ -101,7 +101,7 @@ static void rejections() {
   GeometrySpec bad = bench_blocks();
   bad.block = 0;
   CHECK(throws<ConfigError>([&] { make_kernel(make_descriptor("aa-soa"), bad); }));
-  // the peer transport needs nranks > 1 and an AA z-slab split
+  // the peer transport needs nranks > 1 and a direct SoA z-slab split
   CHECK(throws<ConfigError>([&] { k->peer_export(); }));
   GeometrySpec small;
   small.nx = 16;
@@ -112,7 +112,7 @@ static void rejections() {
   CHECK(throws<ConfigError>([&] { ka.peer_export(); }));
   lbmgpu_dist dp{0, 1, -1, 3, nullptr, 1};
   CHECK(throws<ConfigError>(
-      [&] { Kernel kp(make_descriptor("blk-push-soa"), small, PaddingPolicy::automatic(), 0, &dp); }));
+      [&] { Kernel kp(make_descriptor("list-aa-soa"), small, PaddingPolicy::automatic(), 0, &dp); }));
 }
 
 // verify_kernel (verification.cpp) through the C++ API

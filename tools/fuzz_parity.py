@@ -44,7 +44,7 @@ for case in range(cases):
     if parts > 1 and nz >= parts and (name in ("aa-soa", "aa-vec-soa", "blk-push-soa", "blk-pull-soa")
                                       or (name in ("list-aa-soa", "list-aa-aos") and blk == 0)):
         dist = {"virtual_parts": parts}
-        if name.startswith("aa") and rng.random() < 0.5:
+        if not name.startswith("list") and rng.random() < 0.5:
             dist["transport"] = "peer"  # boundary odd sweeps in the neighbour slab, epoch flags
     os.environ["LBMGPU_RIA_MODE"] = str(rng.choice(["-1", "0", "1", "2"]))  # ria / pv names
     init = port.perturbed(nf, seed0 + case)
