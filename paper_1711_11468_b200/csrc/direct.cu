@@ -350,6 +350,7 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_FUSED_SHAPE")) fused_shape_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_GRID_SYNC")) barrier_mode_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_PUSH_TMASK")) use_tmask_ = std::atoi(e) != 0;
+      if (const char* e = std::getenv("LBMGPU_GRAPH")) graph_mode_ = std::atoi(e) != 0;
       if (flow_threads_ < 0 || flow_threads_ > 256 || flow_threads_ % 32)
         throw ConfigError("LBMGPU_FUSED_FLOW must be 0 or a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
@@ -469,6 +470,7 @@ class DirectEngine final : public Engine {
 
   ~DirectEngine() override {
     if (stream_) cudaStreamSynchronize(stream_);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
     if (peer_err_) cudaFreeHost(peer_err_);
     tr_.reset();
@@ -736,6 +738,10 @@ class DirectEngine final : public Engine {
 
   void advance(const TrtArgs& t, long steps) override {
     if (peer_) peer_check();
+    if (graph_mode_ && !graph_capturing_ && nparts_ == 1 && !use_fused(steps) && steps > 0) {
+      advance_graph(t, steps);
+      return;
+    }
     const bool soa = desc_.soa;
     const bool cs = cs_;
     if (advance_fused(t, steps)) return;
@@ -827,6 +833,58 @@ class DirectEngine final : public Engine {
         peer_ ? aa_pair_peer(t) : aa_pair_slabs(t);
       }
     }
+  }
+
+  // Per-sweep launches of one advance(T) captured once as a CUDA graph and
+  // replayed (LBMGPU_GRAPH=1; single part, lattices above the fused
+  // threshold).  Re-captured when T, the grid parity or the parameters
+  // change; the kernel-stats row is the whole graph (T sweeps).
+  void advance_graph(const TrtArgs& t, long steps) {
+    const bool same = graph_exec_ && graph_steps_ == steps && graph_cur0_ == cur_ &&
+                      std::memcmp(&graph_trt_, &t, sizeof t) == 0;
+    if (!same) {
+      if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+      const int cur0 = cur_;
+      const bool on = stats_.enabled();
+      const long n0 = stats_.launches();
+      stats_.enable(false);
+      graph_capturing_ = true;
+      cudaGraph_t g = nullptr;
+      LBM_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      try {
+        advance(t, steps);
+      } catch (...) {
+        cudaStreamEndCapture(stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        graph_capturing_ = false;
+        stats_.enable(on);
+        cur_ = cur0;
+        throw;
+      }
+      LBM_CUDA(cudaStreamEndCapture(stream_, &g));
+      graph_capturing_ = false;
+      stats_.enable(on);
+      graph_launches_ = stats_.launches() - n0;
+      stats_.add_launches(-graph_launches_);
+      const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+      cudaGraphDestroy(g);
+      LBM_CUDA(e);
+      graph_cur1_ = cur_;
+      cur_ = cur0;
+      graph_steps_ = steps;
+      graph_cur0_ = cur0;
+      graph_trt_ = t;
+    }
+    const std::string name = std::string("full_") +
+                             (desc_.prop == Prop::Aa ? "aa" : desc_.prop == Prop::OsPush ? "push"
+                                                                                         : "pull") +
+                             (desc_.soa ? "_soa_graph" : "_aos_graph");
+    const int tok = stats_.begin(name.c_str(), stream_, steps);
+    LBM_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    stats_.end(tok, stream_);
+    stats_.add_launches(graph_launches_ - 1);  // begin() counted one
+    cur_ = graph_cur1_;
   }
 
   // One-step sweeps over z-slabs (halo.hpp phases 2 / 3), per lattice step:
@@ -1404,6 +1462,12 @@ class DirectEngine final : public Engine {
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;
+  // CUDA graph of one advance(T) (advance_graph)
+  bool graph_mode_ = false, graph_capturing_ = false;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  long graph_steps_ = 0, graph_launches_ = 0;
+  int graph_cur0_ = 0, graph_cur1_ = 0;
+  TrtArgs graph_trt_{};
   bool ring_ = false;                   // the halo plan includes the z ring
   bool peer_ = false, peer_ready_ = false;
   unsigned long long epoch_ = 0;        // AA pairs run with the peer transport

@@ -166,6 +166,7 @@ class KernelStats {
   const std::vector<Row>& rows() { collect(); return rows_; }
   long launches() const { return launches_; }
   void count_launch() { ++launches_; }
+  void add_launches(long n) { launches_ += n; }
   ~KernelStats();
 
  private:
@@ -184,7 +185,7 @@ struct DistSpec {
   int rank = 0, nranks = 1, device = -1, virtual_parts = 1;
   std::array<uint8_t, 128> nccl_id{};
   bool have_id = false;
-  int transport = 0;  // 0: halo copies (NCCL / device), 1: peer memory (AA z slabs)
+  int transport = 0;  // 0: halo copies (NCCL / device), 1: peer memory (direct z slabs)
 };
 
 // One GPU-resident sweep implementation of the reference's Kernel

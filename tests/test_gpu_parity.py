@@ -503,6 +503,32 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
+@pytest.mark.parametrize("name", ["aa-soa", "aa-aos", "aa-vec-soa", "blk-push-soa", "blk-push-aos",
+                                  "blk-pull-soa", "blk-pull-aos"])
+@pytest.mark.parametrize("kind,dims", [("channel", (32, 12, 16)), ("blocks", (16, 16, 16))])
+def test_cuda_graph_advance_bitwise(name, kind, dims, monkeypatch):
+    """LBMGPU_GRAPH=1: the per-sweep launches of advance(T) are captured once
+    as a CUDA graph and replayed (re-captured when T or the grid parity
+    changes).  Bitwise equal to the plain launches, over advance() calls
+    with changing T; the launch count still counts every captured kernel."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    steps = (4, 4, 2, 4) if name.startswith("aa") else (3, 3, 2, 3)
+    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    ref.load_perturbed(55)
+    for st in steps:
+        ref.advance(PARAMS, FORCE, st)
+    monkeypatch.setenv("LBMGPU_GRAPH", "1")
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    k.load_perturbed(55)
+    k.kernel_stats_enable(True)
+    for st in steps:
+        k.advance(PARAMS, FORCE, st)
+    assert k.fingerprint() == ref.fingerprint(), name
+    assert any(n.endswith("_graph") for n in k.kernel_stats())
+    assert k.launch_count() >= sum(steps)
+
+
 @pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims,parts", [
     ("channel", (16, 12, 24), 2), ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2),
