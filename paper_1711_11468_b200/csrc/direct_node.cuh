@@ -110,10 +110,28 @@ template <bool SOA, bool COLLIDE, bool CS, bool CG>
 __device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, uint32_t n) {
   const Idx<SOA> I{a.P, a.nx, a.ny};
   double q[kQ];
-  q[0] = ldp<CG>(a.src + I(c.Z[1], dslot(0), c.y, c.x));
+  // Warp-uniform fast path (cf. aa_odd_node): no active lane wraps in x, y
+  // or (single part) z, so the gather of direction d -- slot d of x - c_d --
+  // is the own slot-0 element + odd_off[d] moved from slot opp(d) to slot d.
+  // (The same form for the push's stores measured slower: cfg-5 box
+  // 21.4k -> 20.2k MFLUP/s.)
+  // (Not in the fused L2-resident launch (CG): there it costs registers
+  // and measured 2 % slower on cfg 1.)
+  constexpr bool kFast = SOA && !CG;
+  const bool inner = kFast && c.x - 1u < a.nx - 2u && c.y - 1u < a.ny - 2u &&
+                     (!a.zwrap || c.z - 1u < a.nzl - 2u);
+  if (kFast && __all_sync(__activemask(), inner)) {
+    const double* own = a.src + I(c.Z[1], 0, c.y, c.x);
+    const long long P = a.P;
 #pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    q[d] = ldp<CG>(a.src + I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)]));
+    for (int d = 0; d < kQ; ++d)
+      q[d] = ldp<CG>(own + a.odd_off[d] + static_cast<long long>(dslot(d) - dslot(opp(d))) * P);
+  } else {
+    q[0] = ldp<CG>(a.src + I(c.Z[1], dslot(0), c.y, c.x));
+#pragma unroll
+    for (int d = 1; d < kQ; ++d)
+      q[d] = ldp<CG>(a.src + I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)]));
+  }
   const bool solid = solid_node(a, c.x, c.y, c.z, n);
   if (COLLIDE && !solid) collide(q, a.trt);
   st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
