@@ -35,6 +35,7 @@
 #include "direct_fused.cuh"
 #include "direct_experimental.cuh"
 #include "direct_peer.cuh"
+#include "direct_tb.cuh"
 
 namespace lbmgpu {
 
@@ -351,6 +352,12 @@ class DirectEngine final : public Engine {
       if (const char* e = std::getenv("LBMGPU_GRID_SYNC")) barrier_mode_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_PUSH_TMASK")) use_tmask_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_GRAPH")) graph_mode_ = std::atoi(e) != 0;
+      if (const char* e = std::getenv("LBMGPU_AA_TB")) {  // "W,G"
+        tb_w_ = std::atoi(e);
+        const char* comma = std::strchr(e, ',');
+        tb_g_ = comma ? std::atoi(comma + 1) : 4;
+        if (tb_w_ < 0 || tb_g_ < 1) throw ConfigError("LBMGPU_AA_TB must be W,G with W >= 0, G >= 1");
+      }
       if (flow_threads_ < 0 || flow_threads_ > 256 || flow_threads_ % 32)
         throw ConfigError("LBMGPU_FUSED_FLOW must be 0 or a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
@@ -801,6 +808,10 @@ class DirectEngine final : public Engine {
       return;
     }
     // AA pattern: even/odd pairs, in place
+    if (tb_w_ > 0 && soa && nparts_ == 1 && tb_ok()) {
+      advance_tb(t, steps);
+      return;
+    }
     for (long s = 0; s < steps; s += 2) {
       if (nparts_ == 1) {
         const Part& pt = parts_[0];
@@ -833,6 +844,31 @@ class DirectEngine final : public Engine {
         peer_ ? aa_pair_peer(t) : aa_pair_slabs(t);
       }
     }
+  }
+
+  // Temporal blocking (direct_tb.cuh): geometries without y / z wrap
+  // traffic only (channel, pipe: extreme rows and planes solid).
+  bool tb_ok() const { return geom_.kind == 0 || geom_.kind == 2; }
+
+  void advance_tb(const TrtArgs& t, long steps) {
+    const Part& pt = parts_[0];
+    DirectArgs a = args(pt, 0, pt.nzl * static_cast<uint32_t>(P_), t, 0, 0);
+    auto kern = k_full_aa_tb<256, 2>;
+    int per_sm = 0;
+    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const int grid = std::max(per_sm, 1) * sm_count_;
+    GridBarrier bar{barrier_.get(), barrier_.get() + 1, barrier_mode_};
+    uint32_t W = static_cast<uint32_t>(std::min<int>(tb_w_, ny_)), G = static_cast<uint32_t>(tb_g_);
+    const uint32_t nb = (static_cast<uint32_t>(ny_) + W - 1) / W;
+    const uint32_t last_e = ny_ - (nb - 1) * W;
+    TbDivs dv{FastDiv(W), FastDiv(W > 1 ? W - 1 : 1), FastDiv(last_e),
+              FastDiv(nb == 1 ? ny_ : last_e + 1)};
+    long pairs = steps / 2;
+    void* params[] = {&a, &W, &G, &pairs, &dv, &bar};
+    const int tok = stats_.begin("full_aa_soa_tb", stream_, steps);
+    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, params, 0,
+                                         stream_));
+    stats_.end(tok, stream_);
   }
 
   // Per-sweep launches of one advance(T) captured once as a CUDA graph and
@@ -1462,6 +1498,7 @@ class DirectEngine final : public Engine {
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;
+  int tb_w_ = 0, tb_g_ = 4;  // temporal blocking band rows / plane group (0: off)
   // CUDA graph of one advance(T) (advance_graph)
   bool graph_mode_ = false, graph_capturing_ = false;
   cudaGraphExec_t graph_exec_ = nullptr;

@@ -503,6 +503,29 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
+@pytest.mark.parametrize("tb", ["4,2", "7,3", "64,8", "1,1", "5,1"])
+@pytest.mark.parametrize("kind,dims", [("channel", (32, 20, 24)), ("pipe", (16, 14, 13)),
+                                       ("channel", (9, 7, 30))])
+def test_aa_temporal_blocking_bitwise(tb, kind, dims, monkeypatch):
+    """LBMGPU_AA_TB=W,G (direct_tb.cuh): one AA pair per pass over skewed
+    y-bands of W rows with a z-wavefront of G-plane groups, one cooperative
+    launch.  Bitwise equal to the even/odd sweeps for channel and pipe
+    (no y / z wrap traffic), bands narrower and wider than the box."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    ref.load_perturbed(88)
+    ref.advance(PARAMS, FORCE, 6)
+    monkeypatch.setenv("LBMGPU_AA_TB", tb)
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
+    k.load_perturbed(88)
+    k.kernel_stats_enable(True)
+    k.advance(PARAMS, FORCE, 4)
+    k.advance(PARAMS, FORCE, 2)
+    assert "full_aa_soa_tb" in k.kernel_stats()
+    assert k.fingerprint() == ref.fingerprint()
+
+
 @pytest.mark.parametrize("name", ["aa-soa", "aa-aos", "aa-vec-soa", "blk-push-soa", "blk-push-aos",
                                   "blk-pull-soa", "blk-pull-aos"])
 @pytest.mark.parametrize("kind,dims", [("channel", (32, 12, 16)), ("blocks", (16, 16, 16))])
