@@ -96,7 +96,9 @@ typedef struct {
  * sweeps (AA odd, pull, push) load / store the neighbour slab in peer memory
  * (CUDA IPC over NVLink between processes: lbmgpu_peer_export / _attach
  * before the first advance; device pointers with virtual_parts), with
- * per-sub-step epoch flags in peer memory as the only synchronisation. */
+ * per-sub-step epoch flags in peer memory as the only synchronisation.
+ * With transport = 1 the nccl_id is optional; without it total_mass over
+ * several processes is a ConfigError (NCCL does the mass reduction). */
 typedef struct {
   int rank, nranks;
   int device;        /* CUDA ordinal; -1 = current */
@@ -264,6 +266,11 @@ int lbmgpu_load_state_local(lbmgpu_ctx* ctx, const double* host,
 int lbmgpu_peer_export(lbmgpu_ctx* ctx, void* out, size_t cap, size_t* len);
 int lbmgpu_peer_attach(lbmgpu_ctx* ctx, const void* records, size_t record_len,
                        int nranks);
+/* Peer-transport plumbing check (no sweep): one boundary plane, 19 x nx*ny
+ * doubles in device layout ([slot][y][x]) -- which = 0 lower neighbour's top
+ * plane, 1 upper neighbour's bottom plane (read through the peer mapping),
+ * 2 own bottom plane, 3 own top plane. */
+int lbmgpu_peer_probe(lbmgpu_ctx* ctx, int which, double* out, uint64_t count);
 /* This process's slab(s): part index < number of local parts. */
 int lbmgpu_part_info(lbmgpu_ctx* ctx, int part, int* z0, int* z1,
                      uint64_t* n_fluid_part);

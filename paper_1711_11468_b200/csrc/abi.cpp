@@ -833,6 +833,19 @@ int lbmgpu_peer_attach(lbmgpu_ctx* c, const void* recs, size_t rec_len, int nran
   });
 }
 
+int lbmgpu_peer_probe(lbmgpu_ctx* c, int which, double* out, uint64_t count) {
+  return guard([&] {
+    need(c, "ctx");
+    need(out, "out");
+    std::vector<double> v;
+    c->eng->peer_probe(which, v);
+    if (count != v.size())
+      throw ConfigError("peer probe: buffer holds " + std::to_string(count) + " values, plane has " +
+                        std::to_string(v.size()));
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+  });
+}
+
 int lbmgpu_part_info(lbmgpu_ctx* c, int part, int* z0, int* z1, uint64_t* nf) {
   return guard([&] {
     need(c, "ctx");

@@ -327,7 +327,7 @@ class DirectEngine final : public Engine {
       throw ConfigError("dist: transport must be 0 (halo copies) or 1 (peer memory)");
     if (dist.transport == 1 && nparts_ < 2)
       throw ConfigError("peer transport: needs a z-slab decomposition (>= 2 slabs)");
-    if (nranks_ > 1 && !dist.have_id)
+    if (nranks_ > 1 && !dist.have_id && dist.transport != 1)
       throw ConfigError("dist: nranks > 1 needs the NCCL unique id");
     {
       int dev = 0;
@@ -464,10 +464,12 @@ class DirectEngine final : public Engine {
       // NCCL between processes; with one process the copies are local, and
       // an NCCL id selects NCCL self send/recv instead (tests the NCCL path on
       // one GPU).
-      if (nranks_ > 1 || dist.have_id)
+      // (the peer transport between processes needs NCCL only for the
+      // total-mass reduction; without an id there is no Transport at all)
+      if (dist.have_id)
         tr_ = std::make_unique<NcclTransport>(std::move(plan), rank_, nranks_,
                                               nparts_, dist.nccl_id.data());
-      else
+      else if (nranks_ == 1)
         tr_ = std::make_unique<LocalTransport>(std::move(plan));
       ring_ = end_fluid || d.prop != Prop::Aa;  // one-step plans always carry the ring
       if (dist.transport == 1) setup_peer();
@@ -1175,6 +1177,26 @@ class DirectEngine final : public Engine {
     peer_ready_ = true;
   }
 
+  // Copy of a boundary plane (19 slots x P, device layout) for the IPC
+  // plumbing test: which = 0 lower neighbour's top plane, 1 upper
+  // neighbour's bottom plane (both through the peer mapping), 2 own bottom
+  // plane, 3 own top plane (first local part).
+  void peer_probe(int which, std::vector<double>& out) override {
+    if (!peer_ready_) throw ConfigError("peer transport: not attached");
+    const Part& pt = parts_[0];
+    const PeerLink& L = links_[0];
+    const uint64_t plane = uint64_t(kQ) * P_;
+    const double* src = nullptr;
+    if (which == 0 && L.lo[0]) src = L.lo[0] + L.lo_plane * plane;
+    if (which == 1 && L.hi[0]) src = L.hi[0] + L.hi_plane * plane;
+    if (which == 2) src = pt.buf[0].get() + uint64_t(pt.zoff) * plane;
+    if (which == 3) src = pt.buf[0].get() + uint64_t(pt.zoff + pt.nzl - 1) * plane;
+    if (!src) throw ConfigError("peer transport: no such plane");
+    out.resize(plane);
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    LBM_CUDA(cudaMemcpy(out.data(), src, plane * sizeof(double), cudaMemcpyDefault));
+  }
+
   void peer_check() const {
     if (!peer_ready_)
       throw ConfigError("peer transport: lbmgpu_peer_attach has not been called");
@@ -1453,6 +1475,8 @@ class DirectEngine final : public Engine {
       m += device_sum(pt.buf[cur_].get() + uint64_t(pt.zoff) * per_plane,
                       uint64_t(pt.nzl) * per_plane, stream_);
     }
+    if (nranks_ > 1 && !tr_)
+      throw ConfigError("total_mass over several processes needs the NCCL id (mass reduction)");
     return tr_ && nranks_ > 1 ? tr_->sum(m) : m;
   }
 

@@ -234,6 +234,10 @@ class Engine {
     (void)recs; (void)rec_len; (void)nranks;
     throw ConfigError("peer transport: not enabled for this lattice");
   }
+  virtual void peer_probe(int which, std::vector<double>& out) {
+    (void)which; (void)out;
+    throw ConfigError("peer transport: not enabled for this lattice");
+  }
   virtual int parts() const { return 1; }
   virtual void part_info(int p, int* z0, int* z1, uint64_t* nf) const {
     (void)p; *z0 = 0; *z1 = 0; *nf = n_fluid_;

@@ -105,6 +105,7 @@ def _load():
     L.lbmgpu_guard_selftest.argtypes = [P(i)]
     L.lbmgpu_peer_export.argtypes = [vp, vp, C.c_size_t, P(C.c_size_t)]
     L.lbmgpu_peer_attach.argtypes = [vp, vp, C.c_size_t, i]
+    L.lbmgpu_peer_probe.argtypes = [vp, i, vp, u64]
     return L
 
 
@@ -604,6 +605,14 @@ class Kernel:
         blob = b"".join(records)
         _check(lib.lbmgpu_peer_attach(self._h, blob, len(records[0]) if records else 0,
                                       len(records)))
+
+    def peer_probe(self, which: int, plane_values: int) -> np.ndarray:
+        """Boundary plane in device layout (19 x nx*ny): 0 lower neighbour's
+        top plane, 1 upper neighbour's bottom plane (through the peer
+        mapping), 2 own bottom plane, 3 own top plane."""
+        out = np.empty(plane_values, np.float64)
+        _check(lib.lbmgpu_peer_probe(self._h, which, out.ctypes.data, out.size))
+        return out
 
     def part_info(self, part: int):
         z0, z1, nf = C.c_int(), C.c_int(), C.c_uint64()

@@ -1,0 +1,96 @@
+"""CUDA IPC plumbing of the peer-memory transport on ONE GPU: two processes
+(ranks of a 2-slab aa-soa lattice) export their records, all-gather them
+over gloo and attach -- then each reads its neighbour's boundary plane
+through the mapping (lbmgpu_peer_probe) and compares it with the plane the
+neighbour reads from its own memory.  No sweep runs, so no kernel ever waits
+on the other process (B200_PROFILING.md: ranks whose kernels wait on one
+another must not share a GPU); the sweeps themselves are covered by the
+emulated-slab tests (test_gpu_parity.py) and the CPU protocol tests
+(test_halo_gloo.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, name, kind, dims, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1711_11468_b200 as lbm
+        k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims),
+                            dist={"rank": rank, "nranks": world, "device": 0,
+                                  "transport": "peer"})
+        k.load_perturbed(4242)
+        plane = 19 * dims[0] * dims[1]
+        try:
+            k.total_mass()
+            mass_raised = False
+        except lbm.ConfigError:
+            mass_raised = True  # no NCCL id: no cross-process mass reduction
+        recs = [None] * world
+        dist.all_gather_object(recs, k.peer_export())
+        k.peer_attach(recs)
+        own = {2: k.peer_probe(2, plane), 3: k.peer_probe(3, plane)}
+        seen = {}
+        for which in (0, 1):
+            try:
+                seen[which] = k.peer_probe(which, plane)
+            except lbm.ConfigError:
+                pass
+        allp = [None] * world
+        dist.all_gather_object(allp, (own, seen))
+        ok = True
+        for r, (o, sn) in enumerate(allp):
+            lo, hi = r - 1, r + 1
+            if 1 in sn:  # upper neighbour's bottom plane == its own view
+                ok &= bool(np.array_equal(sn[1], allp[hi % world][0][2]))
+            if 0 in sn:
+                ok &= bool(np.array_equal(sn[0], allp[lo % world][0][3]))
+            rg = ring(kind) or name != "aa-soa"  # one-step plans always carry the ring
+            ok &= (1 in sn) == (hi < world or rg) and (0 in sn) == (lo >= 0 or rg)
+        q.put((rank, bool(ok), mass_raised))
+        del k
+    finally:
+        dist.destroy_process_group()
+
+
+def ring(kind):
+    return kind == "blocks"  # fluid on z = 0 / nz - 1: the z ring is exchanged
+
+
+@pytest.mark.parametrize("name,kind,dims", [("aa-soa", "channel", (16, 12, 24)),
+                                            ("aa-soa", "blocks", (16, 16, 16)),
+                                            ("blk-push-soa", "channel", (16, 12, 24))])
+def test_peer_ipc_export_attach_two_processes(name, kind, dims):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, name, kind, dims, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(ok for _, ok, _ in res), res
+    assert all(raised for _, _, raised in res)
