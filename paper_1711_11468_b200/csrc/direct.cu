@@ -672,7 +672,7 @@ class DirectEngine final : public Engine {
                        long sweeps) {
     auto kern = k_full_fused<SOA, KIND, TPB, MINB>;
     int per_sm = 0;
-    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, 0));
+    per_sm = occupancy_blocks(reinterpret_cast<const void*>(kern), TPB);
     const uint64_t want = ceil_div(a.count, TPB);
     const int grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(per_sm, 1)) * sm_count_)));
@@ -699,7 +699,7 @@ class DirectEngine final : public Engine {
     const int threads =
         flow_threads_ == 160 || flow_threads_ == 128 || flow_threads_ == 64 ? flow_threads_ : 256;
     int per_sm = 0;
-    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+    per_sm = occupancy_blocks(reinterpret_cast<const void*>(kern), threads);
     const uint64_t tasks = uint64_t(parts_[0].nzl) * ceil_div(P_, threads);
     const int grid = static_cast<int>(std::max<uint64_t>(
         1, std::min<uint64_t>(tasks, uint64_t(std::max(per_sm, 1)) * sm_count_)));
@@ -857,7 +857,7 @@ class DirectEngine final : public Engine {
     DirectArgs a = args(pt, 0, pt.nzl * static_cast<uint32_t>(P_), t, 0, 0);
     auto kern = k_full_aa_tb<256, 2>;
     int per_sm = 0;
-    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    per_sm = occupancy_blocks(reinterpret_cast<const void*>(kern), 256);
     const int grid = std::max(per_sm, 1) * sm_count_;
     GridBarrier bar{barrier_.get(), barrier_.get() + 1, barrier_mode_};
     uint32_t W = static_cast<uint32_t>(std::min<int>(tb_w_, ny_)), G = static_cast<uint32_t>(tb_g_);

@@ -1,5 +1,7 @@
 // Device-resident geometry (reference src/geometry.cpp:40-117), fluid scans,
 // compensated reductions and per-kernel event statistics.
+#include <map>
+#include <mutex>
 #include <cub/cub.cuh>
 
 #include "lbm.hpp"
@@ -192,6 +194,18 @@ cudaEvent_t KernelStats::get_event() {
   cudaEvent_t e;
   LBM_CUDA(cudaEventCreate(&e));
   return e;
+}
+
+int occupancy_blocks(const void* kern, int threads) {
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lk(m);
+  auto it = cache.find({kern, threads});
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+  cache[{kern, threads}] = per_sm;
+  return per_sm;
 }
 
 int KernelStats::begin(const char* name, cudaStream_t s, long sweeps) {

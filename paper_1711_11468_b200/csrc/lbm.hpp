@@ -179,6 +179,10 @@ class KernelStats {
   cudaEvent_t get_event();
 };
 
+// Resident blocks per SM of a kernel at a block size (no dynamic shared
+// memory), cached: the fused launches query it on every advance().
+int occupancy_blocks(const void* kern, int threads);
+
 // ------------------------------------------------------------- engines
 // Distribution request (see lbmgpu_dist in include/lbmgpu.h).
 struct DistSpec {

@@ -502,7 +502,7 @@ class ListEngine final : public Engine {
     constexpr int TPB = 256, MINB = 2;
     auto kern = k_list_fused<SOA, KIND, TPB, MINB>;
     int per_sm = 0;
-    LBM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, 0));
+    per_sm = occupancy_blocks(reinterpret_cast<const void*>(kern), TPB);
     const int grid = static_cast<int>(std::max<uint64_t>(
         1, std::min<uint64_t>(ceil_div(a.N, TPB), uint64_t(std::max(per_sm, 1)) * sm_count_)));
     void* params[] = {&a, &other, &sweeps};

@@ -47,6 +47,9 @@ for case in range(cases):
         if not name.startswith("list") and rng.random() < 0.5:
             dist["transport"] = "peer"  # boundary odd sweeps in the neighbour slab, epoch flags
     os.environ["LBMGPU_RIA_MODE"] = str(rng.choice(["-1", "0", "1", "2"]))  # ria / pv names
+    # temporal blocking of the AA pair (channel / pipe, per-sweep path only)
+    os.environ["LBMGPU_AA_TB"] = (f"{int(rng.integers(1, 12))},{int(rng.integers(1, 5))}"
+                                  if rng.random() < 0.3 else "0,1")
     init = port.perturbed(nf, seed0 + case)
     fam = "half" if name.startswith("list-") else "full"
     params = lbm.TrtParams.from_tau(tau)
@@ -65,6 +68,7 @@ for case in range(cases):
     if not ok:
         bad += 1
         print("MISMATCH", case, name, kind, (nx, ny, nz), block, spacing, blk, tau, steps,
-              os.environ["LBMGPU_FUSED_MB"], os.environ["LBMGPU_RIA_MODE"], dist, flush=True)
+              os.environ["LBMGPU_FUSED_MB"], os.environ["LBMGPU_RIA_MODE"],
+              os.environ["LBMGPU_AA_TB"], dist, flush=True)
 print(f"{cases} cases, {bad} mismatches", flush=True)
 sys.exit(1 if bad else 0)
