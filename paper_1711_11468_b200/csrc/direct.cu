@@ -479,6 +479,12 @@ class DirectEngine final : public Engine {
 
   ~DirectEngine() override {
     if (stream_) cudaStreamSynchronize(stream_);
+    if (bstream_) {
+      cudaStreamSynchronize(bstream_);
+      cudaStreamDestroy(bstream_);
+    }
+    for (cudaEvent_t e : pev_)
+      if (e) cudaEventDestroy(e);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
     if (peer_err_) cudaFreeHost(peer_err_);
@@ -1227,9 +1233,39 @@ class DirectEngine final : public Engine {
     }
   }
 
+  // Boundary work of the peer AA path runs on its own high-priority stream
+  // beside the interior sweeps (helpers launch on stream_, so it is swapped
+  // for the scope).
+  struct StreamSwap {
+    cudaStream_t& x;
+    cudaStream_t& y;
+    StreamSwap(cudaStream_t& a, cudaStream_t& b) : x(a), y(b) { std::swap(x, y); }
+    ~StreamSwap() { std::swap(x, y); }
+  };
+
+  void ensure_bstream() {
+    if (bstream_) return;
+    int least = 0, greatest = 0;
+    LBM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    LBM_CUDA(cudaStreamCreateWithPriority(&bstream_, cudaStreamNonBlocking, greatest));
+    for (cudaEvent_t& e : pev_) LBM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+
+  // One AA pair, epoch e; boundary stream B, interior stream I:
+  //   B: [I's previous work] even(b) signal(even)                wait(ev_ie) wait(even) odd(b) signal(odd) wait(odd)
+  //   I:                     even(i) --ev_ie-->     [ev_be] odd(i) [ev_bo]
+  // even(b) and even(i) touch disjoint own slots, and so do odd(b) and
+  // odd(i) (the bottom plane's odd step uses plane 1's up-slots, plane 1's
+  // uses plane 0's down-slots): each sub-step's boundary work -- with the
+  // neighbour traffic and the flag waits -- overlaps the interior sweep.
+  // odd(b) follows even(i) (it reads planes 1 / nzl-2), odd(i) follows
+  // even(b); the next pair's even(b) follows odd(i) and the neighbours'
+  // odd(b) (wait(odd)), its even(i) follows odd(b) (ev_bo).
   void aa_pair_peer(const TrtArgs& t) {
     const uint32_t P = static_cast<uint32_t>(P_);
     const unsigned long long e = ++epoch_;
+    ensure_bstream();
+    cudaEvent_t ev_prev = pev_[0], ev_be = pev_[1], ev_ie = pev_[2], ev_bo = pev_[3];
     auto sweep = [&](bool odd, bool boundary) {
       for (size_t i = 0; i < parts_.size(); ++i) {
         Part& pt = parts_[i];
@@ -1258,14 +1294,28 @@ class DirectEngine final : public Engine {
         }
       }
     };
-    sweep(false, true);
-    peer_signal(0, e);
+    LBM_CUDA(cudaEventRecord(ev_prev, stream_));
+    {
+      StreamSwap on_b(stream_, bstream_);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, ev_prev, 0));
+      sweep(false, true);
+      peer_signal(0, e);
+      LBM_CUDA(cudaEventRecord(ev_be, stream_));
+    }
     sweep(false, false);
-    peer_wait(0, e);
-    sweep(true, true);
-    peer_signal(1, e);
+    LBM_CUDA(cudaEventRecord(ev_ie, stream_));
+    {
+      StreamSwap on_b(stream_, bstream_);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, ev_ie, 0));
+      peer_wait(0, e);
+      sweep(true, true);
+      peer_signal(1, e);
+      peer_wait(1, e);
+      LBM_CUDA(cudaEventRecord(ev_bo, stream_));
+    }
+    LBM_CUDA(cudaStreamWaitEvent(stream_, ev_be, 0));
     sweep(true, false);
-    peer_wait(1, e);
+    LBM_CUDA(cudaStreamWaitEvent(stream_, ev_bo, 0));
   }
 
   // One-step sweeps with the peer transport.  Every op (the pull's collide
@@ -1537,6 +1587,8 @@ class DirectEngine final : public Engine {
   int* peer_err_ = nullptr;             // host-mapped wait-timeout flag
   int* peer_err_dev_ = nullptr;
   std::vector<void*> ipc_open_;         // CUDA IPC mappings to close
+  cudaStream_t bstream_ = nullptr;      // peer AA path: boundary stream (aa_pair_peer)
+  cudaEvent_t pev_[4] = {nullptr, nullptr, nullptr, nullptr};
   GeomSpec geom_;  // kind/parameters for the analytic solid test (custom: flags)
 };
 
