@@ -1342,12 +1342,22 @@ class DirectEngine final : public Engine {
         }
       }
     };
+    // boundary part on the boundary stream beside the interior part (the two
+    // write disjoint slots and only read the source grid); each op joins both
+    ensure_bstream();
     auto op = [&](auto&& boundary_fn, auto&& interior_fn) {
       const unsigned long long e = ++epoch_;
-      peer_wait(0, e - 1);
-      each(true, boundary_fn);
-      peer_signal(0, e);
+      LBM_CUDA(cudaEventRecord(pev_[0], stream_));
+      {
+        StreamSwap on_b(stream_, bstream_);
+        LBM_CUDA(cudaStreamWaitEvent(stream_, pev_[0], 0));
+        peer_wait(0, e - 1);
+        each(true, boundary_fn);
+        peer_signal(0, e);
+        LBM_CUDA(cudaEventRecord(pev_[1], stream_));
+      }
       each(false, interior_fn);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, pev_[1], 0));
     };
     if (!push) {
       auto coll = [&](size_t, Part& pt, uint32_t n0, uint32_t cnt) {
