@@ -220,10 +220,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
-    ap.add_argument("--transport", default="copy", choices=["copy", "peer"],
-                    help="z-slab halo transport: copy = NCCL send/recv (device copies "
-                         "with --virtual-parts), peer = boundary sweeps load/store the "
-                         "neighbour slab in peer memory (CUDA IPC), epoch flags")
+    ap.add_argument("--transport", default="auto", choices=["auto", "copy", "peer"],
+                    help="z-slab halo transport: peer = boundary sweeps load/store the "
+                         "neighbour slab in peer memory (CUDA IPC), epoch flags, boundary "
+                         "work on its own stream; copy = NCCL send/recv (device copies with "
+                         "--virtual-parts); auto = peer for the direct SoA z slabs, copy for "
+                         "the list node ranges")
     ap.add_argument("--decompose", action="store_true",
                     help="at N>1: z-slab decomposition of direct push/pull and node-range "
                          "decomposition of list AA instead of replicas")
@@ -279,10 +281,13 @@ def main():
     decomposable = (aa and desc.addr == "direct") or (
         args.decompose and not desc.ria and (desc.addr == "direct" or aa))
     replicas = world > 1 and not decomposable
+    if args.transport == "auto":
+        args.transport = "peer" if desc.addr == "direct" else "copy"
     if world == 1 and args.virtual_parts > 1:
         dspec = {"virtual_parts": args.virtual_parts, "transport": args.transport}
         if args.nccl_self:
             dspec["nccl_id"] = lbm.nccl_unique_id()
+            dspec["transport"] = "copy"  # NCCL self send/recv halos
     if world > 1 and not replicas:
         obj = [lbm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -396,9 +401,9 @@ def main():
         line["config"]["parallelism"] = f"node-range (x-slab) decomposition x{world}, NCCL index-list halos"
     if world == 1 and args.virtual_parts > 1:
         line["config"]["parallelism"] = (f"EMULATED {args.virtual_parts}-part decomposition on 1 GPU "
-                                         + ("(peer-memory boundary sweeps, epoch flags"
+                                         + ("(NCCL self send/recv halos" if args.nccl_self
+                                            else "(peer-memory boundary sweeps, epoch flags"
                                             if args.transport == "peer"
-                                            else "(NCCL self send/recv halos" if args.nccl_self
                                             else "(device-copy halos")
                                          + "; overhead probe)")
     line.update({
