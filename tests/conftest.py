@@ -13,6 +13,16 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running full-size check")
 
 
+def pytest_collection_modifyitems(config, items):
+    # full-size extras (~50 s each) run only with LBMGPU_SLOW=1
+    if os.environ.get("LBMGPU_SLOW") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow full-size check (LBMGPU_SLOW=1 runs it)")
+    for item in items:
+        if "slow" in item.keywords:
+            item.add_marker(skip)
+
+
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 

@@ -708,6 +708,44 @@ def test_baseline_config_fingerprint(cid):
     assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
 
 
+@pytest.mark.parametrize("cid,variant", [("2", "ria"), ("4", "ria"), ("5", "peer8"),
+                                         pytest.param("5", "copy4", marks=pytest.mark.slow),
+                                         pytest.param("5", "tb", marks=pytest.mark.slow)])
+def test_baseline_config_fingerprint_alternative_paths(cid, variant, monkeypatch):
+    """The BASELINE golden fingerprints at full size through the other paths:
+    list-aa-ria-soa (cfg 2: 8-bit pattern ids, cfg 4: 32-bit ids), cfg 5 as
+    8 emulated z slabs over the peer transport (boundary stream, flags) and
+    as 4 slabs over device-copy halos, and cfg 5 through the AA temporal
+    blocking prototype (the last two marked slow: ~50 s each; all five
+    passed on the B200, profiles/r01h_fullsize_alt_paths.log)."""
+    if not os.path.exists(CONFIGS):
+        pytest.skip("configs.json not generated")
+    gold = json.load(open(CONFIGS))
+    if cid not in gold:
+        pytest.skip(f"config {cid} golden not generated")
+    c = gold[cid]
+    spec = lbm.GeometrySpec(c["kind"], *c["dims"], c.get("block", 4), c.get("spacing", 4),
+                            c.get("pipe_diameter", 0))
+    name, dist = c["kernel"], None
+    if variant == "ria":
+        name = "list-aa-ria-soa"
+    elif variant == "peer8":
+        dist = {"virtual_parts": 8, "transport": "peer"}
+    elif variant == "copy4":
+        dist = {"virtual_parts": 4}
+    elif variant == "tb":
+        monkeypatch.setenv("LBMGPU_AA_TB", "32,1")
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec, dist=dist)
+    k.kernel_stats_enable(True)
+    k.advance(lbm.TrtParams(1.0, 3.0 / 16.0), lbm.BodyForce(tuple(c["g"])), c["steps"])
+    assert f"{k.fingerprint():016x}" == c["fingerprint"], (cid, variant)
+    assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
+    names = set(k.kernel_stats())
+    expect = {"ria": "list_aa_odd_ria_pid", "peer8": "full_aa_odd_soa_peer",
+              "copy4": "full_aa_odd_soa_halo", "tb": "full_aa_soa_tb"}[variant]
+    assert any(n.startswith(expect) for n in names), names
+
+
 def test_custom_flagfield_path(port):
     """make_kernel takes any FlagField (kernels.hpp:102-105): a host flag
     field uploaded through LBMGPU_CUSTOM gives the same results as the device
