@@ -27,9 +27,11 @@ def _free_port():
     return p
 
 
-def _rank(rank, world, port, name, kind, dims, q):
+def _rank(rank, world, port, name, kind, dims, q, guard=False):
     import sys
     sys.path.insert(0, ROOT)
+    if guard:  # guard-zone allocator: lattice pointers sit 4 KiB into their allocation
+        os.environ["LBMGPU_GUARD"] = "1"
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -76,15 +78,16 @@ def ring(kind):
     return kind == "blocks"  # fluid on z = 0 / nz - 1: the z ring is exchanged
 
 
-@pytest.mark.parametrize("name,kind,dims", [("aa-soa", "channel", (16, 12, 24)),
-                                            ("aa-soa", "blocks", (16, 16, 16)),
-                                            ("blk-push-soa", "channel", (16, 12, 24))])
-def test_peer_ipc_export_attach_two_processes(name, kind, dims):
+@pytest.mark.parametrize("name,kind,dims,guard", [("aa-soa", "channel", (16, 12, 24), False),
+                                                  ("aa-soa", "blocks", (16, 16, 16), False),
+                                                  ("blk-push-soa", "channel", (16, 12, 24), False),
+                                                  ("aa-soa", "blocks", (16, 16, 16), True)])
+def test_peer_ipc_export_attach_two_processes(name, kind, dims, guard):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, name, kind, dims, q))
+    procs = [ctx.Process(target=_rank, args=(r, world, port, name, kind, dims, q, guard))
              for r in range(world)]
     for p in procs:
         p.start()
