@@ -201,8 +201,9 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
     pool): with LBMGPU_GUARD=1 every device buffer carries 4 KiB guard zones
     of a fixed byte pattern; after every kernel family has run -- each name
     per-sweep and fused, the TMA tiles and 3-D halo tiles, RIA codings,
-    z-slab and node-range decompositions with both transports, snapshot /
-    load / verify -- no guard byte may have changed."""
+    z-slab and node-range decompositions with every transport (device
+    copies, NCCL, peer memory), AA temporal blocking, CUDA-graph replay,
+    snapshot / load / verify -- no guard byte may have changed."""
     monkeypatch.setenv("LBMGPU_GUARD", "1")
     assert lbm.lbmgpu.guard_selftest() == 1  # a planted 8-byte overrun is seen
     small = lbm.GeometrySpec("blocks", 12, 10, 10)
@@ -225,7 +226,7 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
         k.advance(PARAMS, FORCE, 4)
         keep.append(k)
     for name in ("aa-soa", "blk-push-soa", "blk-pull-soa"):
-        for extra in ({}, {"nccl_id": lbm.lbmgpu.nccl_unique_id()}):
+        for extra in ({}, {"nccl_id": lbm.lbmgpu.nccl_unique_id()}, {"transport": "peer"}):
             k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec("channel", 16, 12, 24),
                                 dist={"virtual_parts": 3, **extra})
             k.advance(PARAMS, FORCE, 4)
@@ -237,6 +238,22 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
         k.advance(PARAMS, FORCE, 4)
         k.snapshot()
         keep.append(k)
+    # peer transport over the z ring (blocks), AA temporal blocking, CUDA graphs
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("blocks", 16, 16, 16),
+                        dist={"virtual_parts": 4, "transport": "peer"})
+    k.advance(PARAMS, FORCE, 4)
+    keep.append(k)
+    monkeypatch.setenv("LBMGPU_AA_TB", "5,2")
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("channel", 32, 20, 24))
+    k.advance(PARAMS, FORCE, 4)
+    keep.append(k)
+    monkeypatch.delenv("LBMGPU_AA_TB")
+    monkeypatch.setenv("LBMGPU_GRAPH", "1")
+    for name in ("aa-soa", "blk-push-soa", "blk-pull-aos"):
+        k = lbm.make_kernel(lbm.make_descriptor(name), tiled)
+        k.advance(PARAMS, FORCE, 4)
+        keep.append(k)
+    monkeypatch.delenv("LBMGPU_GRAPH")
     rep = lbm.verify_kernel(lbm.make_descriptor("aa-soa"))
     assert rep["passed"]
     bad, msg = lbm.lbmgpu.guard_check()
