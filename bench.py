@@ -347,7 +347,7 @@ def main():
         # every sweep launch of the timed region touches each fluid node once:
         # 19 reads + 19 writes of 8 B (+ 72 B of adjacency for list one-step,
         # 72 B for the odd AA list sub-step only)
-        if "ria_pid" in name:
+        if "ria_pid" in name or "pull_pid" in name or "pull_stream_pid" in name:
             # pattern-id coding: 304 B of PDFs + a 1/2/4-byte pattern id per
             # node (the pattern table stays in L1 / L2)
             per_node = 304 + (4 if "pid32" in name else 2 if "pid16" in name else 1)

@@ -159,6 +159,11 @@ class ListEngine final : public Engine {
     // streaming stores for the nt names and for lattices far beyond L2
     cs_nt_ = d.nt_streams > 0;
     if (d.ria) build_ria();
+    if (const char* e = std::getenv("LBMGPU_PULL_PID"))
+      if (std::atoi(e) != 0 && !d.ria && d.prop == Prop::OsPull && d.soa) {
+        build_ria();  // pattern ids of the Gather table
+        pull_pid_ = ria_npat_ > 0;
+      }
     {
       int dev = 0;
       LBM_CUDA(cudaGetDevice(&dev));
@@ -513,7 +518,7 @@ class ListEngine final : public Engine {
   }
 
   bool advance_fused(const TrtArgs& t, long steps) {
-    if (!lparts_.empty() || desc_.ria || steps < 2 || fused_bytes_ == 0) return false;
+    if (!lparts_.empty() || desc_.ria || pull_pid_ || steps < 2 || fused_bytes_ == 0) return false;
     const uint64_t nbuf = desc_.prop == Prop::Aa ? 1 : 2;
     if (nbuf * total_slots_ * 8 + 72 * n_fluid_ > fused_bytes_) return false;
     ListArgs a = base_args();
@@ -613,7 +618,9 @@ class ListEngine final : public Engine {
       a.src = buf_[cur_].get();
       a.dst = buf_[1 - cur_].get();
       const bool last = s == steps - 1;
-      if (soa) {
+      if (soa && pull_pid_) {
+        launch_pull_pid(a, !last);
+      } else if (soa) {
         if (last)
           launch("list_pull_stream_soa", k_list_pull<true, false, false>, a, pull_pf_);
         else if (cs_nt_)
@@ -722,6 +729,28 @@ class ListEngine final : public Engine {
       for (int q = 0; q < kQ; ++q) starts[q] = desc_.soa ? starts_[q] : 0;
     if (total) *total = total_slots_;
     LBM_CUDA(cudaStreamSynchronize(stream_));
+  }
+
+  void launch_pull_pid(const ListArgs& a, bool collide) {
+    const unsigned g = static_cast<unsigned>(ceil_div(a.N, 256));
+    const char* w = ria_npat_ > 65536 ? "32" : ria_npat_ > 256 ? "16" : "";
+    const std::string nm = std::string(collide ? "list_pull_pid" : "list_pull_stream_pid") + w + "_soa";
+    const int tok = stats_.begin(nm.c_str(), stream_);
+    auto go = [&](auto* nid) {
+      using ID = std::remove_const_t<std::remove_pointer_t<decltype(nid)>>;
+      if (collide)
+        k_list_pull_pid<true, false, ID><<<g, 256, 0, stream_>>>(a, ria_ptab_.get(), nid, pf_);
+      else
+        k_list_pull_pid<false, false, ID><<<g, 256, 0, stream_>>>(a, ria_ptab_.get(), nid, pf_);
+    };
+    if (ria_npat_ > 65536)
+      go(ria_nid32_.get());
+    else if (ria_npat_ > 256)
+      go(ria_nid16_.get());
+    else
+      go(ria_nid_.get());
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, stream_);
   }
 
   template <typename ID>
@@ -872,6 +901,7 @@ class ListEngine final : public Engine {
   // patterns, else the run table), 0 run table, 1 group patterns, 2 pattern
   // ids (LBMGPU_RIA_MODE)
   int ria_mode_ = -1;
+  bool pull_pid_ = false;       // one-step pull through Gather-table pattern ids (LBMGPU_PULL_PID)
   int ria_npat_ = -1;           // distinct run patterns (-1: more than 2^20)
   DevBuf<int32_t> ria_ptab_;    // [pattern id][18]
   DevBuf<uint8_t> ria_nid_;     // pattern id of every node (<= 256 patterns)

@@ -140,6 +140,30 @@ __global__ void __launch_bounds__(256, 2)
   for (int d = 1; d < kQ; ++d) lst<CS>(buf + int64_t(a.starts[d] + n) + off[d - 1], q[d]);
 }
 
+// The same pattern-id coding applied to the one-step pull's Gather table
+// (experimental, LBMGPU_PULL_PID=1): entry(n, d) = starts[d] + n + row[d-1]
+// -- 2-4 B of id per node instead of 72 B of indices; same loads, collision
+// and stores as k_list_pull, so bitwise equal.
+template <bool COLLIDE, bool CS, typename ID>
+__global__ void __launch_bounds__(256, 2)
+    k_list_pull_pid(const ListArgs a, const int32_t* __restrict__ ptab,
+                    const ID* __restrict__ nid, uint64_t pf) {
+  const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (n >= a.N) return;
+  if (pf && (threadIdx.x & 31) == 0) {
+    const uint64_t m = n + pf;
+    if (m < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(nid + m));
+  }
+  const int32_t* p = ptab + uint32_t(__ldg(nid + n)) * 18;
+  double q[kQ];
+  q[0] = a.src[a.starts[0] + n];
+#pragma unroll
+  for (int d = 1; d < kQ; ++d) q[d] = a.src[int64_t(a.starts[d] + n) + __ldg(p + d - 1)];
+  if (COLLIDE) collide(q, a.trt);
+#pragma unroll
+  for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + a.starts[d] + n, q[d]);
+}
+
 // Group-pattern form of the run coding: a 32-node group (one warp) that lies
 // inside a single run carries that run's 18 offsets inline (72 B per 32
 // nodes, loaded as warp broadcasts with no dependent lookup in front); a

@@ -133,6 +133,29 @@ def test_ria_codings_bitwise_equal(kind, dims, monkeypatch):
             del k
 
 
+@pytest.mark.parametrize("name", ["list-pull-soa", "list-pull-split-nt-1s-soa"])
+@pytest.mark.parametrize("kind,dims", [("channel", (16, 12, 10)), ("pipe", (16, 14, 13)),
+                                       ("blocks", (24, 24, 24)), ("slit", (6, 5, 9))])
+def test_list_pull_pattern_ids_bitwise(name, kind, dims, monkeypatch):
+    """LBMGPU_PULL_PID=1: the one-step pull gathers through pattern ids of
+    its Gather table (the RIA coding applied to the pull); bitwise equal to
+    the indexed pull, odd and even step counts."""
+    spec = lbm.GeometrySpec(kind, *dims)
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    for steps in (5, 4):
+        ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        ref.load_perturbed(31)
+        ref.advance(PARAMS, FORCE, steps)
+        monkeypatch.setenv("LBMGPU_PULL_PID", "1")
+        k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+        monkeypatch.delenv("LBMGPU_PULL_PID")
+        k.load_perturbed(31)
+        k.kernel_stats_enable(True)
+        k.advance(PARAMS, FORCE, steps)
+        assert any(n.startswith("list_pull_pid") for n in k.kernel_stats())
+        assert k.fingerprint() == ref.fingerprint(), (name, steps)
+
+
 @pytest.mark.parametrize("dims,expect", [((16, 12, 10, 4, 4), "list_aa_odd_ria_pid_soa"),
                                          ((24, 24, 24, 4, 4), "list_aa_odd_ria_pid16_soa"),
                                          ((192, 192, 192, 4, 4), "list_aa_odd_ria_pid32_soa")])
