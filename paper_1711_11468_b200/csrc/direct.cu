@@ -1024,14 +1024,33 @@ class DirectEngine final : public Engine {
         }
       }
     };
-    sweep(false, true);
-    tr_->exchange(0, parts_, P_, stream_);
+    // boundary sweeps and the exchanges on the boundary stream, beside the
+    // interior sweeps (the same dependencies as the peer path, aa_pair_peer;
+    // the exchanged slot sets are touched by no interior node)
+    ensure_bstream();
+    cudaEvent_t ev_prev = pev_[0], ev_be = pev_[1], ev_ie = pev_[2], ev_bx = pev_[3];
+    LBM_CUDA(cudaEventRecord(ev_prev, stream_));
+    {
+      StreamSwap on_b(stream_, bstream_);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, ev_prev, 0));
+      sweep(false, true);
+      LBM_CUDA(cudaEventRecord(ev_be, stream_));
+      tr_->exchange(0, parts_, P_, stream_);
+    }
     sweep(false, false);
-    tr_->wait(0, stream_);
-    sweep(true, true);
-    tr_->exchange(1, parts_, P_, stream_);
+    LBM_CUDA(cudaEventRecord(ev_ie, stream_));
+    {
+      StreamSwap on_b(stream_, bstream_);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, ev_ie, 0));
+      tr_->wait(0, stream_);
+      sweep(true, true);
+      tr_->exchange(1, parts_, P_, stream_);
+      tr_->wait(1, stream_);
+      LBM_CUDA(cudaEventRecord(ev_bx, stream_));
+    }
+    LBM_CUDA(cudaStreamWaitEvent(stream_, ev_be, 0));
     sweep(true, false);
-    tr_->wait(1, stream_);
+    LBM_CUDA(cudaStreamWaitEvent(stream_, ev_bx, 0));
   }
 
   // ---- peer-memory transport (direct_peer.cuh) --------------
