@@ -953,6 +953,7 @@ class DirectEngine final : public Engine {
       }
     };
     const bool push = desc_.prop == Prop::OsPush;
+    ensure_bstream();
     if (!push)
       for (Part& pt : parts_)
         launch("full_collide_soa", k_full_collide<true>,
@@ -965,21 +966,30 @@ class DirectEngine final : public Engine {
             launch(name, k_full_push<true, false>, args(pt, n0, cnt, t, src, dst), stream_);
           };
         };
-        each(true, sweep("full_push_soa_halo"));
-        tr_->exchange(3, parts_, P_, stream_, dst);
-        each(false, sweep("full_push_soa"));
-        tr_->wait(3, stream_);
-        const int g = grid_for(P_, 256);
-        for (Part& pt : parts_) {
-          const DirectArgs a = args(pt, 0, 0, t, src, dst);
-          for (int face = 0; face < 2; ++face) {
-            const int tok = stats_.begin("push_halo_merge", stream_);
-            k_push_halo_merge<<<g, 256, 0, stream_>>>(
-                a, pt.stage.get() + uint64_t(face) * kQ * P_, face ? pt.nzl - 1 : 0, face == 0);
-            LBM_CHECK_LAUNCH();
-            stats_.end(tok, stream_);
+        // boundary stream: push(boundary) -> exchange 3 -> merge, beside
+        // push(interior) (each destination slot has one writer per sweep)
+        LBM_CUDA(cudaEventRecord(pev_[0], stream_));
+        {
+          StreamSwap on_b(stream_, bstream_);
+          LBM_CUDA(cudaStreamWaitEvent(stream_, pev_[0], 0));
+          each(true, sweep("full_push_soa_halo"));
+          tr_->exchange(3, parts_, P_, stream_, dst);
+          tr_->wait(3, stream_);
+          const int g = grid_for(P_, 256);
+          for (Part& pt : parts_) {
+            const DirectArgs a = args(pt, 0, 0, t, src, dst);
+            for (int face = 0; face < 2; ++face) {
+              const int tok = stats_.begin("push_halo_merge", stream_);
+              k_push_halo_merge<<<g, 256, 0, stream_>>>(
+                  a, pt.stage.get() + uint64_t(face) * kQ * P_, face ? pt.nzl - 1 : 0, face == 0);
+              LBM_CHECK_LAUNCH();
+              stats_.end(tok, stream_);
+            }
           }
+          LBM_CUDA(cudaEventRecord(pev_[1], stream_));
         }
+        each(false, sweep("full_push_soa"));
+        LBM_CUDA(cudaStreamWaitEvent(stream_, pev_[1], 0));
       } else {
         const bool collide = s + 1 < steps;
         auto sweep = [&](const char* name) {
@@ -989,10 +999,19 @@ class DirectEngine final : public Engine {
                     : launch(name, k_full_pull<true, false, false>, a, stream_);
           };
         };
-        tr_->exchange(2, parts_, P_, stream_, src);
+        // boundary stream: exchange 2 (source ghosts) -> pull(boundary),
+        // beside pull(interior) (disjoint destination planes, no ghost reads)
+        LBM_CUDA(cudaEventRecord(pev_[0], stream_));
+        {
+          StreamSwap on_b(stream_, bstream_);
+          LBM_CUDA(cudaStreamWaitEvent(stream_, pev_[0], 0));
+          tr_->exchange(2, parts_, P_, stream_, src);
+          tr_->wait(2, stream_);
+          each(true, sweep(collide ? "full_pull_soa_halo" : "full_pull_stream_soa_halo"));
+          LBM_CUDA(cudaEventRecord(pev_[1], stream_));
+        }
         each(false, sweep(collide ? "full_pull_soa" : "full_pull_stream_soa"));
-        tr_->wait(2, stream_);
-        each(true, sweep(collide ? "full_pull_soa_halo" : "full_pull_stream_soa_halo"));
+        LBM_CUDA(cudaStreamWaitEvent(stream_, pev_[1], 0));
       }
       cur_ ^= 1;
     }
