@@ -192,6 +192,13 @@ class ListEngine final : public Engine {
   }
 
   ~ListEngine() override {
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (bstream_) {
+      cudaStreamSynchronize(bstream_);
+      cudaStreamDestroy(bstream_);
+    }
+    for (cudaEvent_t e : bev_)
+      if (e) cudaEventDestroy(e);
     if (lnccl_) nccl_destroy(lnccl_);
     if (stream_) cudaStreamDestroy(stream_);
   }
@@ -426,14 +433,44 @@ class ListEngine final : public Engine {
         }
       }
     };
-    sweep(false, true);
-    list_exchange(0);
+    // boundary sweeps and exchanges on a boundary stream beside the interior
+    // sweeps, as in the direct z-slab paths (direct.cu aa_pair_peer): each
+    // slot is touched by one node per sub-step, and the exchanged slots
+    // belong to boundary nodes only
+    if (!bstream_) {
+      int least = 0, greatest = 0;
+      LBM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      LBM_CUDA(cudaStreamCreateWithPriority(&bstream_, cudaStreamNonBlocking, greatest));
+      for (cudaEvent_t& e : bev_) LBM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    struct Swap {
+      cudaStream_t& x;
+      cudaStream_t& y;
+      Swap(cudaStream_t& a, cudaStream_t& b) : x(a), y(b) { std::swap(x, y); }
+      ~Swap() { std::swap(x, y); }
+    };
+    LBM_CUDA(cudaEventRecord(bev_[0], stream_));
+    {
+      Swap on_b(stream_, bstream_);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, bev_[0], 0));
+      sweep(false, true);
+      LBM_CUDA(cudaEventRecord(bev_[1], stream_));
+      list_exchange(0);
+    }
     sweep(false, false);
-    list_wait(0);
-    sweep(true, true);
-    list_exchange(1);
+    LBM_CUDA(cudaEventRecord(bev_[2], stream_));
+    {
+      Swap on_b(stream_, bstream_);
+      LBM_CUDA(cudaStreamWaitEvent(stream_, bev_[2], 0));
+      list_wait(0);
+      sweep(true, true);
+      list_exchange(1);
+      list_wait(1);
+      LBM_CUDA(cudaEventRecord(bev_[3], stream_));
+    }
+    LBM_CUDA(cudaStreamWaitEvent(stream_, bev_[1], 0));
     sweep(true, false);
-    list_wait(1);
+    LBM_CUDA(cudaStreamWaitEvent(stream_, bev_[3], 0));
   }
 
   int parts() const override { return lparts_.empty() ? 1 : static_cast<int>(lparts_.size()); }
@@ -901,6 +938,8 @@ class ListEngine final : public Engine {
   // patterns, else the run table), 0 run table, 1 group patterns, 2 pattern
   // ids (LBMGPU_RIA_MODE)
   int ria_mode_ = -1;
+  cudaStream_t bstream_ = nullptr;  // node-range parts: boundary stream (aa_pair_parts)
+  cudaEvent_t bev_[4] = {nullptr, nullptr, nullptr, nullptr};
   bool pull_pid_ = false;       // one-step pull through Gather-table pattern ids (LBMGPU_PULL_PID)
   int ria_npat_ = -1;           // distinct run patterns (-1: more than 2^20)
   DevBuf<int32_t> ria_ptab_;    // [pattern id][18]
