@@ -33,9 +33,7 @@
 #include "direct_node.cuh"
 #include "direct_aos.cuh"
 #include "direct_fused.cuh"
-#include "direct_experimental.cuh"
 #include "direct_peer.cuh"
-#include "direct_tb.cuh"
 
 namespace lbmgpu {
 
@@ -334,39 +332,9 @@ class DirectEngine final : public Engine {
       LBM_CUDA(cudaGetDevice(&dev));
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
       // tuning knobs (defaults are the measured best)
-      if (const char* e = std::getenv("LBMGPU_AA_TMA_STAGES")) tma_stages_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_AA_CS")) cs_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_AA_THREADS")) aa_threads_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_AA_ODD_SX")) odd_sx_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
-      if (const char* e = std::getenv("LBMGPU_AOS_BAND")) aos_band_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_PULL_TILE")) pull_tile_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_ODD_TILE")) odd_tile_ = std::atoi(e) != 0;
-      if (const char* e = std::getenv("LBMGPU_AA_PF_WAVES")) aa_pf_waves_ = std::atof(e);
-      if (aa_threads_ < 32 || aa_threads_ > 256 || aa_threads_ % 32)
-        throw ConfigError("LBMGPU_AA_THREADS must be a multiple of 32 in [32, 256]");
-      if (const char* e = std::getenv("LBMGPU_AA_PIPE")) pipe_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_FUSED_FLOW")) flow_threads_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_FUSED_SHAPE")) fused_shape_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_GRID_SYNC")) barrier_mode_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_PUSH_TMASK")) use_tmask_ = std::atoi(e) != 0;
-      if (const char* e = std::getenv("LBMGPU_GRAPH")) graph_mode_ = std::atoi(e) != 0;
-      if (const char* e = std::getenv("LBMGPU_AA_TB")) {  // "W,G"
-        tb_w_ = std::atoi(e);
-        const char* comma = std::strchr(e, ',');
-        tb_g_ = comma ? std::atoi(comma + 1) : 4;
-        if (tb_w_ < 0 || tb_g_ < 1) throw ConfigError("LBMGPU_AA_TB must be W,G with W >= 0, G >= 1");
-      }
-      if (flow_threads_ < 0 || flow_threads_ > 256 || flow_threads_ % 32)
-        throw ConfigError("LBMGPU_FUSED_FLOW must be 0 or a multiple of 32 in [32, 256]");
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
         fused_bytes_ = uint64_t(std::atoll(e)) << 20;
-      barrier_.alloc(2);
-      LBM_CUDA(cudaMemsetAsync(barrier_.get(), 0, 2 * sizeof(unsigned), stream_));
-      if (tma_stages_ != 0 && tma_stages_ != 3 && tma_stages_ != 4 &&
-          tma_stages_ != 5 && tma_stages_ != 12)
-        tma_stages_ = 4;
     }
 
     DeviceGeometry geo = build_geometry_device(g, stream_);
@@ -419,7 +387,7 @@ class DirectEngine final : public Engine {
       LBM_CHECK_LAUNCH();
       // push: solid-target masks (required with several parts: the
       // targets in the ghost planes have no flags of their own here)
-      if (d.prop == Prop::OsPush && (nparts_ > 1 || use_tmask_)) {
+      if (d.prop == Prop::OsPush) {
         pt.tmask.alloc(uint64_t(pt.nzl) * P_);
         k_push_tmask<<<grid_for(uint64_t(pt.nzl) * P_, 256), 256, 0, stream_>>>(
             geo.flags.get(), nx_, ny_, nz_, pt.z0, pt.nzl, pt.tmask.get());
@@ -485,7 +453,6 @@ class DirectEngine final : public Engine {
     }
     for (cudaEvent_t e : pev_)
       if (e) cudaEventDestroy(e);
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
     if (peer_err_) cudaFreeHost(peer_err_);
     tr_.reset();
@@ -528,7 +495,6 @@ class DirectEngine final : public Engine {
                                                 : (long long)std::min(ny_, nz_) - 2;
     a.d2 = D * D;
     a.band = 0;
-    a.pf = 0;
     for (int d = 0; d < kQ; ++d) {
       const long long dn = -(long long)cz(d) * (long long)P_ - (long long)cy(d) * nx_ - cx(d);
       a.odd_off[d] = desc_.soa
@@ -556,8 +522,8 @@ class DirectEngine final : public Engine {
   // DirectArgs::band); plain order when ny has no suitable divisor
   DirectArgs banded(DirectArgs a) const {
     if (a.node0 != 0 || a.count != a.nzl * a.P) return a;
-    for (int b : {aos_band_, 8, 4, 2})
-      if (b > 1 && b <= aos_band_ && ny_ % b == 0) {
+    for (int b : {16, 8, 4, 2})
+      if (ny_ % b == 0) {
         a.band = static_cast<uint32_t>(b);
         break;
       }
@@ -574,69 +540,27 @@ class DirectEngine final : public Engine {
     stats_.end(tok, s);
   }
 
-  // One SoA AA sub-step over a node range: the TMA-staged persistent kernel
-  // when the row shape allows it (direct_tma.cu), else the register kernel.
+  // One SoA AA sub-step over a node range, one node per thread, 128-thread
+  // CTAs.  minb_ = min CTAs/SM of the launch bounds, i.e. the register cap
+  // (2 at 256: 128 registers, 16 warps/SM; DESIGN.md §4 has the sweep).
   void aa_sub(bool odd, const DirectArgs& a, const char* name) {
     if (a.count == 0) return;
-    if (tma_stages_ > 0 && a.nx % kTmaTile == 0 && a.node0 % kTmaTile == 0 &&
-        a.count % kTmaTile == 0) {
-      const int tok = stats_.begin(name, stream_);
-      launch_aa_tma(odd, a, sm_count_, tma_stages_, stream_);
-      stats_.end(tok, stream_);
-      return;
-    }
-    if (pipe_ != 0) {
-      const int tok = stats_.begin(name, stream_);
-      switch (pipe_) {
-        case 21:
-          odd ? launch_aa_pipe<true, 2, 1>(a, sm_count_, stream_)
-              : launch_aa_pipe<false, 2, 1>(a, sm_count_, stream_);
-          break;
-        case 31:
-          odd ? launch_aa_pipe<true, 3, 1>(a, sm_count_, stream_)
-              : launch_aa_pipe<false, 3, 1>(a, sm_count_, stream_);
-          break;
-        case 41:
-          odd ? launch_aa_pipe<true, 4, 1>(a, sm_count_, stream_)
-              : launch_aa_pipe<false, 4, 1>(a, sm_count_, stream_);
-          break;
-        default:
-          odd ? launch_aa_pipe<true, 2, 2>(a, sm_count_, stream_)
-              : launch_aa_pipe<false, 2, 2>(a, sm_count_, stream_);
-      }
-      stats_.end(tok, stream_);
-      return;
-    }
-    if (cs_) {
-      odd ? launch(name, k_full_aa_odd<true, true>, a, stream_)
-          : launch(name, k_full_aa_even<true, true>, a, stream_);
-      return;
-    }
-    DirectArgs ap = a;
-    ap.pf = static_cast<uint32_t>(aa_pf_waves_ * sm_count_ * 16 * 32);
-    const DirectArgs& a2 = ap;
-    if (odd && odd_sx_ && a.nx % kSxThreads == 0 && a.node0 % kSxThreads == 0 &&
-        a.count % kSxThreads == 0) {
-      odd_sx_ == 4 ? launch(name, k_full_aa_odd_sx<4>, a, stream_, kSxThreads)
-                   : launch(name, k_full_aa_odd_sx<3>, a, stream_, kSxThreads);
-      return;
-    }
     switch (minb_) {
-      case 2:
-        odd ? launch(name, k_full_aa_odd<true, false, 2>, a2, stream_, aa_threads_)
-            : launch(name, k_full_aa_even<true, false, 2>, a2, stream_, aa_threads_);
-        break;
       case 3:
-        odd ? launch(name, k_full_aa_odd<true, false, 3>, a, stream_, aa_threads_)
-            : launch(name, k_full_aa_even<true, false, 3>, a, stream_, aa_threads_);
+        odd ? launch(name, k_full_aa_odd<true, false, 128, 3>, a, stream_, 128)
+            : launch(name, k_full_aa_even<true, false, 128, 3>, a, stream_, 128);
         break;
-      case 4:
-        odd ? launch(name, k_full_aa_odd<true, false, 4>, a, stream_, aa_threads_)
-            : launch(name, k_full_aa_even<true, false, 4>, a, stream_, aa_threads_);
+      case 5:
+        odd ? launch(name, k_full_aa_odd<true, false, 128, 5>, a, stream_, 128)
+            : launch(name, k_full_aa_even<true, false, 128, 5>, a, stream_, 128);
+        break;
+      case 6:
+        odd ? launch(name, k_full_aa_odd<true, false, 128, 6>, a, stream_, 128)
+            : launch(name, k_full_aa_even<true, false, 128, 6>, a, stream_, 128);
         break;
       default:
-        odd ? launch(name, k_full_aa_odd<true, false>, a, stream_)
-            : launch(name, k_full_aa_even<true, false>, a, stream_);
+        odd ? launch(name, k_full_aa_odd<true, false, 128, 4>, a, stream_, 128)
+            : launch(name, k_full_aa_even<true, false, 128, 4>, a, stream_, 128);
     }
   }
 
@@ -653,24 +577,15 @@ class DirectEngine final : public Engine {
   template <bool SOA, int KIND>
   void launch_fused(const DirectArgs& a, double* other, long steps, const char* name,
                     long sweeps) {
-    if (flow_threads_ > 0) {
-      launch_flow<SOA, KIND>(a, other, sweeps, name);
-      return;
-    }
     // block shape, measured on cfg 1 (B200, cooperative-groups grid sync,
     // 20 sweeps per launch): push (160, 4) 18.1k MFLUP/s [(320, 2) 17.4k],
     // pull (160, 4) 19.6k, AA SoA (256, 2) 24.6k [(160, 4) 19.6k], AA AoS
     // (160, 4); the unconstrained (256, 1) compile lands at 132-146
     // registers, one block per SM
-    const int shape = fused_shape_ >= 0 ? fused_shape_ : (KIND == kFusedAA && SOA) ? 5 : 3;
-    switch (shape) {
-      case 1: launch_fused_as<SOA, KIND, 320, 2>(a, other, steps, name, sweeps); break;
-      case 2: launch_fused_as<SOA, KIND, 224, 3>(a, other, steps, name, sweeps); break;
-      case 3: launch_fused_as<SOA, KIND, 160, 4>(a, other, steps, name, sweeps); break;
-      case 4: launch_fused_as<SOA, KIND, 128, 5>(a, other, steps, name, sweeps); break;
-      case 5: launch_fused_as<SOA, KIND, 256, 2>(a, other, steps, name, sweeps); break;
-      default: launch_fused_as<SOA, KIND, 256, 1>(a, other, steps, name, sweeps);
-    }
+    if (KIND == kFusedAA && SOA)
+      launch_fused_as<SOA, KIND, 256, 2>(a, other, steps, name, sweeps);
+    else
+      launch_fused_as<SOA, KIND, 160, 4>(a, other, steps, name, sweeps);
   }
 
   template <bool SOA, int KIND, int TPB, int MINB>
@@ -682,50 +597,12 @@ class DirectEngine final : public Engine {
     const uint64_t want = ceil_div(a.count, TPB);
     const int grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(per_sm, 1)) * sm_count_)));
-    GridBarrier bar{barrier_.get(), barrier_.get() + 1, barrier_mode_};
     DirectArgs aa = a;
-    void* params[] = {&aa, &other, &steps, &bar};
+    void* params[] = {&aa, &other, &steps};
     const int tok = stats_.begin(name, stream_, sweeps);
     LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, TPB, params, 0,
                                          stream_));
     stats_.end(tok, stream_);
-  }
-
-  // Dataflow variant (k_full_flow): persistent co-resident blocks, plane
-  // counters instead of grid barriers.
-  template <bool SOA, int KIND>
-  void launch_flow(const DirectArgs& a, double* other, long sweeps, const char* name) {
-    // block shapes as for the barrier kernel: (threads, min blocks per SM)
-    // (cfg 1, 160 threads x 4 blocks/SM: push 15.8k, pull 16.4k, AA 16.8k
-    // MFLUP/s against 16.5k / 18.1k / 18.0k for the barrier kernel)
-    auto kern = flow_threads_ == 160   ? k_full_flow<SOA, KIND, 160, 4>
-                : flow_threads_ == 128 ? k_full_flow<SOA, KIND, 128, 5>
-                : flow_threads_ == 64  ? k_full_flow<SOA, KIND, 64, 8>
-                                       : k_full_flow<SOA, KIND, 256, 2>;
-    const int threads =
-        flow_threads_ == 160 || flow_threads_ == 128 || flow_threads_ == 64 ? flow_threads_ : 256;
-    int per_sm = 0;
-    per_sm = occupancy_blocks(reinterpret_cast<const void*>(kern), threads);
-    const uint64_t tasks = uint64_t(parts_[0].nzl) * ceil_div(P_, threads);
-    const int grid = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>(tasks, uint64_t(std::max(per_sm, 1)) * sm_count_)));
-    const uint32_t nz = parts_[0].nzl;
-    if (flow_ctr_.size() < nz) {
-      flow_ctr_.alloc(nz);
-      LBM_CUDA(cudaMemsetAsync(flow_ctr_.get(), 0, nz * sizeof(unsigned), stream_));
-      flow_base_ = 0;
-    }
-    // the plane counters run on across launches (no reset memset per
-    // advance): this launch's sweep s is complete on z at flow_base_ + (s+1)*cpp
-    const int tok = stats_.begin(name, stream_, sweeps);
-    DirectArgs aa = a;
-    unsigned* planes = flow_ctr_.get();
-    unsigned base = flow_base_;
-    void* params[] = {&aa, &other, &sweeps, &planes, &base};
-    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, threads, params, 0,
-                                         stream_));
-    stats_.end(tok, stream_);
-    flow_base_ += static_cast<unsigned>(uint64_t(sweeps) * ceil_div(P_, threads));
   }
 
   bool advance_fused(const TrtArgs& t, long steps) {
@@ -751,17 +628,45 @@ class DirectEngine final : public Engine {
     return true;
   }
 
+  // AoS 3-D halo tiles (direct_aos.cuh): single part, nx % 16, ny % 4, nz % 4
+  bool aos_tiles() const {
+    return nparts_ == 1 && nx_ % kPtX == 0 && ny_ % 4 == 0 && nz_ % 4 == 0;
+  }
+
+  // One-step AoS sweeps in pull order: collide pass, T-1 gather + collide
+  // sweeps, one gather-only sweep (kernels_full_os.cpp:173-190), every
+  // destination record assembled whole in a CTA's shared-memory tile.  The
+  // push names run the same schedule: push and pull realise the identical
+  // per-step mapping (reference tests/test_kernels.cpp:96-126) -- the value
+  // a push stores at (x, d) [bounce-back: (x, opp d) when x is solid] is the
+  // post-collision q_d of x - c_d, which is exactly what the pull gathers --
+  // so the state after advance(T) is bitwise the push's, with each node
+  // collided once per step and the scattered 8-byte stores of a push
+  // (one 32-byte sector each) replaced by whole-record bulk stores.
+  void os_aos_tiles(const TrtArgs& t, long steps, bool push) {
+    const Part& pt = parts_[0];
+    const uint32_t N = pt.nzl * static_cast<uint32_t>(P_);
+    launch(push ? "full_push_aos_collide" : "full_collide_aos", k_full_aos_tile<false>,
+           args(pt, 0, N, t, cur_, cur_), stream_, kAosTile);
+    for (long s = 0; s < steps; ++s) {
+      const bool last = s == steps - 1;
+      const char* name = push ? (last ? "full_push_stream_aos" : "full_push_aos")
+                              : (last ? "full_pull_stream_aos" : "full_pull_aos");
+      pull_aos_tile3d<4, 4>(args(pt, 0, N, t, cur_, 1 - cur_), last, name);
+      cur_ ^= 1;
+    }
+  }
+
   void advance(const TrtArgs& t, long steps) override {
     if (peer_) peer_check();
-    if (graph_mode_ && !graph_capturing_ && nparts_ == 1 && !use_fused(steps) && steps > 0) {
-      advance_graph(t, steps);
-      return;
-    }
     const bool soa = desc_.soa;
-    const bool cs = cs_;
     if (advance_fused(t, steps)) return;
     if (desc_.prop != Prop::Aa && nparts_ > 1) {
       peer_ ? os_sweeps_peer(t, steps) : os_sweeps_slabs(t, steps);
+      return;
+    }
+    if (desc_.prop != Prop::Aa && !soa && aos_tiles()) {
+      os_aos_tiles(t, steps, desc_.prop == Prop::OsPush);
       return;
     }
     if (desc_.prop == Prop::OsPush) {
@@ -770,8 +675,7 @@ class DirectEngine final : public Engine {
       for (long s = 0; s < steps; ++s) {
         DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
         if (soa)
-          cs ? launch("full_push_soa", k_full_push<true, true>, a, stream_)
-             : launch("full_push_soa", k_full_push<true, false>, a, stream_);
+          launch("full_push_soa", k_full_push<true, false>, a, stream_);
         else
           launch("full_push_aos", k_full_push<false, false>, banded(a), stream_);
         cur_ ^= 1;
@@ -786,8 +690,7 @@ class DirectEngine final : public Engine {
       {
         DirectArgs a = args(pt, 0, N, t, cur_, cur_);
         soa ? launch("full_collide_soa", k_full_collide<true>, a, stream_)
-            : aos_tile_ ? launch("full_collide_aos", k_full_aos_tile<false>, a, stream_, kAosTile)
-                        : launch("full_collide_aos", k_full_collide<false>, a, stream_);
+            : launch("full_collide_aos", k_full_aos_tile<false>, a, stream_, kAosTile);
       }
       for (long s = 0; s < steps; ++s) {
         DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
@@ -796,15 +699,7 @@ class DirectEngine final : public Engine {
           if (last)
             launch("full_pull_stream_soa", k_full_pull<true, false, false>, a, stream_);
           else
-            cs ? launch("full_pull_soa", k_full_pull<true, true, true>, a, stream_)
-               : launch("full_pull_soa", k_full_pull<true, true, false>, a, stream_);
-        } else if (aos_tile_ && pull_tile_ && nparts_ == 1 && nx_ % kPtX == 0 &&
-                   ny_ % pull_tile_ == 0 && nz_ % pull_tile_ == 0) {
-          const char* name = last ? "full_pull_stream_aos" : "full_pull_aos";
-          switch (pull_tile_) {
-            case 2: pull_aos_tile3d<2, 2>(a, last, name); break;
-            default: pull_aos_tile3d<4, 4>(a, last, name);
-          }
+            launch("full_pull_soa", k_full_pull<true, true, false>, a, stream_);
         } else {
           if (last)
             launch("full_pull_stream_aos", k_full_pull<false, false, false>, banded(a), stream_);
@@ -816,10 +711,6 @@ class DirectEngine final : public Engine {
       return;
     }
     // AA pattern: even/odd pairs, in place
-    if (tb_w_ > 0 && soa && nparts_ == 1 && tb_ok()) {
-      advance_tb(t, steps);
-      return;
-    }
     for (long s = 0; s < steps; s += 2) {
       if (nparts_ == 1) {
         const Part& pt = parts_[0];
@@ -829,11 +720,10 @@ class DirectEngine final : public Engine {
           aa_sub(false, a, "full_aa_even_soa");
           aa_sub(true, a, "full_aa_odd_soa");
         } else {
-          aos_tile_ ? launch("full_aa_even_aos", k_full_aos_tile<true>, a, stream_, kAosTile)
-                    : launch("full_aa_even_aos", k_full_aa_even<false, false>, a, stream_);
+          launch("full_aa_even_aos", k_full_aos_tile<true>, a, stream_, kAosTile);
           // (y-band order measured slower for the AA odd step: 1922 -> 1103
           // GB/s at band 16, although it halves the DRAM traffic)
-          if (aos_tile_ && odd_tile_ && nx_ % kPtX == 0 && ny_ % 4 == 0 && nz_ % 4 == 0) {
+          if (aos_tiles()) {
             const unsigned grid =
                 static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / 4) * (nz_ / 4));
             auto kern = k_full_aa_odd_aos_tile3d<4, 4>;
@@ -852,83 +742,6 @@ class DirectEngine final : public Engine {
         peer_ ? aa_pair_peer(t) : aa_pair_slabs(t);
       }
     }
-  }
-
-  // Temporal blocking (direct_tb.cuh): geometries without y / z wrap
-  // traffic only (channel, pipe: extreme rows and planes solid).
-  bool tb_ok() const { return geom_.kind == 0 || geom_.kind == 2; }
-
-  void advance_tb(const TrtArgs& t, long steps) {
-    const Part& pt = parts_[0];
-    DirectArgs a = args(pt, 0, pt.nzl * static_cast<uint32_t>(P_), t, 0, 0);
-    auto kern = k_full_aa_tb<256, 2>;
-    int per_sm = 0;
-    per_sm = occupancy_blocks(reinterpret_cast<const void*>(kern), 256);
-    const int grid = std::max(per_sm, 1) * sm_count_;
-    GridBarrier bar{barrier_.get(), barrier_.get() + 1, barrier_mode_};
-    uint32_t W = static_cast<uint32_t>(std::min<int>(tb_w_, ny_)), G = static_cast<uint32_t>(tb_g_);
-    const uint32_t nb = (static_cast<uint32_t>(ny_) + W - 1) / W;
-    const uint32_t last_e = ny_ - (nb - 1) * W;
-    TbDivs dv{FastDiv(W), FastDiv(W > 1 ? W - 1 : 1), FastDiv(last_e),
-              FastDiv(nb == 1 ? ny_ : last_e + 1)};
-    long pairs = steps / 2;
-    void* params[] = {&a, &W, &G, &pairs, &dv, &bar};
-    const int tok = stats_.begin("full_aa_soa_tb", stream_, steps);
-    LBM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, params, 0,
-                                         stream_));
-    stats_.end(tok, stream_);
-  }
-
-  // Per-sweep launches of one advance(T) captured once as a CUDA graph and
-  // replayed (LBMGPU_GRAPH=1; single part, lattices above the fused
-  // threshold).  Re-captured when T, the grid parity or the parameters
-  // change; the kernel-stats row is the whole graph (T sweeps).
-  void advance_graph(const TrtArgs& t, long steps) {
-    const bool same = graph_exec_ && graph_steps_ == steps && graph_cur0_ == cur_ &&
-                      std::memcmp(&graph_trt_, &t, sizeof t) == 0;
-    if (!same) {
-      if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-      graph_exec_ = nullptr;
-      const int cur0 = cur_;
-      const bool on = stats_.enabled();
-      const long n0 = stats_.launches();
-      stats_.enable(false);
-      graph_capturing_ = true;
-      cudaGraph_t g = nullptr;
-      LBM_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-      try {
-        advance(t, steps);
-      } catch (...) {
-        cudaStreamEndCapture(stream_, &g);
-        if (g) cudaGraphDestroy(g);
-        graph_capturing_ = false;
-        stats_.enable(on);
-        cur_ = cur0;
-        throw;
-      }
-      LBM_CUDA(cudaStreamEndCapture(stream_, &g));
-      graph_capturing_ = false;
-      stats_.enable(on);
-      graph_launches_ = stats_.launches() - n0;
-      stats_.add_launches(-graph_launches_);
-      const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
-      cudaGraphDestroy(g);
-      LBM_CUDA(e);
-      graph_cur1_ = cur_;
-      cur_ = cur0;
-      graph_steps_ = steps;
-      graph_cur0_ = cur0;
-      graph_trt_ = t;
-    }
-    const std::string name = std::string("full_") +
-                             (desc_.prop == Prop::Aa ? "aa" : desc_.prop == Prop::OsPush ? "push"
-                                                                                         : "pull") +
-                             (desc_.soa ? "_soa_graph" : "_aos_graph");
-    const int tok = stats_.begin(name.c_str(), stream_, steps);
-    LBM_CUDA(cudaGraphLaunch(graph_exec_, stream_));
-    stats_.end(tok, stream_);
-    stats_.add_launches(graph_launches_ - 1);  // begin() counted one
-    cur_ = graph_cur1_;
   }
 
   // One-step sweeps over z-slabs (halo.hpp phases 2 / 3), per lattice step:
@@ -1583,50 +1396,16 @@ class DirectEngine final : public Engine {
   uint64_t P_ = 0;
   int nparts_ = 1, rank_ = 0, nranks_ = 1;
   int cur_ = 0;
-  bool cs_ = false;       // st.global.cs stores in the register AA kernels
-  int tma_stages_ = 0;    // >0: TMA-staged AA kernels (direct_tma.cu)
-  // min CTAs/SM of the register AA kernels: 2 caps them at 128 registers,
-  // i.e. 16 resident warps/SM (measured best on B200: 1 -> 140 registers and
-  // 8 warps runs 33% slower; 3 -> 80 registers spills and hits the power cap)
-  int minb_ = 2;
-  // CTA size of the AA sweeps: 128 (4 CTAs x 4 warps per SM at 128
-  // registers) retires and refills warps in smaller groups than 2 x 8 warps;
-  // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830 (64: 6567/6695).
-  int aa_threads_ = 128;
-  // odd step with shared-memory realigned x-shifted stores (k_full_aa_odd_sx):
-  // 0 off, 3 / 4 = min blocks per SM of its 128-thread blocks
-  int odd_sx_ = 0;
-  bool aos_tile_ = true;  // AoS own-record sweeps through shared-memory tiles
-  // AoS push / pull sweeps: y-band height (0/1: plain order); cfg-5-sized
-  // box: push 959 -> 1507 GB/s, pull 2014 -> 2115 at 16
-  int aos_band_ = 16;
-  int pull_tile_ = 4;  // AoS pull halo tiles: 16 x T x T nodes (0: per-node kernel)
-  bool odd_tile_ = true;  // AoS AA odd step: gathers through 16 x 4 x 4 halo tiles
-  double aa_pf_waves_ = 0.0;  // SoA AA sweeps: L2 prefetch distance in waves (0 = off)
-  int pipe_ = 0;  // cp.async-pipelined AA kernels: stages*10 + CTAs/SM
+  // min CTAs/SM of the 128-thread register AA kernels: 4 caps them at 128
+  // registers, i.e. 16 resident warps/SM (DESIGN.md §4 has the sweep; one
+  // 256-thread CTA at 140 registers, 8 warps, ran 33% slower).  128-thread
+  // CTAs retire and refill warps in smaller groups than 2 x 8 warps:
+  // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830.
+  int minb_ = 4;
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
-  DevBuf<unsigned> barrier_;            // grid barrier {count, generation}
-  DevBuf<unsigned> flow_ctr_;           // k_full_flow: plane_done[nz] (monotone, wrapping)
-  unsigned flow_base_ = 0;              // plane_done value at the start of the next launch
-  // > 0: k_full_flow with this block size instead of the grid-barrier
-  // kernel (measured slower on cfg 1: 12.8k vs 14.8k MFLUP/s; opt-in)
-  int flow_threads_ = 0;
-  bool use_tmask_ = true;  // push: precomputed solid-target masks
-  // fused kernel grid barrier: 1 = cooperative_groups grid sync (cfg 1: push
-  // 16.5k -> 17.3k, pull 18.1k -> 19.5k, AA 18.0k -> 19.7k MFLUP/s against
-  // the counter + generation barrier, mode 0)
-  int barrier_mode_ = 1;
-  int fused_shape_ = -1;  // grid-barrier kernel block shape (-1: per kind, see launch_fused)
   int sm_count_ = 148;
   std::vector<Part> parts_;
   std::unique_ptr<Transport> tr_;
-  int tb_w_ = 0, tb_g_ = 4;  // temporal blocking band rows / plane group (0: off)
-  // CUDA graph of one advance(T) (advance_graph)
-  bool graph_mode_ = false, graph_capturing_ = false;
-  cudaGraphExec_t graph_exec_ = nullptr;
-  long graph_steps_ = 0, graph_launches_ = 0;
-  int graph_cur0_ = 0, graph_cur1_ = 0;
-  TrtArgs graph_trt_{};
   bool ring_ = false;                   // the halo plan includes the z ring
   bool peer_ = false, peer_ready_ = false;
   unsigned long long epoch_ = 0;        // AA pairs run with the peer transport

@@ -33,9 +33,6 @@ struct DirectArgs {
   // before y inside a band, so the z +- 1 rows whose records a row's
   // gathers touch are processed close in time (L2 reuse); 0 = plain order.
   uint32_t band;
-  // AA sweeps: L2 prefetch of the 19 slot lines of the warp `pf` nodes ahead
-  // (one resident-grid wave = SMs x warps/SM x 32); 0 = off
-  uint32_t pf;
 };
 
 // Solid flag of own node (x, y, own-plane z) without touching memory for the
@@ -60,11 +57,5 @@ __device__ __forceinline__ bool solid_node(const DirectArgs& a, uint32_t x, uint
       return a.flags[n] != 0;
   }
 }
-
-constexpr uint32_t kTmaTile = 256;  // nodes per TMA row tile
-
-// TMA-staged AA sub-step (direct_tma.cu); false = shape not supported.
-bool launch_aa_tma(bool odd, const DirectArgs& a, int sm_count, int stages,
-                   cudaStream_t s);
 
 }  // namespace lbmgpu

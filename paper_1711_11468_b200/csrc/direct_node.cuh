@@ -194,16 +194,16 @@ __device__ __forceinline__ void aa_odd_node(const DirectArgs& a, const Coords& c
     for (int d = 0; d < kQ; ++d) st<CS>(own + a.odd_off[d], q[opp(d)]);
     return;
   }
-  double* p[kQ];
-  p[0] = buf + I(c.Z[1], dslot(0), c.y, c.x);
+  // (addresses recomputed for the stores: 19 live pointers across the
+  // collision would set the kernel's register count)
+  auto slot = [&](int d) {
+    return buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+  };
 #pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    p[d] = buf + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
-#pragma unroll
-  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(p[d]);
+  for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(slot(d));
   collide(q, a.trt);
 #pragma unroll
-  for (int d = 0; d < kQ; ++d) st<CS>(p[d], q[opp(d)]);
+  for (int d = 0; d < kQ; ++d) st<CS>(slot(d), q[opp(d)]);
 }
 
 // ---- one sweep per launch, one node per thread ------------------------------
@@ -231,36 +231,16 @@ __global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
   collide_node_pass<SOA, false>(a, c, n);
 }
 
-// SoA AA sweeps: lanes 0..18 of a warp prefetch into L2 the two 128-byte
-// lines of slot `lane` of the 32 nodes `a.pf` nodes ahead (blocks dispatch in
-// index order, so that warp runs about one wave later; the odd step's
-// +-1-row gathers hit lines the neighbouring rows' warps prefetched).
-__device__ __forceinline__ void aa_prefetch(const DirectArgs& a) {
-  const uint32_t lane = threadIdx.x & 31;
-  if (a.pf == 0 || lane >= kQ) return;
-  const uint32_t m = a.node0 + blockIdx.x * blockDim.x + (threadIdx.x & ~31u) + a.pf;
-  if (m >= a.node0 + a.count) return;
-  const uint32_t z = a.fdP.div(m);
-  const uint32_t r = m - z * a.P;
-  const uint32_t y = a.fdx.div(r);
-  const double* p =
-      a.dst + (uint64_t(z + a.zoff) * kQ + lane) * a.P + uint64_t(y) * a.nx + (r - y * a.nx);
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 16));
-}
-
-template <bool SOA, bool CS, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_full_aa_even(const DirectArgs a) {
-  if (SOA) aa_prefetch(a);
+template <bool SOA, bool CS, int TPB = 256, int MINB = 1>
+__global__ void __launch_bounds__(TPB, MINB) k_full_aa_even(const DirectArgs a) {
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
   aa_even_node<SOA, CS, false>(a, c, n);
 }
 
-template <bool SOA, bool CS, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_full_aa_odd(const DirectArgs a) {
-  if (SOA) aa_prefetch(a);
+template <bool SOA, bool CS, int TPB = 256, int MINB = 1>
+__global__ void __launch_bounds__(TPB, MINB) k_full_aa_odd(const DirectArgs a) {
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;

@@ -168,24 +168,12 @@ class ListEngine final : public Engine {
       int dev = 0;
       LBM_CUDA(cudaGetDevice(&dev));
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
-      if (const char* e = std::getenv("LBMGPU_LIST_ODD_PIPE")) odd_pipe_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_RIA_MODE")) ria_mode_ = std::atoi(e);
-      if (const char* e = std::getenv("LBMGPU_AOS_TILE")) aos_tile_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
         fused_bytes_ = uint64_t(std::atoll(e)) << 20;
-      if (const char* e = std::getenv("LBMGPU_LIST_THREADS")) {
-        threads_ = std::atoi(e);
-        threads_env_ = true;
-      }
-      if (threads_ < 32 || threads_ > 256 || threads_ % 32)
-        throw ConfigError("LBMGPU_LIST_THREADS must be a multiple of 32 in [32, 256]");
       // adjacency L2 prefetch distance, in resident-grid waves (0 = off)
-      int waves = 1;  // measured best on B200 (cfg 2 list-aa odd: 5946 -> 6530 GB/s)
-      if (const char* e = std::getenv("LBMGPU_LIST_PF_WAVES")) waves = std::atoi(e);
-      pf_ = uint64_t(waves) * uint64_t(sm_count_) * 2 * 256;
-      int pwaves = 0;
-      if (const char* e = std::getenv("LBMGPU_PULL_PF_WAVES")) pwaves = std::atoi(e);
-      pull_pf_ = uint64_t(pwaves) * uint64_t(sm_count_) * 2 * 256;
+      // one wave: measured best on B200 (cfg 2 list-aa odd: 5946 -> 6530 GB/s)
+      pf_ = uint64_t(sm_count_) * 2 * 256;
     }
     const int parts = dist.nranks > 1 ? dist.nranks : std::max(1, dist.virtual_parts);
     if (parts > 1) setup_parts(dist, parts);
@@ -422,8 +410,7 @@ class ListEngine final : public Engine {
                 : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a, pf_);
           else
             soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
-                : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
-                            : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+                : launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a);
         };
         if (boundary) {
           run(0, p.head);
@@ -592,8 +579,7 @@ class ListEngine final : public Engine {
       a.src = a.dst = buf_[0].get();
       for (long s = 0; s < steps; s += 2) {
         soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
-            : aos_tile_ ? launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a)
-                        : launch("list_aa_even_aos", k_list_aa_even<false, false>, a);
+            : launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a);
         if (desc_.ria && soa) {
           const int mode = ria_mode_ >= 0 ? ria_mode_ : (ria_npat_ > 0 ? 2 : 0);
           const int tok = stats_.begin(mode == 2 && ria_npat_ > 65536 ? "list_aa_odd_ria_pid32_soa"
@@ -603,7 +589,7 @@ class ListEngine final : public Engine {
                                        stream_);
           // 128-thread CTAs: cfg 2 RIA odd 5228 -> 5431 GB/s (the indexed
           // sweeps measured equal or better at 256)
-          const int rt = threads_env_ ? threads_ : 128;
+          const int rt = 128;
           const unsigned g = static_cast<unsigned>(ceil_div(a.N, rt));
           if (mode == 2 && ria_npat_ > 65536)
             launch_pid(g, rt, a, ria_nid32_.get());
@@ -616,16 +602,6 @@ class ListEngine final : public Engine {
           else
             k_list_aa_odd_ria<false><<<g, rt, 0, stream_>>>(
                 a, ria_pat_.get(), ria_run0_.get(), ria_mask_.get(), pf_);
-          LBM_CHECK_LAUNCH();
-          stats_.end(tok, stream_);
-        } else if (odd_pipe_) {
-          const int tok = stats_.begin(soa ? "list_aa_odd_soa" : "list_aa_odd_aos", stream_);
-          const unsigned grid = static_cast<unsigned>(
-              std::min<uint64_t>(ceil_div(a.N, 256), uint64_t(sm_count_) * 2));
-          if (soa)
-            k_list_aa_odd_pipe<true><<<grid, 256, 0, stream_>>>(a);
-          else
-            k_list_aa_odd_pipe<false><<<grid, 256, 0, stream_>>>(a);
           LBM_CHECK_LAUNCH();
           stats_.end(tok, stream_);
         } else {
@@ -649,8 +625,7 @@ class ListEngine final : public Engine {
     // (kernels_list_os.cpp:74-91, kernels_list_nt.cpp:146-158)
     a.src = a.dst = buf_[cur_].get();
     soa ? launch("list_collide_soa", k_list_collide<true>, a)
-        : aos_tile_ ? launch_tile("list_collide_aos", k_list_aos_tile<false>, a)
-                    : launch("list_collide_aos", k_list_collide<false>, a);
+        : launch_tile("list_collide_aos", k_list_aos_tile<false>, a);
     for (long s = 0; s < steps; ++s) {
       a.src = buf_[cur_].get();
       a.dst = buf_[1 - cur_].get();
@@ -659,18 +634,16 @@ class ListEngine final : public Engine {
         launch_pull_pid(a, !last);
       } else if (soa) {
         if (last)
-          launch("list_pull_stream_soa", k_list_pull<true, false, false>, a, pull_pf_);
+          launch("list_pull_stream_soa", k_list_pull<true, false, false>, a);
         else if (cs_nt_)
-          launch("list_pull_soa", k_list_pull<true, true, true>, a, pull_pf_);
+          launch("list_pull_soa", k_list_pull<true, true, true>, a);
         else
-          launch("list_pull_soa", k_list_pull<true, true, false>, a, pull_pf_);
+          launch("list_pull_soa", k_list_pull<true, true, false>, a);
       } else {
         if (last)
-          launch("list_pull_stream_aos", k_list_pull<false, false, false>, a, pull_pf_);
-        else if (aos_tile_)
-          launch_tile("list_pull_aos", k_list_pull_aos_tile<true>, a);
+          launch("list_pull_stream_aos", k_list_pull<false, false, false>, a);
         else
-          launch("list_pull_aos", k_list_pull<false, true, false>, a, pull_pf_);
+          launch_tile("list_pull_aos", k_list_pull_aos_tile<true>, a);
       }
       cur_ ^= 1;
     }
@@ -913,9 +886,6 @@ class ListEngine final : public Engine {
   uint64_t total_slots_ = 0;
   bool scatter_ = false;
   bool cs_nt_ = false;
-  // index-prefetching persistent odd kernel: measured 4-8 % slower than the
-  // one-node-per-thread kernel on B200 (cfg 2/4), kept opt-in
-  bool odd_pipe_ = false;
   int sm_count_ = 148;
   int cur_ = 0;
   DevBuf<int32_t> nodes_;
@@ -947,11 +917,8 @@ class ListEngine final : public Engine {
   DevBuf<uint16_t> ria_nid16_;  // pattern id of every node (257 .. 65,536 patterns)
   DevBuf<uint32_t> ria_nid32_;  // pattern id of every node (more than 65,536 patterns)
   int threads_ = 256;           // CTA size of the sweeps
-  bool aos_tile_ = true;        // AoS own-record sweeps through shared-memory tiles
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold (PDFs + adjacency)
-  bool threads_env_ = false;    // threads_ set by LBMGPU_LIST_THREADS
   uint64_t pf_ = 0;             // adjacency L2 prefetch distance in nodes (AA odd)
-  uint64_t pull_pf_ = 0;        // same for the one-step pull sweeps
 };
 
 }  // namespace

@@ -116,15 +116,9 @@ __device__ __forceinline__ void list_aa_odd_node(const ListArgs& a, uint64_t n) 
 // stream-only exit pass.  CS selects st.global.cs (the GPU's counterpart of
 // the nt split-store variants, kernels_list_nt.cpp).
 template <bool SOA, bool COLLIDE, bool CS>
-__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a, uint64_t pf) {
+__global__ void __launch_bounds__(256) k_list_pull(const ListArgs a) {
   const uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (n >= a.N) return;
-  if (pf) {  // adjacency L2 prefetch for a later wave (see k_list_aa_odd)
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t m = (n & ~uint64_t(31)) + pf;
-    if (lane < 18 && m < a.N)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.adj + lane * a.N + m));
-  }
   list_pull_node<SOA, COLLIDE, CS, false>(a, n);
 }
 
@@ -218,40 +212,6 @@ __global__ void __launch_bounds__(256) k_list_aa_odd(const ListArgs a, uint64_t 
   }
   (void)buf;
   list_aa_odd_node<SOA, CS, false>(a, n);
-}
-
-// Persistent variant of k_list_aa_odd: every thread walks n, n+G, ... and
-// loads the 18 adjacency entries of its NEXT node while the current node's
-// gathers and collision are in flight, so the index-load latency no longer
-// sits in series in front of the dependent PDF gathers.
-template <bool SOA>
-__global__ void __launch_bounds__(256, 2) k_list_aa_odd_pipe(const ListArgs a) {
-  const uint64_t G = uint64_t(gridDim.x) * blockDim.x;
-  uint64_t n = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  double* buf = a.dst;
-  uint32_t an[18];
-  if (n < a.N) {
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) an[d - 1] = __ldg(a.adj + (d - 1) * a.N + n);
-  }
-  for (; n < a.N; n += G) {
-    double q[kQ];
-    q[0] = buf[lslot<SOA>(a, n, 0)];
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) q[d] = buf[an[opp(d) - 1]];
-    uint32_t nx[18];
-    const uint64_t m = n + G;
-    if (m < a.N) {
-#pragma unroll
-      for (int d = 1; d < kQ; ++d) nx[d - 1] = __ldg(a.adj + (d - 1) * a.N + m);
-    }
-    collide(q, a.trt);
-    buf[lslot<SOA>(a, n, 0)] = q[0];
-#pragma unroll
-    for (int d = 1; d < kQ; ++d) buf[an[d - 1]] = q[d];
-#pragma unroll
-    for (int d = 0; d < 18; ++d) an[d] = nx[d];
-  }
 }
 
 // ---- fused multi-sweep launch for L2-resident list lattices ---------------

@@ -56,23 +56,20 @@ def test_kernel_matches_golden_bitwise(idx, small_golden, small_snapshots):
     assert abs(k.total_mass() - case["mass"]) <= 1e-12 * abs(case["mass"])
 
 
-@pytest.mark.parametrize("fused", ["default", "per-sweep", "flow-256", "flow-64"])
+@pytest.mark.parametrize("fused", ["default", "per-sweep"])
 @pytest.mark.parametrize("name", NAMES)
 def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
-    """Host load_state path + a second geometry, against our C restatement
+    """Host load_state path + several geometries, against our C restatement
     of the reference steppers (tests/support/reference.hpp:33-105).  Small
     direct lattices normally run as one fused grid-barrier launch; the
     per-sweep kernels (used for large lattices) are forced with
-    LBMGPU_FUSED_MB=0 and the dataflow variant (k_full_flow) with
-    LBMGPU_FUSED_FLOW=256 / 64 (64: several chunks per plane, partial last
-    chunk), so every path is checked bit for bit."""
-    if fused.startswith("flow-") and name.startswith("list-"):
-        pytest.skip("direct-addressing knob")
+    LBMGPU_FUSED_MB=0, so every path is checked bit for bit.  channel
+    32x12x8 takes the AoS 3-D halo-tile sweeps (nx % 16, ny and nz % 4),
+    the other two boxes the per-node AoS kernels."""
     if fused == "per-sweep":
         monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    elif fused.startswith("flow-"):
-        monkeypatch.setenv("LBMGPU_FUSED_FLOW", fused[5:])
-    for kind, dims in [("blocks", (12, 12, 12)), ("channel", (33, 7, 9))]:
+    for kind, dims in [("blocks", (12, 12, 12)), ("channel", (33, 7, 9)),
+                       ("channel", (32, 12, 8))]:
         _, _, nf = port.geometry(kind, *dims)
         init = port.perturbed(nf, 99)
         fam = "half" if name.startswith("list-") else "full"
@@ -89,27 +86,6 @@ def test_against_port_oracle_steppers(name, fused, port, monkeypatch):
             expect2, _ = port.run(fam, kind, *dims, steps + 2, PARAMS.omega_plus, g=G_TEST,
                                   init=init)
             assert np.array_equal(k.snapshot(), expect2), (name, kind, steps + 2)
-
-
-@pytest.mark.parametrize("kind,dims", [("channel", (128, 12, 10)), ("blocks", (256, 16, 16)),
-                                       ("slit", (128, 5, 9))])
-def test_aa_odd_shared_realigned_variant(kind, dims, monkeypatch):
-    """k_full_aa_odd_sx (x-shifted scatters realigned through shared memory,
-    rows of 128-node blocks incl. the x wrap at both row ends) is bitwise the
-    register odd step, on one slab and on three z slabs."""
-    spec = lbm.GeometrySpec(kind, *dims)
-    res = []
-    for sx in ("0", "4"):
-        for parts in (1, 3):
-            monkeypatch.setenv("LBMGPU_AA_ODD_SX", sx)
-            monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-            k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec,
-                                dist={"virtual_parts": parts} if parts > 1 else None)
-            k.load_perturbed(5)
-            k.advance(PARAMS, FORCE, 8)
-            res.append(k.fingerprint())
-            del k
-    assert len(set(res)) == 1, [f"{r:016x}" for r in res]
 
 
 @pytest.mark.parametrize("kind,dims", [("channel", (16, 12, 10)), ("blocks", (24, 20, 20)),
@@ -177,46 +153,35 @@ def test_ria_pattern_id_widths(dims, expect):
     assert k.fingerprint() == ref.fingerprint()
 
 
+@pytest.mark.parametrize("name", ["blk-pull-aos", "blk-push-aos", "aa-aos"])
 @pytest.mark.parametrize("kind,dims", [("channel", (16, 8, 8)), ("channel", (32, 12, 8)),
                                        ("blocks", (32, 16, 16)), ("slit", (48, 4, 12)),
                                        ("pipe", (16, 12, 12))])
-def test_aos_pull_halo_tiles_bitwise(kind, dims, monkeypatch):
-    """blk-pull-aos through 3-D halo tiles (TMA row copies split at the x
-    wrap, y/z wrap of the halo rows, bulk stores of the tile) equals the
-    per-node AoS pull and the SoA pull bit for bit (odd step count: collide
-    pass, pulls, stream-only pass)."""
-    spec = lbm.GeometrySpec(kind, *dims)
+def test_aos_halo_tiles_against_oracle(name, kind, dims, port, monkeypatch):
+    """The AoS 3-D halo-tile sweeps (TMA row copies split at the x wrap,
+    y / z wrap of the halo rows, bulk stores of whole destination records)
+    against the oracle's family stepper, bit for bit: blk-pull-aos and
+    blk-push-aos (which runs the push mapping in pull order: collide pass,
+    gather sweeps, stream-only pass -- reference tests/test_kernels.cpp:
+    96-126) over odd and even step counts and repeated advance(1) calls, and
+    aa-aos (odd step gathers through the tiles)."""
     monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    res = []
-    for name, tile in (("blk-pull-aos", "1"), ("blk-pull-aos", "0"), ("blk-pull-soa", "1")):
-        monkeypatch.setenv("LBMGPU_AOS_TILE", tile)
-        k = lbm.make_kernel(lbm.make_descriptor(name), spec)
-        k.load_perturbed(17)
-        k.advance(PARAMS, FORCE, 5)
-        k.advance(PARAMS, FORCE, 2)
-        res.append((k.fingerprint(), k.total_mass()))
-        del k
-    assert res[0][0] == res[1][0] == res[2][0], [f"{r[0]:016x}" for r in res]
-    assert abs(res[0][1] - res[2][1]) <= 1e-12 * abs(res[2][1])
-
-
-@pytest.mark.parametrize("kind,dims", [("channel", (16, 8, 8)), ("channel", (32, 12, 8)),
-                                       ("blocks", (32, 16, 16)), ("slit", (48, 4, 12)),
-                                       ("pipe", (16, 12, 12))])
-def test_aos_aa_odd_halo_tiles_bitwise(kind, dims, monkeypatch):
-    """aa-aos with the odd step's gathers through 3-D halo tiles equals the
-    per-node AoS odd step and aa-soa bit for bit."""
-    spec = lbm.GeometrySpec(kind, *dims)
-    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    res = []
-    for name, tile in (("aa-aos", "1"), ("aa-aos", "0"), ("aa-soa", "1")):
-        monkeypatch.setenv("LBMGPU_ODD_TILE", tile)
-        k = lbm.make_kernel(lbm.make_descriptor(name), spec)
-        k.load_perturbed(19)
-        k.advance(PARAMS, FORCE, 6)
-        res.append(k.fingerprint())
-        del k
-    assert len(set(res)) == 1, [f"{r:016x}" for r in res]
+    _, _, nf = port.geometry(kind, *dims)
+    init = port.perturbed(nf, 17)
+    k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
+    k.load_state(init)
+    k.kernel_stats_enable(True)
+    runs = [6, 2] if name.startswith("aa") else [5, 2, 1, 1]
+    done = 0
+    for st in runs:
+        k.advance(PARAMS, FORCE, st)
+        done += st
+        expect, _ = port.run("full", kind, *dims, done, PARAMS.omega_plus, g=G_TEST, init=init)
+        assert np.array_equal(k.snapshot(), expect), (name, kind, dims, done)
+    rows = set(k.kernel_stats())
+    tile = {"blk-pull-aos": "full_pull_aos", "blk-push-aos": "full_push_aos",
+            "aa-aos": "full_aa_odd_aos"}[name]
+    assert tile in rows, rows
 
 
 def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
@@ -261,22 +226,11 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
         k.advance(PARAMS, FORCE, 4)
         k.snapshot()
         keep.append(k)
-    # peer transport over the z ring (blocks), AA temporal blocking, CUDA graphs
+    # peer transport over the z ring (blocks)
     k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("blocks", 16, 16, 16),
                         dist={"virtual_parts": 4, "transport": "peer"})
     k.advance(PARAMS, FORCE, 4)
     keep.append(k)
-    monkeypatch.setenv("LBMGPU_AA_TB", "5,2")
-    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("channel", 32, 20, 24))
-    k.advance(PARAMS, FORCE, 4)
-    keep.append(k)
-    monkeypatch.delenv("LBMGPU_AA_TB")
-    monkeypatch.setenv("LBMGPU_GRAPH", "1")
-    for name in ("aa-soa", "blk-push-soa", "blk-pull-aos"):
-        k = lbm.make_kernel(lbm.make_descriptor(name), tiled)
-        k.advance(PARAMS, FORCE, 4)
-        keep.append(k)
-    monkeypatch.delenv("LBMGPU_GRAPH")
     rep = lbm.verify_kernel(lbm.make_descriptor("aa-soa"))
     assert rep["passed"]
     bad, msg = lbm.lbmgpu.guard_check()
@@ -311,18 +265,15 @@ def test_edge_shapes_match_reference(edge_golden):
 @pytest.mark.parametrize("name", ["blk-push-soa", "blk-pull-soa", "aa-soa", "blk-push-aos",
                                   "aa-aos"])
 @pytest.mark.parametrize("kind,dims", [("channel", (64, 64, 64)), ("blocks", (48, 40, 36))])
-def test_flow_launch_equals_per_sweep_at_scale(name, kind, dims, monkeypatch):
-    """The multi-sweep launches -- grid barrier (default) and dataflow (plane
-    counters, LBMGPU_FUSED_FLOW) -- at a cfg-1-sized lattice, where hundreds
-    of blocks race through 21 sweeps (odd count for push/pull), are bitwise
-    the per-sweep kernels' result."""
+def test_fused_launch_equals_per_sweep_at_scale(name, kind, dims, monkeypatch):
+    """The multi-sweep grid-barrier launch at a cfg-1-sized lattice, where
+    hundreds of blocks race through 21 sweeps (odd count for push/pull), is
+    bitwise the per-sweep kernels' result."""
     steps = 20 if name.startswith("aa") else 21
     res = []
-    for env in ("0", "256", "128", None):
-        if env is None:
-            monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-        else:
-            monkeypatch.setenv("LBMGPU_FUSED_FLOW", env)
+    for mb in (None, "0"):
+        if mb is not None:
+            monkeypatch.setenv("LBMGPU_FUSED_MB", mb)
         k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
         k.load_perturbed(7)
         k.advance(PARAMS, FORCE, steps)
@@ -543,55 +494,6 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
-@pytest.mark.parametrize("tb", ["4,2", "7,3", "64,8", "1,1", "5,1"])
-@pytest.mark.parametrize("kind,dims", [("channel", (32, 20, 24)), ("pipe", (16, 14, 13)),
-                                       ("channel", (9, 7, 30))])
-def test_aa_temporal_blocking_bitwise(tb, kind, dims, monkeypatch):
-    """LBMGPU_AA_TB=W,G (direct_tb.cuh): one AA pair per pass over skewed
-    y-bands of W rows with a z-wavefront of G-plane groups, one cooperative
-    launch.  Bitwise equal to the even/odd sweeps for channel and pipe
-    (no y / z wrap traffic), bands narrower and wider than the box."""
-    spec = lbm.GeometrySpec(kind, *dims)
-    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    ref = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
-    ref.load_perturbed(88)
-    ref.advance(PARAMS, FORCE, 6)
-    monkeypatch.setenv("LBMGPU_AA_TB", tb)
-    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), spec)
-    k.load_perturbed(88)
-    k.kernel_stats_enable(True)
-    k.advance(PARAMS, FORCE, 4)
-    k.advance(PARAMS, FORCE, 2)
-    assert "full_aa_soa_tb" in k.kernel_stats()
-    assert k.fingerprint() == ref.fingerprint()
-
-
-@pytest.mark.parametrize("name", ["aa-soa", "aa-aos", "aa-vec-soa", "blk-push-soa", "blk-push-aos",
-                                  "blk-pull-soa", "blk-pull-aos"])
-@pytest.mark.parametrize("kind,dims", [("channel", (32, 12, 16)), ("blocks", (16, 16, 16))])
-def test_cuda_graph_advance_bitwise(name, kind, dims, monkeypatch):
-    """LBMGPU_GRAPH=1: the per-sweep launches of advance(T) are captured once
-    as a CUDA graph and replayed (re-captured when T or the grid parity
-    changes).  Bitwise equal to the plain launches, over advance() calls
-    with changing T; the launch count still counts every captured kernel."""
-    spec = lbm.GeometrySpec(kind, *dims)
-    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    steps = (4, 4, 2, 4) if name.startswith("aa") else (3, 3, 2, 3)
-    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
-    ref.load_perturbed(55)
-    for st in steps:
-        ref.advance(PARAMS, FORCE, st)
-    monkeypatch.setenv("LBMGPU_GRAPH", "1")
-    k = lbm.make_kernel(lbm.make_descriptor(name), spec)
-    k.load_perturbed(55)
-    k.kernel_stats_enable(True)
-    for st in steps:
-        k.advance(PARAMS, FORCE, st)
-    assert k.fingerprint() == ref.fingerprint(), name
-    assert any(n.endswith("_graph") for n in k.kernel_stats())
-    assert k.launch_count() >= sum(steps)
-
-
 @pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims,parts", [
     ("channel", (16, 12, 24), 2), ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2),
@@ -749,15 +651,16 @@ def test_baseline_config_fingerprint(cid):
 
 
 @pytest.mark.parametrize("cid,variant", [("2", "ria"), ("4", "ria"), ("5", "peer8"),
-                                         pytest.param("5", "copy4", marks=pytest.mark.slow),
-                                         pytest.param("5", "tb", marks=pytest.mark.slow)])
+                                         ("2", "ranges4"),
+                                         pytest.param("5", "copy4", marks=pytest.mark.slow)])
 def test_baseline_config_fingerprint_alternative_paths(cid, variant, monkeypatch):
     """The BASELINE golden fingerprints at full size through the other paths:
     list-aa-ria-soa (cfg 2: 8-bit pattern ids, cfg 4: 32-bit ids), cfg 5 as
     8 emulated z slabs over the peer transport (boundary stream, flags) and
-    as 4 slabs over device-copy halos, and cfg 5 through the AA temporal
-    blocking prototype (the last two marked slow: ~50 s each; all five
-    passed on the B200, profiles/r01h_fullsize_alt_paths.log)."""
+    as 4 slabs over device-copy halos (marked slow: ~50 s), and cfg 2 as 4
+    emulated node ranges (list-aa-soa node-range decomposition, index-list
+    halos; reference kernels_list_aa.cpp:63-74 splits the same contiguous
+    node ranges over its workers)."""
     if not os.path.exists(CONFIGS):
         pytest.skip("configs.json not generated")
     gold = json.load(open(CONFIGS))
@@ -773,8 +676,8 @@ def test_baseline_config_fingerprint_alternative_paths(cid, variant, monkeypatch
         dist = {"virtual_parts": 8, "transport": "peer"}
     elif variant == "copy4":
         dist = {"virtual_parts": 4}
-    elif variant == "tb":
-        monkeypatch.setenv("LBMGPU_AA_TB", "32,1")
+    elif variant == "ranges4":
+        dist = {"virtual_parts": 4}
     k = lbm.make_kernel(lbm.make_descriptor(name), spec, dist=dist)
     k.kernel_stats_enable(True)
     k.advance(lbm.TrtParams(1.0, 3.0 / 16.0), lbm.BodyForce(tuple(c["g"])), c["steps"])
@@ -782,7 +685,7 @@ def test_baseline_config_fingerprint_alternative_paths(cid, variant, monkeypatch
     assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
     names = set(k.kernel_stats())
     expect = {"ria": "list_aa_odd_ria_pid", "peer8": "full_aa_odd_soa_peer",
-              "copy4": "full_aa_odd_soa_halo", "tb": "full_aa_soa_tb"}[variant]
+              "copy4": "full_aa_odd_soa_halo", "ranges4": "list_aa_odd"}[variant]
     assert any(n.startswith(expect) for n in names), names
 
 

@@ -1,5 +1,5 @@
-// lbmbench-gpu: the reference CLI's bench / verify / geometry / list-kernels /
-// model subcommands (reference src/cli.cpp:406-576) on the B200 sweep library,
+// lbmbench-gpu: the reference CLI's bench / verify / geometry / list-kernels
+// subcommands (reference src/cli.cpp:406-576) on the B200 sweep library,
 // written against the C++ host API (include/lbmgpu.hpp).  Exit codes follow
 // the reference: 0 ok, 1 ConfigError, 2 NumericalError, 3 verification
 // failed (cli.cpp:330,566-572), 4 device failure.
@@ -53,7 +53,7 @@ struct Args {
 };
 
 Args parse(int argc, char** argv) {
-  if (argc < 2) throw ConfigError("usage: lbmbench-gpu <list-kernels|geometry|bench|verify|model> [--opt value ...]");
+  if (argc < 2) throw ConfigError("usage: lbmbench-gpu <list-kernels|geometry|bench|verify> [--opt value ...]");
   Args a;
   a.cmd = argv[1];
   for (int i = 2; i < argc; ++i) {
@@ -234,24 +234,6 @@ int cmd_verify(const Args& a) {
   return r.passed ? 0 : 3;
 }
 
-// model: reference B_l (perfmodel.cpp:10-47) next to the GPU algorithmic
-// bytes and the HBM roofline P_max = GB/s * 1000 / B (perfmodel.cpp:74-87).
-int cmd_model(const Args& a) {
-  const double hbm = a.getd("--hbm-gbps", 6553.6);
-  std::printf("%-26s %14s %16s %18s\n", "kernel", "B_l ref [B/FLUP]", "B_gpu [B/FLUP]",
-              "P_max GPU [MFLUP/s]");
-  for (const auto& n : kernel_names()) {
-    const LoopBalance b = loop_balance(n);
-    char bl[40];
-    if (b.ref_min != b.ref_max)
-      std::snprintf(bl, sizeof(bl), "%.1f-%.1f", b.ref_min, b.ref_max);
-    else
-      std::snprintf(bl, sizeof(bl), "%.1f", b.ref_min);
-    std::printf("%-26s %14s %16.1f %18.1f\n", n.c_str(), bl, b.gpu, hbm * 1000.0 / b.gpu);
-  }
-  return 0;
-}
-
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -261,9 +243,8 @@ int main(int argc, char** argv) {
     if (a.cmd == "geometry") return cmd_geometry(a);
     if (a.cmd == "bench") return cmd_bench(a);
     if (a.cmd == "verify") return cmd_verify(a);
-    if (a.cmd == "model") return cmd_model(a);
     throw ConfigError("unknown subcommand '" + a.cmd +
-                      "' (valid: list-kernels, geometry, bench, verify, model)");
+                      "' (valid: list-kernels, geometry, bench, verify)");
   } catch (const ConfigError& e) {
     std::cerr << "configuration error: " << e.what() << '\n';
     return 1;
