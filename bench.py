@@ -14,7 +14,13 @@ kernels.cpp:87-91).  MFLUP/s = N_fluid * lattice_steps / s / 1e6
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/liblbm_ref.so = lbmbench compiled from its sources) on the
-host cores, on a bounded sample of the same workload.
+host cores (pinned pool, one worker per core), on the full BASELINE
+workload: W warm-up and K timed bench steps on the whole box.  The b200
+arm's `cpu_baseline` is the same library on a bounded sample box.
+
+--gpus N outside torchrun re-executes under torch.distributed.run with N
+ranks; N > visible GPUs or WORLD_SIZE != N exits non-zero.  At N > 1 a
+bitwise pre-flight of the decomposition runs before anything is timed.
 """
 from __future__ import annotations
 
@@ -125,41 +131,72 @@ def ncu_traffic(kernel_name, cid=5, dims=None):
 
 
 # --------------------------------------------------------------- CPU legs
-def cpu_reference_run(cid, steps_per_sample, samples, warmup_samples):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    """Cores this process may run on (sorted), i.e. the reference's --pin
+    list for a pool of all of them."""
+    try:
+        return sorted(os.sched_getaffinity(0))
+    except AttributeError:
+        return list(range(os.cpu_count() or 1))
+
+
+def cpu_reference_run(cid, steps_per_sample, samples, warmup_samples, full=False):
     """The reference lbmbench (oracle/_ref) on the host cores: every sample is
-    `steps_per_sample` lattice steps of the reference kernel on the bounded
-    sample box.  Returns (MFLUP/s, cores, description, kind)."""
+    `steps_per_sample` lattice steps of the reference kernel, on the full
+    BASELINE box (full=True) or the bounded sample box.  The WorkerPool has
+    one worker per available core, worker w pinned to core w (reference
+    --pin semantics, workers.cpp:26-39).  Returns (MFLUP/s, cores,
+    description, kind, seconds per sample)."""
     kernel, kind, dims, extra, _, sdims = CONFIGS[cid]
-    threads = os.cpu_count() or 1
+    box = dims if full else sdims
+    cores = host_cores()
+    threads = len(cores)
     from oracle.oracle import Ref, Port  # test/baseline infrastructure only
     try:
         ref = Ref()
     except FileNotFoundError:
         ref = None
     if ref is not None:
-        k = ref.kernel(kernel, kind, *sdims, threads=threads, block=extra.get("block", 4),
-                       spacing=extra.get("spacing", 4), pipe_diameter=extra.get("pipe_diameter", 0))
+        k = ref.kernel(kernel, kind, *box, threads=threads, block=extra.get("block", 4),
+                       spacing=extra.get("spacing", 4), pipe_diameter=extra.get("pipe_diameter", 0),
+                       pin=cores)
+        pinned = k.pinned()
         for _ in range(warmup_samples):
             k.advance(OMEGA_PLUS, LAMBDA, G, steps_per_sample)
         secs = [k.advance(OMEGA_PLUS, LAMBDA, G, steps_per_sample) for _ in range(samples)]
         n = k.n_fluid
         tot = sum(secs)
         desc = (f"reference lbmbench {kernel} (oracle/_ref, -O3 -ffp-contract=off -march=x86-64-v4, "
-                f"WorkerPool({threads})) on {kind} {'x'.join(map(str, sdims))} "
-                f"({n} fluid nodes), {samples} x {steps_per_sample} steps timed")
-        return n * steps_per_sample * samples / tot / 1e6, threads, desc, "reference"
+                f"WorkerPool({threads}) pinned to cores {cores[0]}..{cores[-1]} ({pinned} bound)) "
+                f"on {cpu_model()}; {kind} {'x'.join(map(str, box))} "
+                f"({'the full BASELINE box' if full else 'bounded sample box'}, {n} fluid nodes), "
+                f"{warmup_samples} x {steps_per_sample} steps warm-up, "
+                f"{samples} x {steps_per_sample} steps timed (Kernel::advance wall clock)")
+        return n * steps_per_sample * samples / tot / 1e6, threads, desc, "reference", tot / samples
     # fallback: our C restatement, textbook stepper, single thread
     port = Port()
     fam = "half" if kernel.startswith("list-") else "full"
     t0 = time.perf_counter()
-    port.run(fam, kind, *sdims, steps_per_sample * samples, OMEGA_PLUS, g=G,
+    port.run(fam, kind, *box, steps_per_sample * samples, OMEGA_PLUS, g=G,
              block=extra.get("block", 4), spacing=extra.get("spacing", 4),
              pipe_diameter=extra.get("pipe_diameter", 0))
     dt = time.perf_counter() - t0
-    _, _, nf = port.geometry(kind, *sdims, extra.get("block", 4), extra.get("spacing", 4),
+    _, _, nf = port.geometry(kind, *box, extra.get("block", 4), extra.get("spacing", 4),
                              extra.get("pipe_diameter", 0))
     return (nf * steps_per_sample * samples / dt / 1e6, 1,
-            f"port oracle textbook stepper on {kind} {'x'.join(map(str, sdims))}", "port")
+            f"port oracle textbook stepper on {cpu_model()}; {kind} {'x'.join(map(str, box))}",
+            "port", dt / samples)
 
 
 def base_line(cid, n_gpus, steps, warmup, lattice_per_step):
@@ -190,28 +227,140 @@ def base_line(cid, n_gpus, steps, warmup, lattice_per_step):
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU implementation on the host cores, on the FULL
+    BASELINE workload: W warm-up and K timed bench steps of the config's
+    kernel on its whole box (cfg 5: 1024x512x512, 41 GB, one AA pair per
+    step), pinned pool, measured ms per step.  Rank 0 only."""
     if rank != 0:
         return
     cid = args.config
     kernel = CONFIGS[cid][0]
     per = 2 if "aa" in kernel.split("-") else 1
-    mflups, cores, desc, kind = cpu_reference_run(cid, per, args.steps, args.warmup)
-    line = base_line(cid, args.gpus, args.steps, args.warmup, per)
-    # ms per bench step of the FULL workload at the measured CPU rate (the
-    # timed samples run on the bounded sample box, see cpu_baseline.sample)
-    n_full = {1: 246016, 2: 16516096, 3: 25128960, 4: 56000000, 5: 266342400}[cid]
+    mflups, cores, desc, kind, sec = cpu_reference_run(cid, per, args.steps, args.warmup,
+                                                       full=True)
+    line = base_line(cid, args.gpus or world, args.steps, args.warmup, per)
     line.update({"impl": "reference", "value": mflups,
-                 "ms_per_step": n_full * per / (mflups * 1e6) * 1e3,
+                 "ms_per_step": sec * 1e3,
                  "cpu_baseline": {"value": mflups, "unit": "MFLUP/s", "cores": cores,
-                                  "kind": kind, "sample": desc},
+                                  "kind": kind, "sample": desc, "cpu_model": cpu_model()},
                  "e2e": {"value": mflups, "unit": "MFLUP/s", "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 0}})
     print(json.dumps(line), flush=True)
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def visible_gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def relaunch(n, launch_check):
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with N ranks (one per GPU), same arguments; the
+    exit code is the launcher's.  Refuses (exit 2) when N exceeds the
+    visible GPUs instead of silently measuring one."""
+    if not launch_check:
+        have = visible_gpus()
+        if n > have:
+            print(f"bench.py: --gpus {n} but only {have} GPU(s) visible; refusing to run "
+                  f"(no silent single-GPU line)", file=sys.stderr, flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
+def preflight(lbm, dist, rank, world, local, desc, transport):
+    """Bitwise pre-flight of the decomposition before anything is timed:
+    every rank advances its part of a small lattice (channel 64 x 32 x 6N,
+    perturbed init, 10 steps) with the chosen transport; rank 0 assembles the
+    local rows and compares them with its own single-GPU run of the same
+    kernel (the invariance of reference tests/test_kernels.cpp:177-195
+    across decompositions).  Every stage ends in a collective flag, so a rank
+    that fails (e.g. a CUDA IPC error on the peer path) cannot leave the
+    others blocked.  Returns (ok, detail)."""
+    import numpy as np
+    import torch
+
+    def all_ok(flag):
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    spec = lbm.GeometrySpec("channel", 64, 32, 6 * world)
+    params, force = lbm.TrtParams.from_tau(0.9), lbm.BodyForce((1e-5, 2e-6, -3e-6))
+    err = ""
+    k = None
+    obj = [lbm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    try:
+        k = lbm.make_kernel(desc, spec, dist={"rank": rank, "nranks": world, "device": local,
+                                              "nccl_id": obj[0], "transport": transport})
+        ok = True
+    except Exception as e:  # noqa: BLE001 -- reported, then the flag decides
+        ok, err = False, f"create: {e}"
+    if not all_ok(ok):
+        return False, err or "create failed on another rank"
+    if transport == "peer":
+        recs = [None] * world
+        try:
+            rec = k.peer_export()
+        except Exception as e:  # noqa: BLE001
+            rec, err = b"", f"peer_export: {e}"
+        dist.all_gather_object(recs, rec)
+        try:
+            if err or any(not r for r in recs):
+                raise RuntimeError(err or "peer_export failed on another rank")
+            k.peer_attach(recs)
+            ok = True
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, f"peer_attach: {e}"
+        if not all_ok(ok):
+            return False, err or "peer_attach failed on another rank"
+    try:
+        k.load_perturbed(4242)
+        k.advance(params, force, 10)
+        rows = (k.local_canonical_index(), k.snapshot_local())
+        ok = True
+    except Exception as e:  # noqa: BLE001
+        rows, ok, err = None, False, f"advance: {e}"
+    if not all_ok(ok):
+        return False, err or "advance failed on another rank"
+    out = [None] * world
+    dist.gather_object(rows, out if rank == 0 else None, dst=0)
+    ok = True
+    if rank == 0:
+        ref = lbm.make_kernel(desc, spec)
+        ref.load_perturbed(4242)
+        ref.advance(params, force, 10)
+        expect = ref.snapshot().reshape(-1, 19)
+        got = np.full_like(expect, np.nan)
+        for idx, snap in out:
+            got[idx.astype(np.int64)] = snap.reshape(-1, 19)
+        ok = bool(np.array_equal(got, expect))
+        err = "" if ok else "decomposed state differs from the single-GPU run"
+        del ref
+    ok = all_ok(ok)
+    del k
+    return ok, (f"bitwise equal to 1 GPU: {desc.name} channel 64x32x{6 * world}, "
+                f"{world} parts, 10 steps, transport {transport}" if ok else err)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="number of GPUs (ranks); outside torchrun, N > 1 re-executes this "
+                         "script under torch.distributed.run with N ranks")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -221,11 +370,11 @@ def main():
     ap.add_argument("--no-micro", action="store_true",
                     help="skip the device update-19/copy-19 micro-benchmark ceiling")
     ap.add_argument("--transport", default="auto", choices=["auto", "copy", "peer"],
-                    help="z-slab halo transport: peer = boundary sweeps load/store the "
-                         "neighbour slab in peer memory (CUDA IPC), epoch flags, boundary "
-                         "work on its own stream; copy = NCCL send/recv (device copies with "
-                         "--virtual-parts); auto = peer for the direct SoA z slabs, copy for "
-                         "the list node ranges")
+                    help="z-slab halo transport: copy = NCCL send/recv of the halo slots "
+                         "(device copies with --virtual-parts); peer = boundary sweeps "
+                         "load/store the neighbour slab in peer memory (CUDA IPC), epoch "
+                         "flags (opt-in: falls back to copy if its pre-flight fails); "
+                         "auto = copy at N > 1, peer for --virtual-parts emulation")
     ap.add_argument("--decompose", action="store_true",
                     help="at N>1: z-slab decomposition of direct push/pull and node-range "
                          "decomposition of list AA instead of replicas")
@@ -239,6 +388,9 @@ def main():
                     help="run another kernel name on the config's geometry (extra lines)")
     ap.add_argument("--dims", default=None,
                     help="override the box (NXxNYxNZ) -- profiling only, not a bench line")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="test hook: after the (re-)launch every rank reports its rank / world "
+                         "and rank 0 prints one line; no GPU work")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -247,6 +399,24 @@ def main():
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+        return
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        sys.exit(relaunch(args.gpus, args.launch_check))
+    if args.gpus is not None and args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to run",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+    if args.launch_check:
+        import torch.distributed as tdist
+        if world > 1:
+            tdist.init_process_group("gloo")
+            ranks = [None] * world
+            tdist.all_gather_object(ranks, rank)
+            tdist.destroy_process_group()
+        else:
+            ranks = [0]
+        if rank == 0:
+            print(json.dumps({"launch_check": True, "n_gpus": world, "ranks": ranks}), flush=True)
         return
 
     import torch
@@ -282,13 +452,35 @@ def main():
         args.decompose and not desc.ria and (desc.addr == "direct" or aa))
     replicas = world > 1 and not decomposable
     if args.transport == "auto":
-        args.transport = "peer" if desc.addr == "direct" else "copy"
+        # emulation on one GPU: the peer schedule (boundary stream, epoch
+        # flags) on device pointers; several GPUs: NCCL halo copies unless
+        # --transport peer asks for the peer-memory path
+        args.transport = "peer" if desc.addr == "direct" and world == 1 else "copy"
     if world == 1 and args.virtual_parts > 1:
         dspec = {"virtual_parts": args.virtual_parts, "transport": args.transport}
         if args.nccl_self:
             dspec["nccl_id"] = lbm.nccl_unique_id()
             dspec["transport"] = "copy"  # NCCL self send/recv halos
+    pre = None
     if world > 1 and not replicas:
+        if args.transport == "peer" and desc.addr != "direct":
+            args.transport = "copy"
+        # bitwise pre-flight of the decomposition with the chosen transport;
+        # the peer path falls back to NCCL copies, a failing copy path stops
+        # the run (no number from a wrong decomposition)
+        ok, detail = preflight(lbm, dist, rank, world, local, desc, args.transport)
+        pre = {"transport": args.transport, "ok": ok, "detail": detail}
+        if not ok and args.transport == "peer":
+            args.transport = "copy"
+            ok, detail = preflight(lbm, dist, rank, world, local, desc, "copy")
+            pre = {"transport": "copy", "ok": ok, "detail": detail,
+                   "peer_failed": pre["detail"]}
+        if not ok:
+            if rank == 0:
+                print(f"bench.py: multi-GPU pre-flight failed: {detail}", file=sys.stderr,
+                      flush=True)
+            dist.destroy_process_group()
+            sys.exit(3)
         obj = [lbm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         dspec = {"rank": rank, "nranks": world, "device": local, "nccl_id": obj[0],
@@ -327,6 +519,19 @@ def main():
     k.kernel_stats_enable(False)
     stats = k.kernel_stats()
     clk = clocks.stop()
+    clk_ranks = [clk]
+    if dist is not None:
+        # every rank sampled its own GPU: the line carries all of them, and
+        # the headline clocks are the worst rank's (lowest median, union of
+        # the throttle reasons)
+        clk_ranks = [None] * world
+        dist.all_gather_object(clk_ranks, clk)
+        meds = [c["sm_mhz"] for c in clk_ranks if c.get("sm_mhz")]
+        maxs = [c["sm_max_mhz"] for c in clk_ranks if c.get("sm_max_mhz")]
+        clk = {"sm_mhz": min(meds) if meds else None, "sm_max_mhz": max(maxs) if maxs else None,
+               "reasons": sorted({r for c in clk_ranks for r in c.get("reasons", [])}),
+               "samples": sum(c.get("samples", 0) for c in clk_ranks),
+               "of": "worst rank (lowest median SM clock; union of reasons)"}
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -397,6 +602,9 @@ def main():
     elif world > 1 and args.transport == "peer":
         line["config"]["parallelism"] = (f"z-slab x{world}, peer-memory boundary sweeps "
                                          "(CUDA IPC over NVLink, epoch flags)")
+    elif world > 1 and desc.addr == "direct":
+        line["config"]["parallelism"] = (f"z-slab x{world}, NCCL send/recv halo slots "
+                                         "overlapped with the interior sweeps")
     elif world > 1 and desc.addr == "indirect":
         line["config"]["parallelism"] = f"node-range (x-slab) decomposition x{world}, NCCL index-list halos"
     if world == 1 and args.virtual_parts > 1:
@@ -418,6 +626,10 @@ def main():
         "step_roofline_frac": step_gbps / hbm,
         "gpu_bytes_per_flup": gpu_b,
     })
+    if world > 1:
+        line["clocks_per_rank"] = clk_ranks
+        line["config"]["transport"] = args.transport if not replicas else None
+        line["preflight"] = pre
 
     # ---- end to end through the public API with host buffers: the initial
     # state is loaded from pinned host memory, the job's steps run, the final
@@ -432,9 +644,9 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, sdesc, skind = cpu_reference_run(cid, per, 3 if cid != 1 else 20, 1)
+            v, cores, sdesc, skind, _ = cpu_reference_run(cid, per, 3 if cid != 1 else 20, 1)
             line["cpu_baseline"] = {"value": v, "unit": "MFLUP/s", "cores": cores,
-                                    "kind": skind, "sample": sdesc}
+                                    "kind": skind, "sample": sdesc, "cpu_model": cpu_model()}
         except Exception as e:  # report, never fail the GPU line
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

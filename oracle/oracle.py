@@ -185,7 +185,9 @@ class Ref:
         L.ref_last_error.restype = C.c_char_p
         L.ref_geometry.argtypes = [C.c_int] * 7 + [C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
         L.ref_create.argtypes = [C.c_char_p] + [C.c_int] * 9 + [C.c_void_p, C.c_int, C.c_int,
+                                                                 C.c_void_p, C.c_int,
                                                                  C.POINTER(C.c_void_p)]
+        L.ref_pinned.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
         L.ref_destroy.argtypes = [C.c_void_p]
         L.ref_n_fluid.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.ref_load_state.argtypes = [C.c_void_p, _dp, C.c_uint64]
@@ -293,9 +295,10 @@ class Ref:
         return f
 
     def kernel(self, name, kind, nx, ny, nz, block=4, spacing=4, pipe_diameter=0, blk=0,
-               padding="auto", pads=None, threads=1, vector_width=4):
+               padding="auto", pads=None, threads=1, vector_width=4, pin=None):
+        """pin: core ids for the workers (reference --pin, workers.cpp:26-39)."""
         return RefKernel(self, name, kind, nx, ny, nz, block, spacing, pipe_diameter, blk,
-                         padding, pads, threads, vector_width)
+                         padding, pads, threads, vector_width, pin)
 
     def verify(self, name, nx=8, ny=8, nz=34, g=1e-6, tau=0.9, magic_lambda=3.0 / 16.0,
                threads=1, interval=200, tol=1e-12, max_steps=200000):
@@ -315,13 +318,15 @@ class Ref:
 
 class RefKernel:
     def __init__(self, ref, name, kind, nx, ny, nz, block, spacing, pipe_diameter, blk, padding,
-                 pads, threads, vector_width):
+                 pads, threads, vector_width, pin=None):
         self.ref = ref
         self.h = C.c_void_p()
+        pin_arr = np.asarray(list(pin or []), np.int32)
         ref._chk(ref.L.ref_create(name.encode(), KINDS[kind], nx, ny, nz, block, spacing,
                                   pipe_diameter, blk, PADDING[padding],
                                   _pads_arr(pads).ctypes.data, threads, vector_width,
-                                  C.byref(self.h)))
+                                  pin_arr.ctypes.data if pin_arr.size else None,
+                                  int(pin_arr.size), C.byref(self.h)))
         n = C.c_uint64()
         ref._chk(ref.L.ref_n_fluid(self.h, C.byref(n)))
         self.n_fluid = n.value
@@ -349,6 +354,11 @@ class RefKernel:
         v = C.c_double()
         self.ref._chk(self.ref.L.ref_total_mass(self.h, C.byref(v)))
         return v.value
+
+    def pinned(self):
+        n = C.c_int()
+        self.ref._chk(self.ref.L.ref_pinned(self.h, C.byref(n)))
+        return n.value
 
     def advance(self, omega_plus, magic_lambda, g, steps):
         sec = C.c_double()

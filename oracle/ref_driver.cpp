@@ -118,14 +118,18 @@ int ref_geometry(int kind, int nx, int ny, int nz, int block, int spacing,
   });
 }
 
+// pin / npin: core ids for the workers (reference --pin semantics,
+// workers.cpp:26-39: worker w is bound to pin[w]); npin = 0 leaves them
+// unpinned.
 int ref_create(const char* name, int kind, int nx, int ny, int nz, int block,
                int spacing, int pipe_diameter, int blk, int pad_mode,
                const std::int64_t* pads, int threads, int vector_width,
-               void** out) {
+               const int* pin, int npin, void** out) {
   return guard([&] {
     auto h = std::make_unique<Handle>();
     h->ff = make_flags(kind, nx, ny, nz, block, spacing, pipe_diameter);
-    h->pool = std::make_unique<lbm::WorkerPool>(threads);
+    h->pool = std::make_unique<lbm::WorkerPool>(
+        threads, npin > 0 ? std::vector<int>(pin, pin + npin) : std::vector<int>{});
     h->kernel = lbm::make_kernel(lbm::make_descriptor(name, blk, vector_width),
                                  h->ff, make_padding(pad_mode, pads),
                                  *h->pool);
@@ -134,6 +138,15 @@ int ref_create(const char* name, int kind, int nx, int ny, int nz, int block,
 }
 
 void ref_destroy(void* h) { delete static_cast<Handle*>(h); }
+
+// number of workers whose core binding was applied
+int ref_pinned(void* h, int* out) {
+  return guard([&] {
+    int n = 0;
+    for (const auto& a : static_cast<Handle*>(h)->pool->affinity()) n += a.applied ? 1 : 0;
+    *out = n;
+  });
+}
 
 int ref_n_fluid(void* h, std::uint64_t* out) {
   return guard([&] { *out = static_cast<Handle*>(h)->kernel->n_fluid(); });

@@ -366,6 +366,7 @@ int lbmgpu_advance(lbmgpu_ctx* c, double wp, double lambda, const double* g,
     if (steps == 0) return;
     c->eng->advance(t, steps);
     LBM_CUDA(cudaStreamSynchronize(c->eng->stream()));
+    c->eng->check_health();
   });
 }
 
@@ -386,6 +387,7 @@ int lbmgpu_time_advance(lbmgpu_ctx* c, double wp, double lambda,
     LBM_CUDA(cudaEventElapsedTime(&f, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    c->eng->check_health();
     *ms = f;
   });
 }
@@ -406,6 +408,7 @@ int lbmgpu_snapshot(lbmgpu_ctx* c, double* host, uint64_t count) {
       throw ConfigError("snapshot: buffer holds " + std::to_string(count) +
                         " values, lattice has " + std::to_string(N * kQ));
     need(host, "host buffer");
+    c->eng->check_health();
     pipelined(c, host, N, true, [&](uint64_t c0, uint64_t n, double* st, bool) {
       c->eng->gather_canonical(c0, n, st);
     });
@@ -457,6 +460,7 @@ static void local_transfer(lbmgpu_ctx* c, double* host, uint64_t count,
 int lbmgpu_snapshot_local(lbmgpu_ctx* c, double* host, uint64_t count) {
   return guard([&] {
     need(c, "ctx");
+    c->eng->check_health();
     local_transfer(c, host, count, true);
   });
 }
@@ -480,6 +484,7 @@ int lbmgpu_total_mass(lbmgpu_ctx* c, double* out) {
   return guard([&] {
     need(c, "ctx");
     need(out, "out");
+    c->eng->check_health();
     *out = c->eng->total_mass();
   });
 }
@@ -491,6 +496,7 @@ int lbmgpu_fingerprint(lbmgpu_ctx* c, uint64_t* out) {
     if (!c->eng->holds_all())
       throw ConfigError("fingerprint: the state is split across processes; "
                         "gather the local rows (lbmgpu_snapshot_local) first");
+    c->eng->check_health();
     const uint64_t N = c->eng->n_fluid();
     const uint64_t chunk = std::min(N, kChunkNodes);
     cudaStream_t s = c->eng->stream();

@@ -929,6 +929,8 @@ class DirectEngine final : public Engine {
                            cudaHostAllocMapped));
     *peer_err_ = 0;
     LBM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&peer_err_dev_), peer_err_, 0));
+    peer_abort_.alloc(1);
+    LBM_CUDA(cudaMemsetAsync(peer_abort_.get(), 0, sizeof(int), stream_));
     for (Part& pt : parts_) {
       pt.pflag.alloc(4);
       LBM_CUDA(cudaMemsetAsync(pt.pflag.get(), 0, 4 * sizeof(unsigned long long), stream_));
@@ -1058,7 +1060,18 @@ class DirectEngine final : public Engine {
     if (!peer_ready_)
       throw ConfigError("peer transport: lbmgpu_peer_attach has not been called");
     if (*static_cast<volatile int*>(peer_err_))
-      throw DeviceError("peer transport: a neighbour's sub-step signal timed out");
+      throw DeviceError("peer transport: a neighbour's sub-step signal timed out (ranks must "
+                        "call advance collectively within LBMGPU_PEER_TIMEOUT_MS); the slab "
+                        "state is no longer consistent");
+  }
+
+  // After the stream work of a host call: a wait that timed out inside it
+  // is reported by that call (and by every later one).
+  void check_health() override {
+    if (!peer_) return;
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    if (bstream_) LBM_CUDA(cudaStreamSynchronize(bstream_));
+    peer_check();
   }
 
   void peer_signal(int kind, unsigned long long e) {
@@ -1078,7 +1091,7 @@ class DirectEngine final : public Engine {
       const int tok = stats_.begin("peer_wait", stream_);
       k_peer_wait<<<1, 32, 0, stream_>>>(L.lo_flags ? own + 2 * kind : nullptr,
                                          L.hi_flags ? own + 2 * kind + 1 : nullptr, e,
-                                         peer_err_dev_, peer_timeout_ns_);
+                                         peer_err_dev_, peer_abort_.get(), peer_timeout_ns_);
       LBM_CHECK_LAUNCH();
       stats_.end(tok, stream_);
     }
@@ -1129,7 +1142,7 @@ class DirectEngine final : public Engine {
             aa_sub(false, a, "full_aa_even_soa_halo");
           } else {
             const PeerLink& L = links_[i];
-            const PeerArgs pa{L.lo[0], L.hi[0], L.lo_plane, L.hi_plane};
+            const PeerArgs pa{L.lo[0], L.hi[0], L.lo_plane, L.hi_plane, peer_abort_.get()};
             const int tok = stats_.begin("full_aa_odd_soa_peer", stream_);
             k_full_aa_odd_peer<<<static_cast<unsigned>(ceil_div(cnt, 128)), 128, 0, stream_>>>(
                 a, pa);
@@ -1233,7 +1246,7 @@ class DirectEngine final : public Engine {
         const DirectArgs a = args(pt, n0, cnt, t, src, dst);
         const PeerLink& L = links_[i];
         const int g = push ? dst : src;  // the neighbour grid the boundary touches
-        const PeerArgs pa{L.lo[g], L.hi[g], L.lo_plane, L.hi_plane};
+        const PeerArgs pa{L.lo[g], L.hi[g], L.lo_plane, L.hi_plane, peer_abort_.get()};
         const unsigned grid = static_cast<unsigned>(ceil_div(cnt, 256));
         const int tok = stats_.begin(push ? "full_push_soa_peer"
                                      : collide ? "full_pull_soa_peer"
@@ -1413,6 +1426,7 @@ class DirectEngine final : public Engine {
   std::vector<PeerLink> links_;         // per local part
   int* peer_err_ = nullptr;             // host-mapped wait-timeout flag
   int* peer_err_dev_ = nullptr;
+  DevBuf<int> peer_abort_;              // device copy of the timeout flag (PeerArgs::abort)
   std::vector<void*> ipc_open_;         // CUDA IPC mappings to close
   cudaStream_t bstream_ = nullptr;      // peer AA path: boundary stream (aa_pair_peer)
   cudaEvent_t pev_[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -23,7 +23,15 @@ struct PeerArgs {
   double* hi;         // upper neighbour's lattice (grid); null = own storage plane z+1
   uint32_t lo_plane;  // lower neighbour's storage plane of global z0 - 1
   uint32_t hi_plane;  // upper neighbour's storage plane of global z1
+  // device word set by k_peer_wait on a timeout: every later boundary sweep
+  // returns before touching the neighbour's memory (a late but healthy
+  // neighbour is never written out of turn)
+  const int* abort;
 };
+
+__device__ __forceinline__ bool peer_aborted(const PeerArgs& pa) {
+  return *static_cast<const volatile int*>(pa.abort) != 0;
+}
 
 // AA odd sub-step (kernels_full_aa.cpp:83-92, same expression as
 // aa_odd_node) over boundary planes whose out-of-slab neighbours live in
@@ -37,6 +45,7 @@ struct PeerArgs {
 __global__ void __launch_bounds__(128) k_full_aa_odd_peer(const DirectArgs a, const PeerArgs pa) {
   Coords c;
   uint32_t n;
+  if (peer_aborted(pa)) return;
   if (decode(a, c, n) && !solid_node(a, c.x, c.y, c.z, n)) {
     const Idx<true> I{a.P, a.nx, a.ny};
     double* zb[3] = {a.dst, a.dst, a.dst};
@@ -90,7 +99,7 @@ template <bool COLLIDE>
 __global__ void __launch_bounds__(256) k_full_pull_peer(const DirectArgs a, const PeerArgs pa) {
   Coords c;
   uint32_t n;
-  if (!decode(a, c, n)) return;
+  if (peer_aborted(pa) || !decode(a, c, n)) return;
   const Idx<true> I{a.P, a.nx, a.ny};
   const double* zb[3] = {a.src, a.src, a.src};
   uint32_t zp[3] = {c.Z[0], c.Z[1], c.Z[2]};
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(256) k_full_pull_peer(const DirectArgs a, cons
 __global__ void __launch_bounds__(256) k_full_push_peer(const DirectArgs a, const PeerArgs pa) {
   Coords c;
   uint32_t n;
-  if (!decode(a, c, n)) return;
+  if (peer_aborted(pa) || !decode(a, c, n)) return;
   const Idx<true> I{a.P, a.nx, a.ny};
   const uint32_t tm = a.tmask[n];  // always built for several parts
   double q[kQ];
@@ -171,17 +180,22 @@ __device__ __forceinline__ unsigned long long global_ns() {
 
 // Wait until the own flags f0 / f1 (null = skip) reach `epoch`.  Bounded:
 // after timeout_ns the kernel records the failure in *err (host-mapped) and
-// returns, so a dead neighbour cannot hang the device; the engine raises
-// the error at its next host call.
+// in *abort (device), and returns, so a dead neighbour cannot hang the
+// device; the boundary sweeps behind it skip their peer accesses (abort)
+// and the engine raises the error after the stream sync of the same
+// advance() call and at every later host call (check_health).
 __global__ void k_peer_wait(const unsigned long long* f0, const unsigned long long* f1,
-                            unsigned long long epoch, int* err, unsigned long long timeout_ns) {
+                            unsigned long long epoch, int* err, int* abort,
+                            unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
+  if (*static_cast<volatile int*>(abort)) return;  // already failed: no more waiting
   const unsigned long long t0 = global_ns();
   const unsigned long long* fs[2] = {f0, f1};
   for (int i = 0; i < 2; ++i) {
     if (!fs[i]) continue;
     while (ld_acquire_sys(fs[i]) < epoch) {
       if (global_ns() - t0 > timeout_ns) {
+        atomicExch(abort, 1);
         atomicExch_system(err, 1);
         return;
       }

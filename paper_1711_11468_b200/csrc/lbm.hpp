@@ -205,6 +205,10 @@ class Engine {
   // steps already validated (>= 0, even for AA).
   virtual void advance(const TrtArgs& t, long steps) = 0;
 
+  // Throws if the engine's stream work failed in a way only the device can
+  // see (peer transport: a neighbour's signal timed out).  Synchronises.
+  virtual void check_health() {}
+
   // Canonical nodes [c0, c0+count) -> device staging (count*19 doubles,
   // node-major) and back.  Runs on stream().
   virtual void gather_canonical(uint64_t c0, uint64_t count, double* d_out) = 0;

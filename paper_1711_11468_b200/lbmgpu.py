@@ -411,6 +411,18 @@ class KernelCaps:
     huge_pages_advised: bool = False
 
 
+def _check_out(out, n, what):
+    """The C ABI writes `n` doubles at out's data pointer: anything but a
+    C-contiguous float64 array of exactly n elements would be scribbled over
+    or overrun."""
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64:
+        raise ValueError(f"{what}: out must be a float64 numpy array")
+    if not out.flags.c_contiguous:
+        raise ValueError(f"{what}: out must be C-contiguous")
+    if out.size != n:
+        raise ValueError(f"{what}: out holds {out.size} values, expected {n}")
+
+
 class Kernel:
     """A GPU-resident lattice + sweep, the reference's lbm::Kernel
     (kernels.hpp:58-96).  Create with make_kernel()."""
@@ -475,9 +487,11 @@ class Kernel:
         return ms.value
 
     def snapshot(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        """Canonical N*19 PDFs, fluid nodes in x,y,z order."""
+        """Canonical N*19 PDFs, fluid nodes in x,y,z order.  `out`, if given,
+        must be a C-contiguous float64 array of N*19 elements."""
         if out is None:
             out = np.empty(self._n * Q, np.float64)
+        _check_out(out, self._n * Q, "snapshot")
         _check(lib.lbmgpu_snapshot(self._h, out.ctypes.data, out.size))
         return out
 
@@ -502,6 +516,7 @@ class Kernel:
     def snapshot_local(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.local_state_size(), np.float64)
+        _check_out(out, self.local_state_size(), "snapshot_local")
         _check(lib.lbmgpu_snapshot_local(self._h, out.ctypes.data, out.size))
         return out
 

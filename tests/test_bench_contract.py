@@ -34,3 +34,41 @@ def test_reference_arm_nonzero_rank_is_silent():
                         "--steps", "1", "--warmup", "0"],
                        capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_gpus_more_than_visible_fails_loudly():
+    """`bench.py --gpus 2` outside torchrun with fewer visible GPUs exits
+    non-zero and prints no bench line (never a silent n_gpus: 1)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0
+    assert r.stdout.strip() == ""
+    assert "--gpus 2" in r.stderr
+
+
+def test_world_mismatch_fails_loudly():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4",
+                        "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2 and r.stdout.strip() == ""
+    assert "WORLD_SIZE=1" in r.stderr
+
+
+def test_gpus_relaunches_under_torchrun():
+    """The re-exec path: `bench.py --gpus 2` (no WORLD_SIZE) runs itself
+    under torch.distributed.run with 2 ranks; rank 0 prints the only line and
+    n_gpus equals the launched world (the launch-check hook does no GPU work,
+    so this runs on CPU with gloo)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--launch-check"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and sorted(line["ranks"]) == [0, 1]

@@ -802,3 +802,19 @@ def test_randomized_against_oracle(case, port, monkeypatch):
     k.advance(params, lbm.BodyForce(g), steps)
     got = k.snapshot()
     assert np.array_equal(got, expect), (name, kind, (nx, ny, nz), blk, tau, steps)
+
+
+def test_snapshot_out_buffer_validation():
+    """snapshot(out=...) / snapshot_local(out=...) write N*19 doubles at the
+    array's data pointer: float32, strided or wrongly sized arrays are
+    rejected before the C ABI is called."""
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("blocks", 12, 10, 10))
+    n = k.n_fluid() * 19
+    for bad in (np.empty(n, np.float32), np.empty(2 * n)[::2], np.empty(n - 1),
+                np.empty(n + 19), np.empty(n, np.int64)):
+        with pytest.raises(ValueError):
+            k.snapshot(out=bad)
+        with pytest.raises(ValueError):
+            k.snapshot_local(out=bad)
+    good = np.empty(n)
+    assert k.snapshot(out=good) is good and np.array_equal(good, k.snapshot())
