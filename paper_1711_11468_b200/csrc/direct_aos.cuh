@@ -141,15 +141,39 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(con
   }
 }
 
-// AoS AA odd step with the gathers through the same 3-D halo tiles: the
-// tile's source rows arrive by TMA as whole records, each node reads its 18
-// neighbour values (x - c_d, opp d) in shared memory, and writes them back to
-// global memory slot by slot (every slot is read and written by exactly one
-// node in this sub-step, so the other, possibly stale, slots of the staged
-// records are never used).
+// c_x + 1 (resp. c_y + 1, c_z + 1) of the direction stored in slot s, as
+// 2-bit fields of one constant: a register shift per element instead of a
+// table lookup with a lane-dependent index.
+template <int AXIS>
+__host__ __device__ constexpr uint64_t slot_c_bits() {
+  uint64_t m = 0;
+  for (int s = 0; s < kQ; ++s) {
+    const int d = ddir(s);
+    const int c = AXIS == 0 ? cx(d) : AXIS == 1 ? cy(d) : cz(d);
+    m |= uint64_t(c + 1) << (2 * s);
+  }
+  return m;
+}
+
+// AoS AA odd step through the same 3-D halo tiles, both ways.  The tile's
+// source rows arrive by TMA as whole records; each node reads its 19 values
+// (x - c_d, opp d) in shared memory and collides.  The slot a node gathers
+// direction d from is the one it scatters opp(d) to (kernels_full_aa.cpp:
+// 83-92), and slot s of record r is read and written in this sub-step only
+// by node r - c_s (s = 0: r itself).  Results whose record lies in one of
+// the tile's own (y, z) rows go back into the shared-memory copy; those
+// rows then leave by coalesced 8-byte stores of exactly the slots whose
+// owner lies in the tile (no slot has two writers; solid owners store
+// their unchanged value; slots owned by other CTAs are neither used nor
+// written).  Results for records in the y / z halo rows -- a minority,
+// from the tile's face nodes -- are stored straight to global memory.  The
+// own rows thus leave as full 32-byte sectors instead of one sector per
+// scattered 8-byte element.
 template <int kPtY, int kPtZ>
 __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(const DirectArgs a) {
   constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
+  constexpr int kT = kPtX * kPtY * kPtZ;
+  constexpr int kRowElems = kPtW * kQ;  // 380 doubles per halo row
   extern __shared__ __align__(128) unsigned char pt_smem[];
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
@@ -162,23 +186,86 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(c
   pt_load_halo<kPtY, kPtZ>(a, a.dst, sh, bar, x0, y0, z0);
   const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
   const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
-  Coords c;
-  decode_node(a, n, c);
-  const bool solid = solid_node(a, c.x, c.y, c.z, n);
+  const bool solid = solid_node(a, x0 + tx, y0 + ty, z0 + tz, n);
   tma::mbar_wait(bar, 0);
-  if (solid) return;
   auto at = [&](int hx, int hy, int hz) {
     return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
   };
-  double q[kQ];
+  if (!solid) {
+    double q[kQ];
 #pragma unroll
-  for (int d = 0; d < kQ; ++d)
-    q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(opp(d))];
-  collide(q, a.trt);
-  const Idx<false> I{a.P, a.nx, a.ny};
+    for (int d = 0; d < kQ; ++d)
+      q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(opp(d))];
+    collide(q, a.trt);
+    const Idx<false> I{a.P, a.nx, a.ny};
+    Coords c;
+    decode_node(a, n, c);
 #pragma unroll
-  for (int d = 0; d < kQ; ++d)
-    a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])] = q[opp(d)];
+    for (int d = 0; d < kQ; ++d) {
+      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+      if (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ)
+        at(int(tx) + 2 - cx(d), hy, hz)[dslot(opp(d))] = q[opp(d)];
+      else
+        a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])] = q[opp(d)];
+    }
+  }
+  __syncthreads();
+  // owned-slot write-back of the tile's own rows, one warp per row: lane l
+  // handles elements i = l + 32 j (j < 12) of the row, slot i % 19 of record
+  // i / 19 (records x0-2 .. x0+17).  Which of them the tile owns depends on
+  // the row only through its first / last y and z position, so the lane's
+  // masks are built once: bit j of kx = owner inside the tile in x, of
+  // ypos / yneg / zpos / zneg = the slot's direction has c = +1 / -1.
+  constexpr int kJ = (kRowElems + 31) / 32;
+  constexpr uint64_t kX = slot_c_bits<0>(), kY = slot_c_bits<1>(), kZ = slot_c_bits<2>();
+  const uint32_t lane = t & 31, warp = t >> 5;
+  uint32_t mx = 0, ypos = 0, yneg = 0, zpos = 0, zneg = 0;
+#pragma unroll
+  for (int jj = 0; jj < kJ; ++jj) {
+    const int i = static_cast<int>(lane) + 32 * jj;
+    if (i >= kRowElems) continue;
+    const int hx = i / kQ, s = i - hx * kQ;
+    const int ox = hx + 1 - static_cast<int>((kX >> (2 * s)) & 3u);
+    const int ey = static_cast<int>((kY >> (2 * s)) & 3u) - 1;
+    const int ez = static_cast<int>((kZ >> (2 * s)) & 3u) - 1;
+    if (ox >= 2 && ox < 2 + kPtX) mx |= 1u << jj;
+    if (ey > 0) ypos |= 1u << jj;
+    if (ey < 0) yneg |= 1u << jj;
+    if (ez > 0) zpos |= 1u << jj;
+    if (ez < 0) zneg |= 1u << jj;
+  }
+  const uint64_t nx = a.nx;
+  const bool xwrap = x0 < 2 || uint64_t(x0) + kPtX + 2 > nx;
+  for (uint32_t r = warp; r < uint32_t(kPtY * kPtZ); r += kT / 32) {
+    const int hy = 1 + static_cast<int>(r % kPtY), hz = 1 + static_cast<int>(r / kPtY);
+    // owner y = hy - c_y must stay in [1, kPtY]: the first row excludes
+    // c_y = +1, the last c_y = -1 (likewise in z)
+    uint32_t m = mx;
+    if (hy == 1) m &= ~ypos;
+    if (hy == kPtY) m &= ~yneg;
+    if (hz == 1) m &= ~zpos;
+    if (hz == kPtZ) m &= ~zneg;
+    const double* src = sh + size_t(hz * (kPtY + 2) + hy) * kRowElems;
+    const uint64_t y = y0 + hy - 1, z = z0 + hz - 1;  // own rows: no y / z wrap
+    double* row = a.dst + (z * a.ny + y) * nx * kQ;
+    if (!xwrap) {
+      double* g = row + (uint64_t(x0) - 2) * kQ;
+#pragma unroll
+      for (int jj = 0; jj < kJ; ++jj)
+        if ((m >> jj) & 1u) g[lane + 32 * jj] = src[lane + 32 * jj];
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < kJ; ++jj) {
+        if (!((m >> jj) & 1u)) continue;
+        const int i = static_cast<int>(lane) + 32 * jj;
+        const int hx = i / kQ;
+        int64_t gx = int64_t(x0) + hx - 2;
+        if (gx < 0) gx += nx;
+        if (gx >= int64_t(nx)) gx -= nx;
+        row[uint64_t(gx) * kQ + (i - hx * kQ)] = src[i];
+      }
+    }
+  }
 }
 
 }  // namespace lbmgpu

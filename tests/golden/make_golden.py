@@ -8,6 +8,7 @@ build_structure, padding_offsets.  Run in this container (the GPU box has no
     python tests/golden/make_golden.py small      # seconds
     python tests/golden/make_golden.py edge       # seconds
     python tests/golden/make_golden.py configs    # BASELINE configs 1-4, ~25 min
+    python tests/golden/make_golden.py nodes      # node-list FNVs of cfgs 2-4, ~1 min
 """
 import json
 import os
@@ -174,6 +175,27 @@ def edge(ref: Ref):
     print(len(out["cases"]), "edge cases")
 
 
+def nodes(ref: Ref):
+    """FNV-1a of the reference's node list (order_nodes, list_lattice.cpp:
+    123-141; blk = 0) for the list configs, over the int32 little-endian
+    (x, y, z) triples -- the bytes lbmgpu_export_structure returns -- added to
+    configs.json next to the adjacency FNVs."""
+    path = os.path.join(HERE, "configs.json")
+    out = json.load(open(path))
+    for cid, name, kind, dims, extra, _ in CONFIGS:
+        if not name.startswith("list-"):
+            continue
+        s = ref.structure(kind, *dims, padding="none", scatter=False,
+                          block=extra.get("block", 4), spacing=extra.get("spacing", 4),
+                          pipe_diameter=extra.get("pipe_diameter", 0))
+        nodes = np.ascontiguousarray(s["nodes"], np.int32).view(np.uint32).ravel()
+        out[str(cid)]["nodes_fnv"] = f"{ref.fingerprint_u32(nodes):016x}"
+        assert f"{ref.fingerprint_u32(s['adj']):016x}" == out[str(cid)]["adj_fnv_none_gather"]
+        print(f"cfg {cid}: nodes {out[str(cid)]['nodes_fnv']}", flush=True)
+        del s, nodes
+    json.dump(out, open(path, "w"), indent=1)
+
+
 if __name__ == "__main__":
     ref = Ref()
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
@@ -181,5 +203,7 @@ if __name__ == "__main__":
         small(ref)
     elif what == "edge":
         edge(ref)
+    elif what == "nodes":
+        nodes(ref)
     else:
         configs(ref, [int(a) for a in sys.argv[2:]])

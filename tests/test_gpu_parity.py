@@ -28,6 +28,16 @@ def spec_of(case):
                             case.get("pipe_diameter", 0))
 
 
+def oracle_state(port, name, kind, dims, steps, seed):
+    """The oracle's family stepper (full-way for direct names, half-way for
+    list names) from perturbed_equilibrium(seed): the checker the
+    decomposition tests compare against directly."""
+    _, _, nf = port.geometry(kind, *dims)
+    fam = "half" if name.startswith("list-") else "full"
+    return port.run(fam, kind, *dims, steps, PARAMS.omega_plus, g=G_TEST,
+                    init=port.perturbed(nf, seed))[0]
+
+
 def test_seventeen_names_and_registry():
     assert len(NAMES) == 17
     with pytest.raises(lbm.ConfigError) as e:
@@ -453,13 +463,13 @@ def test_capabilities():
     ("channel", (16, 12, 24), 2), ("channel", (16, 12, 24), 3), ("channel", (16, 12, 24), 4),
     ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2), ("blocks", (12, 10, 16), 4),
     ("slit", (6, 5, 9), 3), ("pipe", (9, 12, 13), 13)])
-def test_zslab_parts_bitwise_equal_single(name, kind, dims, parts):
+def test_zslab_parts_bitwise_equal_single(name, kind, dims, parts, port):
     """z-slab decomposition (the multi-GPU plan, emulated on one device):
-    fingerprint identical for 1..N parts -- the worker-count invariance of
-    tests/test_kernels.cpp:177-195 carried to the slab split.  AA: halo
-    phases 0/1; one-step push / pull: phases 2/3 with the z ring (solid
-    nodes stream too), down to one plane per slab; odd step counts leave
-    push/pull on the second grid."""
+    state bitwise the oracle's and the single-part run's for 1..N parts --
+    the worker-count invariance of tests/test_kernels.cpp:177-195 carried to
+    the slab split.  AA: halo phases 0/1; one-step push / pull: phases 2/3
+    with the z ring (solid nodes stream too), down to one plane per slab;
+    odd step counts leave push/pull on the second grid."""
     spec = lbm.GeometrySpec(kind, *dims)
     steps = (4, 6) if name.startswith("aa") else (3, 6)
     ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
@@ -471,13 +481,14 @@ def test_zslab_parts_bitwise_equal_single(name, kind, dims, parts):
     assert np.array_equal(init, lbm.perturbed_equilibrium(k.n_fluid(), 4242))
     for st in steps:
         k.advance(PARAMS, FORCE, st)
+    assert np.array_equal(k.snapshot(), oracle_state(port, name, kind, dims, sum(steps), 4242))
     assert np.array_equal(k.snapshot(), ref.snapshot()), name
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
 
 @pytest.mark.parametrize("name", ["aa-soa", "blk-push-soa", "blk-pull-soa"])
 @pytest.mark.parametrize("kind,dims,parts", [("channel", (32, 12, 24), 3), ("blocks", (16, 16, 16), 2)])
-def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
+def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts, port):
     """The NCCL halo transport (grouped ncclSend/ncclRecv on a comm stream,
     event-ordered against the compute stream) exercised on one GPU: one NCCL
     rank owning all slabs, self send/recv per plan row.  Bitwise equal to the
@@ -490,6 +501,7 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
                         dist={"virtual_parts": parts, "nccl_id": lbm.lbmgpu.nccl_unique_id()})
     k.load_perturbed(31)
     k.advance(PARAMS, FORCE, 8)
+    assert np.array_equal(k.snapshot(), oracle_state(port, name, kind, dims, 8, 31))
     assert np.array_equal(k.snapshot(), ref.snapshot())
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
 
@@ -499,7 +511,7 @@ def test_zslab_nccl_transport_single_gpu(name, kind, dims, parts):
     ("channel", (16, 12, 24), 2), ("channel", (33, 10, 17), 5), ("blocks", (12, 10, 16), 2),
     ("blocks", (12, 10, 16), 4), ("slit", (6, 5, 9), 3), ("pipe", (9, 12, 13), 13),
     ("blocks", (16, 16, 16), 16)])
-def test_zslab_peer_transport_bitwise_equal_single(name, kind, dims, parts):
+def test_zslab_peer_transport_bitwise_equal_single(name, kind, dims, parts, port):
     """Peer-memory transport (direct_peer.cuh): no halo copy at all -- the
     AA boundary planes' odd sub-step loads and stores the neighbour slab's
     slots, the pull's boundary gathers read the neighbour's source grid,
@@ -524,6 +536,7 @@ def test_zslab_peer_transport_bitwise_equal_single(name, kind, dims, parts):
     k.kernel_stats_enable(True)
     for st in steps:
         k.advance(PARAMS, FORCE, st)
+    assert np.array_equal(k.snapshot(), oracle_state(port, name, kind, dims, sum(steps), 777))
     assert np.array_equal(k.snapshot(), ref.snapshot()), name
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
     names = set(k.kernel_stats())
@@ -548,13 +561,15 @@ def test_zslab_peer_transport_errors():
 
 @pytest.mark.parametrize("name", ["list-aa-soa", "list-aa-aos"])
 @pytest.mark.parametrize("kind,dims,parts", [
-    ("channel", (20, 12, 10), 2), ("channel", (20, 12, 10), 3), ("blocks", (16, 16, 16), 2),
-    ("blocks", (16, 16, 16), 5), ("pipe", (12, 14, 13), 4)])
-def test_list_node_range_parts_bitwise(name, kind, dims, parts):
-    """List AA decomposed into contiguous node ranges (x-slabs for blk = 0)
-    with index-list halos, emulated on one GPU: bitwise
-    equal to the single-part run, including the periodic wrap between the
-    last and the first part (blocks)."""
+    ("channel", (20, 12, 10), 2), ("channel", (20, 12, 10), 3), ("channel", (20, 12, 10), 4),
+    ("blocks", (16, 16, 16), 2), ("blocks", (16, 16, 16), 5), ("pipe", (12, 14, 13), 4),
+    ("blocks", (12, 10, 10), 3)])
+def test_list_node_range_parts_bitwise(name, kind, dims, parts, port):
+    """List AA decomposed into contiguous node ranges (x-slabs for blk = 0,
+    the split of reference kernels_list_aa.cpp:63-74) with index-list halos
+    (SURVEY 8(f) row 2), emulated on one GPU: bitwise equal to the oracle's
+    half-way stepper and to the single-part run, including the periodic
+    wrap between the last and the first part (blocks)."""
     spec = lbm.GeometrySpec(kind, *dims)
     ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
     ref.load_perturbed(17)
@@ -563,6 +578,7 @@ def test_list_node_range_parts_bitwise(name, kind, dims, parts):
     k.load_perturbed(17)
     k.advance(PARAMS, FORCE, 4)
     k.advance(PARAMS, FORCE, 4)
+    assert np.array_equal(k.snapshot(), oracle_state(port, name, kind, dims, 8, 17))
     assert np.array_equal(k.snapshot(), ref.snapshot())
     assert abs(k.total_mass() - ref.total_mass()) <= 1e-12 * ref.total_mass()
     # macro fields and the fingerprint go through the per-part local arrays
@@ -572,7 +588,7 @@ def test_list_node_range_parts_bitwise(name, kind, dims, parts):
         k.export_structure()
 
 
-def test_list_parts_nccl_transport_single_gpu():
+def test_list_parts_nccl_transport_single_gpu(port):
     """The list halo over NCCL (pack -> grouped send/recv -> unpack on the comm
     stream), one NCCL rank owning every part (self send/recv)."""
     spec = lbm.GeometrySpec("blocks", 16, 16, 16)
@@ -583,6 +599,8 @@ def test_list_parts_nccl_transport_single_gpu():
                         dist={"virtual_parts": 3, "nccl_id": lbm.lbmgpu.nccl_unique_id()})
     k.load_perturbed(23)
     k.advance(PARAMS, FORCE, 6)
+    assert np.array_equal(k.snapshot(), oracle_state(port, "list-aa-soa", "blocks", (16, 16, 16),
+                                                     6, 23))
     assert np.array_equal(k.snapshot(), ref.snapshot())
 
 
@@ -648,6 +666,36 @@ def test_baseline_config_fingerprint(cid):
     k.advance(lbm.TrtParams(1.0, 3.0 / 16.0), lbm.BodyForce(tuple(c["g"])), c["steps"])
     assert f"{k.fingerprint():016x}" == c["fingerprint"]
     assert abs(k.total_mass() - c["mass1"]) <= 1e-12 * c["mass1"]
+
+
+@pytest.mark.parametrize("cid", ["2", "3", "4"])
+def test_baseline_config_structure_bitwise(cid, port):
+    """north_star: node lists and adjacency bit-exact at full size.  For the
+    list configs the device-built structure is exported (canonical order:
+    nodes as int32 (x, y, z), adjacency adj[n*18 + d-1] as u32) and its
+    FNV-1a must equal the reference's build_structure (list_lattice.cpp:
+    149-204; goldens from tests/golden/make_golden.py) for both orientations
+    (Gather: list-pull-soa, Scatter: list-aa-soa) and both paddings (auto,
+    none), together with the 19 start offsets and the slot total."""
+    if not os.path.exists(CONFIGS):
+        pytest.skip("configs.json not generated")
+    gold = json.load(open(CONFIGS))
+    c = gold[cid]
+    spec = lbm.GeometrySpec(c["kind"], *c["dims"], c.get("block", 4), c.get("spacing", 4),
+                            c.get("pipe_diameter", 0))
+    for pad, policy in (("auto", lbm.PaddingPolicy.automatic()), ("none", lbm.PaddingPolicy.none())):
+        for orient, name in (("gather", "list-pull-soa"), ("scatter", "list-aa-soa")):
+            k = lbm.make_kernel(lbm.make_descriptor(name), spec, policy)
+            nodes, adj, starts, total = k.export_structure()
+            k.close()
+            del k
+            assert [int(v) for v in starts] == c[f"starts_{pad}"], (pad, orient)
+            assert total == c[f"total_slots_{pad}"], (pad, orient)
+            assert f"{port.fingerprint(adj):016x}" == c[f"adj_fnv_{pad}_{orient}"], (pad, orient)
+            if pad == "auto" and orient == "gather":
+                nv = np.ascontiguousarray(nodes, np.int32).view(np.uint32).ravel()
+                assert f"{port.fingerprint(nv):016x}" == c["nodes_fnv"]
+            del nodes, adj
 
 
 @pytest.mark.parametrize("cid,variant", [("2", "ria"), ("4", "ria"), ("5", "peer8"),
