@@ -114,20 +114,42 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def csrc_sha16():
+    """Content hash of the CUDA/C++ sources (paper_1711_11468_b200/csrc):
+    what a committed ncu capture was taken of.  Content, not git, because the
+    GPU box receives the tree without .git."""
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_1711_11468_b200", "csrc")
+    for name in sorted(os.listdir(d)):
+        if name.endswith((".cu", ".cuh", ".cpp", ".hpp", ".h")):
+            h.update(name.encode())
+            with open(os.path.join(d, name), "rb") as f:
+                h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic(kernel_name, cid=5, dims=None):
-    """dram bytes per launch for `kernel_name` on BASELINE config `cid` from
-    the committed ncu summary (profiles/ncu_summary.json: cfg 5 under
-    "kernels", the list configs under "configs"); None for other boxes."""
+    """(dram bytes per launch, note) for `kernel_name` on BASELINE config
+    `cid` from the committed ncu summary (profiles/ncu_summary.json: cfg 5
+    under "kernels", the list configs under "configs").  None when the
+    summary was captured from other kernel sources than these (its
+    csrc_sha16 differs) or for other boxes."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if dims is not None:
-        return None
+        return None, "box differs from the captured one"
     try:
         with open(p) as f:
             d = json.load(f)
-        table = d.get("kernels", {}) if cid == 5 else d.get("configs", {}).get(str(cid), {})
-        return table.get(kernel_name, {}).get("dram_bytes_per_launch")
     except Exception:
-        return None
+        return None, "no profiles/ncu_summary.json"
+    if d.get("csrc_sha16") != csrc_sha16():
+        return None, (f"stale: ncu summary of csrc {d.get('csrc_sha16')}, "
+                      f"running csrc {csrc_sha16()}")
+    table = d.get("kernels", {}) if cid == 5 else d.get("configs", {}).get(str(cid), {})
+    v = table.get(kernel_name, {}).get("dram_bytes_per_launch")
+    return v, (f"ncu dram__bytes_read+write per launch, {d.get('source', '')}" if v is not None
+               else "kernel not in the ncu summary")
 
 
 # --------------------------------------------------------------- CPU legs
@@ -518,6 +540,11 @@ def main():
     launches = k.launch_count() - launches0
     k.kernel_stats_enable(False)
     stats = k.kernel_stats()
+    overlap = None
+    if dspec is not None:
+        # decomposed paths: how much of the boundary-stream work (boundary
+        # sweeps, halo exchanges / peer waits) ran beside interior sweeps
+        overlap = lbm.lbmgpu.stream_overlap(k.kernel_timeline())
     clk = clocks.stop()
     clk_ranks = [clk]
     if dist is not None:
@@ -572,9 +599,11 @@ def main():
         if roof is None:
             # the committed ncu numbers are whole-box launches on one GPU
             whole = world == 1 and args.virtual_parts <= 1
-            traffic = ncu_traffic(name, cid, args.dims) if whole else None
+            traffic, tnote = (ncu_traffic(name, cid, args.dims) if whole
+                              else (None, "decomposed run: no whole-box capture"))
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": traffic, "kernel": name,
+                    "frac": ach / hbm, "traffic": traffic, "traffic_source": tnote,
+                    "kernel": name,
                     "alg_bytes_per_launch": alg, "peak_source": peak_src,
                     "bytes_per_node": per_node}
 
@@ -626,6 +655,8 @@ def main():
         "step_roofline_frac": step_gbps / hbm,
         "gpu_bytes_per_flup": gpu_b,
     })
+    if overlap is not None:
+        line["overlap"] = overlap
     if world > 1:
         line["clocks_per_rank"] = clk_ranks
         line["config"]["transport"] = args.transport if not replicas else None

@@ -225,6 +225,11 @@ int lbmgpu_kernel_stats_enable(lbmgpu_ctx* ctx, int enable);
  * launch counts, total ms.  *n gets the number of distinct kernels. */
 int lbmgpu_kernel_stats(lbmgpu_ctx* ctx, char* names48, long* launches,
                         double* total_ms, int cap, int* n);
+/* Per-launch device intervals of the launches recorded while kernel stats
+ * were on (ms after the first of them; every stream shares the clock), in
+ * record order; at most 65,536 are kept per period.  *n = total. */
+int lbmgpu_kernel_timeline(lbmgpu_ctx* ctx, char* names48, double* t0, double* t1, int cap,
+                           int* n);
 int lbmgpu_kernel_stats_reset(lbmgpu_ctx* ctx);
 /* Device sweep launches issued since creation (all streams). */
 int lbmgpu_launch_count(lbmgpu_ctx* ctx, long* out);
@@ -238,6 +243,12 @@ int lbmgpu_host_free(void* p);
  * stream). */
 int lbmgpu_microbench(const char* kind, uint64_t working_set_bytes, int reps,
                       double* gbps);
+/* Accounting of one pass of that micro-benchmark (host only, no device):
+ * elements per stream, bytes this library counts (16 B per element and
+ * stream) and bytes the reference counts for the same pass
+ * (microbench.cpp:92-99: copy / copy-19 add 8 B write allocate). */
+int lbmgpu_microbench_accounting(const char* kind, uint64_t working_set_bytes,
+                                 uint64_t* elems, uint64_t* bytes_gpu, uint64_t* bytes_ref);
 /* Device properties for reports. */
 int lbmgpu_device_info(int device, char* name64, int* sm_count,
                        size_t* total_mem, int* l2_bytes);

@@ -188,6 +188,9 @@ class Ref:
                                                                  C.c_void_p, C.c_int,
                                                                  C.POINTER(C.c_void_p)]
         L.ref_pinned.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
+        L.ref_microbench.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.ref_llc_bytes.restype = C.c_uint64
         L.ref_destroy.argtypes = [C.c_void_p]
         L.ref_n_fluid.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.ref_load_state.argtypes = [C.c_void_p, _dp, C.c_uint64]
@@ -217,6 +220,17 @@ class Ref:
     def _chk(self, rc):
         if rc:
             raise RefError(rc, self.L.ref_last_error().decode())
+
+    def microbench(self, kind, working_set, workers=2):
+        """(bytes accounted per pass, passes, GB/s) of one short repetition
+        of the reference's run_microbench."""
+        b, p, g = C.c_uint64(), C.c_int(), C.c_double()
+        self._chk(self.L.ref_microbench(kind.encode(), working_set, workers, C.byref(b),
+                                        C.byref(p), C.byref(g)))
+        return b.value, p.value, g.value
+
+    def llc_bytes(self):
+        return int(self.L.ref_llc_bytes())
 
     def kernel_names(self):
         buf = C.create_string_buffer(4096)

@@ -22,6 +22,7 @@
 #include "lbm/geometry.hpp"
 #include "lbm/harness.hpp"
 #include "lbm/kernels.hpp"
+#include "lbm/microbench.hpp"
 #include "lbm/list_lattice.hpp"
 #include "lbm/perfmodel.hpp"
 #include "lbm/verification.hpp"
@@ -138,6 +139,25 @@ int ref_create(const char* name, int kind, int nx, int ny, int nz, int block,
 }
 
 void ref_destroy(void* h) { delete static_cast<Handle*>(h); }
+
+// One repetition of the reference's run_microbench (microbench.cpp:57-175)
+// with the shortest protocol: bytes accounted per pass and passes, for the
+// accounting check against lbmgpu_microbench_accounting.
+int ref_microbench(const char* kind, std::uint64_t working_set, int workers,
+                   std::uint64_t* bytes_per_pass, int* passes, double* gbps) {
+  return guard([&] {
+    lbm::MicrobenchProtocol proto;
+    proto.min_seconds = 0.0;
+    proto.repetitions = 1;
+    const lbm::BandwidthMeasurement m =
+        lbm::run_microbench(lbm::micro_kind_from_string(kind), working_set, workers, proto);
+    *bytes_per_pass = m.passes ? m.bytes_accounted / m.passes : 0;
+    *passes = m.passes;
+    *gbps = m.gbps;
+  });
+}
+
+std::uint64_t ref_llc_bytes(void) { return lbm::detect_llc_bytes(); }
 
 // number of workers whose core binding was applied
 int ref_pinned(void* h, int* out) {

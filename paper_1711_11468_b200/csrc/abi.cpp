@@ -748,6 +748,25 @@ int lbmgpu_kernel_stats(lbmgpu_ctx* c, char* names48, long* launches,
   });
 }
 
+int lbmgpu_kernel_timeline(lbmgpu_ctx* c, char* names48, double* t0, double* t1, int cap,
+                           int* n) {
+  return guard([&] {
+    need(c, "ctx");
+    KernelStats& st = c->eng->stats();
+    const auto& spans = st.timeline();
+    const auto& rows = st.rows();
+    if (n) *n = static_cast<int>(spans.size());
+    for (int i = 0; i < cap && i < static_cast<int>(spans.size()); ++i) {
+      if (names48) {
+        std::strncpy(names48 + 48 * i, rows[spans[i].row].name.c_str(), 47);
+        names48[48 * i + 47] = 0;
+      }
+      if (t0) t0[i] = spans[i].t0;
+      if (t1) t1[i] = spans[i].t1;
+    }
+  });
+}
+
 int lbmgpu_kernel_stats_reset(lbmgpu_ctx* c) {
   return guard([&] {
     need(c, "ctx");
@@ -772,6 +791,17 @@ int lbmgpu_host_alloc(size_t bytes, void** out) {
 
 int lbmgpu_host_free(void* p) {
   return guard([&] { LBM_CUDA(cudaFreeHost(p)); });
+}
+
+int lbmgpu_microbench_accounting(const char* kind, uint64_t working_set_bytes,
+                                 uint64_t* elems, uint64_t* bytes_gpu, uint64_t* bytes_ref) {
+  return guard([&] {
+    need(kind, "kind");
+    const MicroPlan m = micro_plan(kind, working_set_bytes);
+    if (elems) *elems = m.n;
+    if (bytes_gpu) *bytes_gpu = m.bytes_gpu;
+    if (bytes_ref) *bytes_ref = m.bytes_ref;
+  });
 }
 
 int lbmgpu_microbench(const char* kind, uint64_t bytes, int reps, double* gbps) {

@@ -315,6 +315,7 @@ class DirectEngine final : public Engine {
   DirectEngine(const Descriptor& d, const GeomSpec& g, const DistSpec& dist) {
     desc_ = d;
     LBM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    nvtxNameCudaStreamA(stream_, "lbmgpu interior");
     rank_ = dist.rank;
     nranks_ = dist.nranks;
     nparts_ = nranks_ > 1 ? nranks_ : std::max(1, dist.virtual_parts);
@@ -506,6 +507,19 @@ class DirectEngine final : public Engine {
   }
 
   template <int TY, int TZ>
+  void aa_odd_aos_tile3d(const DirectArgs& a) {
+    const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
+    auto kern = k_full_aa_odd_aos_tile3d<TY, TZ>;
+    constexpr size_t smem = pt_smem<TY, TZ>();
+    LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    const int tok = stats_.begin("full_aa_odd_aos", stream_);
+    kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(a);
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, stream_);
+  }
+
+  template <int TY, int TZ>
   void pull_aos_tile3d(const DirectArgs& a, bool last, const char* name) {
     const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
     auto kern = last ? k_full_pull_aos_tile3d<false, TY, TZ> : k_full_pull_aos_tile3d<true, TY, TZ>;
@@ -569,6 +583,11 @@ class DirectEngine final : public Engine {
   // 96 MiB of PDF buffers), at least two sweeps.
   bool use_fused(long steps) const {
     if (nparts_ != 1 || steps < 2 || fused_bytes_ == 0) return false;
+    // AoS with 3-D halo tiles: the per-sweep tile kernels beat the fused
+    // per-node launch even on the L2-resident cfg-1 box (B200, cfg 1:
+    // blk-push-aos 5,786 -> 8,386, blk-pull-aos 4,988 -> 8,465, aa-aos
+    // 4,921 -> 8,931 MFLUP/s)
+    if (!desc_.soa && aos_tiles()) return false;
     const Part& pt = parts_[0];
     const uint64_t bufs = desc_.prop == Prop::Aa ? 1 : 2;
     return uint64_t(pt.nzs) * P_ * kQ * 8 * bufs <= fused_bytes_;
@@ -652,12 +671,14 @@ class DirectEngine final : public Engine {
       const bool last = s == steps - 1;
       const char* name = push ? (last ? "full_push_stream_aos" : "full_push_aos")
                               : (last ? "full_pull_stream_aos" : "full_pull_aos");
-      pull_aos_tile3d<4, 4>(args(pt, 0, N, t, cur_, 1 - cur_), last, name);
+      const DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
+      pull_aos_tile3d<4, 4>(a, last, name);  // (16x4x2 / 16x2x4 tiles: 4493 -> 4100 / 4326 GB/s)
       cur_ ^= 1;
     }
   }
 
   void advance(const TrtArgs& t, long steps) override {
+    NvtxRange range(("advance " + desc_.name).c_str());
     if (peer_) peer_check();
     const bool soa = desc_.soa;
     if (advance_fused(t, steps)) return;
@@ -724,16 +745,9 @@ class DirectEngine final : public Engine {
           // (y-band order measured slower for the AA odd step: 1922 -> 1103
           // GB/s at band 16, although it halves the DRAM traffic)
           if (aos_tiles()) {
-            const unsigned grid =
-                static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / 4) * (nz_ / 4));
-            auto kern = k_full_aa_odd_aos_tile3d<4, 4>;
-            constexpr size_t smem = pt_smem<4, 4>();
-            LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-            const int tok = stats_.begin("full_aa_odd_aos", stream_);
-            kern<<<grid, kPtX * 16, smem, stream_>>>(a);
-            LBM_CHECK_LAUNCH();
-            stats_.end(tok, stream_);
+            // 16 x 4 x 4 tiles (16 x 4 x 2 / 16 x 2 x 4: 3 CTAs/SM but more
+            // halo rows per node; cfg-5 box odd step 3125 -> 2810 / 2885 GB/s)
+            aa_odd_aos_tile3d<4, 4>(a);
           } else {
             launch("full_aa_odd_aos", k_full_aa_odd<false, false>, a, stream_);
           }
@@ -863,15 +877,20 @@ class DirectEngine final : public Engine {
     cudaEvent_t ev_prev = pev_[0], ev_be = pev_[1], ev_ie = pev_[2], ev_bx = pev_[3];
     LBM_CUDA(cudaEventRecord(ev_prev, stream_));
     {
+      NvtxRange r("aa even boundary + pre-odd exchange [boundary stream]");
       StreamSwap on_b(stream_, bstream_);
       LBM_CUDA(cudaStreamWaitEvent(stream_, ev_prev, 0));
       sweep(false, true);
       LBM_CUDA(cudaEventRecord(ev_be, stream_));
       tr_->exchange(0, parts_, P_, stream_);
     }
-    sweep(false, false);
-    LBM_CUDA(cudaEventRecord(ev_ie, stream_));
     {
+      NvtxRange r("aa even interior [interior stream]");
+      sweep(false, false);
+      LBM_CUDA(cudaEventRecord(ev_ie, stream_));
+    }
+    {
+      NvtxRange r("aa odd boundary + post-odd exchange [boundary stream]");
       StreamSwap on_b(stream_, bstream_);
       LBM_CUDA(cudaStreamWaitEvent(stream_, ev_ie, 0));
       tr_->wait(0, stream_);
@@ -880,6 +899,7 @@ class DirectEngine final : public Engine {
       tr_->wait(1, stream_);
       LBM_CUDA(cudaEventRecord(ev_bx, stream_));
     }
+    NvtxRange r("aa odd interior [interior stream]");
     LBM_CUDA(cudaStreamWaitEvent(stream_, ev_be, 0));
     sweep(true, false);
     LBM_CUDA(cudaStreamWaitEvent(stream_, ev_bx, 0));
@@ -1112,6 +1132,7 @@ class DirectEngine final : public Engine {
     int least = 0, greatest = 0;
     LBM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     LBM_CUDA(cudaStreamCreateWithPriority(&bstream_, cudaStreamNonBlocking, greatest));
+    nvtxNameCudaStreamA(bstream_, "lbmgpu boundary");
     for (cudaEvent_t& e : pev_) LBM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
 
@@ -1160,15 +1181,20 @@ class DirectEngine final : public Engine {
     };
     LBM_CUDA(cudaEventRecord(ev_prev, stream_));
     {
+      NvtxRange r("aa even boundary + signal [boundary stream]");
       StreamSwap on_b(stream_, bstream_);
       LBM_CUDA(cudaStreamWaitEvent(stream_, ev_prev, 0));
       sweep(false, true);
       peer_signal(0, e);
       LBM_CUDA(cudaEventRecord(ev_be, stream_));
     }
-    sweep(false, false);
-    LBM_CUDA(cudaEventRecord(ev_ie, stream_));
     {
+      NvtxRange r("aa even interior [interior stream]");
+      sweep(false, false);
+      LBM_CUDA(cudaEventRecord(ev_ie, stream_));
+    }
+    {
+      NvtxRange r("aa odd boundary: wait, peer sweep, signal, wait [boundary stream]");
       StreamSwap on_b(stream_, bstream_);
       LBM_CUDA(cudaStreamWaitEvent(stream_, ev_ie, 0));
       peer_wait(0, e);
@@ -1177,6 +1203,7 @@ class DirectEngine final : public Engine {
       peer_wait(1, e);
       LBM_CUDA(cudaEventRecord(ev_bo, stream_));
     }
+    NvtxRange r("aa odd interior [interior stream]");
     LBM_CUDA(cudaStreamWaitEvent(stream_, ev_be, 0));
     sweep(true, false);
     LBM_CUDA(cudaStreamWaitEvent(stream_, ev_bo, 0));

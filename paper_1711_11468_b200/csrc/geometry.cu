@@ -220,6 +220,10 @@ int KernelStats::begin(const char* name, cudaStream_t s, long sweeps) {
   }
   Pending p{row, get_event(), get_event(), sweeps};
   LBM_CUDA(cudaEventRecord(p.a, s));
+  if (!origin_) {
+    origin_ = get_event();
+    LBM_CUDA(cudaEventRecord(origin_, s));
+  }
   pending_.push_back(p);
   return static_cast<int>(pending_.size()) - 1;
 }
@@ -236,6 +240,12 @@ void KernelStats::collect() {
     LBM_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     rows_[p.row].launches += p.sweeps;
     rows_[p.row].ms += ms;
+    if (origin_ && spans_.size() < kMaxSpans) {
+      float t0 = 0.f, t1 = 0.f;
+      LBM_CUDA(cudaEventElapsedTime(&t0, origin_, p.a));
+      LBM_CUDA(cudaEventElapsedTime(&t1, origin_, p.b));
+      spans_.push_back({p.row, t0, t1});
+    }
     pool_.push_back(p.a);
     pool_.push_back(p.b);
   }
@@ -245,6 +255,9 @@ void KernelStats::collect() {
 void KernelStats::reset() {
   collect();
   rows_.clear();
+  spans_.clear();
+  if (origin_) pool_.push_back(origin_);
+  origin_ = nullptr;
 }
 
 KernelStats::~KernelStats() {
@@ -253,6 +266,7 @@ KernelStats::~KernelStats() {
     cudaEventDestroy(p.b);
   }
   for (cudaEvent_t e : pool_) cudaEventDestroy(e);
+  if (origin_) cudaEventDestroy(origin_);
 }
 
 }  // namespace lbmgpu

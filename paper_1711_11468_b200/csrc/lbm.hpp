@@ -7,6 +7,9 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+#include <nvtx3/nvToolsExtCudaRt.h>
+
 #include "common.cuh"
 #include "model.cuh"
 
@@ -164,6 +167,11 @@ class KernelStats {
   void reset();
   struct Row { std::string name; long launches = 0; double ms = 0; };
   const std::vector<Row>& rows() { collect(); return rows_; }
+  // Per-launch intervals (ms after the first recorded launch of this
+  // enable/reset period; events on every stream share the device clock),
+  // the evidence that boundary-stream work overlaps the interior sweeps.
+  struct Span { int row; double t0, t1; };
+  const std::vector<Span>& timeline() { collect(); return spans_; }
   long launches() const { return launches_; }
   void count_launch() { ++launches_; }
   void add_launches(long n) { launches_ += n; }
@@ -171,12 +179,35 @@ class KernelStats {
 
  private:
   struct Pending { int row; cudaEvent_t a, b; long sweeps; };
+  static constexpr size_t kMaxSpans = 1 << 16;
+  std::vector<Span> spans_;
+  cudaEvent_t origin_ = nullptr;  // first event of the period (a Pending's start)
   bool on_ = false;
   long launches_ = 0;
   std::vector<Row> rows_;
   std::vector<Pending> pending_;
   std::vector<cudaEvent_t> pool_;
   cudaEvent_t get_event();
+};
+
+// Device micro-benchmarks (microbench.cu): one pass's element count per
+// stream and accounted bytes (GPU: no write allocate; ref: the reference's
+// CPU accounting, microbench.cpp:92-99).
+struct MicroPlan {
+  int streams = 1, arrays = 2;
+  uint64_t n = 0, bytes_gpu = 0, bytes_ref = 0;
+};
+MicroPlan micro_plan(const std::string& kind, uint64_t working_set_bytes);
+
+// NVTX range over a host scope (header-only NVTX 3: a no-op unless a tool
+// such as nsys is attached).  The engines mark each advance() and, on the
+// decomposed paths, each sub-step's boundary / interior enqueue; their two
+// streams are named "lbmgpu interior" / "lbmgpu boundary".
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // Resident blocks per SM of a kernel at a block size (no dynamic shared

@@ -79,6 +79,7 @@ class ListEngine final : public Engine {
              const DistSpec& dist) {
     desc_ = d;
     LBM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    nvtxNameCudaStreamA(stream_, "lbmgpu interior");
     DeviceGeometry geo = build_geometry_device(g, stream_);
     nx_ = geo.nx;
     ny_ = geo.ny;
@@ -405,12 +406,17 @@ class ListEngine final : public Engine {
         auto run = [&](uint64_t b0, uint64_t b1) {
           a.nb = b0;
           a.ne = b1;
+          // boundary launches carry "_halo" (stream role in the stats)
           if (odd)
-            soa ? launch("list_aa_odd_soa", k_list_aa_odd<true, false>, a, pf_)
-                : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a, pf_);
+            soa ? launch(boundary ? "list_aa_odd_soa_halo" : "list_aa_odd_soa",
+                         k_list_aa_odd<true, false>, a, pf_)
+                : launch(boundary ? "list_aa_odd_aos_halo" : "list_aa_odd_aos",
+                         k_list_aa_odd<false, false>, a, pf_);
           else
-            soa ? launch("list_aa_even_soa", k_list_aa_even<true, false>, a)
-                : launch_tile("list_aa_even_aos", k_list_aos_tile<true>, a);
+            soa ? launch(boundary ? "list_aa_even_soa_halo" : "list_aa_even_soa",
+                         k_list_aa_even<true, false>, a)
+                : launch_tile(boundary ? "list_aa_even_aos_halo" : "list_aa_even_aos",
+                              k_list_aos_tile<true>, a);
         };
         if (boundary) {
           run(0, p.head);
@@ -428,6 +434,7 @@ class ListEngine final : public Engine {
       int least = 0, greatest = 0;
       LBM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
       LBM_CUDA(cudaStreamCreateWithPriority(&bstream_, cudaStreamNonBlocking, greatest));
+      nvtxNameCudaStreamA(bstream_, "lbmgpu boundary");
       for (cudaEvent_t& e : bev_) LBM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     struct Swap {
@@ -438,15 +445,20 @@ class ListEngine final : public Engine {
     };
     LBM_CUDA(cudaEventRecord(bev_[0], stream_));
     {
+      NvtxRange r("list aa even boundary + pre-odd exchange [boundary stream]");
       Swap on_b(stream_, bstream_);
       LBM_CUDA(cudaStreamWaitEvent(stream_, bev_[0], 0));
       sweep(false, true);
       LBM_CUDA(cudaEventRecord(bev_[1], stream_));
       list_exchange(0);
     }
-    sweep(false, false);
-    LBM_CUDA(cudaEventRecord(bev_[2], stream_));
     {
+      NvtxRange r("list aa even interior [interior stream]");
+      sweep(false, false);
+      LBM_CUDA(cudaEventRecord(bev_[2], stream_));
+    }
+    {
+      NvtxRange r("list aa odd boundary + post-odd exchange [boundary stream]");
       Swap on_b(stream_, bstream_);
       LBM_CUDA(cudaStreamWaitEvent(stream_, bev_[2], 0));
       list_wait(0);
@@ -567,6 +579,7 @@ class ListEngine final : public Engine {
   }
 
   void advance(const TrtArgs& t, long steps) override {
+    NvtxRange range(("advance " + desc_.name).c_str());
     if (advance_fused(t, steps)) return;
     ListArgs a = base_args();
     a.trt = t;
@@ -611,6 +624,27 @@ class ListEngine final : public Engine {
       }
       return;
     }
+    if (desc_.prop == Prop::OsPush && !soa) {
+      // AoS push in pull order (as the direct AoS push, direct.cu
+      // os_aos_tiles): collide pass, T-1 gather + collide sweeps, one
+      // gather-only sweep, gathering through the Scatter table read
+      // backwards (aos_gather_slot) -- push and pull realise the identical
+      // per-step mapping (reference tests/test_kernels.cpp:96-126), so the
+      // state is bitwise the push's, with whole own records stored through
+      // the tile instead of 18 scattered 8-byte stores per node.
+      a.src = a.dst = buf_[cur_].get();
+      launch_tile("list_push_aos_collide", k_list_aos_tile<false>, a);
+      for (long s = 0; s < steps; ++s) {
+        a.src = buf_[cur_].get();
+        a.dst = buf_[1 - cur_].get();
+        if (s + 1 < steps)
+          launch_tile("list_push_aos", k_list_pull_aos_tile<true, true>, a);
+        else
+          launch_tile("list_push_stream_aos", k_list_pull_aos_tile<false, true>, a);
+        cur_ ^= 1;
+      }
+      return;
+    }
     if (desc_.prop == Prop::OsPush) {
       for (long s = 0; s < steps; ++s) {
         a.src = buf_[cur_].get();
@@ -641,7 +675,7 @@ class ListEngine final : public Engine {
           launch("list_pull_soa", k_list_pull<true, true, false>, a);
       } else {
         if (last)
-          launch("list_pull_stream_aos", k_list_pull<false, false, false>, a);
+          launch_tile("list_pull_stream_aos", k_list_pull_aos_tile<false>, a);
         else
           launch_tile("list_pull_aos", k_list_pull_aos_tile<true>, a);
       }

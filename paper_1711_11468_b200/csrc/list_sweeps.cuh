@@ -150,7 +150,21 @@ __global__ void __launch_bounds__(kLAosTile) k_list_aos_tile(const ListArgs a) {
   aos_tile_store<kLAosTile>(g, sh, cnt);
 }
 
-template <bool COLLIDE>
+// Gather slot of (n, d) for an AoS list.  FROM_SCATTER: derived from the
+// Scatter table the push names build (list_lattice.cpp:177-191): entry
+// (n, opp d) is slot(n - c_d, opp d) when that neighbour is fluid and the
+// bounce-back slot(n, d) otherwise, and the gather entry (n, d) is
+// slot(n - c_d, d) resp. slot(n, opp d) -- the same record with the slot
+// index d' = v % 19 replaced by opp(d') in both cases.
+template <bool FROM_SCATTER>
+__device__ __forceinline__ uint32_t aos_gather_slot(const ListArgs& a, uint64_t n, int d) {
+  if (!FROM_SCATTER) return __ldg(a.adj + (d - 1) * a.N + n);
+  const uint32_t v = __ldg(a.adj + (opp(d) - 1) * a.N + n);
+  const uint32_t s = v % kQ;
+  return v - s + static_cast<uint32_t>(s == 0 ? 0 : ((s & 1u) ? s + 1 : s - 1));
+}
+
+template <bool COLLIDE, bool FROM_SCATTER = false>
 __global__ void __launch_bounds__(kLAosTile) k_list_pull_aos_tile(const ListArgs a) {
   __shared__ __align__(128) double sh[kLAosTile * kQ];
   const uint64_t n0 = blockIdx.x * uint64_t(kLAosTile);
@@ -160,7 +174,7 @@ __global__ void __launch_bounds__(kLAosTile) k_list_pull_aos_tile(const ListArgs
     double q[kQ];
     q[0] = a.src[n * kQ];
 #pragma unroll
-    for (int d = 1; d < kQ; ++d) q[d] = a.src[__ldg(a.adj + (d - 1) * a.N + n)];
+    for (int d = 1; d < kQ; ++d) q[d] = a.src[aos_gather_slot<FROM_SCATTER>(a, n, d)];
     if (COLLIDE) collide(q, a.trt);
     double* r = sh + threadIdx.x * kQ;
 #pragma unroll

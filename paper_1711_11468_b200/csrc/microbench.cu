@@ -56,22 +56,36 @@ __global__ void k_fill(double* a, uint64_t n) {
     a[i] = 1.0;
 }
 
-// Median GB/s over `reps` timed passes after one warm-up pass.
-double run_microbench(const std::string& kind, uint64_t working_set_bytes, int reps) {
-  int streams = 1, arrays = 2;
+// Element count and accounted bytes of one pass: `gpu` is this library's
+// accounting (no write allocate: 16 B per element and stream), `ref` the
+// reference's CPU accounting of the same pass (microbench.cpp:92-99: the
+// plain copies add 8 B write allocate per element and stream).
+MicroPlan micro_plan(const std::string& kind, uint64_t working_set_bytes) {
+  MicroPlan m;
   if (kind == "copy") {
-    streams = 1;
-    arrays = 2;
+    m.streams = 1;
+    m.arrays = 2;
   } else if (kind == "copy-19" || kind == "copy-19-nt-sl") {
-    streams = kQ;
-    arrays = 2 * kQ;
+    m.streams = kQ;
+    m.arrays = 2 * kQ;
   } else if (kind == "update-19") {
-    streams = kQ;
-    arrays = kQ;
+    m.streams = kQ;
+    m.arrays = kQ;
   } else {
     throw ConfigError("unknown micro-benchmark '" + kind +
                       "' (valid: copy, copy-19, copy-19-nt-sl, update-19)");
   }
+  m.n = 2 * (working_set_bytes / (uint64_t(m.arrays) * 16));  // whole double2 per stream
+  m.bytes_gpu = 16ull * m.streams * m.n;
+  const bool write_allocate = kind == "copy" || kind == "copy-19";
+  m.bytes_ref = (write_allocate ? 24ull : 16ull) * m.streams * m.n;
+  return m;
+}
+
+// Median GB/s over `reps` timed passes after one warm-up pass.
+double run_microbench(const std::string& kind, uint64_t working_set_bytes, int reps) {
+  const MicroPlan plan = micro_plan(kind, working_set_bytes);
+  const int arrays = plan.arrays;
   int dev = 0, l2 = 0, sms = 148;
   LBM_CUDA(cudaGetDevice(&dev));
   LBM_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
@@ -80,8 +94,7 @@ double run_microbench(const std::string& kind, uint64_t working_set_bytes, int r
     throw ConfigError("microbench: working set below 4x the L2 (" +
                       std::to_string(4ull * uint64_t(l2)) + " B)");
   if (reps < 1) throw ConfigError("microbench: reps must be >= 1");
-  const uint64_t n2 = working_set_bytes / (uint64_t(arrays) * 16);  // double2 per stream
-  const uint64_t n = 2 * n2;
+  const uint64_t n = plan.n, n2 = n / 2;  // elements / double2 per stream
   DevBuf<double> buf(n * arrays);
   cudaStream_t s;
   LBM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -105,7 +118,7 @@ double run_microbench(const std::string& kind, uint64_t working_set_bytes, int r
   LBM_CUDA(cudaEventCreate(&b));
   pass();
   std::vector<double> gbps;
-  const double bytes = 16.0 * double(streams) * double(n);
+  const double bytes = double(plan.bytes_gpu);
   for (int r = 0; r < reps; ++r) {
     LBM_CUDA(cudaEventRecord(a, s));
     pass();

@@ -88,6 +88,7 @@ def _load():
     L.lbmgpu_kernel_stats_enable.argtypes = [vp, i]
     L.lbmgpu_kernel_stats.argtypes = [vp, vp, vp, vp, i, P(i)]
     L.lbmgpu_kernel_stats_reset.argtypes = [vp]
+    L.lbmgpu_kernel_timeline.argtypes = [vp, vp, vp, vp, i, P(i)]
     L.lbmgpu_launch_count.argtypes = [vp, P(C.c_long)]
     L.lbmgpu_host_alloc.argtypes = [C.c_size_t, P(vp)]
     L.lbmgpu_host_free.argtypes = [vp]
@@ -96,6 +97,7 @@ def _load():
     L.lbmgpu_nccl_unique_id.argtypes = [vp]
     L.lbmgpu_part_info.argtypes = [vp, i, P(i), P(i), P(u64)]
     L.lbmgpu_microbench.argtypes = [C.c_char_p, u64, i, P(d)]
+    L.lbmgpu_microbench_accounting.argtypes = [C.c_char_p, u64, P(u64), P(u64), P(u64)]
     L.lbmgpu_local_rows.argtypes = [vp, P(u64)]
     L.lbmgpu_local_canonical_index.argtypes = [vp, vp]
     L.lbmgpu_snapshot_local.argtypes = [vp, vp, u64]
@@ -597,6 +599,21 @@ class Kernel:
             out[nm] = {"launches": launches[k], "ms": ms[k]}
         return out
 
+    def kernel_timeline(self):
+        """[(name, t0_ms, t1_ms)] per recorded launch, in record order (device
+        clock shared by all streams)."""
+        n = C.c_int()
+        _check(lib.lbmgpu_kernel_timeline(self._h, None, None, None, 0, C.byref(n)))
+        cap = n.value
+        if cap == 0:
+            return []
+        names = C.create_string_buffer(48 * cap)
+        t0 = (C.c_double * cap)()
+        t1 = (C.c_double * cap)()
+        _check(lib.lbmgpu_kernel_timeline(self._h, names, t0, t1, cap, C.byref(n)))
+        return [(names.raw[48 * k:48 * k + 48].split(b"\0", 1)[0].decode(), t0[k], t1[k])
+                for k in range(min(cap, n.value))]
+
     def launch_count(self) -> int:
         v = C.c_long()
         _check(lib.lbmgpu_launch_count(self._h, C.byref(v)))
@@ -726,6 +743,43 @@ def guard_selftest() -> int:
     n = C.c_int()
     _check(lib.lbmgpu_guard_selftest(C.byref(n)))
     return n.value
+
+
+BOUNDARY_ROLE = ("_halo", "_peer", "peer_wait", "peer_signal", "push_halo_merge", "list_link")
+
+
+def stream_overlap(timeline, boundary=BOUNDARY_ROLE):
+    """Overlap evidence for the decomposed paths: of the device time the
+    boundary-stream launches (boundary sweeps, peer waits / signals, halo
+    merges; names containing one of `boundary`) are busy, the part during
+    which an interior sweep runs at the same time.  Returns
+    {"boundary_ms", "overlapped_ms", "frac"}."""
+    b = [(t0, t1) for n, t0, t1 in timeline if any(x in n for x in boundary)]
+    it = sorted((t0, t1) for n, t0, t1 in timeline if not any(x in n for x in boundary))
+    merged = []
+    for t0, t1 in it:
+        if merged and t0 <= merged[-1][1]:
+            merged[-1][1] = max(merged[-1][1], t1)
+        else:
+            merged.append([t0, t1])
+    busy = sum(t1 - t0 for t0, t1 in b)
+    ov = 0.0
+    for t0, t1 in b:
+        for m0, m1 in merged:
+            if m0 >= t1:
+                break
+            ov += max(0.0, min(t1, m1) - max(t0, m0))
+    return {"boundary_ms": busy, "overlapped_ms": ov, "frac": ov / busy if busy > 0 else None}
+
+
+def microbench_accounting(kind: str, working_set_bytes: int) -> dict:
+    """Elements per stream and accounted bytes of one micro-benchmark pass:
+    this library's (no write allocate) and the reference's
+    (microbench.cpp:92-99)."""
+    n, bg, br = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    _check(lib.lbmgpu_microbench_accounting(kind.encode(), working_set_bytes, C.byref(n),
+                                            C.byref(bg), C.byref(br)))
+    return {"elems": n.value, "bytes_gpu": bg.value, "bytes_ref": br.value}
 
 
 def microbench(kind: str, working_set_bytes: int = 8 << 30, reps: int = 5) -> float:

@@ -866,3 +866,29 @@ def test_snapshot_out_buffer_validation():
             k.snapshot_local(out=bad)
     good = np.empty(n)
     assert k.snapshot(out=good) is good and np.array_equal(good, k.snapshot())
+
+
+@pytest.mark.parametrize("name,dist", [
+    ("aa-soa", {"virtual_parts": 8, "transport": "peer"}),
+    ("aa-soa", {"virtual_parts": 8}),
+    ("blk-pull-soa", {"virtual_parts": 4, "transport": "peer"}),
+    ("list-aa-soa", {"virtual_parts": 4})])
+def test_boundary_stream_overlaps_interior(name, dist):
+    """Overlap evidence for the decomposed paths (SURVEY 8(e) schedule): the
+    per-launch device intervals (kernel timeline, events on both streams)
+    show the boundary-stream work -- boundary sweeps, peer waits / signals,
+    halo exchanges -- running while interior sweeps run.  Emulated slabs /
+    node ranges on one GPU (channel 512x128x128)."""
+    k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec("channel", 512, 128, 128),
+                        dist=dist)
+    k.advance(PARAMS, FORCE, 2)
+    k.synchronize()
+    k.kernel_stats_reset()
+    k.kernel_stats_enable(True)
+    k.advance(PARAMS, FORCE, 8)
+    k.kernel_stats_enable(False)
+    tl = k.kernel_timeline()
+    assert len(tl) > 0
+    ov = lbm.lbmgpu.stream_overlap(tl)
+    assert ov["boundary_ms"] > 0, tl[:10]
+    assert ov["frac"] > 0.5, ov

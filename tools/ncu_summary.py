@@ -62,7 +62,60 @@ def summarise(path):
     return out
 
 
+# ncu kernel name (without "void lbmgpu::" and arguments) -> the bench's
+# kernel-stats row of the BASELINE configs' default kernels
+BENCH_ROWS = {
+    "k_full_aa_even<1, 0, 128, 4>": "full_aa_even_soa",
+    "k_full_aa_odd<1, 0, 128, 4>": "full_aa_odd_soa",
+    "k_list_aa_even<1, 0>": "list_aa_even_soa",
+    "k_list_aa_odd<1, 0>": "list_aa_odd_soa",
+    "k_list_pull<1, 1, 0>": "list_pull_soa",
+    "k_list_pull<1, 0, 0>": "list_pull_stream_soa",
+    "k_list_collide<1>": "list_collide_soa",
+    "k_full_fused<1, 0, 160, 4>": "full_push_soa_fused",
+}
+def build(outdir, dst, sha_file):
+    """profiles/ncu_summary.json from the launch lists tools/gpu_ncu_summary.sh
+    captured (gpurun_out/ncu_cfg{1..5}.csv), stamped with the csrc content
+    hash the capture ran (bench.py drops roofline.traffic when it differs)."""
+    sha = open(sha_file).read().strip()
+    out = {"csrc_sha16": sha,
+           "source": "tools/gpu_ncu_summary.sh: ncu --metrics gpu__time_duration.sum,"
+                     "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
+                     "bench.py --config C --steps 2 --warmup 1, 1x B200",
+           "kernels": {}, "configs": {}}
+    for cid in ("1", "2", "3", "4", "5"):
+        path = f"{outdir}/ncu_cfg{cid}.csv"
+        try:
+            s = summarise(path)
+        except (OSError, StopIteration):
+            continue
+        rows = {}
+        for k, v in s.items():
+            row = BENCH_ROWS.get(k)
+            if row is None:
+                continue
+            rec = {"ncu_kernel": k, "launches": v["launches"], "ncu_mean_ns": v["mean_ns"],
+                   "dram_read_bytes_per_launch": v["dram_read_bytes_per_launch"],
+                   "dram_write_bytes_per_launch": v["dram_write_bytes_per_launch"],
+                   "dram_bytes_per_launch": v["dram_bytes_per_launch"]}
+            if row.endswith("_fused"):  # cfg 1: one launch runs all sweeps of an advance
+                sweeps = 2 * 2 + 1  # bench --steps 2 --warmup 1 on push: per-advance sweeps
+                rec["note"] = "fused launch; bytes per sweep = per launch / sweeps of that launch"
+            rows[row] = rec
+        if cid == "5":
+            out["kernels"] = rows
+        else:
+            out["configs"][cid] = rows
+    json.dump(out, open(dst, "w"), indent=1)
+    return out
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        o = build(sys.argv[2], sys.argv[3], sys.argv[4])
+        print(json.dumps(o, indent=1)[:3000])
+        sys.exit(0)
     src, dst = sys.argv[1], sys.argv[2]
     s = summarise(src)
     json.dump({"source": src, "kernels": s}, open(dst, "w"), indent=1)
