@@ -134,6 +134,7 @@ __device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, 
   }
   const bool solid = solid_node(a, c.x, c.y, c.z, n);
   if (COLLIDE && !solid) collide(q, a.trt);
+  if (!COLLIDE) loads_before_stores();
   st<CS>(a.dst + I(c.Z[1], dslot(0), c.y, c.x), q[0]);
 #pragma unroll
   for (int d = 1; d < kQ; ++d) {

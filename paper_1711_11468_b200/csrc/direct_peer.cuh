@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(256) k_full_pull_peer(const DirectArgs a, cons
     q[d] = zb[1 - cz(d)][I(zp[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
   const bool solid = solid_node(a, c.x, c.y, c.z, n);
   if (COLLIDE && !solid) collide(q, a.trt);
+  if (!COLLIDE) loads_before_stores();
   a.dst[I(c.Z[1], dslot(0), c.y, c.x)] = q[0];
 #pragma unroll
   for (int d = 1; d < kQ; ++d)

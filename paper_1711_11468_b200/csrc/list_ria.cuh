@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int d = 1; d < kQ; ++d) q[d] = a.src[int64_t(a.starts[d] + n) + __ldg(p + d - 1)];
   if (COLLIDE) collide(q, a.trt);
+  if (!COLLIDE) loads_before_stores();
 #pragma unroll
   for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + a.starts[d] + n, q[d]);
 }

@@ -54,6 +54,7 @@ __device__ __forceinline__ void list_pull_node(const ListArgs& a, uint64_t n) {
 #pragma unroll
   for (int d = 1; d < kQ; ++d) q[d] = lld<CG>(a.src + an[d - 1]);
   if (COLLIDE) collide(q, a.trt);
+  if (!COLLIDE) loads_before_stores();
 #pragma unroll
   for (int d = 0; d < kQ; ++d) lst<CS>(a.dst + lslot<SOA>(a, n, d), q[d]);
 }
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kLAosTile) k_list_pull_aos_tile(const ListArgs
 #pragma unroll
     for (int d = 1; d < kQ; ++d) q[d] = a.src[aos_gather_slot<FROM_SCATTER>(a, n, d)];
     if (COLLIDE) collide(q, a.trt);
+    if (!COLLIDE) loads_before_stores();
     double* r = sh + threadIdx.x * kQ;
 #pragma unroll
     for (int d = 0; d < kQ; ++d) r[d] = q[d];
