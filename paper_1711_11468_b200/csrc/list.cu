@@ -515,10 +515,18 @@ class ListEngine final : public Engine {
     return a;
   }
 
-  // AoS own-record tile kernels: kLAosTile-node blocks over [nb, ne)
+  // AoS own-record tile kernels: kLAosTile-node blocks over [nb, ne).
+  // gathers = the kernel also gathers 18 scattered values per node from
+  // global memory: those hit L1 only if the shared-memory carve-out leaves
+  // it room (at the default carve-out 11 CTAs x 19.5 KB of tiles leave
+  // ~40 KB of L1).  A 33 % carve-out (5 CTAs/SM) measured best on cfg 2:
+  // list-push-aos 8,854 -> 10,824 MFLUP/s, its stream pass 1,580 -> 4,105
+  // GB/s (50 %: 10,409; 20 %: 10,207); the own-record tiles keep the default.
   template <class K>
-  void launch_tile(const char* name, K kern, const ListArgs& a) {
+  void launch_tile(const char* name, K kern, const ListArgs& a, bool gathers = false) {
     if (a.ne <= a.nb) return;
+    if (gathers)
+      LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 33));
     const int tok = stats_.begin(name, stream_);
     kern<<<static_cast<unsigned>(ceil_div(a.ne - a.nb, kLAosTile)), kLAosTile, 0, stream_>>>(a);
     LBM_CHECK_LAUNCH();
@@ -638,9 +646,9 @@ class ListEngine final : public Engine {
         a.src = buf_[cur_].get();
         a.dst = buf_[1 - cur_].get();
         if (s + 1 < steps)
-          launch_tile("list_push_aos", k_list_pull_aos_tile<true, true>, a);
+          launch_tile("list_push_aos", k_list_pull_aos_tile<true, true>, a, true);
         else
-          launch_tile("list_push_stream_aos", k_list_pull_aos_tile<false, true>, a);
+          launch_tile("list_push_stream_aos", k_list_pull_aos_tile<false, true>, a, true);
         cur_ ^= 1;
       }
       return;
@@ -675,9 +683,9 @@ class ListEngine final : public Engine {
           launch("list_pull_soa", k_list_pull<true, true, false>, a);
       } else {
         if (last)
-          launch_tile("list_pull_stream_aos", k_list_pull_aos_tile<false>, a);
+          launch_tile("list_pull_stream_aos", k_list_pull_aos_tile<false>, a, true);
         else
-          launch_tile("list_pull_aos", k_list_pull_aos_tile<true>, a);
+          launch_tile("list_pull_aos", k_list_pull_aos_tile<true>, a, true);
       }
       cur_ ^= 1;
     }
