@@ -1,5 +1,6 @@
 // Device reductions for the steady-state driver and the Poiseuille check
 // (reference src/harness.cpp:141-174, src/verification.cpp:75-85).
+#include <algorithm>
 #include <cstring>
 
 #include "lbm.hpp"
@@ -37,7 +38,13 @@ void velocity_change(const double* u, const double* uprev, uint64_t n3,
                      cudaStream_t s) {
   DevBuf<unsigned long long> o(3);
   LBM_CUDA(cudaMemsetAsync(o.get(), 0, 24, s));
-  k_velocity_change<<<148 * 4, 256, 0, s>>>(u, uprev, n3, o.get());
+  int dev = 0, sms = 148;
+  LBM_CUDA(cudaGetDevice(&dev));
+  LBM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // grid-stride: 4 CTAs per SM, no more than the data needs
+  const uint64_t want = ceil_div(n3, 256);
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 4ull * sms)));
+  k_velocity_change<<<grid, 256, 0, s>>>(u, uprev, n3, o.get());
   LBM_CHECK_LAUNCH();
   unsigned long long h[3];
   LBM_CUDA(cudaMemcpyAsync(h, o.get(), 24, cudaMemcpyDeviceToHost, s));
@@ -48,7 +55,10 @@ void velocity_change(const double* u, const double* uprev, uint64_t n3,
 }
 
 // One thread per fluid layer, summing u_x over the columns in canonical
-// (snapshot) order -- the reference's loop order, hence the same rounding.
+// (snapshot) order -- the reference's loop order, hence the same rounding
+// (verification.cpp:75-85 sums sequentially; a tree reduction would change
+// the last bits of the reported profile).  The verification slit has 64
+// columns and 32 layers, so the serial loop costs microseconds.
 __global__ void k_layer_sums(const double* __restrict__ u, uint64_t cols,
                              int layers, double* __restrict__ out) {
   const int kz = blockIdx.x * blockDim.x + threadIdx.x;

@@ -74,6 +74,8 @@ BENCH_ROWS = {
     "k_list_collide<1>": "list_collide_soa",
     "k_full_fused<1, 0, 160, 4>": "full_push_soa_fused",
 }
+
+
 def build(outdir, dst, sha_file):
     """profiles/ncu_summary.json from the launch lists tools/gpu_ncu_summary.sh
     captured (gpurun_out/ncu_cfg{1..5}.csv), stamped with the csrc content
@@ -82,7 +84,7 @@ def build(outdir, dst, sha_file):
     out = {"csrc_sha16": sha,
            "source": "tools/gpu_ncu_summary.sh: ncu --metrics gpu__time_duration.sum,"
                      "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
-                     "bench.py --config C --steps 2 --warmup 1, 1x B200",
+                     "bench.py --config C --steps 2 --warmup 1 (cfg 1: --steps 20 --warmup 0), 1x B200",
            "kernels": {}, "configs": {}}
     for cid in ("1", "2", "3", "4", "5"):
         path = f"{outdir}/ncu_cfg{cid}.csv"
@@ -99,9 +101,15 @@ def build(outdir, dst, sha_file):
                    "dram_read_bytes_per_launch": v["dram_read_bytes_per_launch"],
                    "dram_write_bytes_per_launch": v["dram_write_bytes_per_launch"],
                    "dram_bytes_per_launch": v["dram_bytes_per_launch"]}
-            if row.endswith("_fused"):  # cfg 1: one launch runs all sweeps of an advance
-                sweeps = 2 * 2 + 1  # bench --steps 2 --warmup 1 on push: per-advance sweeps
-                rec["note"] = "fused launch; bytes per sweep = per launch / sweeps of that launch"
+            if row.endswith("_fused"):
+                # cfg 1 is captured with --steps 20 --warmup 0: one fused
+                # launch of 20 sweeps; the bench counts sweeps as launches
+                rec["sweeps_per_launch"] = 20
+                for key in ("dram_read_bytes_per_launch", "dram_write_bytes_per_launch",
+                            "dram_bytes_per_launch"):
+                    rec[key] /= 20
+                rec["note"] = ("per sweep of the 20-sweep fused launch; the lattice is "
+                               "L2-resident, the DRAM bytes are mostly write-back")
             rows[row] = rec
         if cid == "5":
             out["kernels"] = rows
