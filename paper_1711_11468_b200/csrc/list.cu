@@ -35,6 +35,7 @@
 #include "list_build.cuh"
 #include "list_ria.cuh"
 #include "list_parts.cuh"
+#include "list_aos_tile.cuh"
 
 namespace lbmgpu {
 
@@ -105,7 +106,10 @@ class ListEngine final : public Engine {
     for (int q = 0; q < kQ; ++q) starts_[q] = st[q];
 
     // ranks in traversal order and canonical order
-    DevBuf<uint32_t> crank(V);
+    // the AoS AA odd step's staging tiles keep the box-order scan (V + 1
+    // entries: crank[V] = N closes the last row)
+    const bool aos_tiles = !d.soa && d.prop == Prop::Aa && d.blk == 0 && !d.ria;
+    DevBuf<uint32_t> crank(V + 1);
     scan_fluid(geo.flags.get(), crank.get(), V, stream_);
     DevBuf<uint32_t> trank;
     if (d.blk > 0) {
@@ -157,6 +161,12 @@ class ListEngine final : public Engine {
       LBM_CHECK_LAUNCH();
     }
     LBM_CUDA(cudaStreamSynchronize(stream_));
+    if (aos_tiles) {
+      const uint32_t nf = static_cast<uint32_t>(n_fluid_);
+      LBM_CUDA(cudaMemcpy(crank.get() + V, &nf, 4, cudaMemcpyHostToDevice));
+      crank_ = std::move(crank);
+      if (const char* e = std::getenv("LBMGPU_LTILE")) ltile_ = std::atoi(e);
+    }
     // streaming stores for the nt names and for lattices far beyond L2
     cs_nt_ = d.nt_streams > 0;
     if (d.ria) build_ria();
@@ -533,6 +543,38 @@ class ListEngine final : public Engine {
     stats_.end(tok, stream_);
   }
 
+  // AoS AA odd step through 3-D staging tiles (list_aos_tile.cuh)
+  template <int TX, int TY, int TZ>
+  void launch_aos_odd_tile_shape(const ListArgs& a) {
+    using S = LTileShape<TX, TY, TZ>;
+    static_assert(TZ % 2 == 0, "staged rows must stay 16-byte aligned");
+    auto kern = k_list_aa_odd_aos_tile<TX, TY, TZ>;
+    LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(S::kSmem)));
+    LTileGeom g{};
+    g.crank = crank_.get();
+    g.nx = nx_;
+    g.ny = ny_;
+    g.nz = nz_;
+    g.tiles_y = static_cast<uint32_t>(ceil_div(ny_, TY));
+    g.tiles_z = static_cast<uint32_t>(ceil_div(nz_, TZ));
+    const uint64_t tiles = ceil_div(nx_, TX) * uint64_t(g.tiles_y) * g.tiles_z;
+    const int tok = stats_.begin("list_aa_odd_aos", stream_);
+    kern<<<static_cast<unsigned>(tiles), S::kT, S::kSmem, stream_>>>(a, g);
+    LBM_CHECK_LAUNCH();
+    stats_.end(tok, stream_);
+  }
+  void launch_aos_odd_tiles(const ListArgs& a) {
+    switch (ltile_) {
+      case 1: launch_aos_odd_tile_shape<4, 4, 16>(a); break;
+      case 2: launch_aos_odd_tile_shape<4, 4, 8>(a); break;
+      case 3: launch_aos_odd_tile_shape<2, 4, 16>(a); break;
+      case 4: launch_aos_odd_tile_shape<4, 8, 4>(a); break;
+      case 5: launch_aos_odd_tile_shape<2, 2, 32>(a); break;
+      default: launch_aos_odd_tile_shape<4, 8, 8>(a); break;
+    }
+  }
+
   template <class K, class... Extra>
   void launch(const char* name, K kern, const ListArgs& a, Extra... extra) {
     const int threads = threads_;
@@ -625,6 +667,8 @@ class ListEngine final : public Engine {
                 a, ria_pat_.get(), ria_run0_.get(), ria_mask_.get(), pf_);
           LBM_CHECK_LAUNCH();
           stats_.end(tok, stream_);
+        } else if (!soa && crank_.get()) {
+          launch_aos_odd_tiles(a);
         } else {
           soa ? launch("list_aa_odd_soa", k_list_aa_odd<true, false>, a, pf_)
               : launch("list_aa_odd_aos", k_list_aa_odd<false, false>, a, pf_);
@@ -933,6 +977,8 @@ class ListEngine final : public Engine {
   DevBuf<int32_t> nodes_;
   DevBuf<uint32_t> adj_;
   DevBuf<uint32_t> list_of_canon_;
+  DevBuf<uint32_t> crank_;      // box-order fluid scan (AoS AA staging tiles), V + 1 entries
+  int ltile_ = 0;               // staging tile shape of the AoS AA odd step (LBMGPU_LTILE)
   DevBuf<double> buf_[2];
   // node-range decomposition (list AA over several GPUs / emulated parts)
   std::vector<LPart> lparts_;

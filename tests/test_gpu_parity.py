@@ -194,6 +194,39 @@ def test_aos_halo_tiles_against_oracle(name, kind, dims, port, monkeypatch):
     assert tile in rows, rows
 
 
+LIST_AOS_TILE_CASES = [
+    ("channel", (16, 12, 10)), ("channel", (9, 7, 13)), ("blocks", (12, 10, 10)),
+    ("blocks", (20, 18, 22)), ("pipe", (9, 12, 13)), ("slit", (6, 5, 9)),
+    ("channel", (5, 6, 34)), ("channel", (3, 4, 6)), ("blocks", (8, 9, 11)), ("slit", (4, 3, 40)),
+]
+
+
+@pytest.mark.parametrize("shape", ["0", "1", "2", "3", "4", "5"])
+@pytest.mark.parametrize("kind,dims", LIST_AOS_TILE_CASES)
+def test_list_aa_aos_staging_tiles_against_oracle(shape, kind, dims, port, monkeypatch):
+    """list-aa-aos odd step through the 3-D staging tiles
+    (list_aos_tile.cuh) for every instantiated tile shape (LBMGPU_LTILE):
+    ragged boxes that no tile divides, rows shorter than the staged z range,
+    z ranges wrapping periodically onto one and two list ranges, tiles wider
+    than the box (halo rows wrapping onto own rows), solid obstacles inside
+    the staged rows -- bit for bit against the oracle's half-way stepper
+    (kernels_list_aa.cpp:22-31) over repeated advance calls."""
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    monkeypatch.setenv("LBMGPU_LTILE", shape)
+    _, _, nf = port.geometry(kind, *dims)
+    init = port.perturbed(nf, 23)
+    k = lbm.make_kernel(lbm.make_descriptor("list-aa-aos"), lbm.GeometrySpec(kind, *dims))
+    k.load_state(init)
+    k.kernel_stats_enable(True)
+    done = 0
+    for st in (4, 2):
+        k.advance(PARAMS, FORCE, st)
+        done += st
+        expect, _ = port.run("half", kind, *dims, done, PARAMS.omega_plus, g=G_TEST, init=init)
+        assert np.array_equal(k.snapshot(), expect), (shape, kind, dims, done)
+    assert "list_aa_odd_aos" in k.kernel_stats()
+
+
 def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
     """Memory-safety check in place of compute-sanitizer (closed on this
     pool): with LBMGPU_GUARD=1 every device buffer carries 4 KiB guard zones
@@ -218,6 +251,14 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
                 k.total_mass()
                 keep.append(k)
     monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    for shape in ("0", "1", "2", "3", "4", "5"):  # list-aa-aos staging tiles (blk = 0)
+        monkeypatch.setenv("LBMGPU_LTILE", shape)
+        for spec in (small, tiled, lbm.GeometrySpec("pipe", 9, 12, 13)):
+            k = lbm.make_kernel(lbm.make_descriptor("list-aa-aos"), spec)
+            k.load_perturbed(3)
+            k.advance(PARAMS, FORCE, 4)
+            keep.append(k)
+    monkeypatch.delenv("LBMGPU_LTILE")
     for mode in ("0", "1", "2"):
         monkeypatch.setenv("LBMGPU_RIA_MODE", mode)
         k = lbm.make_kernel(lbm.make_descriptor("list-aa-ria-soa"), small)
