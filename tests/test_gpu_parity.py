@@ -198,10 +198,11 @@ LIST_AOS_TILE_CASES = [
     ("channel", (16, 12, 10)), ("channel", (9, 7, 13)), ("blocks", (12, 10, 10)),
     ("blocks", (20, 18, 22)), ("pipe", (9, 12, 13)), ("slit", (6, 5, 9)),
     ("channel", (5, 6, 34)), ("channel", (3, 4, 6)), ("blocks", (8, 9, 11)), ("slit", (4, 3, 40)),
+    ("channel", (64, 64, 64)), ("blocks", (40, 36, 44)),  # persistent CTAs: several tiles each
 ]
 
 
-@pytest.mark.parametrize("shape", ["0", "1", "2", "3", "4", "5"])
+@pytest.mark.parametrize("shape", ["1", "2", "5"])
 @pytest.mark.parametrize("kind,dims", LIST_AOS_TILE_CASES)
 def test_list_aa_aos_staging_tiles_against_oracle(shape, kind, dims, port, monkeypatch):
     """list-aa-aos odd step through the 3-D staging tiles
@@ -251,7 +252,7 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
                 k.total_mass()
                 keep.append(k)
     monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    for shape in ("0", "1", "2", "3", "4", "5"):  # list-aa-aos staging tiles (blk = 0)
+    for shape in ("1", "2", "5"):  # list-aa-aos staging tiles (blk = 0)
         monkeypatch.setenv("LBMGPU_LTILE", shape)
         for spec in (small, tiled, lbm.GeometrySpec("pipe", 9, 12, 13)):
             k = lbm.make_kernel(lbm.make_descriptor("list-aa-aos"), spec)
