@@ -164,6 +164,18 @@ int lbmgpu_n_fluid(lbmgpu_ctx* ctx, uint64_t* out);
  * count must equal N*19 (ConfigError otherwise). */
 int lbmgpu_snapshot(lbmgpu_ctx* ctx, double* host, uint64_t count);
 int lbmgpu_load_state(lbmgpu_ctx* ctx, const double* host, uint64_t count);
+/* One job: load_state(host_in) + advance(steps) + snapshot(host_out) -- the
+ * reference harness's load / advance / snapshot-for-the-fingerprint sequence
+ * (harness.cpp:94-130) in one call.  Same validation and errors as the three
+ * calls; the result is bitwise theirs.  Where the engine supports it (direct
+ * SoA AA lattice of one part whose fluid (x, y) columns all hold the same
+ * planes, e.g. the channel and slit geometries) and both buffers are
+ * page-locked (lbmgpu_host_alloc), the host transfers are pipelined with the
+ * sweeps; otherwise the three calls run in sequence.
+ * *pipelined (may be NULL) = 1 when the pipelined schedule ran. */
+int lbmgpu_run(lbmgpu_ctx* ctx, double omega_plus, double magic_lambda, const double* g3,
+               long steps, const double* host_in, uint64_t in_count, double* host_out,
+               uint64_t out_count, int* pipelined);
 /* load_state(perturbed_equilibrium(N, seed, amplitude)) generated on the
  * device (harness.cpp:50-62); bitwise identical to the host formula. */
 int lbmgpu_load_perturbed(lbmgpu_ctx* ctx, uint64_t seed, double amplitude);

@@ -429,6 +429,57 @@ int lbmgpu_load_state(lbmgpu_ctx* c, const double* host, uint64_t count) {
   });
 }
 
+// page-locked (cudaHostAlloc / registered) over [p, p + bytes)
+static bool pinned_range(const void* p, size_t bytes) {
+  for (const char* q : {static_cast<const char*>(p), static_cast<const char*>(p) + bytes - 1}) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
+int lbmgpu_run(lbmgpu_ctx* c, double wp, double lambda, const double* g, long steps,
+               const double* host_in, uint64_t in_count, double* host_out, uint64_t out_count,
+               int* pipelined_out) {
+  return guard([&] {
+    need(c, "ctx");
+    const uint64_t N = c->eng->n_fluid();
+    if (in_count != N * kQ)
+      throw ConfigError("load_state: state size does not match fluid count");
+    need(host_in, "host buffer");
+    TrtArgs t = checked_trt(c, wp, lambda, g, steps);
+    if (out_count != N * kQ)
+      throw ConfigError("snapshot: buffer holds " + std::to_string(out_count) +
+                        " values, lattice has " + std::to_string(N * kQ));
+    need(host_out, "host buffer");
+    if (pipelined_out) *pipelined_out = 0;
+    bool done = false;
+    if (c->eng->holds_all() && N && pinned_range(host_in, N * kQ * 8) &&
+        pinned_range(host_out, N * kQ * 8)) {
+      c->eng->check_health();
+      done = c->eng->run_job(t, steps, host_in, host_out);
+      if (done) c->eng->check_health();
+    }
+    if (done) {
+      if (pipelined_out) *pipelined_out = 1;
+      return;
+    }
+    int rc = lbmgpu_load_state(c, host_in, in_count);
+    if (rc == LBMGPU_OK) rc = lbmgpu_advance(c, wp, lambda, g, steps);
+    if (rc == LBMGPU_OK) rc = lbmgpu_snapshot(c, host_out, out_count);
+    if (rc != LBMGPU_OK) {
+      const std::string m = g_err;
+      if (rc == LBMGPU_ECONFIG) throw ConfigError(m);
+      if (rc == LBMGPU_ENUMERICAL) throw NumericalError(m);
+      throw DeviceError(m);
+    }
+  });
+}
+
 int lbmgpu_local_rows(lbmgpu_ctx* c, uint64_t* rows) {
   return guard([&] {
     need(c, "ctx");

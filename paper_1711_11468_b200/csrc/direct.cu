@@ -34,6 +34,7 @@
 #include "direct_aos.cuh"
 #include "direct_fused.cuh"
 #include "direct_peer.cuh"
+#include "direct_job.cuh"
 
 namespace lbmgpu {
 
@@ -455,6 +456,9 @@ class DirectEngine final : public Engine {
     for (cudaEvent_t e : pev_)
       if (e) cudaEventDestroy(e);
     for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
+    for (cudaEvent_t e : job_ev_) cudaEventDestroy(e);
+    for (cudaStream_t st : {job_s_in_, job_s_out_, job_k_in_, job_k_out_})
+      if (st) cudaStreamDestroy(st);
     if (peer_err_) cudaFreeHost(peer_err_);
     tr_.reset();
     if (stream_) cudaStreamDestroy(stream_);
@@ -756,6 +760,222 @@ class DirectEngine final : public Engine {
         peer_ ? aa_pair_peer(t) : aa_pair_slabs(t);
       }
     }
+  }
+
+  // ---- pipelined job (Engine::run_job) --------------------------------------
+  // load_state(host_in) + advance(T) + snapshot(host_out) with the PCIe
+  // transfers overlapped with the sweeps.  The fluid planes [za, zb) are cut
+  // into S compute slabs of ws planes; sub-step s of slab j touches the
+  // records of slabs j-1 .. j+1 and needs sub-step s-1 of those three, so the
+  // launches go out on the ONE engine stream in diagonal rounds (round L:
+  // slabs j = L, L-1, .., 0 at sub-step L - j), which keeps every pair of
+  // conflicting launches in the order of the plain advance -- the result is
+  // bitwise the plain sequence's.  Slab j can then run ahead of slab j+1 by
+  // one sub-step: while later planes are still crossing PCIe the first slabs
+  // already advance, and the first slabs leave for the host while the last
+  // ones finish.  Transfers move chunks of k slabs: the chunk's canonical
+  // rows are a 2-D array (column-uniform geometries: every fluid (x, y)
+  // column holds the same planes [za, zb)), one cudaMemcpy2DAsync + one
+  // layout kernel on a copy stream each way.  Applies to SoA AA lattices of
+  // one part whose z ends are not both fluid (no z ring); else false.
+  bool job_plan() {
+    if (job_checked_) return job_ok_;
+    job_checked_ = true;
+    const Part& pt = parts_[0];
+    DevBuf<uint32_t> census(3 * P_);
+    k_job_columns<<<grid_for(P_, 256), 256, 0, stream_>>>(pt.flags.get(), P_, nz_, census.get());
+    LBM_CHECK_LAUNCH();
+    std::vector<uint32_t> h(3 * P_);
+    LBM_CUDA(cudaMemcpyAsync(h.data(), census.get(), h.size() * 4, cudaMemcpyDeviceToHost, stream_));
+    LBM_CUDA(cudaStreamSynchronize(stream_));
+    uint32_t za = 0, zb = 0;
+    bool first = true;
+    std::vector<uint32_t> cols;  // in-plane offsets of the fluid columns, x-major
+    for (uint32_t x = 0; x < uint32_t(nx_); ++x)
+      for (uint32_t y = 0; y < uint32_t(ny_); ++y) {
+        const uint64_t c = uint64_t(y) * nx_ + x;
+        const uint32_t cnt = h[3 * c], zmin = h[3 * c + 1], zmax = h[3 * c + 2];
+        if (cnt == 0) continue;
+        if (zmax - zmin + 1 != cnt) return false;  // a solid plane inside the column
+        if (first) {
+          za = zmin;
+          zb = zmax + 1;
+          first = false;
+        } else if (zmin != za || zmax + 1 != zb) {
+          return false;
+        }
+        cols.push_back(static_cast<uint32_t>(c));
+      }
+    if (first || (za == 0 && zb == uint32_t(nz_))) return false;
+    std::vector<uint32_t> col_of(P_, 0xffffffffu);  // in-plane offset -> column rank
+    for (uint32_t r = 0; r < cols.size(); ++r) col_of[cols[r]] = r;
+    job_za_ = za;
+    job_zb_ = zb;
+    job_cols_ = cols.size();
+    job_col_of_.alloc(P_);
+    LBM_CUDA(cudaMemcpy(job_col_of_.get(), col_of.data(), P_ * 4, cudaMemcpyHostToDevice));
+    job_ok_ = true;
+    return true;
+  }
+
+  bool run_job(const TrtArgs& t, long steps, const double* host_in, double* host_out) override {
+    if (nparts_ != 1 || desc_.prop != Prop::Aa || !desc_.soa || steps < 2 || use_fused(steps) ||
+        !host_in || !host_out)
+      return false;
+    if (!job_plan()) return false;
+    NvtxRange range(("run_job " + desc_.name).c_str());
+    const Part& pt = parts_[0];
+    const uint32_t za = job_za_, nzf = job_zb_ - job_za_;
+    const uint64_t R = job_cols_;
+    // S compute slabs of ws planes, chunks of k slabs.  Measured on the cfg-5
+    // job: one plane per slab (the most skew: the first
+    // chunks leave earliest) and 16-plane chunks (2-D copy rows of 2,432 B)
+    int slabs = 512, k = 16;
+    if (const char* e = std::getenv("LBMGPU_JOB_SLABS")) slabs = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LBMGPU_JOB_CHUNK")) k = std::max(1, std::atoi(e));
+    const uint32_t ws = static_cast<uint32_t>(ceil_div(nzf, uint64_t(std::min<uint32_t>(slabs, nzf))));
+    const uint32_t S = static_cast<uint32_t>(ceil_div(nzf, ws));
+    // a chunk's layout tile must fit the shared memory: kJobTx x w x 19 doubles
+    k = static_cast<int>(std::max<uint32_t>(
+        1, std::min<uint32_t>(uint32_t(k), ((200u << 10) / (kJobTx * 8) - 1) / kQ / ws)));
+    const uint32_t C = static_cast<uint32_t>(ceil_div(S, uint64_t(k)));
+    const uint32_t wc = std::min<uint32_t>(k * ws, nzf);  // planes per chunk (staging width)
+    const uint64_t stage_elems = R * wc * kQ;
+    for (int bf = 0; bf < 2; ++bf) {
+      if (job_in_[bf].size() < stage_elems) job_in_[bf].alloc(stage_elems);
+      if (job_out_[bf].size() < stage_elems) job_out_[bf].alloc(stage_elems);
+    }
+    if (!job_s_in_) {
+      // layout-kernel streams at the greatest priority: their CTAs take SM
+      // slots ahead of the sweeps' next CTAs instead of queueing behind them
+      int least = 0, greatest = 0;
+      LBM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      LBM_CUDA(cudaStreamCreateWithFlags(&job_s_in_, cudaStreamNonBlocking));
+      LBM_CUDA(cudaStreamCreateWithFlags(&job_s_out_, cudaStreamNonBlocking));
+      LBM_CUDA(cudaStreamCreateWithPriority(&job_k_in_, cudaStreamNonBlocking, greatest));
+      LBM_CUDA(cudaStreamCreateWithPriority(&job_k_out_, cudaStreamNonBlocking, greatest));
+      nvtxNameCudaStreamA(job_s_in_, "lbmgpu job h2d");
+      nvtxNameCudaStreamA(job_s_out_, "lbmgpu job d2h");
+      nvtxNameCudaStreamA(job_k_in_, "lbmgpu job load layout");
+      nvtxNameCudaStreamA(job_k_out_, "lbmgpu job store layout");
+    }
+    while (job_ev_.size() < 5 * size_t(C) + 1) {
+      cudaEvent_t e;
+      LBM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      job_ev_.push_back(e);
+    }
+    cudaEvent_t* copied = job_ev_.data();        // h2d of chunk i done
+    cudaEvent_t* loaded = copied + C;            // chunk i in the lattice (staging free)
+    cudaEvent_t* final_ev = loaded + C;          // chunk i's planes final
+    cudaEvent_t* gathered = final_ev + C;        // chunk i in its staging buffer
+    cudaEvent_t* stored = gathered + C;          // d2h of chunk i done (staging free)
+    cudaEvent_t start = job_ev_[5 * size_t(C)];
+    // LBMGPU_JOB_TRACE=1: per-chunk timeline (ms after the job start) on stderr
+    const bool trace = std::getenv("LBMGPU_JOB_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t e;
+      LBM_CUDA(cudaEventCreate(&e));
+      LBM_CUDA(cudaEventRecord(e, st));
+      tev.push_back(e);
+    };
+    tmark(stream_);
+    // the side streams start after whatever the engine stream holds
+    LBM_CUDA(cudaEventRecord(start, stream_));
+    for (cudaStream_t st : {job_s_in_, job_s_out_, job_k_in_, job_k_out_})
+      LBM_CUDA(cudaStreamWaitEvent(st, start, 0));
+    double* buf = pt.buf[0].get();
+    auto chunk_planes = [&](uint32_t i, uint32_t& c0, uint32_t& w) {
+      c0 = za + i * k * ws;
+      w = std::min<uint32_t>(k * ws, za + nzf - c0);
+    };
+    const unsigned tiles = static_cast<unsigned>(ceil_div(nx_, kJobTx) * uint64_t(ny_));
+    auto smem_of = [&](uint32_t w) { return size_t(kJobTx) * (w * kQ + 1) * 8; };
+    LBM_CUDA(cudaFuncSetAttribute(k_job_chunk<true, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_of(wc))));
+    LBM_CUDA(cudaFuncSetAttribute(k_job_chunk<true, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_of(wc))));
+    // every load up front: 2-D copy into staging buffer i % 2 (h2d stream),
+    // then the layout kernel (load-layout stream)
+    for (uint32_t i = 0; i < C; ++i) {
+      uint32_t c0, w;
+      chunk_planes(i, c0, w);
+      double* st = job_in_[i & 1].get();
+      if (i >= 2) LBM_CUDA(cudaStreamWaitEvent(job_s_in_, loaded[i - 2], 0));
+      LBM_CUDA(cudaMemcpy2DAsync(st, size_t(w) * kQ * 8, host_in + uint64_t(c0 - za) * kQ,
+                                 size_t(nzf) * kQ * 8, size_t(w) * kQ * 8, R, cudaMemcpyHostToDevice,
+                                 job_s_in_));
+      LBM_CUDA(cudaEventRecord(copied[i], job_s_in_));
+      tmark(job_s_in_);
+      LBM_CUDA(cudaStreamWaitEvent(job_k_in_, copied[i], 0));
+      k_job_chunk<true, false><<<tiles, 256, smem_of(w), job_k_in_>>>(
+          buf, job_col_of_.get(), w, c0, nx_, ny_, st);
+      LBM_CHECK_LAUNCH();
+      LBM_CUDA(cudaEventRecord(loaded[i], job_k_in_));
+      tmark(job_k_in_);
+    }
+    // chunk i leaves: layout kernel into staging buffer i % 2 (store-layout
+    // stream), then the 2-D copy (d2h stream)
+    auto store_chunk = [&](uint32_t i) {
+      LBM_CUDA(cudaEventRecord(final_ev[i], stream_));
+      tmark(stream_);
+      LBM_CUDA(cudaStreamWaitEvent(job_k_out_, final_ev[i], 0));
+      if (i >= 2) LBM_CUDA(cudaStreamWaitEvent(job_k_out_, stored[i - 2], 0));
+      uint32_t c0, w;
+      chunk_planes(i, c0, w);
+      double* st = job_out_[i & 1].get();
+      k_job_chunk<true, true><<<tiles, 256, smem_of(w), job_k_out_>>>(
+          buf, job_col_of_.get(), w, c0, nx_, ny_, st);
+      LBM_CHECK_LAUNCH();
+      LBM_CUDA(cudaEventRecord(gathered[i], job_k_out_));
+      tmark(job_k_out_);
+      LBM_CUDA(cudaStreamWaitEvent(job_s_out_, gathered[i], 0));
+      LBM_CUDA(cudaMemcpy2DAsync(host_out + uint64_t(c0 - za) * kQ, size_t(nzf) * kQ * 8, st,
+                                 size_t(w) * kQ * 8, size_t(w) * kQ * 8, R,
+                                 cudaMemcpyDeviceToHost, job_s_out_));
+      LBM_CUDA(cudaEventRecord(stored[i], job_s_out_));
+      tmark(job_s_out_);
+    };
+    // the sweeps in diagonal rounds on the engine stream
+    const long T = steps;
+    for (long L = 0; L < T + long(S) - 1; ++L) {
+      for (long j = std::min<long>(L, long(S) - 1); j >= 0; --j) {
+        const long s = L - j;
+        if (s >= T) continue;
+        if (s == 0 && j % k == 0) LBM_CUDA(cudaStreamWaitEvent(stream_, loaded[j / k], 0));
+        const uint32_t z0 = za + uint32_t(j) * ws, z1 = std::min<uint32_t>(z0 + ws, za + nzf);
+        DirectArgs a = args(pt, z0 * static_cast<uint32_t>(P_), (z1 - z0) * static_cast<uint32_t>(P_),
+                            t, 0, 0);
+        aa_sub(s & 1, a, (s & 1) ? "full_aa_odd_soa" : "full_aa_even_soa");
+        if (s != T - 1) continue;
+        // chunk i is final once slab (i+1)*k (its upper neighbour) has done
+        // its last sub-step; the last chunk after the last slab
+        if (j % k == 0 && j > 0) store_chunk(static_cast<uint32_t>(j / k - 1));
+        if (j == long(S) - 1) store_chunk(C - 1);
+      }
+    }
+    stats_.add_launches(2 * long(C));
+    for (cudaStream_t st : {job_s_in_, job_k_in_, stream_, job_k_out_, job_s_out_})
+      LBM_CUDA(cudaStreamSynchronize(st));
+    if (trace) {
+      auto ms = [&](size_t i) {
+        float f = 0;
+        cudaEventElapsedTime(&f, tev[0], tev[i]);
+        return f;
+      };
+      fprintf(stderr, "run_job: S=%u slabs x %u planes, C=%u chunks x %u planes, T=%ld\n", S, ws, C,
+              wc, T);
+      for (uint32_t i = 0; i < C; ++i)
+        fprintf(stderr,
+                "  chunk %2u copied %8.2f loaded %8.2f  final %8.2f gathered %8.2f stored %8.2f ms\n",
+                i, ms(1 + 2 * i), ms(2 + 2 * i), ms(1 + 2 * C + 3 * i), ms(2 + 2 * C + 3 * i),
+                ms(3 + 2 * C + 3 * i));
+      for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
+    return true;
   }
 
   // One-step sweeps over z-slabs (halo.hpp phases 2 / 3), per lattice step:
@@ -1442,6 +1662,15 @@ class DirectEngine final : public Engine {
   // CTAs retire and refill warps in smaller groups than 2 x 8 warps:
   // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830.
   int minb_ = 4;
+  // pipelined job (run_job): column plan, staging, copy streams, events
+  bool job_checked_ = false, job_ok_ = false;
+  uint32_t job_za_ = 0, job_zb_ = 0;
+  uint64_t job_cols_ = 0;
+  DevBuf<uint32_t> job_col_of_;
+  DevBuf<double> job_in_[2], job_out_[2];
+  cudaStream_t job_s_in_ = nullptr, job_s_out_ = nullptr;    // PCIe copies
+  cudaStream_t job_k_in_ = nullptr, job_k_out_ = nullptr;    // layout kernels
+  std::vector<cudaEvent_t> job_ev_;
   uint64_t fused_bytes_ = 96ull << 20;  // fused multi-sweep launch threshold
   int sm_count_ = 148;
   std::vector<Part> parts_;

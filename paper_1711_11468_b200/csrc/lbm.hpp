@@ -252,6 +252,16 @@ class Engine {
   // owns the arrays.  Returns device pointers.
   virtual void macro_fields(double* d_rho, double* d_u) = 0;
 
+  // Pipelined job: load_state(host_in) + advance(steps) + snapshot(host_out)
+  // with the host transfers overlapped with the sweeps (pinned host buffers
+  // of n_fluid * 19 doubles).  Returns false, having done nothing, when the
+  // engine cannot pipeline this job; the caller then runs the plain
+  // sequence.  Bitwise the plain sequence's result.
+  virtual bool run_job(const TrtArgs& t, long steps, const double* host_in, double* host_out) {
+    (void)t; (void)steps; (void)host_in; (void)host_out;
+    return false;
+  }
+
   // list structure export (ConfigError for direct engines)
   virtual void export_structure(int32_t* nodes, uint32_t* adj,
                                 uint64_t* starts, uint64_t* total) {

@@ -73,6 +73,7 @@ def _load():
     L.lbmgpu_n_fluid.argtypes = [vp, P(u64)]
     L.lbmgpu_snapshot.argtypes = [vp, vp, u64]
     L.lbmgpu_load_state.argtypes = [vp, vp, u64]
+    L.lbmgpu_run.argtypes = [vp, d, d, vp, C.c_long, vp, u64, vp, u64, P(i)]
     L.lbmgpu_load_perturbed.argtypes = [vp, u64, d]
     L.lbmgpu_total_mass.argtypes = [vp, P(d)]
     L.lbmgpu_fingerprint.argtypes = [vp, P(u64)]
@@ -500,6 +501,22 @@ class Kernel:
     def load_state(self, state) -> None:
         s = np.ascontiguousarray(state, np.float64)
         _check(lib.lbmgpu_load_state(self._h, s.ctypes.data, s.size))
+
+    def run(self, state, params: TrtParams, force: BodyForce, steps: int,
+            out: Optional[np.ndarray] = None):
+        """load_state(state) + advance(steps) + snapshot(out) as one job
+        (lbmgpu_run): bitwise the three calls; the host transfers overlap the
+        sweeps when the lattice supports it and both buffers are page-locked
+        (PinnedBuffer).  Returns (out, pipelined)."""
+        s = np.ascontiguousarray(state, np.float64)
+        if out is None:
+            out = np.empty(self._n * Q, np.float64)
+        _check_out(out, self._n * Q, "snapshot")
+        g = (C.c_double * 3)(*[float(v) for v in force.g])
+        piped = C.c_int()
+        _check(lib.lbmgpu_run(self._h, params.omega_plus, params.magic_lambda, g, int(steps),
+                              s.ctypes.data, s.size, out.ctypes.data, out.size, C.byref(piped)))
+        return out, bool(piped.value)
 
     # process-local rows (split domains; == the whole state with one process)
     def local_rows(self) -> int:

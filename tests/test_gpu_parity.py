@@ -228,6 +228,76 @@ def test_list_aa_aos_staging_tiles_against_oracle(shape, kind, dims, port, monke
     assert "list_aa_odd_aos" in k.kernel_stats()
 
 
+RUN_JOB_CASES = [
+    # (kind, dims, steps, JOB_SLABS, JOB_CHUNK, pipelined for aa-soa)
+    ("channel", (16, 12, 10), 6, "128", "4", True),
+    ("channel", (32, 12, 40), 10, "7", "2", True),     # ragged slabs and chunks
+    ("channel", (24, 16, 67), 12, "3", "1", True),     # fewer slabs than steps
+    ("channel", (16, 8, 130), 4, "128", "4", True),    # more slabs than steps
+    ("slit", (6, 5, 37), 8, "5", "3", True),
+    ("channel", (32, 16, 33), 2, "1", "1", True),      # one slab, one chunk
+    ("pipe", (9, 12, 13), 4, "128", "4", False),       # columns differ: plain sequence
+    ("blocks", (12, 10, 10), 4, "128", "4", False),    # periodic z, obstacles: plain
+]
+
+
+@pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa", "aa-aos", "blk-push-soa", "list-aa-soa"])
+@pytest.mark.parametrize("kind,dims,steps,slabs,chunk,piped", RUN_JOB_CASES)
+def test_run_job_equals_load_advance_snapshot(name, kind, dims, steps, slabs, chunk, piped, port,
+                                              monkeypatch):
+    """lbmgpu_run (load_state + advance + snapshot in one call, host
+    transfers pipelined with diagonal-round sweeps over z slabs where the
+    lattice allows) is bitwise the three separate calls and the oracle, for
+    page-locked and for pageable buffers, in place (out aliases in) or not;
+    the pipelined schedule runs exactly where documented."""
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")  # small boxes: per-sweep launches
+    monkeypatch.setenv("LBMGPU_JOB_SLABS", slabs)
+    monkeypatch.setenv("LBMGPU_JOB_CHUNK", chunk)
+    spec = lbm.GeometrySpec(kind, *dims)
+    _, _, nf = port.geometry(kind, *dims)
+    init = port.perturbed(nf, 41)
+    fam = "half" if name.startswith("list-") else "full"
+    expect, _ = port.run(fam, kind, *dims, steps, PARAMS.omega_plus, g=G_TEST, init=init)
+    ref = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    ref.load_state(init)
+    ref.advance(PARAMS, FORCE, steps)
+    plain = ref.snapshot()
+    assert np.array_equal(plain, expect)
+    k = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    bin_, bout = lbm.PinnedBuffer(nf * 19), lbm.PinnedBuffer(nf * 19)
+    bin_.array[:] = init
+    out, pipelined = k.run(bin_.array, PARAMS, FORCE, steps, out=bout.array)
+    assert pipelined == (piped and name in ("aa-soa", "aa-vec-soa"))
+    assert np.array_equal(out, expect), (name, kind, dims)
+    # again from the result, in place (out aliases in): 2 * steps in all
+    out2, _ = k.run(bout.array, PARAMS, FORCE, steps, out=bout.array)
+    ref.advance(PARAMS, FORCE, steps)
+    assert np.array_equal(out2, ref.snapshot())
+    # pageable buffers: always the plain sequence, same result (a fresh
+    # lattice: load_state writes fluid nodes only, and the solid records of
+    # a full lattice carry the populations in flight -- as in the reference,
+    # full_lattice.cpp:88-100)
+    k3 = lbm.make_kernel(lbm.make_descriptor(name), spec)
+    out3, p3 = k3.run(init, PARAMS, FORCE, steps)
+    assert not p3 and np.array_equal(out3, expect)
+    bin_.free()
+    bout.free()
+
+
+def test_run_job_validation():
+    """lbmgpu_run validates like load_state / advance / snapshot."""
+    k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("channel", 16, 12, 10))
+    n = k.n_fluid() * 19
+    with pytest.raises(lbm.ConfigError) as e:
+        k.run(np.zeros(n - 1), PARAMS, FORCE, 2)
+    assert "state size" in str(e.value)
+    with pytest.raises(lbm.ConfigError) as e:
+        k.run(np.zeros(n), PARAMS, FORCE, 3)
+    assert "even step count" in str(e.value)
+    with pytest.raises(lbm.ConfigError):
+        k.run(np.zeros(n), lbm.TrtParams(2.5), FORCE, 2)
+
+
 def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
     """Memory-safety check in place of compute-sanitizer (closed on this
     pool): with LBMGPU_GUARD=1 every device buffer carries 4 KiB guard zones
