@@ -262,6 +262,15 @@ class Kernel {
   void load_state(std::span<const double> s) {
     check(lbmgpu_load_state(ctx_.get(), s.data(), s.size()));
   }
+  // load_state(in) + advance(steps) + snapshot(out) as one job (lbmgpu_run);
+  // returns whether the transfers were pipelined with the sweeps.
+  bool run(std::span<const double> in, const TrtParams& p, const BodyForce& g, long steps,
+           std::span<double> out) {
+    int piped = 0;
+    check(lbmgpu_run(ctx_.get(), p.omega_plus, p.magic_lambda, g.g.data(), steps, in.data(),
+                     in.size(), out.data(), out.size(), &piped));
+    return piped != 0;
+  }
   void load_perturbed(std::uint64_t seed, double amplitude = 1e-3) {
     check(lbmgpu_load_perturbed(ctx_.get(), seed, amplitude));
   }

@@ -827,23 +827,27 @@ class DirectEngine final : public Engine {
     const Part& pt = parts_[0];
     const uint32_t za = job_za_, nzf = job_zb_ - job_za_;
     const uint64_t R = job_cols_;
-    // S compute slabs of ws planes, chunks of k slabs.  Measured on the cfg-5
-    // job: one plane per slab (the most skew: the first
-    // chunks leave earliest) and 16-plane chunks (2-D copy rows of 2,432 B)
-    int slabs = 512, k = 16;
+    // S compute slabs of ws planes; loads move chunks of ki slabs, stores
+    // chunks of ko slabs.  Measured on the cfg-5 job:
+    // one plane per slab (the most skew: the first chunks leave earliest),
+    // 16-plane loads and 32-plane stores (2-D copy rows of 2,432 / 4,864 B;
+    // the device-to-host 2-D copies need the wider rows)
+    int slabs = 512, ki = 16, ko = 32;
     if (const char* e = std::getenv("LBMGPU_JOB_SLABS")) slabs = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("LBMGPU_JOB_CHUNK")) k = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LBMGPU_JOB_CHUNK")) ki = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LBMGPU_JOB_CHUNK_OUT")) ko = std::max(1, std::atoi(e));
     const uint32_t ws = static_cast<uint32_t>(ceil_div(nzf, uint64_t(std::min<uint32_t>(slabs, nzf))));
     const uint32_t S = static_cast<uint32_t>(ceil_div(nzf, ws));
     // a chunk's layout tile must fit the shared memory: kJobTx x w x 19 doubles
-    k = static_cast<int>(std::max<uint32_t>(
-        1, std::min<uint32_t>(uint32_t(k), ((200u << 10) / (kJobTx * 8) - 1) / kQ / ws)));
-    const uint32_t C = static_cast<uint32_t>(ceil_div(S, uint64_t(k)));
-    const uint32_t wc = std::min<uint32_t>(k * ws, nzf);  // planes per chunk (staging width)
-    const uint64_t stage_elems = R * wc * kQ;
+    const uint32_t kmax = std::max<uint32_t>(1, ((200u << 10) / (kJobTx * 8) - 1) / kQ / ws);
+    ki = static_cast<int>(std::min<uint32_t>(uint32_t(ki), kmax));
+    ko = static_cast<int>(std::min<uint32_t>(uint32_t(ko), kmax));
+    const uint32_t Ci = static_cast<uint32_t>(ceil_div(S, uint64_t(ki)));
+    const uint32_t Co = static_cast<uint32_t>(ceil_div(S, uint64_t(ko)));
+    const uint32_t wci = std::min<uint32_t>(ki * ws, nzf), wco = std::min<uint32_t>(ko * ws, nzf);
     for (int bf = 0; bf < 2; ++bf) {
-      if (job_in_[bf].size() < stage_elems) job_in_[bf].alloc(stage_elems);
-      if (job_out_[bf].size() < stage_elems) job_out_[bf].alloc(stage_elems);
+      if (job_in_[bf].size() < R * wci * kQ) job_in_[bf].alloc(R * wci * kQ);
+      if (job_out_[bf].size() < R * wco * kQ) job_out_[bf].alloc(R * wco * kQ);
     }
     if (!job_s_in_) {
       // layout-kernel streams at the greatest priority: their CTAs take SM
@@ -859,17 +863,18 @@ class DirectEngine final : public Engine {
       nvtxNameCudaStreamA(job_k_in_, "lbmgpu job load layout");
       nvtxNameCudaStreamA(job_k_out_, "lbmgpu job store layout");
     }
-    while (job_ev_.size() < 5 * size_t(C) + 1) {
+    const size_t nev = 2 * size_t(Ci) + 3 * size_t(Co) + 1;
+    while (job_ev_.size() < nev) {
       cudaEvent_t e;
       LBM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       job_ev_.push_back(e);
     }
-    cudaEvent_t* copied = job_ev_.data();        // h2d of chunk i done
-    cudaEvent_t* loaded = copied + C;            // chunk i in the lattice (staging free)
-    cudaEvent_t* final_ev = loaded + C;          // chunk i's planes final
-    cudaEvent_t* gathered = final_ev + C;        // chunk i in its staging buffer
-    cudaEvent_t* stored = gathered + C;          // d2h of chunk i done (staging free)
-    cudaEvent_t start = job_ev_[5 * size_t(C)];
+    cudaEvent_t* copied = job_ev_.data();      // h2d of load chunk i done
+    cudaEvent_t* loaded = copied + Ci;         // load chunk i in the lattice (staging free)
+    cudaEvent_t* final_ev = loaded + Ci;       // store chunk i's planes final
+    cudaEvent_t* gathered = final_ev + Co;     // store chunk i in its staging buffer
+    cudaEvent_t* stored = gathered + Co;       // d2h of store chunk i done (staging free)
+    cudaEvent_t start = job_ev_[nev - 1];
     // LBMGPU_JOB_TRACE=1: per-chunk timeline (ms after the job start) on stderr
     const bool trace = std::getenv("LBMGPU_JOB_TRACE") != nullptr;
     std::vector<cudaEvent_t> tev;
@@ -886,23 +891,23 @@ class DirectEngine final : public Engine {
     for (cudaStream_t st : {job_s_in_, job_s_out_, job_k_in_, job_k_out_})
       LBM_CUDA(cudaStreamWaitEvent(st, start, 0));
     double* buf = pt.buf[0].get();
-    auto chunk_planes = [&](uint32_t i, uint32_t& c0, uint32_t& w) {
-      c0 = za + i * k * ws;
-      w = std::min<uint32_t>(k * ws, za + nzf - c0);
+    auto chunk_planes = [&](uint32_t i, int kk, uint32_t& c0, uint32_t& w) {
+      c0 = za + i * kk * ws;
+      w = std::min<uint32_t>(kk * ws, za + nzf - c0);
     };
     const unsigned tiles = static_cast<unsigned>(ceil_div(nx_, kJobTx) * uint64_t(ny_));
     auto smem_of = [&](uint32_t w) { return size_t(kJobTx) * (w * kQ + 1) * 8; };
     LBM_CUDA(cudaFuncSetAttribute(k_job_chunk<true, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_of(wc))));
+                                  static_cast<int>(smem_of(wci))));
     LBM_CUDA(cudaFuncSetAttribute(k_job_chunk<true, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_of(wc))));
+                                  static_cast<int>(smem_of(wco))));
     // every load up front: 2-D copy into staging buffer i % 2 (h2d stream),
     // then the layout kernel (load-layout stream)
-    for (uint32_t i = 0; i < C; ++i) {
+    for (uint32_t i = 0; i < Ci; ++i) {
       uint32_t c0, w;
-      chunk_planes(i, c0, w);
+      chunk_planes(i, ki, c0, w);
       double* st = job_in_[i & 1].get();
       if (i >= 2) LBM_CUDA(cudaStreamWaitEvent(job_s_in_, loaded[i - 2], 0));
       LBM_CUDA(cudaMemcpy2DAsync(st, size_t(w) * kQ * 8, host_in + uint64_t(c0 - za) * kQ,
@@ -917,15 +922,15 @@ class DirectEngine final : public Engine {
       LBM_CUDA(cudaEventRecord(loaded[i], job_k_in_));
       tmark(job_k_in_);
     }
-    // chunk i leaves: layout kernel into staging buffer i % 2 (store-layout
-    // stream), then the 2-D copy (d2h stream)
+    // store chunk i leaves: layout kernel into staging buffer i % 2
+    // (store-layout stream), then the 2-D copy (d2h stream)
     auto store_chunk = [&](uint32_t i) {
       LBM_CUDA(cudaEventRecord(final_ev[i], stream_));
       tmark(stream_);
       LBM_CUDA(cudaStreamWaitEvent(job_k_out_, final_ev[i], 0));
       if (i >= 2) LBM_CUDA(cudaStreamWaitEvent(job_k_out_, stored[i - 2], 0));
       uint32_t c0, w;
-      chunk_planes(i, c0, w);
+      chunk_planes(i, ko, c0, w);
       double* st = job_out_[i & 1].get();
       k_job_chunk<true, true><<<tiles, 256, smem_of(w), job_k_out_>>>(
           buf, job_col_of_.get(), w, c0, nx_, ny_, st);
@@ -945,19 +950,19 @@ class DirectEngine final : public Engine {
       for (long j = std::min<long>(L, long(S) - 1); j >= 0; --j) {
         const long s = L - j;
         if (s >= T) continue;
-        if (s == 0 && j % k == 0) LBM_CUDA(cudaStreamWaitEvent(stream_, loaded[j / k], 0));
+        if (s == 0 && j % ki == 0) LBM_CUDA(cudaStreamWaitEvent(stream_, loaded[j / ki], 0));
         const uint32_t z0 = za + uint32_t(j) * ws, z1 = std::min<uint32_t>(z0 + ws, za + nzf);
         DirectArgs a = args(pt, z0 * static_cast<uint32_t>(P_), (z1 - z0) * static_cast<uint32_t>(P_),
                             t, 0, 0);
         aa_sub(s & 1, a, (s & 1) ? "full_aa_odd_soa" : "full_aa_even_soa");
         if (s != T - 1) continue;
-        // chunk i is final once slab (i+1)*k (its upper neighbour) has done
-        // its last sub-step; the last chunk after the last slab
-        if (j % k == 0 && j > 0) store_chunk(static_cast<uint32_t>(j / k - 1));
-        if (j == long(S) - 1) store_chunk(C - 1);
+        // store chunk i is final once slab (i+1)*ko (its upper neighbour) has
+        // done its last sub-step; the last chunk after the last slab
+        if (j % ko == 0 && j > 0) store_chunk(static_cast<uint32_t>(j / ko - 1));
+        if (j == long(S) - 1) store_chunk(Co - 1);
       }
     }
-    stats_.add_launches(2 * long(C));
+    stats_.add_launches(long(Ci) + long(Co));
     for (cudaStream_t st : {job_s_in_, job_k_in_, stream_, job_k_out_, job_s_out_})
       LBM_CUDA(cudaStreamSynchronize(st));
     if (trace) {
@@ -966,13 +971,13 @@ class DirectEngine final : public Engine {
         cudaEventElapsedTime(&f, tev[0], tev[i]);
         return f;
       };
-      fprintf(stderr, "run_job: S=%u slabs x %u planes, C=%u chunks x %u planes, T=%ld\n", S, ws, C,
-              wc, T);
-      for (uint32_t i = 0; i < C; ++i)
-        fprintf(stderr,
-                "  chunk %2u copied %8.2f loaded %8.2f  final %8.2f gathered %8.2f stored %8.2f ms\n",
-                i, ms(1 + 2 * i), ms(2 + 2 * i), ms(1 + 2 * C + 3 * i), ms(2 + 2 * C + 3 * i),
-                ms(3 + 2 * C + 3 * i));
+      fprintf(stderr, "run_job: S=%u slabs x %u planes, loads %u x %u planes, stores %u x %u planes, "
+              "T=%ld\n", S, ws, Ci, wci, Co, wco, T);
+      for (uint32_t i = 0; i < Ci; ++i)
+        fprintf(stderr, "  load  %2u copied %8.2f loaded %8.2f ms\n", i, ms(1 + 2 * i), ms(2 + 2 * i));
+      for (uint32_t i = 0; i < Co; ++i)
+        fprintf(stderr, "  store %2u final %8.2f gathered %8.2f stored %8.2f ms\n", i,
+                ms(1 + 2 * Ci + 3 * i), ms(2 + 2 * Ci + 3 * i), ms(3 + 2 * Ci + 3 * i));
       for (cudaEvent_t e : tev) cudaEventDestroy(e);
     }
     return true;

@@ -229,22 +229,23 @@ def test_list_aa_aos_staging_tiles_against_oracle(shape, kind, dims, port, monke
 
 
 RUN_JOB_CASES = [
-    # (kind, dims, steps, JOB_SLABS, JOB_CHUNK, pipelined for aa-soa)
-    ("channel", (16, 12, 10), 6, "128", "4", True),
-    ("channel", (32, 12, 40), 10, "7", "2", True),     # ragged slabs and chunks
-    ("channel", (24, 16, 67), 12, "3", "1", True),     # fewer slabs than steps
-    ("channel", (16, 8, 130), 4, "128", "4", True),    # more slabs than steps
-    ("slit", (6, 5, 37), 8, "5", "3", True),
-    ("channel", (32, 16, 33), 2, "1", "1", True),      # one slab, one chunk
-    ("pipe", (9, 12, 13), 4, "128", "4", False),       # columns differ: plain sequence
-    ("blocks", (12, 10, 10), 4, "128", "4", False),    # periodic z, obstacles: plain
+    # (kind, dims, steps, JOB_SLABS, JOB_CHUNK, JOB_CHUNK_OUT, pipelined for aa-soa)
+    ("channel", (16, 12, 10), 6, "512", "16", "32", True),   # the defaults
+    ("channel", (32, 12, 40), 10, "7", "2", "3", True),      # ragged slabs and chunks
+    ("channel", (24, 16, 67), 12, "3", "1", "1", True),      # fewer slabs than steps
+    ("channel", (16, 8, 130), 4, "128", "4", "9", True),     # more slabs than steps
+    ("slit", (6, 5, 37), 8, "5", "3", "2", True),
+    ("channel", (32, 16, 33), 2, "1", "1", "1", True),       # one slab, one chunk
+    ("channel", (40, 8, 24), 6, "512", "1", "64", True),     # chunk wider than the box
+    ("pipe", (9, 12, 13), 4, "512", "16", "32", False),      # columns differ: plain sequence
+    ("blocks", (12, 10, 10), 4, "512", "16", "32", False),   # periodic z, obstacles: plain
 ]
 
 
 @pytest.mark.parametrize("name", ["aa-soa", "aa-vec-soa", "aa-aos", "blk-push-soa", "list-aa-soa"])
-@pytest.mark.parametrize("kind,dims,steps,slabs,chunk,piped", RUN_JOB_CASES)
-def test_run_job_equals_load_advance_snapshot(name, kind, dims, steps, slabs, chunk, piped, port,
-                                              monkeypatch):
+@pytest.mark.parametrize("kind,dims,steps,slabs,chunk,chunk_out,piped", RUN_JOB_CASES)
+def test_run_job_equals_load_advance_snapshot(name, kind, dims, steps, slabs, chunk, chunk_out,
+                                              piped, port, monkeypatch):
     """lbmgpu_run (load_state + advance + snapshot in one call, host
     transfers pipelined with diagonal-round sweeps over z slabs where the
     lattice allows) is bitwise the three separate calls and the oracle, for
@@ -253,6 +254,7 @@ def test_run_job_equals_load_advance_snapshot(name, kind, dims, steps, slabs, ch
     monkeypatch.setenv("LBMGPU_FUSED_MB", "0")  # small boxes: per-sweep launches
     monkeypatch.setenv("LBMGPU_JOB_SLABS", slabs)
     monkeypatch.setenv("LBMGPU_JOB_CHUNK", chunk)
+    monkeypatch.setenv("LBMGPU_JOB_CHUNK_OUT", chunk_out)
     spec = lbm.GeometrySpec(kind, *dims)
     _, _, nf = port.geometry(kind, *dims)
     init = port.perturbed(nf, 41)
