@@ -944,8 +944,12 @@ class DirectEngine final : public Engine {
       LBM_CUDA(cudaEventRecord(stored[i], job_s_out_));
       tmark(job_s_out_);
     };
-    // the sweeps in diagonal rounds on the engine stream
+    // the sweeps in diagonal rounds on the engine stream; programmatic
+    // dependent launches (pdl_enter) hide the launch gap between slab
+    // launches (LBMGPU_JOB_PDL=0: plain launches)
     const long T = steps;
+    bool pdl = minb_ == 4 && !stats_.enabled();
+    if (const char* e = std::getenv("LBMGPU_JOB_PDL")) pdl = pdl && std::atoi(e) != 0;
     for (long L = 0; L < T + long(S) - 1; ++L) {
       for (long j = std::min<long>(L, long(S) - 1); j >= 0; --j) {
         const long s = L - j;
@@ -954,7 +958,22 @@ class DirectEngine final : public Engine {
         const uint32_t z0 = za + uint32_t(j) * ws, z1 = std::min<uint32_t>(z0 + ws, za + nzf);
         DirectArgs a = args(pt, z0 * static_cast<uint32_t>(P_), (z1 - z0) * static_cast<uint32_t>(P_),
                             t, 0, 0);
-        aa_sub(s & 1, a, (s & 1) ? "full_aa_odd_soa" : "full_aa_even_soa");
+        if (pdl) {
+          auto kern = (s & 1) ? k_full_aa_odd<true, false, 128, 4> : k_full_aa_even<true, false, 128, 4>;
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3(static_cast<unsigned>(ceil_div(a.count, 128)));
+          cfg.blockDim = dim3(128);
+          cfg.stream = stream_;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          LBM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+          stats_.count_launch();
+        } else {
+          aa_sub(s & 1, a, (s & 1) ? "full_aa_odd_soa" : "full_aa_even_soa");
+        }
         if (s != T - 1) continue;
         // store chunk i is final once slab (i+1)*ko (its upper neighbour) has
         // done its last sub-step; the last chunk after the last slab

@@ -232,8 +232,19 @@ __global__ void __launch_bounds__(256) k_full_collide(const DirectArgs a) {
   collide_node_pass<SOA, false>(a, c, n);
 }
 
+// Programmatic dependent launch (the pipelined job's slab launches,
+// DirectEngine::run_job): let the next grid in the stream be scheduled as
+// soon as every CTA of this one runs, then wait for the previous grid to
+// complete (its writes visible) before touching the lattice.  Both are
+// no-ops for a launch without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <bool SOA, bool CS, int TPB = 256, int MINB = 1>
 __global__ void __launch_bounds__(TPB, MINB) k_full_aa_even(const DirectArgs a) {
+  pdl_enter();
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
@@ -242,6 +253,7 @@ __global__ void __launch_bounds__(TPB, MINB) k_full_aa_even(const DirectArgs a) 
 
 template <bool SOA, bool CS, int TPB = 256, int MINB = 1>
 __global__ void __launch_bounds__(TPB, MINB) k_full_aa_odd(const DirectArgs a) {
+  pdl_enter();
   Coords c;
   uint32_t n;
   if (!decode(a, c, n)) return;
