@@ -173,6 +173,16 @@ def test_compute_without_gpu_fails_loudly():
         lbm.build_geometry(lbm.GeometrySpec("channel", 8, 6, 6))
 
 
+def test_run_entry_validates_without_device():
+    """lbmgpu_run (the pipelined job) rejects a missing context with the
+    ConfigError status before touching a device."""
+    g = (ctypes.c_double * 3)(1e-5, 0.0, 0.0)
+    piped = ctypes.c_int(7)
+    rc = L.lib.lbmgpu_run(None, 1.0, 3.0 / 16.0, g, 2, None, 0, None, 0, ctypes.byref(piped))
+    assert rc == 1
+    assert "ctx" in L.lib.lbmgpu_last_error().decode()
+
+
 def test_config_errors_before_device_work():
     """ConfigError is raised before any device allocation (harness.cpp:84-93):
     these fail with ConfigError even without a GPU."""
