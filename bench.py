@@ -670,8 +670,13 @@ def main():
     # state from the host, advance, read the final state back.
     if not args.no_e2e:
         job_steps = max(args.steps, CONFIGS[cid][4] // per)
-        e2e = run_e2e(lbm, k, params, force, per, job_steps, world, dist, torch, N)
-        e2e["job_lattice_steps"] = per * job_steps
+        try:
+            e2e = run_e2e(lbm, k, params, force, per, job_steps, world, dist, torch, N)
+            e2e["job_lattice_steps"] = per * job_steps
+        except Exception as e:  # report, never lose the device-timed line
+            if world > 1:
+                raise
+            e2e = {"value": None, "error": str(e)}
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
