@@ -845,9 +845,18 @@ class DirectEngine final : public Engine {
     const uint32_t Ci = static_cast<uint32_t>(ceil_div(S, uint64_t(ki)));
     const uint32_t Co = static_cast<uint32_t>(ceil_div(S, uint64_t(ko)));
     const uint32_t wci = std::min<uint32_t>(ki * ws, nzf), wco = std::min<uint32_t>(ko * ws, nzf);
-    for (int bf = 0; bf < 2; ++bf) {
-      if (job_in_[bf].size() < R * wci * kQ) job_in_[bf].alloc(R * wci * kQ);
-      if (job_out_[bf].size() < R * wco * kQ) job_out_[bf].alloc(R * wco * kQ);
+    try {  // no room for the staging (a lattice filling the GPU): plain sequence
+      for (int bf = 0; bf < 2; ++bf) {
+        if (job_in_[bf].size() < R * wci * kQ) job_in_[bf].alloc(R * wci * kQ);
+        if (job_out_[bf].size() < R * wco * kQ) job_out_[bf].alloc(R * wco * kQ);
+      }
+    } catch (const DeviceError&) {
+      for (int bf = 0; bf < 2; ++bf) {
+        job_in_[bf].release();
+        job_out_[bf].release();
+      }
+      cudaGetLastError();
+      return false;
     }
     if (!job_s_in_) {
       // layout-kernel streams at the greatest priority: their CTAs take SM
