@@ -16,12 +16,12 @@
 // exclusive scan of the fluid flags in box order.  A CTA owns a TX x TY x TZ
 // box tile; it stages the (TX+2) x (TY+2) halo rows over z in [z0-1, z0+TZ]
 // (two list ranges where the range wraps periodically in z) by 1-D TMA bulk
-// copies, every fluid node looks the records of its 18 entries up in the
-// staged rows -- the adjacency values stay the only source of addresses:
-// entry e is found in the staged list range that holds element e --
-// collides, and writes results for records in
-// the tile's own rows into the staged copy (marking the element), results
-// for halo rows straight to global memory.  The own rows then leave by
+// copies, and every fluid node looks each of its 18 entries up in the
+// staged rows (the adjacency values stay the only source of addresses:
+// entry e is found in the staged list range that holds element e),
+// collides, and writes results for records in the tile's own rows into the
+// staged copy (marking the element), results for halo rows straight to
+// global memory.  The own rows then leave by
 // coalesced stores of the marked elements only.  A record that is not found
 // in its expected staged row (cannot happen for a structure built by
 // build_structure, but nothing depends on it) is read and written in global
@@ -55,8 +55,8 @@ struct LTileShape {
   static constexpr int kT = TX * TY * TZ;
   static constexpr int kRows = (TX + 2) * (TY + 2);
   static constexpr int kInner = TX * TY;
-  // two ranges' 16-byte slack; a multiple of 4 so the write-back reads the
-  // marks of 4 elements as one 32-bit word
+  // two ranges' 16-byte slack; a multiple of 4 so the marks of the own rows
+  // are cleared with 16-byte stores
   static constexpr int kRowElems = ((TZ + 2) * kQ + 4 + 3) / 4 * 4;
   static constexpr size_t kStageBytes = size_t(kRows) * kRowElems * 8;
   static constexpr size_t kFlagBytes = size_t(kInner) * kRowElems;  // marks: own rows only
@@ -70,9 +70,10 @@ struct LTileShape {
 __device__ __forceinline__ uint32_t even_down(uint32_t v) { return v & ~1u; }
 __device__ __forceinline__ uint32_t even_up(uint32_t v) { return (v + 1u) & ~1u; }
 
+// 2 CTAs of 256 threads per SM (<= 128 registers); 4 of 128
 template <int TX, int TY, int TZ>
-__global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ)) k_list_aa_odd_aos_tile(const ListArgs a,
-                                                                       const LTileGeom g) {
+__global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
+    k_list_aa_odd_aos_tile(const ListArgs a, const LTileGeom g) {
   using S = LTileShape<TX, TY, TZ>;
   extern __shared__ __align__(128) unsigned char lt_smem[];
   double* sh = reinterpret_cast<double*>(lt_smem);
