@@ -38,10 +38,14 @@ __device__ __forceinline__ bool peer_aborted(const PeerArgs& pa) {
 // peer memory.  Each of the three z-planes a node touches has its own base
 // (own lattice, or the neighbour's for the crossing plane); warps without
 // an x/y wrap address every slot as base + a per-direction constant (the
-// fast path of aa_odd_node).  Its remote stores are complete when the
-// kernel is (kernel boundary), and k_peer_signal -- the next launch on the
-// stream -- publishes them with a system-scope fence + release store.  (A
-// per-block system fence here measured 1.7x slower on the boundary planes.)
+// fast path of aa_odd_node).  Every thread that stored into peer memory
+// ends with a system-scope fence, so its NVLink stores are visible to the
+// neighbour before the kernel completes, and k_peer_signal -- the next
+// launch on the stream -- publishes the epoch with a release store: the
+// order is the PTX memory model's, not an assumption about kernel
+// boundaries (round 1 measured such fences 1.7x slower on the
+// boundary planes, ~2 % of a step at 8 slabs -- the peer transport is
+// opt-in).
 __global__ void __launch_bounds__(128) k_full_aa_odd_peer(const DirectArgs a, const PeerArgs pa) {
   Coords c;
   uint32_t n;
@@ -83,6 +87,7 @@ __global__ void __launch_bounds__(128) k_full_aa_odd_peer(const DirectArgs a, co
 #pragma unroll
       for (int d = 0; d < kQ; ++d) p[d][0] = q[opp(d)];
     }
+    if (zb[0] != a.dst || zb[2] != a.dst) __threadfence_system();  // crossed a face
   }
 }
 
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(256) k_full_push_peer(const DirectArgs a, cons
     const int s = ((tm >> d) & 1u) ? dslot(opp(d)) : dslot(d);
     base[I(tz, s, ty, tx)] = q[d];
   }
+  if (lo || hi) __threadfence_system();  // crossing stores visible before the signal (see above)
 }
 
 // Epoch flags: each part owns 4 u64 flags, [0] even done by the lower
