@@ -53,16 +53,17 @@ struct __align__(16) LTileRow {
 template <int TX, int TY, int TZ>
 struct LTileShape {
   static constexpr int kT = TX * TY * TZ;
-  static constexpr int kRows = (TX + 2) * (TY + 2);
+  static constexpr int kRows = (TX + 2) * (TY + 2);  // halo rows incl. the 4 corners
+  static constexpr int kStaged = kRows - 4;            // corners are not staged
   static constexpr int kInner = TX * TY;
   // two ranges' 16-byte slack; a multiple of 4 so the marks of the own rows
   // are cleared with 16-byte stores
   static constexpr int kRowElems = ((TZ + 2) * kQ + 4 + 3) / 4 * 4;
-  static constexpr size_t kStageBytes = size_t(kRows) * kRowElems * 8;
+  static constexpr size_t kStageBytes = size_t(kStaged) * kRowElems * 8;
   static constexpr size_t kFlagBytes = size_t(kInner) * kRowElems;  // marks: own rows only
   static constexpr size_t kMetaBytes = size_t(kRows) * sizeof(LTileRow);
   static constexpr size_t kSmem = kStageBytes + kFlagBytes + kMetaBytes + 16;
-  static_assert(kRows * kRowElems < (1 << 14) && kInner * kRowElems < (1 << 13),
+  static_assert(kStaged * kRowElems < (1 << 14) && kInner * kRowElems < (1 << 13),
                 "packed staging positions");
   static_assert(kFlagBytes % 16 == 0 && kStageBytes % 16 == 0, "alignment");
 };
@@ -83,6 +84,13 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
                                               S::kMetaBytes);
   const uint32_t t = threadIdx.x;
   const uint32_t b = blockIdx.x;
+  auto is_corner = [](uint32_t h) {
+    const uint32_t hx = h / (TY + 2), hy = h % (TY + 2);
+    return (hx == 0 || hx == TX + 1) && (hy == 0 || hy == TY + 1);
+  };
+  auto staged_row = [](uint32_t h) {  // non-corner halo row -> staged row
+    return h - (h > 0) - (h > TY + 1) - (h > (TX + 1) * (TY + 2));
+  };
   const uint32_t z0 = (b % g.tiles_z) * TZ;
   const uint32_t y0 = ((b / g.tiles_z) % g.tiles_y) * TY;
   const uint32_t x0 = (b / (g.tiles_z * g.tiles_y)) * TX;
@@ -137,7 +145,13 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
   }
   __syncthreads();
   if (t < uint32_t(S::kRows)) {
-    const uint32_t base = t * S::kRowElems;
+    // staged row of halo row t: the corner rows (x0-1 / x0+TX, y0-1 / y0+TY)
+    // are not staged -- only the 4 corner nodes' diagonal entries point
+    // there, and those go to global memory -- so rows after a corner move
+    // up by one
+    const bool corner = is_corner(t);
+    if (corner) r0 = r0e = r1 = r1e = 0;
+    const uint32_t base = staged_row(t) * S::kRowElems;
     LTileRow m;
     m.lo0 = r0 * kQ;
     m.n0 = (r0e - r0) * kQ;
@@ -167,11 +181,12 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
   // halo row (the result is stored straight to global memory); kMiss = not
   // staged (read and written in global memory).
   constexpr uint32_t kDirect = 0x80000000u, kMiss = 0xffffffffu, kPos = (1u << 14) - 1;
-  // own row h_i = (hx, hy) = (i / TY + 1, i % TY + 1) has mark rows at i * kRowElems:
-  // mark index = staged element - (2 hx + TY + 1) * kRowElems
+  // own row h_i = (hx, hy) = (i / TY + 1, i % TY + 1), staged at row h - 2
+  // (two corners before it), has mark rows at i * kRowElems:
+  // mark index = staged element - (2 hx + TY - 1) * kRowElems
   auto mark_delta = [](uint32_t h) -> uint32_t {
     const uint32_t hx = h / (TY + 2);
-    return (2 * hx + TY + 1) * S::kRowElems;
+    return (2 * hx + TY - 1) * S::kRowElems;
   };
   // generic lookup: the row's first range, its second range, else kMiss
   auto lookup = [&](uint32_t h, uint32_t v) -> uint32_t {
@@ -195,20 +210,26 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
     for (int k = 1; k < kQ; ++k) {
       // record n + c_k (fluid neighbour): the first staged range of row h
       const uint32_t h = hown + uint32_t(cx(k) * (TY + 2) + cy(k));
-      const bool inner = uint32_t(int(tx) + cx(k)) < uint32_t(TX) &&
-                         uint32_t(int(ty) + cy(k)) < uint32_t(TY);
+      const bool inx = uint32_t(int(tx) + cx(k)) < uint32_t(TX);
+      const bool iny = uint32_t(int(ty) + cy(k)) < uint32_t(TY);
+      if (!inx && !iny) {  // a corner row (not staged) or bounce-back: global memory
+        pos[k - 1] = kMiss;
+        continue;
+      }
       const uint4 m0 = *reinterpret_cast<const uint4*>(&meta[h]);
       const uint32_t v = e[k - 1];
       const uint32_t p = v + m0.z;
       slow |= !(v - m0.x < m0.y);
-      pos[k - 1] = inner ? (p | ((p - mark_delta(h)) << 14)) : (p | kDirect);
+      pos[k - 1] = inx && iny ? (p | ((p - mark_delta(h)) << 14)) : (p | kDirect);
     }
     if (slow) {  // second ranges (periodic z wrap), bounce-back entries, misses
 #pragma unroll
       for (int k = 1; k < kQ; ++k) {
         uint32_t h = hown + uint32_t(cx(k) * (TY + 2) + cy(k));
-        bool inner = uint32_t(int(tx) + cx(k)) < uint32_t(TX) &&
-                     uint32_t(int(ty) + cy(k)) < uint32_t(TY);
+        const bool inx = uint32_t(int(tx) + cx(k)) < uint32_t(TX);
+        const bool iny = uint32_t(int(ty) + cy(k)) < uint32_t(TY);
+        if (!inx && !iny) continue;  // corner direction: kMiss from the fast path
+        bool inner = inx && iny;
         uint32_t p = lookup(h, e[k - 1]);
         if (p == kMiss) {  // bounce-back closure: the node's own record
           h = hown;
@@ -220,20 +241,22 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
       }
     }
   }
+  // entries outside the staged rows (corner directions, misses): read now,
+  // ahead of the copies
+  double q[kQ];
+  if (fluid) {
+    if (pos0 == kMiss) q[0] = a.dst[uint64_t(n) * kQ];
+#pragma unroll
+    for (int d = 1; d < kQ; ++d)
+      if (pos[opp(d) - 1] == kMiss) q[d] = a.dst[e[opp(d) - 1]];
+  }
   tma::mbar_wait(bar, 0);
   if (fluid) {
-    double q[kQ];
-    if (!slow && pos0 != kMiss) {
-      q[0] = sh[pos0 & kPos];
+    if (pos0 != kMiss) q[0] = sh[pos0 & kPos];
 #pragma unroll
-      for (int d = 1; d < kQ; ++d) q[d] = sh[pos[opp(d) - 1] & kPos];
-    } else {
-      q[0] = pos0 != kMiss ? sh[pos0 & kPos] : a.dst[uint64_t(n) * kQ];
-#pragma unroll
-      for (int d = 1; d < kQ; ++d) {
-        const uint32_t p = pos[opp(d) - 1];
-        q[d] = p == kMiss ? a.dst[e[opp(d) - 1]] : sh[p & kPos];
-      }
+    for (int d = 1; d < kQ; ++d) {
+      const uint32_t p = pos[opp(d) - 1];
+      if (p != kMiss) q[d] = sh[p & kPos];
     }
     collide(q, a.trt);
     if (pos0 != kMiss) {
@@ -261,7 +284,7 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
     const uint32_t h = (i / TY + 1) * (TY + 2) + (i % TY + 1);
     const LTileRow& m = meta[h];
     const uint32_t cnt0 = m.cnt0, cnt = m.cnt0 + m.cnt1;
-    const double* src = sh + h * S::kRowElems;
+    const double* src = sh + (h - 2) * S::kRowElems;  // staged row of an own row
     const uint8_t* fr = flag + i * S::kRowElems;
     double* g0 = a.dst + m.g0;
     double* g1 = a.dst + m.g1 - cnt0;
