@@ -544,11 +544,11 @@ class ListEngine final : public Engine {
   }
 
   // AoS AA odd step through 3-D staging tiles (list_aos_tile.cuh)
-  template <int TX, int TY, int TZ>
+  template <int TX, int TY, int TZ, bool EDGES = true>
   void launch_aos_odd_tile_shape(const ListArgs& a) {
-    using S = LTileShape<TX, TY, TZ>;
+    using S = LTileShape<TX, TY, TZ, EDGES>;
     static_assert(TZ % 2 == 0, "staged rows must stay 16-byte aligned");
-    auto kern = k_list_aa_odd_aos_tile<TX, TY, TZ>;
+    auto kern = k_list_aa_odd_aos_tile<TX, TY, TZ, EDGES>;
     LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(S::kSmem)));
     LTileGeom g{};
@@ -565,13 +565,16 @@ class ListEngine final : public Engine {
     stats_.end(tok, stream_);
   }
   // Tile shape (measured on cfg 2 / cfg 4): 4 x 4 x 16
-  // (256 threads, 2 CTAs/SM).  LBMGPU_LTILE selects the other instantiated
-  // shapes for the tests (2: 4 x 4 x 8, 5: 2 x 2 x 32).
+  // with only the tile's own rows staged (256 threads, 2 CTAs/SM).
+  // LBMGPU_LTILE selects the other instantiated shapes for the tests: 1 =
+  // 4 x 4 x 16 with the edge halo rows staged too, 5 = 2 x 2 x 32 (halo
+  // rows, every wrap case), 12 = 4 x 4 x 8 (own rows, 128 threads).
   void launch_aos_odd_tiles(const ListArgs& a) {
     switch (ltile_) {
-      case 2: launch_aos_odd_tile_shape<4, 4, 8>(a); break;
-      case 5: launch_aos_odd_tile_shape<2, 2, 32>(a); break;
-      default: launch_aos_odd_tile_shape<4, 4, 16>(a); break;
+      case 1: launch_aos_odd_tile_shape<4, 4, 16, true>(a); break;
+      case 5: launch_aos_odd_tile_shape<2, 2, 32, true>(a); break;
+      case 12: launch_aos_odd_tile_shape<4, 4, 8, false>(a); break;
+      default: launch_aos_odd_tile_shape<4, 4, 16, false>(a); break;
     }
   }
 

@@ -14,10 +14,13 @@
 // z fastest, so the fluid nodes of one box row (x, y) inside a z range are
 // ONE contiguous list range: [crank(x, y, za), crank(x, y, zb)) with crank the
 // exclusive scan of the fluid flags in box order.  A CTA owns a TX x TY x TZ
-// box tile; it stages the (TX+2) x (TY+2) halo rows over z in [z0-1, z0+TZ]
-// (two list ranges where the range wraps periodically in z) by 1-D TMA bulk
-// copies, and every fluid node looks each of its 18 entries up in the
-// staged rows (the adjacency values stay the only source of addresses:
+// box tile; it stages its own TX x TY rows -- with EDGES also the edge halo
+// rows around them -- over z in [z0-1, z0+TZ] (two list ranges where the
+// range wraps periodically in z) by 1-D TMA bulk copies; entries into rows
+// that are not staged are read from global memory ahead of the copies and
+// stored there directly (own rows only measured fastest: the halo rows'
+// few needed slots cost more as staged whole records).  Every fluid node
+// looks each of its 18 entries up in the staged rows (the adjacency values stay the only source of addresses:
 // entry e is found in the staged list range that holds element e),
 // collides, and writes results for records in the tile's own rows into the
 // staged copy (marking the element), results for halo rows straight to
@@ -50,11 +53,11 @@ struct __align__(16) LTileRow {
   uint32_t cnt0, cnt1, pad0, pad1;  // elements copied per range (even counts)
 };
 
-template <int TX, int TY, int TZ>
+template <int TX, int TY, int TZ, bool EDGES = true>
 struct LTileShape {
   static constexpr int kT = TX * TY * TZ;
   static constexpr int kRows = (TX + 2) * (TY + 2);  // halo rows incl. the 4 corners
-  static constexpr int kStaged = kRows - 4;            // corners are not staged
+  static constexpr int kStaged = EDGES ? kRows - 4 : TX * TY;  // corners (edges) not staged
   static constexpr int kInner = TX * TY;
   // two ranges' 16-byte slack; a multiple of 4 so the marks of the own rows
   // are cleared with 16-byte stores
@@ -72,10 +75,10 @@ __device__ __forceinline__ uint32_t even_down(uint32_t v) { return v & ~1u; }
 __device__ __forceinline__ uint32_t even_up(uint32_t v) { return (v + 1u) & ~1u; }
 
 // 2 CTAs of 256 threads per SM (<= 128 registers); 4 of 128
-template <int TX, int TY, int TZ>
+template <int TX, int TY, int TZ, bool EDGES = true>
 __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
     k_list_aa_odd_aos_tile(const ListArgs a, const LTileGeom g) {
-  using S = LTileShape<TX, TY, TZ>;
+  using S = LTileShape<TX, TY, TZ, EDGES>;
   extern __shared__ __align__(128) unsigned char lt_smem[];
   double* sh = reinterpret_cast<double*>(lt_smem);
   uint8_t* flag = lt_smem + S::kStageBytes;
@@ -84,11 +87,13 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
                                               S::kMetaBytes);
   const uint32_t t = threadIdx.x;
   const uint32_t b = blockIdx.x;
-  auto is_corner = [](uint32_t h) {
+  auto is_corner = [](uint32_t h) {  // not staged
     const uint32_t hx = h / (TY + 2), hy = h % (TY + 2);
-    return (hx == 0 || hx == TX + 1) && (hy == 0 || hy == TY + 1);
+    const bool ex = hx == 0 || hx == TX + 1, ey = hy == 0 || hy == TY + 1;
+    return EDGES ? ex && ey : ex || ey;
   };
-  auto staged_row = [](uint32_t h) {  // non-corner halo row -> staged row
+  auto staged_row = [](uint32_t h) {  // staged halo row -> staged row
+    if (!EDGES) return (h / (TY + 2) - 1) * TY + (h % (TY + 2) - 1);
     return h - (h > 0) - (h > TY + 1) - (h > (TX + 1) * (TY + 2));
   };
   const uint32_t z0 = (b % g.tiles_z) * TZ;
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
   // mark index = staged element - (2 hx + TY - 1) * kRowElems
   auto mark_delta = [](uint32_t h) -> uint32_t {
     const uint32_t hx = h / (TY + 2);
-    return (2 * hx + TY - 1) * S::kRowElems;
+    return EDGES ? (2 * hx + TY - 1) * S::kRowElems : 0u;
   };
   // generic lookup: the row's first range, its second range, else kMiss
   auto lookup = [&](uint32_t h, uint32_t v) -> uint32_t {
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
       const uint32_t h = hown + uint32_t(cx(k) * (TY + 2) + cy(k));
       const bool inx = uint32_t(int(tx) + cx(k)) < uint32_t(TX);
       const bool iny = uint32_t(int(ty) + cy(k)) < uint32_t(TY);
-      if (!inx && !iny) {  // a corner row (not staged) or bounce-back: global memory
+      if (EDGES ? !inx && !iny : !inx || !iny) {  // not staged (or bounce-back): global memory
         pos[k - 1] = kMiss;
         continue;
       }
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
         uint32_t h = hown + uint32_t(cx(k) * (TY + 2) + cy(k));
         const bool inx = uint32_t(int(tx) + cx(k)) < uint32_t(TX);
         const bool iny = uint32_t(int(ty) + cy(k)) < uint32_t(TY);
-        if (!inx && !iny) continue;  // corner direction: kMiss from the fast path
+        if (EDGES ? !inx && !iny : !inx || !iny) continue;  // kMiss from the fast path
         bool inner = inx && iny;
         uint32_t p = lookup(h, e[k - 1]);
         if (p == kMiss) {  // bounce-back closure: the node's own record
@@ -284,7 +289,7 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
     const uint32_t h = (i / TY + 1) * (TY + 2) + (i % TY + 1);
     const LTileRow& m = meta[h];
     const uint32_t cnt0 = m.cnt0, cnt = m.cnt0 + m.cnt1;
-    const double* src = sh + (h - 2) * S::kRowElems;  // staged row of an own row
+    const double* src = sh + staged_row(h) * S::kRowElems;
     const uint8_t* fr = flag + i * S::kRowElems;
     double* g0 = a.dst + m.g0;
     double* g1 = a.dst + m.g1 - cnt0;

@@ -202,7 +202,7 @@ LIST_AOS_TILE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("shape", ["1", "2", "5"])
+@pytest.mark.parametrize("shape", ["0", "1", "5", "12"])
 @pytest.mark.parametrize("kind,dims", LIST_AOS_TILE_CASES)
 def test_list_aa_aos_staging_tiles_against_oracle(shape, kind, dims, port, monkeypatch):
     """list-aa-aos odd step through the 3-D staging tiles
@@ -324,7 +324,7 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
                 k.total_mass()
                 keep.append(k)
     monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
-    for shape in ("1", "2", "5"):  # list-aa-aos staging tiles (blk = 0)
+    for shape in ("0", "1", "5", "12"):  # list-aa-aos staging tiles (blk = 0)
         monkeypatch.setenv("LBMGPU_LTILE", shape)
         for spec in (small, tiled, lbm.GeometrySpec("pipe", 9, 12, 13)):
             k = lbm.make_kernel(lbm.make_descriptor("list-aa-aos"), spec)
