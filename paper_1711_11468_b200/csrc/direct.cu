@@ -513,8 +513,8 @@ class DirectEngine final : public Engine {
   template <int TY, int TZ>
   void aa_odd_aos_tile3d(const DirectArgs& a) {
     const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
-    auto kern = k_full_aa_odd_aos_tile3d<TY, TZ>;
-    constexpr size_t smem = pt_smem<TY, TZ>();
+    auto kern = k_full_aa_odd_aos_tile3d<TY, TZ, false>;
+    constexpr size_t smem = pt_smem<TY, TZ, false>();
     LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int tok = stats_.begin("full_aa_odd_aos", stream_);

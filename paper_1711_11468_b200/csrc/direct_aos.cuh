@@ -53,17 +53,26 @@ __global__ void __launch_bounds__(kAosTile) k_full_aos_tile(const DirectArgs a) 
 constexpr int kPtX = 16;
 constexpr int kPtW = kPtX + 4;                           // records per halo row
 constexpr uint32_t kPtRowBytes = kPtW * kQ * 8;         // 3040
-template <int kPtY, int kPtZ>
-constexpr size_t pt_smem() {
-  return size_t((kPtY + 2) * (kPtZ + 2)) * kPtRowBytes + 16;
+// staged rows of a 16 x TY x TZ tile: the (TY+2) x (TZ+2) halo rows, or
+// (HALO = false) only the TY x TZ own rows
+template <int kPtY, int kPtZ, bool HALO = true>
+__host__ __device__ constexpr int pt_rows() {
+  return HALO ? (kPtY + 2) * (kPtZ + 2) : kPtY * kPtZ;
 }
-// Halo rows of a 16 x TY x TZ tile at (x0, y0, z0) from AoS grid `src` into
-// shared memory `sh` (block-wide; ends with the copies in flight on `bar`).
-template <int kPtY, int kPtZ>
+template <int kPtY, int kPtZ, bool HALO = true>
+constexpr size_t pt_smem() {
+  return size_t(pt_rows<kPtY, kPtZ, HALO>()) * kPtRowBytes + 16;
+}
+// Rows of a 16 x TY x TZ tile at (x0, y0, z0) from AoS grid `src` into
+// shared memory `sh`, each as 20 whole records x0-2 .. x0+17 (block-wide;
+// ends with the copies in flight on `bar`): the halo rows, staged row
+// hz * (TY+2) + hy for halo position (hy, hz), or (HALO = false) the own
+// rows, staged row (hz-1) * TY + (hy-1).
+template <int kPtY, int kPtZ, bool HALO = true>
 __device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* src, double* sh,
                                              uint64_t* bar, uint32_t x0, uint32_t y0,
                                              uint32_t z0) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
+  constexpr int kPtRows = pt_rows<kPtY, kPtZ, HALO>();
   const uint64_t nx = a.nx;
   auto rec = [&](uint32_t zs, uint32_t y, uint32_t x) {  // record pointer (AoS)
     return src + ((uint64_t(zs) * a.ny + y) * nx + x) * kQ;
@@ -79,7 +88,8 @@ __device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* 
     if (t == 0) tma::mbar_arrive_expect_tx(bar, kPtRows * kPtRowBytes);
     __syncwarp();
     for (uint32_t row = t; row < uint32_t(kPtRows); row += 32) {
-      const uint32_t hy = row % (kPtY + 2), hz = row / (kPtY + 2);
+      const uint32_t hy = HALO ? row % (kPtY + 2) : row % kPtY + 1;
+      const uint32_t hz = HALO ? row / (kPtY + 2) : row / kPtY + 1;
       const uint32_t y = (y0 + a.ny + hy - 1) % a.ny;
       const uint32_t z = (z0 + a.nzl + hz - 1) % a.nzl;  // single part: zwrap
       double* dst = sh + size_t(row) * kPtW * kQ;
@@ -169,11 +179,18 @@ __host__ __device__ constexpr uint64_t slot_c_bits() {
 // from the tile's face nodes -- are stored straight to global memory.  The
 // own rows thus leave as full 32-byte sectors instead of one sector per
 // scattered 8-byte element.
-template <int kPtY, int kPtZ>
-__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(const DirectArgs a) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);
+// HALO = false (the default, measured faster): only the tile's own rows are
+// staged (48.6 KB, so 3 CTAs/SM at <= 80 registers instead of 2 of 109 KB);
+// a node's entries into the y / z halo rows (face nodes only) are loaded
+// from global memory ahead of the copies, and their results are stored
+// there directly as before.  cfg-5 box: odd step 3,098 -> 3,433 GB/s
+// ((256, 2): 120 registers, 3,193; (256, 4): 64 registers + spills, 2,821).
+template <int kPtY, int kPtZ, bool HALO = false>
+__global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
+    k_full_aa_odd_aos_tile3d(const DirectArgs a) {
+  constexpr int kPtRows = pt_rows<kPtY, kPtZ, HALO>();
   constexpr int kT = kPtX * kPtY * kPtZ;
-  constexpr int kRowElems = kPtW * kQ;  // 380 doubles per halo row
+  constexpr int kRowElems = kPtW * kQ;  // 380 doubles per staged row
   extern __shared__ __align__(128) unsigned char pt_smem[];
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
@@ -183,23 +200,35 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(c
   const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
   const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
   const uint32_t t = threadIdx.x;
-  pt_load_halo<kPtY, kPtZ>(a, a.dst, sh, bar, x0, y0, z0);
+  pt_load_halo<kPtY, kPtZ, HALO>(a, a.dst, sh, bar, x0, y0, z0);
   const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
   const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
   const bool solid = solid_node(a, x0 + tx, y0 + ty, z0 + tz, n);
-  tma::mbar_wait(bar, 0);
   auto at = [&](int hx, int hy, int hz) {
-    return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
+    const int row = HALO ? hz * (kPtY + 2) + hy : (hz - 1) * kPtY + (hy - 1);
+    return sh + (size_t(row) * kPtW + hx) * kQ;
   };
-  if (!solid) {
-    double q[kQ];
+  auto staged = [](int hy, int hz) { return HALO || (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ); };
+  const Idx<false> I{a.P, a.nx, a.ny};
+  Coords c;
+  decode_node(a, n, c);
+  double q[kQ];
+  if (!HALO && !solid) {  // entries into rows that are not staged: now, ahead of the copies
 #pragma unroll
-    for (int d = 0; d < kQ; ++d)
-      q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(opp(d))];
+    for (int d = 0; d < kQ; ++d) {
+      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+      if (!staged(hy, hz))
+        q[d] = a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+    }
+  }
+  tma::mbar_wait(bar, 0);
+  if (!solid) {
+#pragma unroll
+    for (int d = 0; d < kQ; ++d) {
+      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+      if (staged(hy, hz)) q[d] = at(int(tx) + 2 - cx(d), hy, hz)[dslot(opp(d))];
+    }
     collide(q, a.trt);
-    const Idx<false> I{a.P, a.nx, a.ny};
-    Coords c;
-    decode_node(a, n, c);
 #pragma unroll
     for (int d = 0; d < kQ; ++d) {
       const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
@@ -245,7 +274,7 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_aa_odd_aos_tile3d(c
     if (hy == kPtY) m &= ~yneg;
     if (hz == 1) m &= ~zpos;
     if (hz == kPtZ) m &= ~zneg;
-    const double* src = sh + size_t(hz * (kPtY + 2) + hy) * kRowElems;
+    const double* src = sh + size_t(HALO ? hz * (kPtY + 2) + hy : (hz - 1) * kPtY + (hy - 1)) * kRowElems;
     const uint64_t y = y0 + hy - 1, z = z0 + hz - 1;  // own rows: no y / z wrap
     double* row = a.dst + (z * a.ny + y) * nx * kQ;
     if (!xwrap) {
