@@ -526,8 +526,9 @@ class DirectEngine final : public Engine {
   template <int TY, int TZ>
   void pull_aos_tile3d(const DirectArgs& a, bool last, const char* name) {
     const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
-    auto kern = last ? k_full_pull_aos_tile3d<false, TY, TZ> : k_full_pull_aos_tile3d<true, TY, TZ>;
-    constexpr size_t smem = pt_smem<TY, TZ>();
+    auto kern = last ? k_full_pull_aos_tile3d<false, TY, TZ, false>
+                     : k_full_pull_aos_tile3d<true, TY, TZ, false>;
+    constexpr size_t smem = pt_smem<TY, TZ, false>();
     LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int tok = stats_.begin(name, stream_);

@@ -108,9 +108,13 @@ __device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* 
   }
 }
 
-template <bool COLLIDE, int kPtY, int kPtZ>
-__global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(const DirectArgs a) {
-  constexpr int kPtRows = (kPtY + 2) * (kPtZ + 2);  // halo rows
+// HALO = false (the default, measured faster): only the tile's own source
+// rows are staged, as in the AA odd step below; the face nodes' gathers
+// from y / z halo rows are loaded from global memory ahead of the copies.
+template <bool COLLIDE, int kPtY, int kPtZ, bool HALO = false>
+__global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
+    k_full_pull_aos_tile3d(const DirectArgs a) {
+  constexpr int kPtRows = pt_rows<kPtY, kPtZ, HALO>();
   extern __shared__ __align__(128) unsigned char pt_smem[];
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
@@ -121,19 +125,33 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ) k_full_pull_aos_tile3d(con
   const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
   const uint64_t nx = a.nx;
   const uint32_t t = threadIdx.x;
-  pt_load_halo<kPtY, kPtZ>(a, a.src, sh, bar, x0, y0, z0);
+  pt_load_halo<kPtY, kPtZ, HALO>(a, a.src, sh, bar, x0, y0, z0);
   const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
   const uint32_t n = ((z0 + tz) * a.ny + (y0 + ty)) * a.nx + (x0 + tx);
   const bool solid = solid_node(a, x0 + tx, y0 + ty, z0 + tz, n);
-  tma::mbar_wait(bar, 0);
   auto at = [&](int hx, int hy, int hz) {
-    return sh + (size_t(hz * (kPtY + 2) + hy) * kPtW + hx) * kQ;
+    const int row = HALO ? hz * (kPtY + 2) + hy : (hz - 1) * kPtY + (hy - 1);
+    return sh + (size_t(row) * kPtW + hx) * kQ;
   };
+  auto staged = [](int hy, int hz) { return HALO || (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ); };
   double q[kQ];
+  if (!HALO) {  // gathers from rows that are not staged: now, ahead of the copies
+    const Idx<false> I{a.P, a.nx, a.ny};
+    Coords c;
+    decode_node(a, n, c);
+#pragma unroll
+    for (int d = 1; d < kQ; ++d) {
+      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+      if (!staged(hy, hz)) q[d] = a.src[I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+    }
+  }
+  tma::mbar_wait(bar, 0);
   q[0] = at(tx + 2, ty + 1, tz + 1)[dslot(0)];
 #pragma unroll
-  for (int d = 1; d < kQ; ++d)
-    q[d] = at(int(tx) + 2 - cx(d), int(ty) + 1 - cy(d), int(tz) + 1 - cz(d))[dslot(d)];
+  for (int d = 1; d < kQ; ++d) {
+    const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+    if (staged(hy, hz)) q[d] = at(int(tx) + 2 - cx(d), hy, hz)[dslot(d)];
+  }
   if (COLLIDE && !solid) collide(q, a.trt);
   __syncthreads();  // every gather done: the centre records may be overwritten
   double* own = at(tx + 2, ty + 1, tz + 1);
