@@ -335,6 +335,7 @@ class DirectEngine final : public Engine {
       LBM_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, dev));
       // tuning knobs (defaults are the measured best)
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
+      if (const char* e = std::getenv("LBMGPU_TILE_BY")) tile_by_ = static_cast<uint32_t>(std::atoi(e));
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
         fused_bytes_ = uint64_t(std::atoll(e)) << 20;
     }
@@ -518,7 +519,9 @@ class DirectEngine final : public Engine {
     LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int tok = stats_.begin("full_aa_odd_aos", stream_);
-    kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(a);
+    DirectArgs at = a;
+    at.band = tile_by_;
+    kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(at);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);
   }
@@ -532,7 +535,9 @@ class DirectEngine final : public Engine {
     LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int tok = stats_.begin(name, stream_);
-    kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(a);
+    DirectArgs at = a;
+    at.band = tile_by_;
+    kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(at);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);
   }
@@ -1696,6 +1701,7 @@ class DirectEngine final : public Engine {
   // CTAs retire and refill warps in smaller groups than 2 x 8 warps:
   // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830.
   int minb_ = 4;
+  uint32_t tile_by_ = 8;  // AoS 3-D tiles: y tiles per traversal block (tile_origin)
   // pipelined job (run_job): column plan, staging, copy streams, events
   bool job_checked_ = false, job_ok_ = false;
   uint32_t job_za_ = 0, job_zb_ = 0;

@@ -108,6 +108,28 @@ __device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* 
   }
 }
 
+// Tile of block b: x fastest; then the (y, z) tiles in blocks of a.band
+// y tiles, y fastest inside a block, then z, then the next block (a.band
+// <= 1 or not dividing: y fastest over the whole box).  Blocking keeps a
+// tile's z neighbours band * (nx / 16) launch positions away, so the
+// records both touch are still in L2.
+template <int kPtY, int kPtZ>
+__device__ __forceinline__ void tile_origin(const DirectArgs& a, uint32_t b, uint32_t& x0,
+                                            uint32_t& y0, uint32_t& z0) {
+  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY, tilesz = a.nzl / kPtZ;
+  x0 = (b % tilesx) * kPtX;
+  const uint32_t r = b / tilesx;
+  const uint32_t by = a.band;
+  if (by > 1 && tilesy % by == 0) {
+    const uint32_t per = by * tilesz, yb = r / per, w = r - yb * per;
+    y0 = (yb * by + w % by) * kPtY;
+    z0 = (w / by) * kPtZ;
+  } else {
+    y0 = (r % tilesy) * kPtY;
+    z0 = (r / tilesy) * kPtZ;
+  }
+}
+
 // HALO = false (the default, measured faster): only the tile's own source
 // rows are staged, as in the AA odd step below; the face nodes' gathers
 // from y / z halo rows are loaded from global memory ahead of the copies.
@@ -118,11 +140,8 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
   extern __shared__ __align__(128) unsigned char pt_smem[];
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
-  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
-  const uint32_t b = blockIdx.x;
-  const uint32_t x0 = (b % tilesx) * kPtX;
-  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
-  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
+  uint32_t x0, y0, z0;
+  tile_origin<kPtY, kPtZ>(a, blockIdx.x, x0, y0, z0);
   const uint64_t nx = a.nx;
   const uint32_t t = threadIdx.x;
   pt_load_halo<kPtY, kPtZ, HALO>(a, a.src, sh, bar, x0, y0, z0);
@@ -212,11 +231,8 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
   extern __shared__ __align__(128) unsigned char pt_smem[];
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
-  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY;
-  const uint32_t b = blockIdx.x;
-  const uint32_t x0 = (b % tilesx) * kPtX;
-  const uint32_t y0 = ((b / tilesx) % tilesy) * kPtY;
-  const uint32_t z0 = (b / (tilesx * tilesy)) * kPtZ;
+  uint32_t x0, y0, z0;
+  tile_origin<kPtY, kPtZ>(a, blockIdx.x, x0, y0, z0);
   const uint32_t t = threadIdx.x;
   pt_load_halo<kPtY, kPtZ, HALO>(a, a.dst, sh, bar, x0, y0, z0);
   const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
