@@ -2,6 +2,7 @@
 // doctest kernel tests (proj/tests/test_kernels.cpp) so an lbmbench user can
 // read them side by side.  Built by tools/Makefile, run by
 // tests/test_cpp_api.py (GPU) and prints "ALL PASSED".
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -125,6 +126,39 @@ static void verification() {
   CHECK(r.converged && r.passed && r.linf_rel < 1e-6);
 }
 
+// lbmgpu_run: one job equals load_state + advance + snapshot, bitwise, with
+// page-locked buffers (pipelined schedule) and with pageable ones
+static void run_job() {
+  setenv("LBMGPU_FUSED_MB", "0", 1);  // small box: per-sweep launches, as for large lattices
+  GeometrySpec ch;
+  ch.kind = GeometryKind::Channel;
+  ch.nx = 32;
+  ch.ny = 16;
+  ch.nz = 40;
+  auto ref = make_kernel(make_descriptor("aa-soa"), ch);
+  auto k = make_kernel(make_descriptor("aa-soa"), ch);
+  ref->load_perturbed(77);
+  const std::vector<double> init = ref->snapshot();
+  ref->advance(kParams, kForce, 10);
+  const std::vector<double> expect = ref->snapshot();
+  const std::size_t n = init.size();
+  void *pin_in = nullptr, *pin_out = nullptr;
+  CHECK(lbmgpu_host_alloc(n * 8, &pin_in) == LBMGPU_OK);
+  CHECK(lbmgpu_host_alloc(n * 8, &pin_out) == LBMGPU_OK);
+  std::span<double> in(static_cast<double*>(pin_in), n), out(static_cast<double*>(pin_out), n);
+  std::copy(init.begin(), init.end(), in.begin());
+  CHECK(k->run(in, kParams, kForce, 10, out));  // pipelined
+  CHECK(std::equal(out.begin(), out.end(), expect.begin()));
+  auto k2 = make_kernel(make_descriptor("aa-soa"), ch);
+  std::vector<double> out2(n);
+  CHECK(!k2->run(init, kParams, kForce, 10, out2));  // pageable: the plain sequence
+  CHECK(out2 == expect);
+  CHECK(throws<ConfigError>([&] { k2->run(init, kParams, kForce, 3, out2); }));
+  lbmgpu_host_free(pin_in);
+  lbmgpu_host_free(pin_out);
+  unsetenv("LBMGPU_FUSED_MB");
+}
+
 int main(int argc, char** argv) {
   if (argc < 3) {
     std::printf("usage: cpp_api_test FULL_FP HALF_FP\n");
@@ -136,6 +170,7 @@ int main(int argc, char** argv) {
     golden(argv[1], argv[2]);
     rejections();
     verification();
+    run_job();
   } catch (const std::exception& e) {
     std::printf("unexpected exception: %s\n", e.what());
     return 1;
