@@ -336,6 +336,7 @@ class DirectEngine final : public Engine {
       // tuning knobs (defaults are the measured best)
       if (const char* e = std::getenv("LBMGPU_AA_MINB")) minb_ = std::atoi(e);
       if (const char* e = std::getenv("LBMGPU_TILE_BY")) tile_by_ = static_cast<uint32_t>(std::atoi(e));
+      if (const char* e = std::getenv("LBMGPU_PUSH_AS_PULL")) fused_push_as_pull_ = std::atoi(e) != 0;
       if (const char* e = std::getenv("LBMGPU_FUSED_MB"))
         fused_bytes_ = uint64_t(std::atoll(e)) << 20;
     }
@@ -647,7 +648,14 @@ class DirectEngine final : public Engine {
     }
     DirectArgs a = args(pt, 0, N, t, cur_, 1 - cur_);
     double* other = parts_[0].buf[1 - cur_].get();
-    if (desc_.prop == Prop::OsPush)
+    // SoA push in pull order (as the AoS push, os_aos_tiles): push and pull
+    // realise the identical per-step mapping (reference
+    // tests/test_kernels.cpp:96-126), and the fused pull -- collide pass,
+    // T-1 gather + collide sweeps, one gather-only sweep -- is the faster
+    // L2-resident launch (cfg 1, 100 steps: DESIGN.md section 4)
+    if (desc_.prop == Prop::OsPush && soa && fused_push_as_pull_)
+      launch_fused<true, kFusedPull>(a, other, steps, "full_push_soa_fused", steps + 1);
+    else if (desc_.prop == Prop::OsPush)
       soa ? launch_fused<true, kFusedPush>(a, other, steps, "full_push_soa_fused", steps)
           : launch_fused<false, kFusedPush>(a, other, steps, "full_push_aos_fused", steps);
     else
@@ -1702,6 +1710,7 @@ class DirectEngine final : public Engine {
   // measured cfg 5 odd 6443 -> 6650 GB/s, even 6793 -> 6830.
   int minb_ = 4;
   uint32_t tile_by_ = 8;  // AoS 3-D tiles: y tiles per traversal block (tile_origin)
+  bool fused_push_as_pull_ = true;  // SoA push's fused launch in pull order
   // pipelined job (run_job): column plan, staging, copy streams, events
   bool job_checked_ = false, job_ok_ = false;
   uint32_t job_za_ = 0, job_zb_ = 0;
