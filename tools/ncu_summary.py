@@ -72,8 +72,12 @@ BENCH_ROWS = {
     "k_list_pull<1, 1, 0>": "list_pull_soa",
     "k_list_pull<1, 0, 0>": "list_pull_stream_soa",
     "k_list_collide<1>": "list_collide_soa",
-    "k_full_fused<1, 0, 160, 4>": "full_push_soa_fused",
+    "k_full_fused<1, 0, 160, 4>": "full_push_soa_fused",   # push kind (LBMGPU_PUSH_AS_PULL=0)
+    "k_full_fused<1, 1, 160, 4>": "full_push_soa_fused",   # push in pull order (default)
 }
+# sweeps of the cfg-1 fused launch captured with --steps 20: the push kind
+# runs 20, the push in pull order 21 (collide pass + 19 pulls + stream pass)
+FUSED_SWEEPS = {"k_full_fused<1, 0, 160, 4>": 20, "k_full_fused<1, 1, 160, 4>": 21}
 
 
 def build(outdir, dst, sha_file):
@@ -103,12 +107,13 @@ def build(outdir, dst, sha_file):
                    "dram_bytes_per_launch": v["dram_bytes_per_launch"]}
             if row.endswith("_fused"):
                 # cfg 1 is captured with --steps 20 --warmup 0: one fused
-                # launch of 20 sweeps; the bench counts sweeps as launches
-                rec["sweeps_per_launch"] = 20
+                # launch of 20 (21) sweeps; the bench counts sweeps as launches
+                sw = FUSED_SWEEPS.get(k, 20)
+                rec["sweeps_per_launch"] = sw
                 for key in ("dram_read_bytes_per_launch", "dram_write_bytes_per_launch",
                             "dram_bytes_per_launch"):
-                    rec[key] /= 20
-                rec["note"] = ("per sweep of the 20-sweep fused launch; the lattice is "
+                    rec[key] /= sw
+                rec["note"] = (f"per sweep of the {sw}-sweep fused launch; the lattice is "
                                "L2-resident, the DRAM bytes are mostly write-back")
             rows[row] = rec
         if cid == "5":
