@@ -122,9 +122,23 @@ int lbmgpu_padding_offsets(uint64_t n_fluid, const lbmgpu_padding* pad,
                            uint64_t* starts19, uint64_t* total_slots);
 /* loop_balance (perfmodel.cpp:10-47): the reference B_l (CPU, with write
  * allocate) and the GPU algorithmic bytes per fluid update (no write
- * allocate; 304 direct, 340 list AA, 376 list one-step). */
+ * allocate; 304 direct, 340 list AA, 376 list one-step, 304.5 for the RIA
+ * names: a one-byte pattern id per node and odd sub-step). */
 int lbmgpu_loop_balance(const char* name, double* ref_bl_min,
                         double* ref_bl_max, double* gpu_bytes_per_flup);
+/* loop_balance with geometry statistics (perfmodel.cpp:21-31): for the RIA
+ * names the index bytes become 76 B of run metadata amortised over the run
+ * and the even/odd pair, 76 * total_runs / (2 * n_fluid), clamped to
+ * [0, 38] (total_runs < 0 or n_fluid <= 0: no statistics, as above); other
+ * names ignore the statistics.  lbmgpu_ria_stats supplies them. */
+int lbmgpu_loop_balance_stats(const char* name, int64_t total_runs,
+                              int64_t n_fluid, double* ref_bl_min,
+                              double* ref_bl_max, double* gpu_bytes_per_flup);
+/* roofline (perfmodel.cpp:73-87): P_max [MFLUP/s] = GB/s * 1000 / B_l; the
+ * lower prediction from the larger balance.  ConfigError when the bandwidth
+ * or a balance is not positive. */
+int lbmgpu_roofline(double gbps, double bl_min, double bl_max,
+                    double* pmax_min_mflups, double* pmax_max_mflups);
 /* omega_minus from (omega_plus, magic Lambda) (d3q19.hpp:70-73). */
 double lbmgpu_omega_minus(double omega_plus, double magic_lambda);
 

@@ -347,6 +347,27 @@ inline LoopBalance loop_balance(const std::string& name) {
   return b;
 }
 
+// loop_balance(desc, RiaStats) (perfmodel.cpp:21-31)
+inline LoopBalance loop_balance(const std::string& name, std::int64_t total_runs,
+                                std::int64_t n_fluid) {
+  LoopBalance b;
+  check(lbmgpu_loop_balance_stats(name.c_str(), total_runs, n_fluid, &b.ref_min, &b.ref_max,
+                                  &b.gpu));
+  return b;
+}
+// roofline (perfmodel.cpp:73-87)
+struct RooflinePrediction {
+  double gbps = 0, min_bflup = 0, max_bflup = 0, pmax_min_mflups = 0, pmax_max_mflups = 0;
+};
+inline RooflinePrediction roofline(double gbps, double bl_min, double bl_max) {
+  RooflinePrediction r;
+  r.gbps = gbps;
+  r.min_bflup = bl_min;
+  r.max_bflup = bl_max;
+  check(lbmgpu_roofline(gbps, bl_min, bl_max, &r.pmax_min_mflups, &r.pmax_max_mflups));
+  return r;
+}
+
 struct PoiseuilleCase {
   int nx = 8, ny = 8, nz = 34;
   double g = 1e-6;

@@ -7,10 +7,12 @@ from .lbmgpu import (BodyForce, ConfigError, DeviceError, FlagField, GeometrySpe
                      KernelDescriptor, NumericalError, PaddingPolicy, PoiseuilleCase, TrtParams,
                      analytic_profile, build_geometry, fluid_count, kernel_names, loop_balance,
                      macro_fields, make_descriptor, make_kernel, padding_offsets,
-                     perturbed_equilibrium, state_fingerprint, steady_state_run, verify_kernel)
+                     perturbed_equilibrium, roofline, state_fingerprint, steady_state_run,
+                     verify_kernel)
 
 __all__ = ["BodyForce", "ConfigError", "DeviceError", "FlagField", "GeometrySpec", "Kernel",
            "KernelDescriptor", "NumericalError", "PaddingPolicy", "PoiseuilleCase", "TrtParams",
            "analytic_profile", "build_geometry", "fluid_count", "kernel_names", "loop_balance",
            "macro_fields", "make_descriptor", "make_kernel", "padding_offsets",
-           "perturbed_equilibrium", "state_fingerprint", "steady_state_run", "verify_kernel"]
+           "perturbed_equilibrium", "roofline", "state_fingerprint", "steady_state_run",
+           "verify_kernel"]

@@ -282,6 +282,25 @@ int lbmgpu_loop_balance(const char* name, double* a, double* b, double* g) {
   });
 }
 
+int lbmgpu_loop_balance_stats(const char* name, int64_t total_runs, int64_t n_fluid, double* a,
+                              double* b, double* g) {
+  return guard([&] {
+    need(name, "name");
+    LoopBalance l = loop_balance(make_descriptor(name, 0, 4), total_runs, n_fluid);
+    if (a) *a = l.ref_min;
+    if (b) *b = l.ref_max;
+    if (g) *g = l.gpu;
+  });
+}
+
+int lbmgpu_roofline(double gbps, double bl_min, double bl_max, double* pmax_min, double* pmax_max) {
+  return guard([&] {
+    Roofline r = roofline(gbps, bl_min, bl_max);
+    if (pmax_min) *pmax_min = r.pmax_min_mflups;
+    if (pmax_max) *pmax_max = r.pmax_max_mflups;
+  });
+}
+
 double lbmgpu_omega_minus(double wp, double lambda) {
   return omega_minus_of(wp, lambda);
 }

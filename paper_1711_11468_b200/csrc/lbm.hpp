@@ -37,7 +37,12 @@ struct LoopBalance {
   double ref_min = 0, ref_max = 0;  // reference B_l incl. CPU write-allocate
   double gpu = 0;                   // algorithmic bytes per FLUP on the GPU
 };
-LoopBalance loop_balance(const Descriptor& d);
+// geometry statistics (RIA names): total_runs < 0 = none
+LoopBalance loop_balance(const Descriptor& d, int64_t total_runs = -1, int64_t n_fluid = 0);
+struct Roofline {
+  double pmax_min_mflups = 0, pmax_max_mflups = 0;
+};
+Roofline roofline(double gbps, double bl_min, double bl_max);
 
 // --------------------------------------------------------------- geometry
 enum GeomKind { kChannel = 0, kSlit = 1, kPipe = 2, kBlocks = 3, kCustom = 4 };

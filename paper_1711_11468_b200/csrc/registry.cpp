@@ -61,12 +61,15 @@ Descriptor make_descriptor(const std::string& name, int blk, int W) {
   return d;
 }
 
-// loop_balance (reference src/perfmodel.cpp:10-47) for the RIA-less case,
-// plus the GPU algorithmic bytes: 19 PDF reads + 19 writes of 8 B (no write
-// allocate on the GPU), + 18 x 4 B adjacency per one-step list update, or per
-// odd AA sub-step (half of it per update).  ria/pv run here on the list-AA
-// sweep, so they carry its 340 B.
-LoopBalance loop_balance(const Descriptor& k) {
+// loop_balance (reference src/perfmodel.cpp:10-47), plus the GPU algorithmic
+// bytes: 19 PDF reads + 19 writes of 8 B (no write allocate on the GPU),
+// + 18 x 4 B adjacency per one-step list update, or per odd AA sub-step
+// (half of it per update), 0.5 B for the RIA names' pattern ids.  Reference
+// side of the RIA names: without geometry statistics the index range is
+// [0, 38] B; with them (total_runs >= 0, n_fluid > 0) both ends are the 76 B
+// of run metadata amortised over the run and the even/odd pair, clamped to
+// [0, 38] (perfmodel.cpp:21-31).
+LoopBalance loop_balance(const Descriptor& k, int64_t total_runs, int64_t n_fluid) {
   LoopBalance b;
   const double rd = 8.0 * kQ, wr = 8.0 * kQ;
   const bool os = k.prop != Prop::Aa;
@@ -75,19 +78,42 @@ LoopBalance loop_balance(const Descriptor& k) {
   double imin = 0, imax = 0, igpu = 0;
   if (k.indirect) {
     if (k.ria) {
-      imin = 0.0;
-      imax = 38.0;
+      if (total_runs >= 0 && n_fluid > 0) {
+        const double per_flup =
+            76.0 * static_cast<double>(total_runs) / (2.0 * static_cast<double>(n_fluid));
+        imin = imax = std::min(std::max(per_flup, 0.0), 38.0);
+      } else {
+        imin = 0.0;
+        imax = 38.0;
+      }
     } else if (os) {
       imin = imax = 18.0 * 4.0;
     } else {
       imin = imax = 18.0 * 4.0 / 2.0;
     }
     igpu = os ? 18.0 * 4.0 : 18.0 * 4.0 / 2.0;
+    // ria / pv: the odd sub-step reads a one-byte pattern id per node instead
+    // of 72 B of adjacency (list_ria.cuh; 2- and 4-byte ids or the run table
+    // where a geometry has more than 256 distinct rows: 305-306 B)
+    if (k.ria) igpu = 1.0 / 2.0;
   }
   b.ref_min = rd + wr + wa + imin;
   b.ref_max = rd + wr + wa + imax;
   b.gpu = rd + wr + igpu;
   return b;
+}
+
+// roofline (reference src/perfmodel.cpp:73-87): P_max = bandwidth / B_l; the
+// lower prediction comes from the larger balance.
+Roofline roofline(double gbps, double bl_min, double bl_max) {
+  if (!(gbps > 0.0))
+    throw ConfigError("roofline: bandwidth must be positive, got " + std::to_string(gbps));
+  if (!(bl_min > 0.0) || !(bl_max > 0.0))
+    throw ConfigError("roofline: loop balance must be positive");
+  Roofline r;
+  r.pmax_min_mflups = gbps * 1000.0 / bl_max;
+  r.pmax_max_mflups = gbps * 1000.0 / bl_min;
+  return r;
 }
 
 // ---- padding (reference src/list_lattice.cpp:63-121) ----------------------

@@ -65,6 +65,8 @@ def _load():
     L.lbmgpu_make_descriptor.argtypes = [C.c_char_p, i, i, vp]
     L.lbmgpu_padding_offsets.argtypes = [u64, vp, vp, P(u64)]
     L.lbmgpu_loop_balance.argtypes = [C.c_char_p, P(d), P(d), P(d)]
+    L.lbmgpu_loop_balance_stats.argtypes = [C.c_char_p, i64, i64, P(d), P(d), P(d)]
+    L.lbmgpu_roofline.argtypes = [d, d, d, P(d), P(d)]
     L.lbmgpu_geometry_build.argtypes = [vp, vp, P(i64), vp]
     L.lbmgpu_create.argtypes = [C.c_char_p, i, i, vp, vp, i, vp, P(vp)]
     L.lbmgpu_destroy.argtypes = [vp]
@@ -232,11 +234,26 @@ def make_descriptor(name: str, blk: int = 0, vector_width: int = 4) -> KernelDes
     return _desc_from_c(name, c)
 
 
-def loop_balance(name: str):
-    """(reference B_l min, max, GPU algorithmic bytes per fluid update)."""
+def loop_balance(name: str, stats: Optional[dict] = None):
+    """(reference B_l min, max, GPU algorithmic bytes per fluid update);
+    stats = Kernel.ria_stats() (perfmodel.cpp:21-31: the RIA names' index
+    bytes from the geometry's run count)."""
     a, b, g = C.c_double(), C.c_double(), C.c_double()
-    _check(lib.lbmgpu_loop_balance(name.encode(), C.byref(a), C.byref(b), C.byref(g)))
+    if stats is None:
+        _check(lib.lbmgpu_loop_balance(name.encode(), C.byref(a), C.byref(b), C.byref(g)))
+    else:
+        _check(lib.lbmgpu_loop_balance_stats(name.encode(), int(stats["total_runs"]),
+                                             int(stats["n_fluid"]), C.byref(a), C.byref(b),
+                                             C.byref(g)))
     return a.value, b.value, g.value
+
+
+def roofline(gbps: float, bl_min: float, bl_max: float):
+    """roofline (perfmodel.cpp:73-87): (P_max from the larger balance, P_max
+    from the smaller one) in MFLUP/s."""
+    lo, hi = C.c_double(), C.c_double()
+    _check(lib.lbmgpu_roofline(float(gbps), float(bl_min), float(bl_max), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 # ------------------------------------------------------------------ geometry

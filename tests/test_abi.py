@@ -81,7 +81,7 @@ def test_loop_balance_table1():
         a, b, g = lbm.loop_balance(name)
         assert a == b == ref_bl and g == gpu, name
     a, b, g = lbm.loop_balance("list-aa-ria-soa")
-    assert (a, b, g) == (304, 342, 340)
+    assert (a, b, g) == (304, 342, 304.5)  # GPU: one-byte pattern id per odd sub-step
 
 
 def test_padding_against_golden(small_golden):
