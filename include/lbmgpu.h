@@ -207,6 +207,15 @@ int lbmgpu_capabilities(lbmgpu_ctx* ctx, int* nt_stores_available,
  * values < 0 mean "not applicable" (std::nullopt). */
 int lbmgpu_ria_stats(lbmgpu_ctx* ctx, int64_t* total_runs, int64_t* n_fluid,
                      double* vector_fraction, double* pv_chunk_fraction);
+/* vectorizable_fraction(coding, W) (list_lattice.cpp:228-236) of a run-coded
+ * kernel's own coding at any width W >= 1; -1 for the other names. */
+int lbmgpu_vectorizable_fraction(lbmgpu_ctx* ctx, int width, double* v);
+/* The run coding's run starts (RiaRun::start, build_ria,
+ * list_lattice.cpp:206-226) in node order: run r covers nodes
+ * [start[r], start[r+1]) (the last up to n_fluid).  *count = number of runs,
+ * -1 for names without a coding; run_starts may be null to query the count. */
+int lbmgpu_export_runs(lbmgpu_ctx* ctx, uint32_t* run_starts, uint64_t cap,
+                       int64_t* count);
 int lbmgpu_descriptor_of(lbmgpu_ctx* ctx, lbmgpu_descriptor* out);
 
 /* List structure export for the bit-exact checks (list_lattice.hpp:86-99):

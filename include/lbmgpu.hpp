@@ -305,6 +305,21 @@ class Kernel {
     if (pv < 0) return std::nullopt;
     return pv;
   }
+  // vectorizable_fraction(coding, W) (list_lattice.cpp:228-236) at any width
+  std::optional<double> vectorizable_fraction(int width) const {
+    double v = 0;
+    check(lbmgpu_vectorizable_fraction(ctx_.get(), width, &v));
+    if (v < 0) return std::nullopt;
+    return v;
+  }
+  // run starts of the run coding (RiaRun::start), node order; empty without a coding
+  std::vector<std::uint32_t> export_runs() const {
+    std::int64_t n = 0;
+    check(lbmgpu_export_runs(ctx_.get(), nullptr, 0, &n));
+    std::vector<std::uint32_t> r(n > 0 ? static_cast<std::size_t>(n) : 0);
+    if (n > 0) check(lbmgpu_export_runs(ctx_.get(), r.data(), r.size(), &n));
+    return r;
+  }
   // Peer-memory transport (lbmgpu_dist.transport = 1, nranks > 1): this
   // rank's CUDA IPC record; all-gather them and pass all ranks' records
   // (rank order) to peer_attach before the first advance.

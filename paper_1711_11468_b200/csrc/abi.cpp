@@ -309,6 +309,7 @@ int lbmgpu_geometry_build(const lbmgpu_geometry* g, uint8_t* flags_out,
                           int64_t* n_fluid, int* periodic_out) {
   return guard([&] {
     GeomSpec s = to_spec(g);
+    validate_geometry(s);  // ConfigError before any device work
     cudaStream_t st;
     LBM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     try {
@@ -623,6 +624,32 @@ int lbmgpu_ria_stats(lbmgpu_ctx* c, int64_t* runs, int64_t* nf, double* vfrac,
     if (nf) *nf = have ? static_cast<int64_t>(c->eng->n_fluid()) : -1;
     if (vfrac) *vfrac = have ? v : -1.0;
     if (pvfrac) *pvfrac = (have && c->desc.pv) ? v : -1.0;
+  });
+}
+
+int lbmgpu_vectorizable_fraction(lbmgpu_ctx* c, int width, double* v) {
+  return guard([&] {
+    need(c, "ctx");
+    need(v, "out");
+    if (!c->eng->ria_vector_fraction(width, v)) *v = -1.0;
+  });
+}
+
+int lbmgpu_export_runs(lbmgpu_ctx* c, uint32_t* run_starts, uint64_t cap, int64_t* count) {
+  return guard([&] {
+    need(c, "ctx");
+    need(count, "count");
+    std::vector<uint32_t> r;
+    if (!c->eng->ria_run_starts(r)) {
+      *count = -1;
+      return;
+    }
+    *count = static_cast<int64_t>(r.size());
+    if (!run_starts) return;
+    if (cap < r.size())
+      throw ConfigError("export_runs: buffer holds " + std::to_string(cap) + " run starts, coding has " +
+                        std::to_string(r.size()));
+    std::copy(r.begin(), r.end(), run_starts);
   });
 }
 

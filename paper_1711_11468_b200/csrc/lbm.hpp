@@ -278,6 +278,15 @@ class Engine {
     (void)runs; (void)vfrac;
     return false;
   }
+  // run-coded names: vectorizable_fraction at any width, the run starts
+  virtual bool ria_vector_fraction(int w, double* v) {
+    (void)w; (void)v;
+    return false;
+  }
+  virtual bool ria_run_starts(std::vector<uint32_t>& out) {
+    (void)out;
+    return false;
+  }
   // Peer-memory transport (nranks > 1): this rank's CUDA IPC record, and
   // the attach of every rank's record (rank order).
   virtual void peer_export(std::vector<uint8_t>& rec) {

@@ -951,14 +951,36 @@ class ListEngine final : public Engine {
     LBM_CUDA(cudaMemcpyAsync(h.data(), run_start.get(), uint64_t(R) * 4,
                              cudaMemcpyDeviceToHost, stream_));
     LBM_CUDA(cudaStreamSynchronize(stream_));
-    const uint64_t W = static_cast<uint64_t>(desc_.vector_width);
-    uint64_t covered = 0;
-    for (uint32_t r = 0; r < R; ++r) {
-      const uint64_t end = r + 1 < R ? h[r + 1] : n_fluid_;
-      covered += (end - h[r]) / W * W;
-    }
     ria_runs_ = R;
-    ria_vfrac_ = static_cast<double>(covered) / static_cast<double>(n_fluid_);
+    ria_run_start_h_ = std::move(h);
+    ria_vfrac_ = vector_fraction(desc_.vector_width);
+  }
+
+  // vectorizable_fraction (list_lattice.cpp:228-236): nodes covered by whole
+  // groups of W inside their run, over all fluid nodes
+  double vector_fraction(int w) const {
+    const uint64_t W = static_cast<uint64_t>(w), R = ria_run_start_h_.size();
+    uint64_t covered = 0;
+    for (uint64_t r = 0; r < R; ++r) {
+      const uint64_t end = r + 1 < R ? ria_run_start_h_[r + 1] : n_fluid_;
+      covered += (end - ria_run_start_h_[r]) / W * W;
+    }
+    return static_cast<double>(covered) / static_cast<double>(n_fluid_);
+  }
+
+  bool ria_vector_fraction(int w, double* v) override {
+    if (!desc_.ria) return false;
+    if (w < 1) throw ConfigError("vectorizable_fraction: W must be >= 1");
+    *v = vector_fraction(w);
+    return true;
+  }
+
+  // run starts of the coding (RiaRun::start, list_lattice.hpp:52-58), in
+  // node order; run r ends where run r+1 starts (the last at n_fluid)
+  bool ria_run_starts(std::vector<uint32_t>& out) override {
+    if (!desc_.ria) return false;
+    out = ria_run_start_h_;
+    return true;
   }
 
   bool ria_stats(int64_t* runs, double* vfrac) override {
@@ -990,6 +1012,7 @@ class ListEngine final : public Engine {
   NcclTransportImpl* lnccl_ = nullptr;
   int64_t ria_runs_ = -1;
   double ria_vfrac_ = 0.0;
+  std::vector<uint32_t> ria_run_start_h_;  // host copy of the run starts
   uint64_t ria_R_ = 0;
   DevBuf<int32_t> ria_pat_;     // [run][18] relative offsets
   DevBuf<uint32_t> ria_run0_;   // run id of node 32w

@@ -67,6 +67,8 @@ def _load():
     L.lbmgpu_loop_balance.argtypes = [C.c_char_p, P(d), P(d), P(d)]
     L.lbmgpu_loop_balance_stats.argtypes = [C.c_char_p, i64, i64, P(d), P(d), P(d)]
     L.lbmgpu_roofline.argtypes = [d, d, d, P(d), P(d)]
+    L.lbmgpu_vectorizable_fraction.argtypes = [vp, i, P(d)]
+    L.lbmgpu_export_runs.argtypes = [vp, vp, u64, P(i64)]
     L.lbmgpu_geometry_build.argtypes = [vp, vp, P(i64), vp]
     L.lbmgpu_create.argtypes = [C.c_char_p, i, i, vp, vp, i, vp, P(vp)]
     L.lbmgpu_destroy.argtypes = [vp]
@@ -590,6 +592,24 @@ class Kernel:
     def vector_fraction(self):
         _, _, v, _ = self._ria()
         return None if v < 0 else v
+
+    def vectorizable_fraction(self, width: int):
+        """vectorizable_fraction(coding, W) (list_lattice.cpp:228-236) at any
+        width; None for names without a run coding."""
+        v = C.c_double()
+        _check(lib.lbmgpu_vectorizable_fraction(self._h, int(width), C.byref(v)))
+        return None if v.value < 0 else v.value
+
+    def export_runs(self):
+        """Run starts of the run coding in node order (run r covers
+        [start[r], start[r+1]), the last up to n_fluid); None without a coding."""
+        n = C.c_int64()
+        _check(lib.lbmgpu_export_runs(self._h, None, 0, C.byref(n)))
+        if n.value < 0:
+            return None
+        out = np.zeros(n.value, np.uint32)
+        _check(lib.lbmgpu_export_runs(self._h, out.ctypes.data, out.size, C.byref(n)))
+        return out
 
     def pv_chunk_fraction(self):
         _, _, _, pv = self._ria()
