@@ -76,3 +76,71 @@ def test_verify_exit_codes():
     # too few steps to converge -> not passed -> exit 3 (cli.cpp:330)
     r = run("verify", "--kernel", "aa-soa", "--dims", "4x4x18", "--max-steps", "4", "--interval", "2")
     assert r.returncode == 3
+
+
+# ---- the remaining cases of proj/tests/test_cli.cpp, one to one --------------
+def test_unknown_kernel_exits_1():
+    """test_cli.cpp:98-101."""
+    assert run("bench", "--kernel", "bogus-kernel").returncode == 1
+    assert run("verify", "--kernel", "bogus-kernel").returncode == 1
+
+
+def test_configuration_errors_exit_1_reference_cases():
+    """test_cli.cpp:103-115: odd iterations with an AA kernel, bad dims
+    syntax, bad geometry kind, bad padding -- all before any device work."""
+    for args in (["bench", "--kernel", "aa-soa", "--geometry", "blocks", "--dims", "12x10x10",
+                  "--iterations", "5"],
+                 ["geometry", "--kind", "channel", "--dims", "chunky"],
+                 ["geometry", "--kind", "torus", "--dims", "4x4x4"],
+                 ["bench", "--kernel", "list-aa-soa", "--geometry", "blocks", "--dims", "12x10x10",
+                  "--iterations", "2", "--padding", "1,2,3"]):
+        assert run(*args).returncode == 1, args
+
+
+@pytest.mark.gpu
+def test_geometry_subcommand_emits_fluid_statistics():
+    """test_cli.cpp:117-120: blocks 16^3, b = s = 4 -> 3584 fluid nodes."""
+    r = run("geometry", "--kind", "blocks", "--dims", "16x16x16", "--block", "4", "--spacing", "4",
+            "--stats")
+    assert r.returncode == 0, r.stderr
+    j = json.loads(r.stdout)
+    assert j["fluid_nodes"] == 16 ** 3 - 8 * 4 ** 3 and j["periodic"] == [True, True, True]
+    assert j["fluid_fraction"] == pytest.approx(1.0 - 0.5 ** 3)
+
+
+@pytest.mark.gpu
+def test_csv_row_and_json_carry_the_same_information():
+    """test_cli.cpp:32-59: blocks 12x10x10, list-aa-soa, seed 9: as many
+    fields as header columns; kernel, geometry and B_l = 340 in both."""
+    args = ["bench", "--kernel", "list-aa-soa", "--geometry", "blocks", "--dims", "12x10x10",
+            "--iterations", "10", "--warmup", "2", "--seed", "9"]
+    head, row = run(*args).stdout.strip().splitlines()
+    js = run(*args, "--format", "json").stdout
+    assert head.startswith(REF_COLUMNS) and row.count(",") == head.count(",")
+    for token in ("list-aa-soa", "blocks", "340"):
+        assert token in row and token in js, token
+    rec, j = dict(zip(head.split(","), row.split(","))), json.loads(js)
+    assert rec["state_hash"] == j["state_hash"] and int(rec["n_fluid"]) == j["n_fluid"] == 1136
+
+
+@pytest.mark.gpu
+def test_bench_appends_csv_rows_with_one_header(tmp_path):
+    """test_cli.cpp:122-140: two runs with --out -> one header, three lines."""
+    path = tmp_path / "lbm_cli_test.csv"
+    for _ in range(2):
+        r = run("bench", "--kernel", "list-aa-soa", "--geometry", "blocks", "--dims", "12x10x10",
+                "--iterations", "4", "--warmup", "0", "--threads", "1", "--out", str(path))
+        assert r.returncode == 0 and r.stdout == "", r.stderr
+    lines = path.read_text().splitlines()
+    assert len(lines) == 3
+    assert sum(1 for ln in lines if ln.startswith("schema_version")) == 1
+    assert lines[1].split(",")[-1] == lines[2].split(",")[-1]  # same state hash both runs
+
+
+@pytest.mark.gpu
+def test_verify_subcommand_exit_codes_reference_case():
+    """test_cli.cpp:159-168."""
+    assert run("verify", "--kernel", "list-aa-soa", "--dims", "4x4x14", "--interval", "400", "--tol",
+               "1e-11").returncode == 0
+    assert run("verify", "--kernel", "list-aa-soa", "--dims", "4x4x14", "--interval", "100", "--tol",
+               "1e-14", "--max-steps", "200").returncode == 3

@@ -159,6 +159,30 @@ static void run_job() {
   unsetenv("LBMGPU_FUSED_MB");
 }
 
+// perf-model arithmetic and the run coding (test_perfmodel.cpp:34-72,
+// test_list_lattice.cpp:192-209) through the C++ wrappers
+static void model_and_runs() {
+  CHECK(std::fabs(loop_balance("list-aa-ria-soa", 3, 98).ref_min - 305.2) < 0.05);
+  CHECK(loop_balance("list-aa-ria-soa", 0, 1000).ref_min == 304.0);
+  CHECK(loop_balance("list-aa-ria-soa", 1000, 1000).ref_max == 342.0);
+  const LoopBalance pull = loop_balance("list-pull-aos");
+  CHECK(std::fabs(roofline(48.0, pull.ref_min, pull.ref_max).pmax_min_mflups - 90.909) < 0.1);
+  CHECK(throws<ConfigError>([] { roofline(0.0, 304.0, 304.0); }));
+  GeometrySpec g;
+  g.kind = GeometryKind::Channel;
+  g.nx = 20;
+  g.ny = 10;
+  g.nz = 10;
+  Kernel ria(make_descriptor("list-aa-ria-soa"), g, PaddingPolicy::none());
+  const std::vector<std::uint32_t> starts = ria.export_runs();
+  CHECK(starts.size() == 3u * 20 * 8);  // (1, 6, 1) per z line of 8
+  CHECK(starts.size() >= 3 && starts[0] == 0 && starts[1] == 1 && starts[2] == 7);
+  CHECK(ria.vectorizable_fraction(4).value_or(-1) == 0.5);
+  CHECK(ria.vectorizable_fraction(1).value_or(-1) == 1.0);
+  Kernel plain(make_descriptor("list-aa-soa"), g, PaddingPolicy::none());
+  CHECK(plain.export_runs().empty() && !plain.vectorizable_fraction(4).has_value());
+}
+
 int main(int argc, char** argv) {
   if (argc < 3) {
     std::printf("usage: cpp_api_test FULL_FP HALF_FP\n");
@@ -171,6 +195,7 @@ int main(int argc, char** argv) {
     rejections();
     verification();
     run_job();
+    model_and_runs();
   } catch (const std::exception& e) {
     std::printf("unexpected exception: %s\n", e.what());
     return 1;

@@ -15,8 +15,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <ctime>
+#include <fstream>
 #include <iostream>
 #include <map>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -142,6 +144,7 @@ int cmd_bench(const Args& a) {
   const long seed = a.geti("--seed", -1);
   const double hbm = a.getd("--hbm-gbps", 6553.6);
   const std::string format = a.get("--format", "csv");
+  const std::string out_path = a.get("--out", "");
   // validate before any allocation (harness.cpp:84-93)
   if (!(p.omega_plus > 0.0) || !(p.omega_plus < 2.0))
     throw ConfigError("TrtParams: omega_plus must be in (0, 2), got " + std::to_string(p.omega_plus));
@@ -177,29 +180,44 @@ int cmd_bench(const Args& a) {
             << " MFLUP/s (" << 100.0 * mflups / pmax << "% of roofline P_max " << pmax << ")\n";
   char hbuf[20];
   std::snprintf(hbuf, sizeof(hbuf), "%016" PRIx64, hash);
+  std::ostringstream text;
   if (format == "csv") {
-    std::cout << kCsvHeader << '\n'
-              << 1 << ',' << iso_now() << ',' << k.name << ',' << to_string(g.kind) << ','
-              << g.nx << ',' << g.ny << ',' << g.nz << ',' << k.blk << ',' << pad.to_string()
-              << ',' << 1 << ',' << iterations << ',' << n << ',' << fmt(seconds) << ','
-              << fmt(mflups) << ',' << fmt(bl.ref_min) << ',' << fmt(pmax) << ','
-              << fmt(vf ? *vf : std::nan("")) << ',' << caps.nt_streams_effective << ',' << 0
-              << ',' << 1 << ',' << fmt(bl.gpu) << ',' << fmt(achieved) << ','
-              << fmt(achieved / hbm) << ',' << hbuf << '\n';
+    text << 1 << ',' << iso_now() << ',' << k.name << ',' << to_string(g.kind) << ','
+         << g.nx << ',' << g.ny << ',' << g.nz << ',' << k.blk << ',' << pad.to_string()
+         << ',' << 1 << ',' << iterations << ',' << n << ',' << fmt(seconds) << ','
+         << fmt(mflups) << ',' << fmt(bl.ref_min) << ',' << fmt(pmax) << ','
+         << fmt(vf ? *vf : std::nan("")) << ',' << caps.nt_streams_effective << ',' << 0
+         << ',' << 1 << ',' << fmt(bl.gpu) << ',' << fmt(achieved) << ','
+         << fmt(achieved / hbm) << ',' << hbuf << '\n';
   } else {
-    std::cout << "{\"schema_version\":1,\"timestamp\":\"" << iso_now() << "\",\"kernel\":\""
-              << k.name << "\",\"geometry\":\"" << to_string(g.kind) << "\",\"nx\":" << g.nx
-              << ",\"ny\":" << g.ny << ",\"nz\":" << g.nz << ",\"blk\":" << k.blk
-              << ",\"padding_mode\":\"" << pad.to_string() << "\",\"threads\":1,\"iterations\":"
-              << iterations << ",\"n_fluid\":" << n << ",\"seconds\":" << fmt(seconds)
-              << ",\"mflups\":" << fmt(mflups) << ",\"bl_theoretical\":" << fmt(bl.ref_min)
-              << ",\"pmax_mflups\":" << fmt(pmax) << ",\"v_fraction\":"
-              << (vf ? fmt(*vf) : std::string("null"))
-              << ",\"nt_streams_effective\":" << caps.nt_streams_effective
-              << ",\"affinity_applied\":0,\"gpus\":1,\"gpu_bytes_per_flup\":" << fmt(bl.gpu)
-              << ",\"achieved_GBps\":" << fmt(achieved) << ",\"roofline_frac\":"
-              << fmt(achieved / hbm) << ",\"state_hash\":\"" << hbuf << "\"}\n";
+    text << "{\"schema_version\":1,\"timestamp\":\"" << iso_now() << "\",\"kernel\":\""
+         << k.name << "\",\"geometry\":\"" << to_string(g.kind) << "\",\"nx\":" << g.nx
+         << ",\"ny\":" << g.ny << ",\"nz\":" << g.nz << ",\"blk\":" << k.blk
+         << ",\"padding_mode\":\"" << pad.to_string() << "\",\"threads\":1,\"iterations\":"
+         << iterations << ",\"n_fluid\":" << n << ",\"seconds\":" << fmt(seconds)
+         << ",\"mflups\":" << fmt(mflups) << ",\"bl_theoretical\":" << fmt(bl.ref_min)
+         << ",\"pmax_mflups\":" << fmt(pmax) << ",\"v_fraction\":"
+         << (vf ? fmt(*vf) : std::string("null"))
+         << ",\"nt_streams_effective\":" << caps.nt_streams_effective
+         << ",\"affinity_applied\":0,\"gpus\":1,\"gpu_bytes_per_flup\":" << fmt(bl.gpu)
+         << ",\"achieved_GBps\":" << fmt(achieved) << ",\"roofline_frac\":"
+         << fmt(achieved / hbm) << ",\"state_hash\":\"" << hbuf << "\"}\n";
   }
+  // stdout, or appended to --out with one header per file (cli.cpp:294-307)
+  if (out_path.empty()) {
+    if (format == "csv") std::cout << kCsvHeader << '\n';
+    std::cout << text.str();
+    return 0;
+  }
+  bool add_header = false;
+  if (format == "csv") {
+    std::ifstream probe(out_path, std::ios::binary | std::ios::ate);
+    add_header = !probe || probe.tellg() == std::streampos(0);
+  }
+  std::ofstream out(out_path, std::ios::app);
+  if (!out) throw ConfigError("cannot open --out file '" + out_path + "'");
+  if (add_header) out << kCsvHeader << '\n';
+  out << text.str();
   return 0;
 }
 
