@@ -383,6 +383,19 @@ inline RooflinePrediction roofline(double gbps, double bl_min, double bl_max) {
   return r;
 }
 
+// Device bandwidth micro-benchmarks (run_microbench, microbench.cpp:57-175)
+// and which of them models which kernel (micro_for, perfmodel.cpp:66-71).
+inline double microbench(const std::string& kind, std::uint64_t working_set_bytes, int reps = 5) {
+  double gbps = 0;
+  check(lbmgpu_microbench(kind.c_str(), working_set_bytes, reps, &gbps));
+  return gbps;
+}
+inline const char* micro_for(const KernelDescriptor& k) {
+  if (k.nt_streams > 0) return "copy-19-nt-sl";
+  if (k.prop == Propagation::Aa) return "update-19";
+  return "copy-19";
+}
+
 struct PoiseuilleCase {
   int nx = 8, ny = 8, nz = 34;
   double g = 1e-6;

@@ -144,3 +144,34 @@ def test_verify_subcommand_exit_codes_reference_case():
                "1e-11").returncode == 0
     assert run("verify", "--kernel", "list-aa-soa", "--dims", "4x4x14", "--interval", "100", "--tol",
                "1e-14", "--max-steps", "200").returncode == 3
+
+
+def test_microbench_unknown_kind_exits_1():
+    """micro_kind_from_string (perfmodel.cpp:59-64): the error lists the kinds."""
+    r = run("microbench", "--which", "triad")
+    assert r.returncode == 1 and "valid: copy, copy-19, copy-19-nt-sl, update-19" in r.stderr
+    assert run("bench", "--kernel", "aa-soa", "--bandwidths", "/nonexistent").returncode == 1
+
+
+@pytest.mark.gpu
+def test_microbench_writes_the_bandwidth_file_bench_reads(tmp_path):
+    """cmd_microbench (cli.cpp:333-358) with the device micro-benchmarks:
+    `--out` writes the reference's bandwidth-file format (perfmodel.cpp:98-
+    128), a second run merges into it, and `bench --bandwidths` takes its
+    roofline ceiling from the micro-benchmark that models the kernel."""
+    path = tmp_path / "bw.txt"
+    r = run("microbench", "--which", "update-19", "--size", str(2 << 30), "--reps", "3", "--out",
+            str(path))
+    assert r.returncode == 0 and "update-19" in r.stdout, r.stderr
+    r = run("microbench", "--which", "copy-19", "--size", str(2 << 30), "--reps", "3", "--out",
+            str(path))
+    assert r.returncode == 0, r.stderr
+    lines = path.read_text().splitlines()
+    assert lines[0] == "# micro-benchmark bandwidths [GB/s]"
+    bw = {ln.split()[0]: float(ln.split()[1]) for ln in lines[1:]}
+    assert set(bw) == {"copy-19", "update-19"} and all(3000 < v < 8000 for v in bw.values())
+    r = run("bench", "--kernel", "aa-soa", "--dims", "64x64x64", "--iterations", "10", "--format",
+            "json", "--bandwidths", str(path))
+    assert r.returncode == 0, r.stderr
+    j = json.loads(r.stdout)
+    assert j["pmax_mflups"] == pytest.approx(bw["update-19"] * 1000 / 304, rel=1e-5)

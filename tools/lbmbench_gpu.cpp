@@ -1,5 +1,5 @@
-// lbmbench-gpu: the reference CLI's bench / verify / geometry / list-kernels
-// subcommands (reference src/cli.cpp:406-576) on the B200 sweep library,
+// lbmbench-gpu: the reference CLI's bench / verify / geometry / list-kernels /
+// microbench subcommands (reference src/cli.cpp:406-576) on the B200 sweep library,
 // written against the C++ host API (include/lbmgpu.hpp).  Exit codes follow
 // the reference: 0 ok, 1 ConfigError, 2 NumericalError, 3 verification
 // failed (cli.cpp:330,566-572), 4 device failure.
@@ -8,7 +8,9 @@
 // GPU columns gpus, gpu_bytes_per_flup, achieved_GBps, roofline_frac,
 // state_hash.  `threads` reports the number of GPUs (the GPU has no worker
 // pool); pmax_mflups is the roofline at --hbm-gbps (default: measured B200
-// copy bandwidth 6553.6 GB/s) with the GPU algorithmic bytes per update.
+// copy bandwidth 6553.6 GB/s), or at the kernel's own micro-benchmark from
+// --bandwidths FILE (written by `microbench --out FILE`), with the GPU
+// algorithmic bytes per update.
 #include <chrono>
 #include <cinttypes>
 #include <cmath>
@@ -55,7 +57,7 @@ struct Args {
 };
 
 Args parse(int argc, char** argv) {
-  if (argc < 2) throw ConfigError("usage: lbmbench-gpu <list-kernels|geometry|bench|verify> [--opt value ...]");
+  if (argc < 2) throw ConfigError("usage: lbmbench-gpu <list-kernels|geometry|bench|verify|microbench> [--opt value ...]");
   Args a;
   a.cmd = argv[1];
   for (int i = 2; i < argc; ++i) {
@@ -125,6 +127,37 @@ int cmd_geometry(const Args& a) {
   return 0;
 }
 
+// BandwidthSet::load / save (reference src/perfmodel.cpp:98-128): "name GB/s"
+// lines, '#' comments -- the file the reference's microbench writes and its
+// bench / model read.
+std::map<std::string, double> load_bandwidths(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ConfigError("cannot read bandwidth file '" + path + "'");
+  std::map<std::string, double> set;
+  std::string line;
+  while (std::getline(in, line)) {
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream ss(line);
+    std::string name;
+    double value;
+    if (!(ss >> name >> value))
+      throw ConfigError("bandwidth file '" + path + "': bad line '" + line + "'");
+    set[name] = value;
+  }
+  return set;
+}
+
+void save_bandwidths(const std::string& path, const std::map<std::string, double>& set) {
+  std::ofstream out(path);
+  if (!out) throw ConfigError("cannot write bandwidth file '" + path + "'");
+  out << "# micro-benchmark bandwidths [GB/s]\n";
+  for (const auto& [name, value] : set) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%.6g", value);
+    out << name << ' ' << buf << '\n';
+  }
+}
+
 // run_benchmark (reference src/harness.cpp:82-139) on the GPU.
 int cmd_bench(const Args& a) {
   const KernelDescriptor k = make_descriptor(a.get("--kernel", ""), static_cast<int>(a.geti("--blk", 0)),
@@ -142,9 +175,18 @@ int cmd_bench(const Args& a) {
   BodyForce f;
   f.g = {a.getd("--gx", 0.0), 0.0, 0.0};
   const long seed = a.geti("--seed", -1);
-  const double hbm = a.getd("--hbm-gbps", 6553.6);
   const std::string format = a.get("--format", "csv");
   const std::string out_path = a.get("--out", "");
+  // --bandwidths FILE (written by `microbench --out`): the roofline ceiling
+  // comes from the micro-benchmark that models the kernel (micro_for) instead
+  // of --hbm-gbps, as in the reference's bench (harness.cpp:118-127)
+  const std::string bw_path = a.get("--bandwidths", "");
+  double hbm = a.getd("--hbm-gbps", 6553.6);
+  if (!bw_path.empty()) {
+    const std::map<std::string, double> bw = load_bandwidths(bw_path);
+    const auto it = bw.find(micro_for(k));
+    if (it != bw.end()) hbm = it->second;
+  }
   // validate before any allocation (harness.cpp:84-93)
   if (!(p.omega_plus > 0.0) || !(p.omega_plus < 2.0))
     throw ConfigError("TrtParams: omega_plus must be in (0, 2), got " + std::to_string(p.omega_plus));
@@ -221,6 +263,34 @@ int cmd_bench(const Args& a) {
   return 0;
 }
 
+// cmd_microbench (reference src/cli.cpp:333-358) with the device
+// micro-benchmarks: the bandwidths behind the adjusted roofline.
+int cmd_microbench(const Args& a) {
+  const std::string which = a.get("--which", "all");
+  const std::uint64_t size = static_cast<std::uint64_t>(a.getd("--size", 8.0 * (1ull << 30)));
+  const int reps = static_cast<int>(a.geti("--reps", 5));
+  const std::string out_path = a.get("--out", "");
+  if (reps < 1) throw ConfigError("--reps must be >= 1, e.g. --reps 5");
+  std::vector<std::string> kinds;
+  if (which == "all")
+    kinds = {"copy", "copy-19", "copy-19-nt-sl", "update-19"};
+  else
+    kinds = {which};
+  std::map<std::string, double> set;
+  {
+    std::ifstream probe(out_path);
+    if (!out_path.empty() && probe) set = load_bandwidths(out_path);
+  }
+  for (const std::string& kind : kinds) {
+    const double gbps = microbench(kind, size, reps);  // ConfigError lists the valid kinds
+    std::printf("%-14s %8.2f GB/s  (best of %d passes over %" PRIu64 " B)\n", kind.c_str(), gbps,
+                reps, size);
+    set[kind] = gbps;
+  }
+  if (!out_path.empty()) save_bandwidths(out_path, set);
+  return 0;
+}
+
 // cmd_verify (reference src/cli.cpp:309-331)
 int cmd_verify(const Args& a) {
   const KernelDescriptor k = make_descriptor(a.get("--kernel", ""));
@@ -261,8 +331,9 @@ int main(int argc, char** argv) {
     if (a.cmd == "geometry") return cmd_geometry(a);
     if (a.cmd == "bench") return cmd_bench(a);
     if (a.cmd == "verify") return cmd_verify(a);
+    if (a.cmd == "microbench") return cmd_microbench(a);
     throw ConfigError("unknown subcommand '" + a.cmd +
-                      "' (valid: list-kernels, geometry, bench, verify)");
+                      "' (valid: list-kernels, geometry, bench, verify, microbench)");
   } catch (const ConfigError& e) {
     std::cerr << "configuration error: " << e.what() << '\n';
     return 1;
