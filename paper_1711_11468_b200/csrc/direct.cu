@@ -512,16 +512,31 @@ class DirectEngine final : public Engine {
     return a;
   }
 
+  // Grid of the AoS 3-D tile kernels and their traversal (tile_origin,
+  // direct_aos.cuh): blocks of tile_by_ y tiles when that is a power of two
+  // dividing the y tile count (and the grid's y extent fits), else plain.
+  template <int TY, int TZ>
+  dim3 tile_grid(DirectArgs& at) const {
+    const unsigned tx = static_cast<unsigned>(nx_ / kPtX), ty = static_cast<unsigned>(ny_ / TY),
+                   tz = static_cast<unsigned>(nz_ / TZ);
+    const unsigned by = tile_by_;
+    if (by > 1 && (by & (by - 1)) == 0 && ty % by == 0 && uint64_t(by) * tz <= 65535u) {
+      at.band = by;
+      return dim3(tx, by * tz, ty / by);
+    }
+    at.band = 0;
+    return dim3(tx, ty, tz);
+  }
+
   template <int TY, int TZ>
   void aa_odd_aos_tile3d(const DirectArgs& a) {
-    const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
     auto kern = k_full_aa_odd_aos_tile3d<TY, TZ, false>;
     constexpr size_t smem = pt_smem<TY, TZ, false>();
     LBM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     const int tok = stats_.begin("full_aa_odd_aos", stream_);
     DirectArgs at = a;
-    at.band = tile_by_;
+    const dim3 grid = tile_grid<TY, TZ>(at);
     kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(at);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);
@@ -529,7 +544,6 @@ class DirectEngine final : public Engine {
 
   template <int TY, int TZ>
   void pull_aos_tile3d(const DirectArgs& a, bool last, const char* name) {
-    const unsigned grid = static_cast<unsigned>(uint64_t(nx_ / kPtX) * (ny_ / TY) * (nz_ / TZ));
     auto kern = last ? k_full_pull_aos_tile3d<false, TY, TZ, false>
                      : k_full_pull_aos_tile3d<true, TY, TZ, false>;
     constexpr size_t smem = pt_smem<TY, TZ, false>();
@@ -537,7 +551,7 @@ class DirectEngine final : public Engine {
                                   static_cast<int>(smem)));
     const int tok = stats_.begin(name, stream_);
     DirectArgs at = a;
-    at.band = tile_by_;
+    const dim3 grid = tile_grid<TY, TZ>(at);
     kern<<<grid, kPtX * TY * TZ, smem, stream_>>>(at);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);

@@ -2,6 +2,8 @@
 // (part of the direct-addressing translation unit, included by direct.cu)
 #pragma once
 
+#include <type_traits>
+
 #include "direct_args.cuh"
 #include "direct_node.cuh"
 #include "tma.cuh"
@@ -108,26 +110,37 @@ __device__ __forceinline__ void pt_load_halo(const DirectArgs& a, const double* 
   }
 }
 
-// Tile of block b: x fastest; then the (y, z) tiles in blocks of a.band
-// y tiles, y fastest inside a block, then z, then the next block (a.band
-// <= 1 or not dividing: y fastest over the whole box).  Blocking keeps a
-// tile's z neighbours band * (nx / 16) launch positions away, so the
-// records both touch are still in L2.
+// Tile of this CTA.  The grid is 3-D so that no division is needed and the
+// launch order (x fastest, then y, then z) is the traversal order: plain
+// (a.band <= 1): grid (nx/16, ny/TY, nz/TZ); banded (a.band = by, a power of
+// two dividing ny/TY): grid (nx/16, by * nz/TZ, ny/TY/by) -- the (y, z)
+// tiles in blocks of by y tiles, y fastest inside a block, then z, then the
+// next block.  Blocking keeps a tile's z neighbours by * (nx / 16) launch
+// positions away, so the records both touch are still in L2.  tile_grid
+// (direct.cu) builds the grid.
 template <int kPtY, int kPtZ>
-__device__ __forceinline__ void tile_origin(const DirectArgs& a, uint32_t b, uint32_t& x0,
-                                            uint32_t& y0, uint32_t& z0) {
-  const uint32_t tilesx = a.nx / kPtX, tilesy = a.ny / kPtY, tilesz = a.nzl / kPtZ;
-  x0 = (b % tilesx) * kPtX;
-  const uint32_t r = b / tilesx;
-  const uint32_t by = a.band;
-  if (by > 1 && tilesy % by == 0) {
-    const uint32_t per = by * tilesz, yb = r / per, w = r - yb * per;
-    y0 = (yb * by + w % by) * kPtY;
-    z0 = (w / by) * kPtZ;
+__device__ __forceinline__ void tile_origin(const DirectArgs& a, uint32_t& x0, uint32_t& y0,
+                                            uint32_t& z0) {
+  x0 = blockIdx.x * kPtX;
+  if (a.band > 1) {
+    const uint32_t by = a.band, w = blockIdx.y;
+    y0 = (blockIdx.z * by + (w & (by - 1))) * kPtY;
+    z0 = (w >> (31 - __clz(by))) * kPtZ;
   } else {
-    y0 = (r % tilesy) * kPtY;
-    z0 = (r / tilesy) * kPtZ;
+    y0 = blockIdx.y * kPtY;
+    z0 = blockIdx.z * kPtZ;
   }
+}
+
+// No node of the tile at (x0, y0, z0) has a wrapped neighbour: every
+// neighbour record sits at a fixed element offset from the node's own record
+// (CTA-uniform, so the gathers / scatters outside the staged rows need no
+// coordinate arithmetic).
+template <int kPtY, int kPtZ>
+__device__ __forceinline__ bool tile_inner(const DirectArgs& a, uint32_t x0, uint32_t y0,
+                                           uint32_t z0) {
+  return x0 >= 1 && x0 + kPtX < a.nx && y0 >= 1 && y0 + kPtY < a.ny && z0 >= 1 &&
+         z0 + kPtZ < a.nzl && a.zoff == 0;
 }
 
 // HALO = false (the default, measured faster): only the tile's own source
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
   uint32_t x0, y0, z0;
-  tile_origin<kPtY, kPtZ>(a, blockIdx.x, x0, y0, z0);
+  tile_origin<kPtY, kPtZ>(a, x0, y0, z0);
   const uint64_t nx = a.nx;
   const uint32_t t = threadIdx.x;
   pt_load_halo<kPtY, kPtZ, HALO>(a, a.src, sh, bar, x0, y0, z0);
@@ -155,13 +168,25 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
   auto staged = [](int hy, int hz) { return HALO || (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ); };
   double q[kQ];
   if (!HALO) {  // gathers from rows that are not staged: now, ahead of the copies
-    const Idx<false> I{a.P, a.nx, a.ny};
-    Coords c;
-    decode_node(a, n, c);
+    if (tile_inner<kPtY, kPtZ>(a, x0, y0, z0)) {
+      // record of x - c_d: a fixed offset from the own record (odd_off is the
+      // AA form, slot opp(d); the pull reads slot d of the same record)
+      const double* own = a.src + uint64_t(n) * kQ;
 #pragma unroll
-    for (int d = 1; d < kQ; ++d) {
-      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
-      if (!staged(hy, hz)) q[d] = a.src[I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+      for (int d = 1; d < kQ; ++d) {
+        const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+        if (!staged(hy, hz)) q[d] = own[a.odd_off[d] + (dslot(d) - dslot(opp(d)))];
+      }
+    } else {
+      const Idx<false> I{a.P, a.nx, a.ny};
+      Coords c;
+      fill_coords(a, x0 + tx, y0 + ty, z0 + tz, c);
+#pragma unroll
+      for (int d = 1; d < kQ; ++d) {
+        const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+        if (!staged(hy, hz))
+          q[d] = a.src[I(c.Z[1 - cz(d)], dslot(d), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+      }
     }
   }
   tma::mbar_wait(bar, 0);
@@ -202,6 +227,37 @@ __host__ __device__ constexpr uint64_t slot_c_bits() {
   return m;
 }
 
+// Which elements of a staged row (20 records x 19 slots, element i = lane +
+// 32 j) a tile owns, per lane: bit j of mx = the slot's owner (record x - c_x
+// of the slot's direction) lies inside the tile in x; of ypos / yneg / zpos /
+// zneg = the slot's direction has c_y (c_z) = +1 / -1.  Constant per lane,
+// so built at compile time and read as five coalesced words.
+constexpr int kOwnRowElems = kPtW * kQ;           // 380 doubles per staged row
+constexpr int kOwnJ = (kOwnRowElems + 31) / 32;  // elements per lane
+struct OwnMasks {
+  uint32_t mx[32], ypos[32], yneg[32], zpos[32], zneg[32];
+};
+constexpr OwnMasks make_own_masks() {
+  OwnMasks m{};
+  constexpr uint64_t kX = slot_c_bits<0>(), kY = slot_c_bits<1>(), kZ = slot_c_bits<2>();
+  for (int lane = 0; lane < 32; ++lane)
+    for (int jj = 0; jj < kOwnJ; ++jj) {
+      const int i = lane + 32 * jj;
+      if (i >= kOwnRowElems) continue;
+      const int hx = i / kQ, s = i - hx * kQ;
+      const int ox = hx + 1 - static_cast<int>((kX >> (2 * s)) & 3u);
+      const int ey = static_cast<int>((kY >> (2 * s)) & 3u) - 1;
+      const int ez = static_cast<int>((kZ >> (2 * s)) & 3u) - 1;
+      if (ox >= 2 && ox < 2 + kPtX) m.mx[lane] |= 1u << jj;
+      if (ey > 0) m.ypos[lane] |= 1u << jj;
+      if (ey < 0) m.yneg[lane] |= 1u << jj;
+      if (ez > 0) m.zpos[lane] |= 1u << jj;
+      if (ez < 0) m.zneg[lane] |= 1u << jj;
+    }
+  return m;
+}
+__device__ const OwnMasks kOwnMasks = make_own_masks();
+
 // AoS AA odd step through the same 3-D halo tiles, both ways.  The tile's
 // source rows arrive by TMA as whole records; each node reads its 19 values
 // (x - c_d, opp d) in shared memory and collides.  The slot a node gathers
@@ -232,7 +288,7 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
   double* sh = reinterpret_cast<double*>(pt_smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(pt_smem + size_t(kPtRows) * kPtRowBytes);
   uint32_t x0, y0, z0;
-  tile_origin<kPtY, kPtZ>(a, blockIdx.x, x0, y0, z0);
+  tile_origin<kPtY, kPtZ>(a, x0, y0, z0);
   const uint32_t t = threadIdx.x;
   pt_load_halo<kPtY, kPtZ, HALO>(a, a.dst, sh, bar, x0, y0, z0);
   const uint32_t tx = t % kPtX, ty = (t / kPtX) % kPtY, tz = t / (kPtX * kPtY);
@@ -243,35 +299,50 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
     return sh + (size_t(row) * kPtW + hx) * kQ;
   };
   auto staged = [](int hy, int hz) { return HALO || (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ); };
-  const Idx<false> I{a.P, a.nx, a.ny};
-  Coords c;
-  decode_node(a, n, c);
-  double q[kQ];
-  if (!HALO && !solid) {  // entries into rows that are not staged: now, ahead of the copies
+  // Entry (x - c_d, opp d) of a node outside the staged rows: a fixed offset
+  // from the own record when no node of the tile wraps (INNER, CTA-uniform:
+  // one instantiation of the body per case), else through the wrapped
+  // coordinates.
+  auto body = [&](auto inner_tag) {
+    constexpr bool INNER = decltype(inner_tag)::value;
+    double* const own_rec = a.dst + uint64_t(n) * kQ;
+    const Idx<false> I{a.P, a.nx, a.ny};
+    Coords c;
+    if (!INNER) fill_coords(a, x0 + tx, y0 + ty, z0 + tz, c);
+    auto far = [&](int d) -> double* {
+      if (INNER) return own_rec + a.odd_off[d];
+      return a.dst + I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)]);
+    };
+    double q[kQ];
+    if (!HALO && !solid) {  // entries into rows that are not staged: now, ahead of the copies
 #pragma unroll
-    for (int d = 0; d < kQ; ++d) {
-      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
-      if (!staged(hy, hz))
-        q[d] = a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])];
+      for (int d = 0; d < kQ; ++d) {
+        const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+        if (!staged(hy, hz)) q[d] = *far(d);
+      }
     }
-  }
-  tma::mbar_wait(bar, 0);
-  if (!solid) {
+    tma::mbar_wait(bar, 0);
+    if (!solid) {
 #pragma unroll
-    for (int d = 0; d < kQ; ++d) {
-      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
-      if (staged(hy, hz)) q[d] = at(int(tx) + 2 - cx(d), hy, hz)[dslot(opp(d))];
-    }
-    collide(q, a.trt);
+      for (int d = 0; d < kQ; ++d) {
+        const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+        if (staged(hy, hz)) q[d] = at(int(tx) + 2 - cx(d), hy, hz)[dslot(opp(d))];
+      }
+      collide(q, a.trt);
 #pragma unroll
-    for (int d = 0; d < kQ; ++d) {
-      const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
-      if (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ)
-        at(int(tx) + 2 - cx(d), hy, hz)[dslot(opp(d))] = q[opp(d)];
-      else
-        a.dst[I(c.Z[1 - cz(d)], dslot(opp(d)), c.Y[1 - cy(d)], c.X[1 - cx(d)])] = q[opp(d)];
+      for (int d = 0; d < kQ; ++d) {
+        const int hy = int(ty) + 1 - cy(d), hz = int(tz) + 1 - cz(d);
+        if (hy >= 1 && hy <= kPtY && hz >= 1 && hz <= kPtZ)
+          at(int(tx) + 2 - cx(d), hy, hz)[dslot(opp(d))] = q[opp(d)];
+        else
+          *far(d) = q[opp(d)];
+      }
     }
-  }
+  };
+  if (tile_inner<kPtY, kPtZ>(a, x0, y0, z0))
+    body(std::true_type{});
+  else
+    body(std::false_type{});
   __syncthreads();
   // owned-slot write-back of the tile's own rows, one warp per row: lane l
   // handles elements i = l + 32 j (j < 12) of the row, slot i % 19 of record
@@ -279,24 +350,10 @@ __global__ void __launch_bounds__(kPtX * kPtY * kPtZ, HALO ? 1 : 3)
   // the row only through its first / last y and z position, so the lane's
   // masks are built once: bit j of kx = owner inside the tile in x, of
   // ypos / yneg / zpos / zneg = the slot's direction has c = +1 / -1.
-  constexpr int kJ = (kRowElems + 31) / 32;
-  constexpr uint64_t kX = slot_c_bits<0>(), kY = slot_c_bits<1>(), kZ = slot_c_bits<2>();
+  constexpr int kJ = kOwnJ;
   const uint32_t lane = t & 31, warp = t >> 5;
-  uint32_t mx = 0, ypos = 0, yneg = 0, zpos = 0, zneg = 0;
-#pragma unroll
-  for (int jj = 0; jj < kJ; ++jj) {
-    const int i = static_cast<int>(lane) + 32 * jj;
-    if (i >= kRowElems) continue;
-    const int hx = i / kQ, s = i - hx * kQ;
-    const int ox = hx + 1 - static_cast<int>((kX >> (2 * s)) & 3u);
-    const int ey = static_cast<int>((kY >> (2 * s)) & 3u) - 1;
-    const int ez = static_cast<int>((kZ >> (2 * s)) & 3u) - 1;
-    if (ox >= 2 && ox < 2 + kPtX) mx |= 1u << jj;
-    if (ey > 0) ypos |= 1u << jj;
-    if (ey < 0) yneg |= 1u << jj;
-    if (ez > 0) zpos |= 1u << jj;
-    if (ez < 0) zneg |= 1u << jj;
-  }
+  const uint32_t mx = kOwnMasks.mx[lane], ypos = kOwnMasks.ypos[lane], yneg = kOwnMasks.yneg[lane],
+                 zpos = kOwnMasks.zpos[lane], zneg = kOwnMasks.zneg[lane];
   const uint64_t nx = a.nx;
   const bool xwrap = x0 < 2 || uint64_t(x0) + kPtX + 2 > nx;
   for (uint32_t r = warp; r < uint32_t(kPtY * kPtZ); r += kT / 32) {

@@ -24,12 +24,9 @@ struct Coords {
   uint32_t Z[3];           // storage planes of z-1, z, z+1
 };
 
-// own-node id n -> coordinates, wrapped x/y neighbours and storage planes
-__device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coords& c) {
-  const uint32_t z = a.fdP.div(n);
-  const uint32_t r = n - z * a.P;
-  const uint32_t y = a.fdx.div(r);
-  const uint32_t x = r - y * a.nx;
+// own-plane coordinates -> wrapped x/y neighbours and storage planes
+__device__ __forceinline__ void fill_coords(const DirectArgs& a, uint32_t x, uint32_t y,
+                                            uint32_t z, Coords& c) {
   c.x = x;
   c.y = y;
   c.z = z;
@@ -48,6 +45,14 @@ __device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coo
     c.Z[2] = zs + 1;
   }
   c.Z[1] = zs;
+}
+
+// own-node id n -> coordinates, wrapped x/y neighbours and storage planes
+__device__ __forceinline__ void decode_node(const DirectArgs& a, uint32_t n, Coords& c) {
+  const uint32_t z = a.fdP.div(n);
+  const uint32_t r = n - z * a.P;
+  const uint32_t y = a.fdx.div(r);
+  fill_coords(a, r - y * a.nx, y, z, c);
 }
 
 __device__ __forceinline__ bool decode(const DirectArgs& a, Coords& c,
