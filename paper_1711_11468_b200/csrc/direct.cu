@@ -615,7 +615,10 @@ class DirectEngine final : public Engine {
     if (!desc_.soa && aos_tiles()) return false;
     const Part& pt = parts_[0];
     const uint64_t bufs = desc_.prop == Prop::Aa ? 1 : 2;
-    return uint64_t(pt.nzs) * P_ * kQ * 8 * bufs <= fused_bytes_;
+    // (the fused bodies index with 32-bit arithmetic: fewer than 2^32
+    // elements per buffer whatever LBMGPU_FUSED_MB says)
+    const uint64_t elems = uint64_t(pt.nzs) * P_ * kQ;
+    return elems * 8 * bufs <= fused_bytes_ && elems < (1ull << 32);
   }
 
   template <bool SOA, int KIND>

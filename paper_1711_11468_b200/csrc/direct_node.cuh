@@ -2,19 +2,24 @@
 // (part of the direct-addressing translation unit, included by direct.cu)
 #pragma once
 
+#include <type_traits>
+
 #include "direct_args.cuh"
 
 namespace lbmgpu {
 
-template <bool SOA>
+// Element index of (storage plane, slot, y, x).  I32: 32-bit arithmetic for
+// lattices of fewer than 2^32 elements (the fused L2-resident launches,
+// DirectEngine::use_fused): three 32-bit multiply-adds per address instead
+// of 64-bit chains.
+template <bool SOA, bool I32 = false>
 struct Idx {
   uint64_t P;
   uint32_t nx, ny;
-  __device__ __forceinline__ uint64_t operator()(uint32_t zs, int slot,
-                                                 uint32_t y, uint32_t x) const {
-    if (SOA)
-      return (uint64_t(zs) * kQ + slot) * P + uint64_t(y) * nx + x;
-    return ((uint64_t(zs) * ny + y) * nx + x) * kQ + slot;
+  using T = std::conditional_t<I32, uint32_t, uint64_t>;
+  __device__ __forceinline__ T operator()(uint32_t zs, int slot, uint32_t y, uint32_t x) const {
+    if (SOA) return (T(zs) * kQ + slot) * T(P) + T(y) * nx + x;
+    return ((T(zs) * ny + y) * nx + x) * kQ + slot;
   }
 };
 
@@ -90,7 +95,7 @@ __device__ __forceinline__ void st(double* p, double v) {
 // kernels_full_os.cpp:56-89 + full_lattice.cpp:42-56 (push, correction on dst)
 template <bool SOA, bool CS, bool CG>
 __device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, uint32_t n) {
-  const Idx<SOA> I{a.P, a.nx, a.ny};
+  const Idx<SOA, CG> I{a.P, a.nx, a.ny};
   double q[kQ];
   const uint32_t tm = a.tmask ? a.tmask[n] : 0u;
 #pragma unroll
@@ -113,7 +118,7 @@ __device__ __forceinline__ void push_node(const DirectArgs& a, const Coords& c, 
 // kernels_full_os.cpp:56-89 (PULL); COLLIDE=false is the stream-only pass
 template <bool SOA, bool COLLIDE, bool CS, bool CG>
 __device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, uint32_t n) {
-  const Idx<SOA> I{a.P, a.nx, a.ny};
+  const Idx<SOA, CG> I{a.P, a.nx, a.ny};
   double q[kQ];
   // Warp-uniform fast path (cf. aa_odd_node): no active lane wraps in x, y
   // or (single part) z, so the gather of direction d -- slot d of x - c_d --
@@ -152,7 +157,7 @@ __device__ __forceinline__ void pull_node(const DirectArgs& a, const Coords& c, 
 template <bool SOA, bool CG>
 __device__ __forceinline__ void collide_node_pass(const DirectArgs& a, const Coords& c, uint32_t n) {
   if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
+  const Idx<SOA, CG> I{a.P, a.nx, a.ny};
   double q[kQ];
 #pragma unroll
   for (int d = 0; d < kQ; ++d) q[d] = ldp<CG>(a.dst + I(c.Z[1], dslot(d), c.y, c.x));
@@ -167,7 +172,7 @@ __device__ __forceinline__ void collide_node_pass(const DirectArgs& a, const Coo
 template <bool SOA, bool CS, bool CG>
 __device__ __forceinline__ void aa_even_node(const DirectArgs& a, const Coords& c, uint32_t n) {
   if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
+  const Idx<SOA, CG> I{a.P, a.nx, a.ny};
   double* buf = a.dst;
   double q[kQ];
 #pragma unroll
@@ -180,7 +185,7 @@ __device__ __forceinline__ void aa_even_node(const DirectArgs& a, const Coords& 
 template <bool SOA, bool CS, bool CG>
 __device__ __forceinline__ void aa_odd_node(const DirectArgs& a, const Coords& c, uint32_t n) {
   if (solid_node(a, c.x, c.y, c.z, n)) return;
-  const Idx<SOA> I{a.P, a.nx, a.ny};
+  const Idx<SOA, CG> I{a.P, a.nx, a.ny};
   double* buf = a.dst;
   // The slot direction d is gathered from, (x - c_d, opp d), is exactly the
   // slot direction opp(d) is scattered to, (x + c_opp(d), opp d): one address
