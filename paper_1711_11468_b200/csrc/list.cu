@@ -108,7 +108,11 @@ class ListEngine final : public Engine {
     // ranks in traversal order and canonical order
     // the AoS AA odd step's staging tiles keep the box-order scan (V + 1
     // entries: crank[V] = N closes the last row)
-    const bool aos_tiles = !d.soa && d.prop == Prop::Aa && d.blk == 0 && !d.ria;
+    // (their grid is (z tiles, y tiles, x tiles): boxes beyond 65535 tiles in
+    // y or x -- ny, nx > 131070 at the narrowest tile shape -- take the
+    // per-node kernel)
+    const bool aos_tiles = !d.soa && d.prop == Prop::Aa && d.blk == 0 && !d.ria &&
+                           ny_ <= 131070 && nx_ <= 131070;
     DevBuf<uint32_t> crank(V + 1);
     scan_fluid(geo.flags.get(), crank.get(), V, stream_);
     DevBuf<uint32_t> trank;
@@ -558,9 +562,9 @@ class ListEngine final : public Engine {
     g.nz = nz_;
     g.tiles_y = static_cast<uint32_t>(ceil_div(ny_, TY));
     g.tiles_z = static_cast<uint32_t>(ceil_div(nz_, TZ));
-    const uint64_t tiles = ceil_div(nx_, TX) * uint64_t(g.tiles_y) * g.tiles_z;
+    const dim3 tiles(g.tiles_z, g.tiles_y, static_cast<unsigned>(ceil_div(nx_, TX)));
     const int tok = stats_.begin("list_aa_odd_aos", stream_);
-    kern<<<static_cast<unsigned>(tiles), S::kT, S::kSmem, stream_>>>(a, g);
+    kern<<<tiles, S::kT, S::kSmem, stream_>>>(a, g);
     LBM_CHECK_LAUNCH();
     stats_.end(tok, stream_);
   }

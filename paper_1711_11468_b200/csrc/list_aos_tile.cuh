@@ -86,7 +86,6 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
   uint64_t* bar = reinterpret_cast<uint64_t*>(lt_smem + S::kStageBytes + S::kFlagBytes +
                                               S::kMetaBytes);
   const uint32_t t = threadIdx.x;
-  const uint32_t b = blockIdx.x;
   auto is_corner = [](uint32_t h) {  // not staged
     const uint32_t hx = h / (TY + 2), hy = h % (TY + 2);
     const bool ex = hx == 0 || hx == TX + 1, ey = hy == 0 || hy == TY + 1;
@@ -96,9 +95,9 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
     if (!EDGES) return (h / (TY + 2) - 1) * TY + (h % (TY + 2) - 1);
     return h - (h > 0) - (h > TY + 1) - (h > (TX + 1) * (TY + 2));
   };
-  const uint32_t z0 = (b % g.tiles_z) * TZ;
-  const uint32_t y0 = ((b / g.tiles_z) % g.tiles_y) * TY;
-  const uint32_t x0 = (b / (g.tiles_z * g.tiles_y)) * TX;
+  // grid (z tiles, y tiles, x tiles): the launch order is z fastest, the
+  // order of the list
+  const uint32_t z0 = blockIdx.x * TZ, y0 = blockIdx.y * TY, x0 = blockIdx.z * TX;
   const uint32_t zend = min(z0 + TZ, g.nz);
   // global loads first, all independent: the own cell's scan entries and
   // the halo rows' range bounds (one round trip before the TMA copies and
@@ -292,11 +291,19 @@ __global__ void __launch_bounds__(TX * TY * TZ, 512 / (TX * TY * TZ))
     const double* src = sh + staged_row(h) * S::kRowElems;
     const uint8_t* fr = flag + i * S::kRowElems;
     double* g0 = a.dst + m.g0;
-    double* g1 = a.dst + m.g1 - cnt0;
+    if (m.cnt1 == 0) {  // one list range (every row but those of a periodic z wrap)
 #pragma unroll
-    for (int it = 0; it < (S::kRowElems + 31) / 32; ++it) {
-      const uint32_t j = lane + 32u * it;
-      if (j < cnt && fr[j]) (j < cnt0 ? g0 : g1)[j] = src[j];
+      for (int it = 0; it < (S::kRowElems + 31) / 32; ++it) {
+        const uint32_t j = lane + 32u * it;
+        if (j < cnt0 && fr[j]) g0[j] = src[j];
+      }
+    } else {
+      double* g1 = a.dst + m.g1 - cnt0;
+#pragma unroll
+      for (int it = 0; it < (S::kRowElems + 31) / 32; ++it) {
+        const uint32_t j = lane + 32u * it;
+        if (j < cnt && fr[j]) (j < cnt0 ? g0 : g1)[j] = src[j];
+      }
     }
   }
 }

@@ -3,4 +3,4 @@
 mkdir -p gpurun_out
 timeout 1500 python tools/fuzz_parity.py 600 151000 > gpurun_out/r02bp_fuzz.log 2>&1; echo rc=$? >> gpurun_out/r02bp_fuzz.log
 FUZZ_BIG=1 timeout 900 python tools/fuzz_parity.py 60 157000 > gpurun_out/r02bp_fuzz_big.log 2>&1; echo rc=$? >> gpurun_out/r02bp_fuzz_big.log
-tail -2 gpurun_out/r02bp_fuzz.log gpurun_out/r02bp_fuzz_big.log
+tail -n 2 gpurun_out/r02bp_fuzz.log; tail -n 2 gpurun_out/r02bp_fuzz_big.log
