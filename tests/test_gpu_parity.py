@@ -166,7 +166,11 @@ def test_ria_pattern_id_widths(dims, expect):
 @pytest.mark.parametrize("name", ["blk-pull-aos", "blk-push-aos", "aa-aos"])
 @pytest.mark.parametrize("kind,dims", [("channel", (16, 8, 8)), ("channel", (32, 12, 8)),
                                        ("blocks", (32, 16, 16)), ("slit", (48, 4, 12)),
-                                       ("pipe", (16, 12, 12))])
+                                       ("pipe", (16, 12, 12)),
+                                       # boxes with interior tiles (no wrapped neighbour:
+                                       # the fixed-offset fast path) beside surface tiles
+                                       ("channel", (64, 16, 16)), ("blocks", (48, 12, 20)),
+                                       ("pipe", (80, 20, 12))])
 def test_aos_halo_tiles_against_oracle(name, kind, dims, port, monkeypatch):
     """The AoS 3-D halo-tile sweeps (TMA row copies split at the x wrap,
     y / z wrap of the halo rows, bulk stores of whole destination records)
@@ -192,6 +196,25 @@ def test_aos_halo_tiles_against_oracle(name, kind, dims, port, monkeypatch):
     tile = {"blk-pull-aos": "full_pull_aos", "blk-push-aos": "full_push_aos",
             "aa-aos": "full_aa_odd_aos"}[name]
     assert tile in rows, rows
+
+
+@pytest.mark.parametrize("by", ["0", "1", "2", "3", "4", "16"])
+def test_aos_tile_traversal_orders_against_oracle(by, port, monkeypatch):
+    """The 3-D grid of the AoS tile kernels in every traversal order
+    (LBMGPU_TILE_BY: plain, blocks of 2 / 4 y tiles, and the values that fall
+    back to plain -- not a power of two, not dividing the y tile count) on a
+    box with interior and surface tiles, bit for bit against the oracle."""
+    monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    monkeypatch.setenv("LBMGPU_TILE_BY", by)
+    kind, dims = "blocks", (64, 16, 12)
+    _, _, nf = port.geometry(kind, *dims)
+    init = port.perturbed(nf, 29)
+    expect, _ = port.run("full", kind, *dims, 4, PARAMS.omega_plus, g=G_TEST, init=init)
+    for name in ("aa-aos", "blk-pull-aos", "blk-push-aos"):
+        k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec(kind, *dims))
+        k.load_state(init)
+        k.advance(PARAMS, FORCE, 4)
+        assert np.array_equal(k.snapshot(), expect), (name, by)
 
 
 LIST_AOS_TILE_CASES = [
