@@ -41,6 +41,20 @@ for case in range(cases):
         if nf > 0:
             break
     name = str(rng.choice(["aa-soa", "aa-vec-soa"] if piped_case else names))
+    if name in ("aa-aos", "blk-pull-aos", "blk-push-aos") and rng.random() < 0.6:
+        # direct AoS tiles with interior tiles (fixed-offset fast path) beside
+        # the surface ones: three or more x tiles, three or more y / z tiles
+        while True:
+            kind = str(rng.choice(["channel", "slit", "pipe", "blocks"]))
+            nx, ny, nz = (int(rng.choice([48, 64, 80])), 4 * int(rng.integers(3, 7)),
+                          4 * int(rng.integers(3, 7)))
+            try:
+                _, _, nf = port.geometry(kind, nx, ny, nz, block, spacing)
+            except ValueError:
+                continue
+            if nf > 0:
+                break
+        os.environ["LBMGPU_TILE_BY"] = str(rng.choice(["8", "0", "2", "3", "4"]))
     blk = int(rng.integers(0, 5)) if name.startswith("list-") else 0
     tau = float(rng.uniform(0.52, 1.95))
     g = tuple(float(v) for v in rng.uniform(-3e-5, 3e-5, 3))
