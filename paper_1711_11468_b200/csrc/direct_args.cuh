@@ -1,4 +1,4 @@
-// Kernel arguments of the direct-addressing sweeps (direct.cu, direct_tma.cu).
+// Kernel arguments of the direct-addressing sweeps (direct.cu and its .cuh parts).
 #pragma once
 
 #include "lbm.hpp"

@@ -329,7 +329,7 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
     of a fixed byte pattern; after every kernel family has run -- each name
     per-sweep and fused, the TMA tiles and 3-D halo tiles, RIA codings,
     z-slab and node-range decompositions with every transport (device
-    copies, NCCL, peer memory), AA temporal blocking, CUDA-graph replay,
+    copies, NCCL, peer memory), the pipelined job,
     snapshot / load / verify -- no guard byte may have changed."""
     monkeypatch.setenv("LBMGPU_GUARD", "1")
     assert lbm.lbmgpu.guard_selftest() == 1  # a planted 8-byte overrun is seen
@@ -347,6 +347,28 @@ def test_no_out_of_bounds_writes_guard_zones(monkeypatch):
                 k.total_mass()
                 keep.append(k)
     monkeypatch.setenv("LBMGPU_FUSED_MB", "0")
+    # direct AoS tiles with interior tiles (fixed-offset fast path) in every
+    # traversal order, beside the surface tiles
+    for by in ("8", "0", "2"):
+        monkeypatch.setenv("LBMGPU_TILE_BY", by)
+        for name in ("aa-aos", "blk-pull-aos", "blk-push-aos"):
+            k = lbm.make_kernel(lbm.make_descriptor(name), lbm.GeometrySpec("blocks", 64, 16, 12))
+            k.load_perturbed(3)
+            k.advance(PARAMS, FORCE, 4)
+            keep.append(k)
+    monkeypatch.delenv("LBMGPU_TILE_BY")
+    # the pipelined job (staging buffers, layout kernels, slab launches)
+    for slabs, chunk, chunk_out in (("512", "16", "32"), ("7", "2", "3")):
+        monkeypatch.setenv("LBMGPU_JOB_SLABS", slabs)
+        monkeypatch.setenv("LBMGPU_JOB_CHUNK", chunk)
+        monkeypatch.setenv("LBMGPU_JOB_CHUNK_OUT", chunk_out)
+        k = lbm.make_kernel(lbm.make_descriptor("aa-soa"), lbm.GeometrySpec("channel", 32, 12, 40))
+        buf = lbm.PinnedBuffer(k.n_fluid() * 19)
+        buf.array[:] = lbm.perturbed_equilibrium(k.n_fluid(), 3)
+        _, piped = k.run(buf.array, PARAMS, FORCE, 6, out=buf.array)
+        assert piped
+        buf.free()
+        keep.append(k)
     for shape in ("0", "1", "5", "12"):  # list-aa-aos staging tiles (blk = 0)
         monkeypatch.setenv("LBMGPU_LTILE", shape)
         for spec in (small, tiled, lbm.GeometrySpec("pipe", 9, 12, 13)):
